@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Benchmark of the Crossover-SGD gossip step (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c3|c5|c1]
+
+A "step" is one full pass of the hot path (device topology,
+momentum-SGD update, segment exchange, mix, push-sum weights) over every worker.
+N = 1 times BASELINE configs[1] (16 workers x 11,689,512 fp32, k = 8) on one GPU;
+N > 1 keeps that per-GPU load (16 workers per GPU, world = 16 N; weak scaling)
+with segments crossing GPUs over NVLink peer memory.  --config c3 is one worker
+per GPU with a ResNet-50-sized vector (25,557,032), c5 eight workers per GPU.
+
+value   = whole-job "params mixed+updated" GB/s = 4 B * world * d / step time
+          (device-timed with CUDA events, max over ranks)
+e2e     = the same metric through the host-buffer entry point (grads copied
+          host->device every step, diagnostics copied back)
+roofline = the hot kernel's algorithmic bytes / its CUDA-event duration vs the
+          measured HBM copy peak (N = 1) or the measured NVLink peer bandwidth (N > 1)
+cpu_baseline = the oracle (oracle/, plain NumPy) timed on this host on a bounded
+          column sample of the same workload (rank 0, N = 1 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "gossip-step time and effective GB/s (params mixed+updated) vs HBM/NVLink roofline"
+UNIT = "GB/s"
+NVLINK_PEER_GBS = 770.0      # B200_PROFILING.md: measured peer copy per direction (nominal 900)
+HBM_FALLBACK_GBS = 6650.0    # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+
+WORKLOADS = {
+    # name: (workers per GPU, d, k, description)
+    "c1": (8, 1_000_000, 4, "8 workers x 1M fp32, k=4 (BASELINE configs[0])"),
+    "c2": (16, 11_689_512, 8, "16 workers x ResNet-18-sized 11,689,512 fp32, k=8 (BASELINE configs[1])"),
+    "c3": (1, 25_557_032, 8, "1 worker/GPU x ResNet-50-sized 25,557,032 fp32, k=8 (BASELINE configs[2])"),
+    "c5": (8, 25_557_032, 8, "8 workers/GPU x ResNet-50-sized 25,557,032 fp32 (BASELINE configs[4])"),
+}
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload: str):
+    """dram bytes per launch of the hot kernel from a committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(workload)
+    return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons while the timed region runs."""
+
+    def __init__(self, index: int, period_s: float = 0.01):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self._nv = None
+            return self
+        names = {
+            "hw_slowdown": getattr(self._nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(self._nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(self._nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(self._nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(self._nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                    r = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                    for k, bit in names.items():
+                        if r & bit:
+                            self.reasons.add(k)
+                except Exception:  # noqa: BLE001
+                    pass
+                time.sleep(self.period)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def cpu_oracle_sample(n: int, d: int, k: int, seed: int, budget_s: float, cols: int):
+    """The oracle as it stands, on all n workers x the first `cols` columns, for ~budget_s."""
+    import synth
+    from oracle import topology as T
+    from oracle.gossip import gossip_step
+    c = np.arange(min(cols, d))
+    x = synth.init_params(seed, range(n), d, c)
+    bank = synth.grad_bank(seed, n, d, c)
+    seg = T.segment_of_columns(T.segment_bounds(d, k), c)
+    m = np.zeros_like(x)
+    w = np.ones((n, k), np.float32)
+    steps, t0 = 0, time.perf_counter()
+    while True:
+        src = T.topology(seed, steps, n, k)
+        x, m, w = gossip_step(x, m, synth.grads_at(bank, n, steps), w, src, seg,
+                              synth.DEFAULT_LR, synth.DEFAULT_MOMENTUM)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or steps >= 1000:
+            break
+    per_step = el / steps
+    return {"value": 4.0 * n * len(c) / per_step / 1e9, "unit": UNIT, "cores": 1,
+            "host_cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+            "sample": f"{n} workers x first {len(c)} of {d} columns, k={k}, {steps} steps, "
+                      f"{per_step:.3f} s/step (NumPy elementwise, single-threaded)",
+            "steps": steps, "s_per_step": per_step}
+
+
+def emit(obj):
+    print(json.dumps(obj), flush=True)
+
+
+def run_reference(args, rank, world_size):
+    if rank != 0:
+        return
+    n_loc, d, k, desc = WORKLOADS[args.config]
+    n = n_loc * world_size
+    budget = max(5.0, 60.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        cpu_oracle_sample(n, d, k, 0, 0.0, args.cpu_cols)
+    res = [cpu_oracle_sample(n, d, k, 0, budget, args.cpu_cols) for _ in range(max(1, args.steps))]
+    v = statistics.median(r["value"] for r in res)
+    cb = dict(res[0])
+    cb["value"] = v
+    emit({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world_size,
+          "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+          "data": "synthetic", "config": {"workload": f"{args.config}: {desc}", "world": n, "d": d, "k": k},
+          "cpu_baseline": cb,
+          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None, choices=sorted(WORKLOADS))
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--d", type=int, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-cols", type=int, default=1_000_000)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world_size = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config is None:
+        args.config = "c2" if world_size == 1 else "c2"
+    if args.impl == "reference":
+        run_reference(args, rank, world_size)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import __graft_entry__ as entry
+    entry.build()
+    import paper_2012_15198_b200 as cs
+    import synth
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world_size > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n_loc, d, k, desc = WORKLOADS[args.config]
+    d = args.d or d
+    k = args.k or k
+    world = n_loc * world_size
+    if world < 2:
+        raise SystemExit(f"config {args.config} needs >= 2 workers in total")
+    seed = 0
+    lr, mu = float(synth.DEFAULT_LR), float(synth.DEFAULT_MOMENTUM)
+    first = rank * n_loc
+    B = world + 1
+
+    cs.cs_init(world, world, k, seed)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        x = torch.empty(n_loc, d, device=dev)
+        m = torch.zeros(n_loc, d, device=dev)
+        w = torch.ones(n_loc, k, device=dev)
+        bank = torch.empty(B + n_loc, d, device=dev)
+    cs.cs_bind(m, d, d, rank, world_size, stream)
+    cs.cs_synth_fill(x, n_loc, d, d, seed, synth.TAG_INIT, first, 1.0)
+    cs.cs_synth_fill(bank, B, d, d, seed, synth.TAG_GRAD, 0, float(synth.GRAD_SCALE))
+    stream.synchronize()
+    bank[B:] = bank[:n_loc]
+    torch.cuda.synchronize()
+    if world_size > 1:
+        cs.setup_peers()
+
+    def grads(t):
+        o = (t + first) % B
+        return bank[o:o + n_loc]
+
+    def barrier():
+        if world_size > 1:
+            dist.barrier()
+
+    t = 0
+    for _ in range(args.warmup):
+        cs.cs_gossip_step(x, grads(t), w, lr, mu)
+        t += 1
+    cs.cs_sync()
+    barrier()
+    torch.cuda.synchronize()
+
+    hbm_b, nvl_b = 0.0, 0.0
+    nvl_max = []
+    for s in range(t, t + args.steps):
+        hb, nb = cs.cs_step_bytes(s, False)
+        hbm_b += hb
+        nvl_max.append(nb)
+    cs.cs_set_timing(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            cs.cs_gossip_step(x, grads(t), w, lr, mu)
+            t += 1
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    cs.cs_sync()
+    ms = ev0.elapsed_time(ev1)
+    kern_ms, kern_launches = cs.cs_get_timing()
+    cs.cs_set_timing(False)
+    nvl_b = float(sum(nvl_max))
+    stats = torch.tensor([ms, kern_ms, nvl_b], dtype=torch.float64, device=dev)
+    if world_size > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    ms, kern_ms_max, nvl_b_max = stats.tolist()
+    ms_step = ms / args.steps
+    value = 4.0 * world * d / (ms_step * 1e-3) / 1e9
+
+    # ---- e2e through the public API: grads from pinned host memory every step ----
+    e2e = None
+    if not args.no_e2e:
+        esteps = max(2, args.e2e_steps)
+        host_bank = torch.empty(B + n_loc, d, dtype=torch.float32, pin_memory=True)
+        host_bank.copy_(bank.cpu())
+        torch.cuda.synchronize()
+        h2d = 4 * n_loc * d
+
+        def hgrads(tt):
+            o = (tt + first) % B
+            return host_bank[o:o + n_loc]
+
+        if world_size == 1:
+            cs.cs_gossip_step_host(x, hgrads(t), w, lr, mu)     # warm the staging buffer
+            t += 1
+            e0 = time.perf_counter()
+            torch.cuda.synchronize()
+            ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ee0.record(stream)
+            for _ in range(esteps):
+                cs.cs_gossip_step_host(x, hgrads(t), w, lr, mu)
+                t += 1
+            ee1.record(stream)
+            torch.cuda.synchronize()
+            ems = ee0.elapsed_time(ee1)
+            wall = time.perf_counter() - e0
+            d2h = 16
+        else:
+            stage = torch.empty(n_loc, d, device=dev)
+            wout = torch.empty(n_loc, k, pin_memory=True)
+            barrier()
+            torch.cuda.synchronize()
+            ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0 = time.perf_counter()
+            ee0.record(stream)
+            with torch.cuda.stream(stream):
+                for _ in range(esteps):
+                    stage.copy_(hgrads(t), non_blocking=True)
+                    cs.cs_gossip_step(x, stage, w, lr, mu)
+                    wout.copy_(w, non_blocking=True)
+                    stream.synchronize()
+                    t += 1
+            ee1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            ems = ee0.elapsed_time(ee1)
+            wall = time.perf_counter() - e0
+            d2h = 4 * n_loc * k
+        et = torch.tensor([ems], dtype=torch.float64, device=dev)
+        if world_size > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        ems = et.item()
+        e2e = {"value": 4.0 * world * d / (ems / esteps * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": esteps,
+               "ms_per_step": ems / esteps, "wall_s": wall,
+               "api": "cs_gossip_step_host" if world_size == 1 else "H2D copy + cs_gossip_step + psw D2H"}
+        del host_bank
+
+    # ---- roofline of the hot kernel --------------------------------------------------
+    avg_kern_s = kern_ms_max / max(1, kern_launches) * 1e-3
+    hpeak, hpeak_src = hbm_peak()
+    hbm_per_launch = hbm_b / args.steps
+    hbm_ach = hbm_per_launch / avg_kern_s / 1e9
+    roof_hbm = {"bound": "hbm", "achieved": hbm_ach, "peak": hpeak, "unit": "GB/s", "frac": hbm_ach / hpeak,
+                "traffic": ncu_traffic(args.config if world_size == 1 else f"{args.config}@{world_size}"),
+                "peak_source": hpeak_src, "kernel": "k_gossip_local" if world_size == 1 else "k_gossip_peer",
+                "algorithmic_bytes_per_launch": hbm_per_launch, "bytes_formula": "20 B x n_loc x d",
+                "avg_kernel_us": avg_kern_s * 1e6, "launches_timed": kern_launches}
+    if world_size == 1:
+        roofline = roof_hbm
+    else:
+        nvl_per_launch = nvl_b_max / args.steps
+        nvl_ach = nvl_per_launch / avg_kern_s / 1e9
+        roofline = {"bound": "nvlink", "achieved": nvl_ach, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                    "frac": nvl_ach / NVLINK_PEER_GBS, "traffic": None,
+                    "peak_source": "measured peer copy per direction (B200_PROFILING.md; 900 nominal)",
+                    "kernel": "k_gossip_peer", "algorithmic_bytes_per_launch": nvl_per_launch,
+                    "bytes_formula": "4 B x remote-sourced segment elements, most-loaded GPU",
+                    "avg_kernel_us": avg_kern_s * 1e6, "launches_timed": kern_launches, "hbm": roof_hbm}
+
+    cpu = None
+    if rank == 0 and world_size == 1 and not args.no_cpu:
+        cpu = cpu_oracle_sample(n_loc * world_size, d, k, seed, args.cpu_seconds, args.cpu_cols)
+
+    if rank == 0:
+        emit({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": args.steps,
+              "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+              "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+              "config": {"workload": f"{args.config}: {desc}", "world": world, "workers_per_gpu": n_loc,
+                         "d": d, "k": k, "seed": seed, "lr": lr, "momentum": mu,
+                         "parallelism": f"workers partitioned over {world_size} GPU(s)",
+                         "l2": f"inputs larger than L2 ({20.0 * n_loc * d / 1e9:.2f} GB moved per step per GPU)"},
+              "step_us": ms_step * 1e3,
+              "traffic_GBps": 20.0 * world * d / (ms_step * 1e-3) / 1e9,
+              "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+              "gpu_launches": 2 * args.steps, "clocks": clk.summary()})
+    if world_size > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    cs.cs_finalize()
+
+
+if __name__ == "__main__":
+    main()

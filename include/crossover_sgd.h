@@ -1,0 +1,224 @@
+/*
+ * crossover_sgd.h — C ABI of the B200-native Crossover-SGD gossip step.
+ *
+ * Method: Yeo et al., "Crossover-SGD: A gossip-based communication in distributed
+ * deep learning for alleviating large mini-batch problem and enhancing
+ * scalability", arXiv 2012.15198.  Citations are PAPER.md line numbers
+ * (section / algorithm line) of /root/reference/PAPER.md; readings C-n are listed
+ * in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *  - Return 0 (CS_OK) on success, a negative CS_E* code on error; no exception
+ *    ever crosses the ABI.  cs_last_error() gives a human-readable message for
+ *    the calling thread's last error.
+ *  - Device pointers are plain CUDA device addresses on the current device;
+ *    host pointers are ordinary (or pinned) host memory.  The caller owns every
+ *    buffer it passes; the library owns its topology tables, diagnostics
+ *    scratch, staging buffers and peer-visible exchange region.
+ *  - Device-side work is enqueued asynchronously on the bound stream.
+ *    Device-detected conditions (non-finite gradient) surface as CS_EDIVERGED
+ *    at the next cs_sync() / cs_get_diag().
+ *  - One process-wide context (cs_init .. cs_finalize).  Not thread-safe.
+ *  - There is no CPU fallback: every compute entry point runs CUDA kernels and
+ *    fails with CS_ECUDA if no sm_100a device is usable.
+ */
+#ifndef CROSSOVER_SGD_H
+#define CROSSOVER_SGD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes --------------------------------------------------------- */
+#define CS_OK                 0
+#define CS_EINVAL_WORLD      -1   /* world < 2, world > CS_MAX_WORLD, or world % nprocs != 0 */
+#define CS_EINVAL_GROUPS     -2   /* groups < 1 or groups does not divide world          */
+#define CS_EINVAL_SEGMENTS   -3   /* k < 1, k > CS_MAX_SEGMENTS, or k > ceil(d/32)       */
+#define CS_ELAYOUT           -4   /* misaligned pointer, ld % 4 != 0, ld < d, d < 1       */
+#define CS_ETOPOLOGY         -5   /* Alg. 2 restart limit (10,000 attempts) exceeded      */
+#define CS_EINVAL_TOPOLOGY   -6   /* injected topology row is not a derangement           */
+#define CS_ENOTINIT          -7   /* cs_init has not been called                          */
+#define CS_ENOTBOUND         -8   /* cs_bind has not been called                          */
+#define CS_ECUDA             -9   /* CUDA runtime / launch failure (see cs_last_error)    */
+#define CS_EDIVERGED        -10   /* a non-finite gradient was seen         */
+#define CS_EINVAL           -11   /* other invalid argument (NULL pointer, step range)    */
+#define CS_EUNSUPPORTED     -12   /* valid request this build does not implement          */
+#define CS_ETIMEOUT         -13   /* a cross-GPU wait exceeded its bound                  */
+
+#define CS_MAX_WORLD       1024   /* device Alg. 2 keeps a 1024-bit availability mask     */
+#define CS_MAX_SEGMENTS    4096
+#define CS_QUANTUM           32   /* segment bounds are multiples of 32 elements (C-2)    */
+#define CS_IPC_HANDLE_BYTES  64   /* sizeof(cudaIpcMemHandle_t)                           */
+
+#define CS_TAG_FLAT 0             /* Philox domain tag of the flat topology               */
+#define CS_TAG_HIER 1             /* Philox domain tag of the leader topology (C-13)      */
+
+/* ---- context -------------------------------------------------------------- */
+
+/* Create the process-wide context.
+ *   world      n = total number of workers across all processes (2..CS_MAX_WORLD).
+ *   groups     G = number of hierarchical groups; must divide world.  Groups are
+ *              contiguous blocks of world/G workers and the lowest rank of each
+ *              block is its leader (§3.3; reading C-12).  G = world
+ *              is the flat method; cs_gossip_step ignores G.
+ *   k_segments k = number of segments the flat parameter vector is split into
+ *              (reading C-2).
+ *   seed       the "random seed which is shared by every process"
+ *              — the Philox4x32-10 key of every topology draw (reading C-4).
+ * Pure host call (no CUDA).  Re-initialising replaces any previous context.
+ * Errors: CS_EINVAL_WORLD, CS_EINVAL_GROUPS, CS_EINVAL_SEGMENTS. */
+int cs_init(int world, int groups, int k_segments, uint64_t seed);
+
+/* Release every library-owned resource (device tables, peer mappings). */
+void cs_finalize(void);
+
+/* Message of the calling thread's most recent error ("" if none).  Owned by the
+ * library; valid until the next cs_* call on this thread. */
+const char* cs_last_error(void);
+
+/* ABI version (major*10000 + minor*100 + patch). */
+int cs_version(void);
+
+/* ---- pure host functions (callable before cs_bind, no GPU needed) ---------- */
+
+/* Segment plan (reading C-2): bounds_out[s] = min(d, 32*floor(s*ceil(d/32)/k)),
+ * bounds_out[k] = d.  bounds_out is caller-owned int64[k+1].
+ * Errors: CS_ENOTINIT, CS_ELAYOUT (d < 1), CS_EINVAL_SEGMENTS (k > ceil(d/32)). */
+int cs_segment_bounds(int64_t d, int64_t* bounds_out);
+
+/* Topology of a flat step (§3.2 Alg. 2, readings C-1, C-4..C-7):
+ * fills the caller-owned host int32 [k][world] with src_out[s*world + i] = the
+ * worker that worker i RECEIVES segment s from at `step` (Alg.1 l.5
+ * "receive_from = destinations[my rank]").  Every row is a
+ * permutation without fixed points.  Pure function of (seed, step, world, k).
+ * Requires 0 <= step < 2^32.  Errors: CS_ENOTINIT, CS_EINVAL, CS_ETOPOLOGY. */
+int cs_topology(int64_t step, int32_t* src_out);
+
+/* Leader topology of a hierarchical step (reading C-13): int32 [k][groups],
+ * indices are dense leader indices 0..G-1, domain tag CS_TAG_HIER.
+ * Errors as cs_topology; CS_EINVAL_GROUPS if groups < 2 (no leader gossip). */
+int cs_topology_hier(int64_t step, int32_t* src_out);
+
+/* ---- binding device state ------------------------------------------------- */
+
+/* Register the caller's device state and this process's place in the job.
+ *   momentum   fp32 device [n_loc][ld] heavy-ball buffer (reading C-9), updated
+ *              in place by every step.  n_loc = world / nprocs local workers;
+ *              local row r is global worker proc_rank*n_loc + r.
+ *   d          parameters per worker (>= 1).   ld  row stride in elements
+ *              (ld >= d, ld % 4 == 0, so rows are 16-byte aligned for 128-bit
+ *              access).  Elements [d, ld) of a row are never written.
+ *   proc_rank, nprocs   this process's index and the number of processes (one
+ *              per GPU).  nprocs == 1: all workers co-resident on this GPU.
+ *              nprocs > 1: call cs_ipc_export / cs_ipc_import next.
+ *   stream     cudaStream_t to enqueue on (NULL = legacy default stream).
+ * Buffers must be 16-byte aligned.  Allocates the library's device tables.
+ * Errors: CS_ENOTINIT, CS_EINVAL_WORLD, CS_ELAYOUT, CS_EINVAL_SEGMENTS, CS_ECUDA. */
+int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, void* stream);
+
+/* Change the stream later steps are enqueued on. */
+int cs_set_stream(void* stream);
+
+/* Multi-GPU (nprocs > 1): export this process's peer-visible exchange region
+ * (allocated by cs_bind) as a CUDA IPC handle (CS_IPC_HANDLE_BYTES bytes into
+ * handle_out).  The caller all-gathers the handles (e.g. over torch.distributed)
+ * and passes all nprocs of them, in rank order, to cs_ipc_import, which maps the
+ * peers' regions (NVLink peer memory).  Collective in the sense that every
+ * process must import before any process steps.
+ * Errors: CS_ENOTBOUND, CS_EINVAL, CS_ECUDA. */
+int cs_ipc_export(char* handle_out);
+int cs_ipc_import(const char* all_handles /* nprocs * CS_IPC_HANDLE_BYTES */);
+
+/* ---- the hot path --------------------------------------------------------- */
+
+/* One flat Crossover-SGD step at the internal step counter t, then t += 1.
+ * Enqueued on the bound stream:
+ *   a2  k topologies src_s = Alg.2(seed, t, s) (device-side, no communication)
+ *   a3  m_i <- fl(fl(momentum*m_i) + g_i);  y_i <- fl(x_i - fl(lr*m_i))
+ *       ("parameter averaging is processed after the gradient is applied",
+ *        PAPER.md:122; readings C-8, C-9)
+ *   a4  worker i obtains y_{src_s(i)} on segment s (Alg.1 l.4-8):
+ *       an HBM read when co-resident, an NVLink peer store when not
+ *   a5  x_i[R_s] <- fl(fl(y_i + y_{src_s(i)}) * 0.5)   (Alg.1 l.17)
+ *       psw_{i,s} <- fl(fl(psw_{i,s} + psw_{src_s(i),s}) * 0.5)  (C-11)
+ *   a6  (if cs_set_diag(1)) consensus distance and mean checksum, fp64.
+ *   params  fp32 device [n_loc][ld], updated in place (push-sum numerator x).
+ *   grads   fp32 device [n_loc][ld], read only.
+ *   psw     fp32 device [n_loc][k] push-sum weights, updated in place (start at 1).
+ *   lr, momentum  fp32 scalars.
+ * Every output reads only the pre-step snapshot.  Multi-GPU: every
+ * process must call with the same t.  Errors: CS_ENOTBOUND, CS_ELAYOUT, CS_EINVAL,
+ * CS_ECUDA, CS_ETOPOLOGY, CS_EDIVERGED (from an earlier step). */
+int cs_gossip_step(float* params, const float* grads, float* psw, float lr, float momentum);
+
+/* End-to-end variant of cs_gossip_step for host-resident gradients: copies
+ * grads_host (n_loc x ld fp32, pinned for full speed) into a library-owned
+ * device staging buffer, runs one step with diagnostics, copies the two fp64
+ * diagnostics into diag_out[2] = {consensus distance, mean checksum} and
+ * synchronises the stream.  params / psw stay device-resident. */
+int cs_gossip_step_host(float* params, const float* grads_host, float* psw, float lr,
+                        float momentum, double* diag_out);
+
+/* One hierarchical step (§3.3) at step t, then t += 1:
+ *   h1  per group, gbar = fl(sum_{i in G, ascending} g_i) * fp32(1/|G|)
+ *   h2  leaders apply a3 with gbar, then a4/a5 among the G leaders with the
+ *       leader topology (tag HIER); G == 1 skips the exchange (x = y)
+ *   h3  every member's params and psw become its leader's (bitwise)
+ * `grads` is read only.  Momentum is defined at leaders only: members' momentum
+ * rows are left unspecified.  Errors as cs_gossip_step. */
+int cs_hier_step(float* params, float* grads, float* psw, float lr, float momentum);
+
+/* ---- state, diagnostics, test hooks ------------------------------------------ */
+
+/* Set / read the step counter t (resume = restore buffers + cs_set_step). */
+int cs_set_step(int64_t step);
+int cs_get_step(int64_t* step_out);
+
+/* Enable (1) / disable (0) the fused diagnostics of later steps (default 0). */
+int cs_set_diag(int enable);
+
+/* Diagnostics of the most recent step that had them enabled:
+ *   cd_out    = sqrt((1/n) sum_i sum_j (z_ij - zbar_j)^2),  z = x / psw
+ *   mean_out  = sum_j zbar_j,   zbar_j = sum_i x_ij / sum_i psw_{i,s(j)}
+ * Synchronises the stream.  Errors: CS_EINVAL if no diagnosed step yet,
+ * CS_EDIVERGED. */
+int cs_get_diag(double* cd_out, double* mean_out);
+
+/* Wait for all enqueued work; reports deferred device errors. */
+int cs_sync(void);
+
+/* Test hook: replace the generated topology of the following steps with
+ * src [k][world] (receiver -> sender, every row a derangement) until called
+ * again with NULL.  Errors: CS_EINVAL_TOPOLOGY. */
+int cs_test_set_topology(const int32_t* src);
+
+/* Test hook: run the device topology generator for `step` and copy its
+ * [k][world] output to src_out (host).  Synchronises. */
+int cs_test_device_topology(int64_t step, int tag, int32_t* src_out);
+
+/* Input generator for tests and the benchmark (NOT part of the method): fills
+ * rows [row0, row0+rows) x [0, d) of a device fp32 matrix with row stride ld with
+ * scale * H(seed, tag, row, j), the SplitMix64 counter hash of synth/__init__.py.
+ * Enqueued on the bound stream (or the legacy stream before cs_bind). */
+int cs_synth_fill(float* out, int64_t rows, int64_t d, int64_t ld, uint64_t seed,
+                  int tag, int64_t row0, float scale);
+
+/* Bytes per step the hot kernel moves, for roofline accounting:
+ * out[0] = algorithmic HBM bytes, out[1] = NVLink bytes into this GPU at step t
+ * (exact, from the topology), for flat (hier = 0) or hierarchical (hier = 1). */
+int cs_step_bytes(int64_t step, int hier, double* out);
+
+/* Kernel timing for roofline accounting: with cs_set_timing(1) every later step
+ * records a CUDA event pair on the bound stream around its hot kernel
+ * (k_gossip_local / k_hier_local / k_gossip_peer).  cs_set_timing(1) also
+ * clears earlier records.  cs_get_timing synchronises and returns the summed
+ * event-measured duration (ms) and the number of timed launches. */
+int cs_set_timing(int enable);
+int cs_get_timing(double* total_ms_out, int64_t* launches_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CROSSOVER_SGD_H */

@@ -1,0 +1,245 @@
+"""ctypes binding of include/crossover_sgd.h — marshalling only.
+
+Tensors are passed as raw device pointers (`tensor.data_ptr()`), streams as the
+raw `cudaStream_t` of a `torch.cuda.Stream`.  Each wrapper raises CSError on a
+negative status.  No computation happens here.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcrossover_sgd.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(there is no CPU fallback)")
+
+lib = ctypes.CDLL(LIB_PATH)
+
+CS_MAX_WORLD = 1024
+CS_QUANTUM = 32
+CS_IPC_HANDLE_BYTES = 64
+CS_TAG_FLAT = 0
+CS_TAG_HIER = 1
+
+STATUS = {
+    0: "CS_OK", -1: "CS_EINVAL_WORLD", -2: "CS_EINVAL_GROUPS", -3: "CS_EINVAL_SEGMENTS",
+    -4: "CS_ELAYOUT", -5: "CS_ETOPOLOGY", -6: "CS_EINVAL_TOPOLOGY", -7: "CS_ENOTINIT",
+    -8: "CS_ENOTBOUND", -9: "CS_ECUDA", -10: "CS_EDIVERGED", -11: "CS_EINVAL",
+    -12: "CS_EUNSUPPORTED", -13: "CS_ETIMEOUT",
+}
+
+_c_int, _c_i64, _c_u64, _c_f, _vp = ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float, ctypes.c_void_p
+
+_SIGS = {
+    "cs_init": (_c_int, [_c_int, _c_int, _c_int, _c_u64]),
+    "cs_finalize": (None, []),
+    "cs_last_error": (ctypes.c_char_p, []),
+    "cs_version": (_c_int, []),
+    "cs_segment_bounds": (_c_int, [_c_i64, _vp]),
+    "cs_topology": (_c_int, [_c_i64, _vp]),
+    "cs_topology_hier": (_c_int, [_c_i64, _vp]),
+    "cs_bind": (_c_int, [_vp, _c_i64, _c_i64, _c_int, _c_int, _vp]),
+    "cs_set_stream": (_c_int, [_vp]),
+    "cs_ipc_export": (_c_int, [_vp]),
+    "cs_ipc_import": (_c_int, [_vp]),
+    "cs_gossip_step": (_c_int, [_vp, _vp, _vp, _c_f, _c_f]),
+    "cs_gossip_step_host": (_c_int, [_vp, _vp, _vp, _c_f, _c_f, _vp]),
+    "cs_hier_step": (_c_int, [_vp, _vp, _vp, _c_f, _c_f]),
+    "cs_set_step": (_c_int, [_c_i64]),
+    "cs_get_step": (_c_int, [_vp]),
+    "cs_set_diag": (_c_int, [_c_int]),
+    "cs_get_diag": (_c_int, [_vp, _vp]),
+    "cs_sync": (_c_int, []),
+    "cs_test_set_topology": (_c_int, [_vp]),
+    "cs_test_device_topology": (_c_int, [_c_i64, _c_int, _vp]),
+    "cs_synth_fill": (_c_int, [_vp, _c_i64, _c_i64, _c_i64, _c_u64, _c_int, _c_i64, _c_f]),
+    "cs_step_bytes": (_c_int, [_c_i64, _c_int, _vp]),
+    "cs_set_timing": (_c_int, [_c_int]),
+    "cs_get_timing": (_c_int, [_vp, _vp]),
+}
+
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+def exported_symbols():
+    return sorted(_SIGS)
+
+
+class CSError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+        super().__init__(f"{where}: {self.status} ({code}): {cs_last_error()}")
+
+
+def _check(rc: int, where: str) -> int:
+    if rc < 0:
+        raise CSError(rc, where)
+    return rc
+
+
+def _ptr(t) -> int:
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def _stream_handle(stream) -> int | None:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def cs_last_error() -> str:
+    return lib.cs_last_error().decode()
+
+
+def cs_version() -> int:
+    return lib.cs_version()
+
+
+def cs_init(world: int, groups: int, k_segments: int, seed: int) -> None:
+    _check(lib.cs_init(world, groups, k_segments, seed & 0xFFFFFFFFFFFFFFFF), "cs_init")
+
+
+def cs_finalize() -> None:
+    lib.cs_finalize()
+
+
+def cs_segment_bounds(d: int, k: int) -> np.ndarray:
+    out = np.zeros(k + 1, dtype=np.int64)
+    _check(lib.cs_segment_bounds(d, out.ctypes.data), "cs_segment_bounds")
+    return out
+
+
+def cs_topology(step: int, world: int, k: int) -> np.ndarray:
+    out = np.zeros((k, world), dtype=np.int32)
+    _check(lib.cs_topology(step, out.ctypes.data), "cs_topology")
+    return out
+
+
+def cs_topology_hier(step: int, groups: int, k: int) -> np.ndarray:
+    out = np.zeros((k, groups), dtype=np.int32)
+    _check(lib.cs_topology_hier(step, out.ctypes.data), "cs_topology_hier")
+    return out
+
+
+def cs_bind(momentum, d: int, ld: int | None = None, proc_rank: int = 0, nprocs: int = 1,
+            stream=None) -> None:
+    ld = d if ld is None else ld
+    _check(lib.cs_bind(_ptr(momentum), d, ld, proc_rank, nprocs, _stream_handle(stream)), "cs_bind")
+
+
+def cs_set_stream(stream) -> None:
+    _check(lib.cs_set_stream(_stream_handle(stream)), "cs_set_stream")
+
+
+def cs_ipc_export() -> bytes:
+    buf = ctypes.create_string_buffer(CS_IPC_HANDLE_BYTES)
+    _check(lib.cs_ipc_export(buf), "cs_ipc_export")
+    return buf.raw
+
+
+def cs_ipc_import(handles: list[bytes]) -> None:
+    blob = b"".join(handles)
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    _check(lib.cs_ipc_import(buf), "cs_ipc_import")
+
+
+def setup_peers(group=None) -> None:
+    """Exchange exchange-region IPC handles over torch.distributed and map the peers."""
+    import torch.distributed as dist
+    mine = cs_ipc_export()
+    allh = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allh, mine, group=group)
+    cs_ipc_import(allh)
+    dist.barrier(group=group)
+
+
+def cs_gossip_step(params, grads, psw, lr: float, momentum: float) -> None:
+    _check(lib.cs_gossip_step(_ptr(params), _ptr(grads), _ptr(psw), lr, momentum), "cs_gossip_step")
+
+
+def cs_gossip_step_host(params, grads_host, psw, lr: float, momentum: float) -> tuple[float, float]:
+    out = np.zeros(2, dtype=np.float64)
+    _check(lib.cs_gossip_step_host(_ptr(params), _ptr(grads_host), _ptr(psw), lr, momentum,
+                                   out.ctypes.data), "cs_gossip_step_host")
+    return float(out[0]), float(out[1])
+
+
+def cs_hier_step(params, grads, psw, lr: float, momentum: float) -> None:
+    _check(lib.cs_hier_step(_ptr(params), _ptr(grads), _ptr(psw), lr, momentum), "cs_hier_step")
+
+
+def cs_set_step(step: int) -> None:
+    _check(lib.cs_set_step(step), "cs_set_step")
+
+
+def cs_get_step() -> int:
+    v = ctypes.c_int64(0)
+    _check(lib.cs_get_step(ctypes.byref(v)), "cs_get_step")
+    return v.value
+
+
+def cs_set_diag(enable: bool) -> None:
+    _check(lib.cs_set_diag(1 if enable else 0), "cs_set_diag")
+
+
+def cs_get_diag() -> tuple[float, float]:
+    cd, mean = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    _check(lib.cs_get_diag(ctypes.byref(cd), ctypes.byref(mean)), "cs_get_diag")
+    return cd.value, mean.value
+
+
+def cs_sync() -> None:
+    _check(lib.cs_sync(), "cs_sync")
+
+
+def cs_test_set_topology(src: np.ndarray | None) -> None:
+    if src is None:
+        _check(lib.cs_test_set_topology(None), "cs_test_set_topology")
+        return
+    arr = np.ascontiguousarray(src, dtype=np.int32)
+    _check(lib.cs_test_set_topology(arr.ctypes.data), "cs_test_set_topology")
+
+
+def cs_test_device_topology(step: int, n: int, k: int, tag: int = CS_TAG_FLAT) -> np.ndarray:
+    out = np.zeros((k, n), dtype=np.int32)
+    _check(lib.cs_test_device_topology(step, tag, out.ctypes.data), "cs_test_device_topology")
+    return out
+
+
+def cs_synth_fill(out, rows: int, d: int, ld: int, seed: int, tag: int, row0: int, scale: float) -> None:
+    _check(lib.cs_synth_fill(_ptr(out), rows, d, ld, seed & 0xFFFFFFFFFFFFFFFF, tag, row0, scale),
+           "cs_synth_fill")
+
+
+def cs_step_bytes(step: int, hier: bool = False) -> tuple[float, float]:
+    out = np.zeros(2, dtype=np.float64)
+    _check(lib.cs_step_bytes(step, 1 if hier else 0, out.ctypes.data), "cs_step_bytes")
+    return float(out[0]), float(out[1])
+
+
+def cs_set_timing(enable: bool) -> None:
+    _check(lib.cs_set_timing(1 if enable else 0), "cs_set_timing")
+
+
+def cs_get_timing() -> tuple[float, int]:
+    ms, n = ctypes.c_double(0.0), ctypes.c_int64(0)
+    _check(lib.cs_get_timing(ctypes.byref(ms), ctypes.byref(n)), "cs_get_timing")
+    return ms.value, n.value

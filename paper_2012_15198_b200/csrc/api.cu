@@ -1,0 +1,610 @@
+// C ABI (include/crossover_sgd.h): process-wide context, argument validation,
+// device tables and kernel launches.  No compute happens on the host except the
+// (pure, cheap) host topology of cs_topology / byte accounting.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/crossover_sgd.h"
+#include "common.cuh"
+#include "peer.cuh"
+
+using namespace cs;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(CS_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CS_CUDA(call)                                  \
+  do {                                                 \
+    cudaError_t _e = (call);                           \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+struct Ctx {
+  bool inited = false;
+  int world = 0, groups = 0, k = 0;
+  uint64_t seed = 0;
+
+  bool bound = false;
+  int64_t d = 0, ld = 0, nq = 0;
+  int rank = 0, nprocs = 1, n_loc = 0, first = 0;
+  float* mom = nullptr;
+  cudaStream_t stream = nullptr;
+  int device = 0;
+
+  int64_t step = 0;
+  int diag = 0;
+  bool diag_valid = false;
+
+  // device tables
+  int64_t* d_bounds = nullptr;
+  int32_t* d_src = nullptr;
+  int32_t* d_dst = nullptr;
+  uint32_t* d_ord = nullptr;
+  int32_t* d_given = nullptr;
+  double* d_rw = nullptr;
+  double* d_inv_wsum = nullptr;
+  int* d_err = nullptr;
+  double* d_partials = nullptr;
+  int partials_cap = 0;
+  double* d_diag = nullptr;
+  bool has_override = false;
+
+  float* d_stage = nullptr;   // cs_gossip_step_host staging buffer
+  size_t stage_bytes = 0;
+
+  PeerState peer;             // multi-GPU exchange region (nprocs > 1)
+
+  // hot-kernel timing (cs_set_timing): event pairs recorded around each launch
+  bool timing = false;
+  std::vector<cudaEvent_t> events;
+  size_t events_used = 0;
+};
+
+Ctx g;
+
+void free_events() {
+  for (cudaEvent_t e : g.events) cudaEventDestroy(e);
+  g.events.clear();
+  g.events_used = 0;
+}
+
+// Two events bracketing the next hot-kernel launch (nullptr pair when timing is off).
+int next_event_pair(cudaEvent_t* ev) {
+  ev[0] = ev[1] = nullptr;
+  if (!g.timing) return CS_OK;
+  while (g.events.size() < g.events_used + 2) {
+    cudaEvent_t e;
+    CS_CUDA(cudaEventCreate(&e));
+    g.events.push_back(e);
+  }
+  ev[0] = g.events[g.events_used];
+  ev[1] = g.events[g.events_used + 1];
+  g.events_used += 2;
+  return CS_OK;
+}
+
+void free_device() {
+  auto f = [](void* p) { if (p) cudaFree(p); };
+  f(g.d_bounds); f(g.d_src); f(g.d_dst); f(g.d_ord); f(g.d_given); f(g.d_rw);
+  f(g.d_inv_wsum); f(g.d_err); f(g.d_partials); f(g.d_diag); f(g.d_stage);
+  g.d_bounds = nullptr; g.d_src = nullptr; g.d_dst = nullptr; g.d_ord = nullptr;
+  g.d_given = nullptr; g.d_rw = nullptr; g.d_inv_wsum = nullptr; g.d_err = nullptr;
+  g.d_partials = nullptr; g.d_diag = nullptr; g.d_stage = nullptr;
+  g.partials_cap = 0; g.stage_bytes = 0;
+  peer_release(g.peer);
+}
+
+std::vector<int64_t> host_bounds(int64_t d, int k) {
+  const int64_t nq = (d + kQuantum - 1) / kQuantum;
+  std::vector<int64_t> b(k + 1);
+  for (int s = 0; s < k; ++s) {
+    int64_t v = kQuantum * ((s * nq) / k);
+    b[s] = v < d ? v : d;
+  }
+  b[k] = d;
+  return b;
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+int check_bound() {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (!g.bound) return fail(CS_ENOTBOUND, "cs_bind has not been called");
+  return CS_OK;
+}
+
+int check_step_args(const float* params, const float* grads, const float* psw) {
+  if (!params || !grads || !psw) return fail(CS_EINVAL, "NULL params/grads/psw");
+  if (!aligned16(params) || !aligned16(grads))
+    return fail(CS_ELAYOUT, "params and grads must be 16-byte aligned");
+  if (((uintptr_t)psw & 3u) != 0) return fail(CS_ELAYOUT, "psw must be 4-byte aligned");
+  if (g.step < 0 || g.step >= (int64_t(1) << 32))
+    return fail(CS_EINVAL, "step %lld outside [0, 2^32)", (long long)g.step);
+  return CS_OK;
+}
+
+// Deferred device errors (topology restart cap, non-finite gradient).
+int poll_device_errors() {
+  int h[kNumErr] = {0, 0, 0};
+  CS_CUDA(cudaMemcpy(h, g.d_err, sizeof(h), cudaMemcpyDeviceToHost));
+  if (h[kErrTopology] || h[kErrDiverged] || h[kErrTimeout]) {
+    int z[kNumErr] = {0, 0, 0};
+    CS_CUDA(cudaMemcpy(g.d_err, z, sizeof(z), cudaMemcpyHostToDevice));
+  }
+  if (h[kErrTimeout]) return fail(CS_ETIMEOUT, "a cross-GPU wait exceeded its bound");
+  if (h[kErrTopology]) return fail(CS_ETOPOLOGY, "Alg.2 restart limit (10,000) exceeded");
+  if (h[kErrDiverged]) return fail(CS_EDIVERGED, "non-finite gradient seen in a step");
+  return CS_OK;
+}
+
+int ensure_partials(int grid) {
+  if (grid <= g.partials_cap) return CS_OK;
+  if (g.d_partials) cudaFree(g.d_partials);
+  g.d_partials = nullptr;
+  CS_CUDA(cudaMalloc(&g.d_partials, sizeof(double) * 2 * (size_t)grid));
+  g.partials_cap = grid;
+  return CS_OK;
+}
+
+TopoArgs topo_args(int n, int tag, float* psw, int group_size) {
+  TopoArgs t;
+  t.seed = g.seed;
+  t.step = (uint32_t)g.step;
+  t.n = n;
+  t.k = g.k;
+  t.tag = tag;
+  t.given = nullptr;
+  t.src = g.d_src;
+  t.dst = g.d_dst;
+  t.ord = g.d_ord;
+  t.psw = psw;
+  t.group_size = group_size;
+  t.rw = g.d_rw;
+  t.inv_wsum = g.d_inv_wsum;
+  t.err = g.d_err;
+  return t;
+}
+
+LocalArgs local_args(float* params, const float* grads, int n, int gs, float lr, float mu) {
+  LocalArgs a;
+  a.x = params;
+  a.m = g.mom;
+  a.g = grads;
+  a.ld = g.ld;
+  a.d = g.d;
+  a.n = n;
+  a.group_size = gs;
+  a.k = g.k;
+  a.nq = g.nq;
+  a.ord = g.d_ord;
+  a.rw = g.d_rw;
+  a.inv_wsum = g.d_inv_wsum;
+  a.lr = lr;
+  a.mu = mu;
+  a.inv_group = 1.0f / (float)gs;
+  a.partials = g.d_partials;
+  a.err = g.d_err;
+  return a;
+}
+
+int validate_derangements(const int32_t* src, int n, int k) {
+  std::vector<int> seen(n);
+  for (int s = 0; s < k; ++s) {
+    std::fill(seen.begin(), seen.end(), 0);
+    for (int i = 0; i < n; ++i) {
+      int r = src[(int64_t)s * n + i];
+      if (r < 0 || r >= n || r == i || seen[r])
+        return fail(CS_EINVAL_TOPOLOGY, "row %d is not a derangement (entry %d -> %d)", s, i, r);
+      seen[r] = 1;
+    }
+  }
+  return CS_OK;
+}
+
+int enqueue_flat_step(float* params, const float* grads, float* psw, float lr, float mu,
+                      bool diag) {
+  const int n = g.world;
+  TopoArgs t = topo_args(n, CS_TAG_FLAT, psw, 1);
+  if (g.has_override) t.given = g.d_given;
+  CS_CUDA(launch_topology(t, g.stream));
+  const int grid = local_grid_size(false, diag, g.d);
+  if (diag) {
+    int rc = ensure_partials(grid);
+    if (rc) return rc;
+  }
+  LocalArgs a = local_args(params, grads, n, 1, lr, mu);
+  cudaEvent_t ev[2];
+  int rc = next_event_pair(ev);
+  if (rc) return rc;
+  if (ev[0]) CS_CUDA(cudaEventRecord(ev[0], g.stream));
+  CS_CUDA(launch_gossip_local(a, diag, grid, g.stream));
+  if (ev[1]) CS_CUDA(cudaEventRecord(ev[1], g.stream));
+  if (diag) CS_CUDA(launch_diag_finalize(g.d_partials, grid, n, g.d_diag, g.stream));
+  return CS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cs_version(void) { return 100; }
+
+const char* cs_last_error(void) { return g_err.c_str(); }
+
+int cs_init(int world, int groups, int k_segments, uint64_t seed) {
+  g_err.clear();
+  if (g.inited) cs_finalize();
+  if (world < 2 || world > CS_MAX_WORLD)
+    return fail(CS_EINVAL_WORLD, "world %d outside [2, %d]", world, CS_MAX_WORLD);
+  if (groups < 1 || world % groups != 0)
+    return fail(CS_EINVAL_GROUPS, "groups %d must be >= 1 and divide world %d", groups, world);
+  if (k_segments < 1 || k_segments > CS_MAX_SEGMENTS)
+    return fail(CS_EINVAL_SEGMENTS, "k %d outside [1, %d]", k_segments, CS_MAX_SEGMENTS);
+  g = Ctx();
+  g.world = world;
+  g.groups = groups;
+  g.k = k_segments;
+  g.seed = seed;
+  g.inited = true;
+  return CS_OK;
+}
+
+void cs_finalize(void) {
+  if (g.bound) {
+    cudaStreamSynchronize(g.stream);
+    free_device();
+  }
+  free_events();
+  g = Ctx();
+}
+
+int cs_segment_bounds(int64_t d, int64_t* bounds_out) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (!bounds_out) return fail(CS_EINVAL, "NULL bounds_out");
+  if (d < 1) return fail(CS_ELAYOUT, "d must be >= 1");
+  if ((d + kQuantum - 1) / kQuantum < g.k)
+    return fail(CS_EINVAL_SEGMENTS, "k %d > ceil(d/32) = %lld", g.k, (long long)((d + 31) / 32));
+  std::vector<int64_t> b = host_bounds(d, g.k);
+  memcpy(bounds_out, b.data(), sizeof(int64_t) * b.size());
+  return CS_OK;
+}
+
+static int topology_common(int64_t step, int n, int tag, int32_t* src_out) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (!src_out) return fail(CS_EINVAL, "NULL src_out");
+  if (step < 0 || step >= (int64_t(1) << 32))
+    return fail(CS_EINVAL, "step %lld outside [0, 2^32)", (long long)step);
+  for (int s = 0; s < g.k; ++s) {
+    if (host_alg2(g.seed, (uint32_t)step, (uint32_t)s, n, tag, src_out + (int64_t)s * n) < 0)
+      return fail(CS_ETOPOLOGY, "Alg.2 restart limit (10,000) exceeded");
+  }
+  return CS_OK;
+}
+
+int cs_topology(int64_t step, int32_t* src_out) {
+  return topology_common(step, g.world, CS_TAG_FLAT, src_out);
+}
+
+int cs_topology_hier(int64_t step, int32_t* src_out) {
+  if (g.inited && g.groups < 2)
+    return fail(CS_EINVAL_GROUPS, "leader topology needs groups >= 2 (have %d)", g.groups);
+  return topology_common(step, g.groups, CS_TAG_HIER, src_out);
+}
+
+int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, void* stream) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (nprocs < 1 || proc_rank < 0 || proc_rank >= nprocs)
+    return fail(CS_EINVAL, "proc_rank %d / nprocs %d invalid", proc_rank, nprocs);
+  if (g.world % nprocs != 0)
+    return fail(CS_EINVAL_WORLD, "world %d not divisible by nprocs %d", g.world, nprocs);
+  if (!momentum) return fail(CS_EINVAL, "NULL momentum");
+  if (d < 1 || ld < d || (ld & 3) != 0)
+    return fail(CS_ELAYOUT, "need d >= 1, ld >= d, ld %% 4 == 0 (d=%lld ld=%lld)", (long long)d,
+                (long long)ld);
+  if (!aligned16(momentum)) return fail(CS_ELAYOUT, "momentum must be 16-byte aligned");
+  if ((d + kQuantum - 1) / kQuantum < g.k)
+    return fail(CS_EINVAL_SEGMENTS, "k %d > ceil(d/32) = %lld", g.k, (long long)((d + 31) / 32));
+  if (g.bound) {
+    cudaStreamSynchronize(g.stream);
+    free_device();
+    g.bound = false;
+  }
+  g.d = d;
+  g.ld = ld;
+  g.nq = (d + kQuantum - 1) / kQuantum;
+  g.rank = proc_rank;
+  g.nprocs = nprocs;
+  g.n_loc = g.world / nprocs;
+  g.first = proc_rank * g.n_loc;
+  g.mom = momentum;
+  g.stream = (cudaStream_t)stream;
+  CS_CUDA(cudaGetDevice(&g.device));
+  const size_t kn = (size_t)g.k * g.world;
+  std::vector<int64_t> b = host_bounds(d, g.k);
+  CS_CUDA(cudaMalloc(&g.d_bounds, sizeof(int64_t) * b.size()));
+  CS_CUDA(cudaMemcpy(g.d_bounds, b.data(), sizeof(int64_t) * b.size(), cudaMemcpyHostToDevice));
+  CS_CUDA(cudaMalloc(&g.d_src, sizeof(int32_t) * kn));
+  CS_CUDA(cudaMalloc(&g.d_dst, sizeof(int32_t) * kn));
+  CS_CUDA(cudaMalloc(&g.d_ord, sizeof(uint32_t) * kn));
+  CS_CUDA(cudaMalloc(&g.d_given, sizeof(int32_t) * kn));
+  CS_CUDA(cudaMalloc(&g.d_rw, sizeof(double) * kn));
+  CS_CUDA(cudaMalloc(&g.d_inv_wsum, sizeof(double) * g.k));
+  CS_CUDA(cudaMalloc(&g.d_err, sizeof(int) * kNumErr));
+  CS_CUDA(cudaMemset(g.d_err, 0, sizeof(int) * kNumErr));
+  CS_CUDA(cudaMalloc(&g.d_diag, sizeof(double) * 2));
+  if (nprocs > 1) {
+    int rc = peer_alloc(g.peer, g.n_loc, d, ld, g.k, nprocs, proc_rank);
+    if (rc) return fail(rc, "%s", peer_error());
+  }
+  g.bound = true;
+  g.diag_valid = false;
+  return CS_OK;
+}
+
+int cs_set_stream(void* stream) {
+  int rc = check_bound();
+  if (rc) return rc;
+  g.stream = (cudaStream_t)stream;
+  return CS_OK;
+}
+
+int cs_ipc_export(char* handle_out) {
+  int rc = check_bound();
+  if (rc) return rc;
+  if (!handle_out) return fail(CS_EINVAL, "NULL handle_out");
+  if (g.nprocs < 2) return fail(CS_EINVAL, "cs_ipc_export needs nprocs > 1");
+  rc = peer_export(g.peer, handle_out);
+  return rc ? fail(rc, "%s", peer_error()) : CS_OK;
+}
+
+int cs_ipc_import(const char* all_handles) {
+  int rc = check_bound();
+  if (rc) return rc;
+  if (!all_handles) return fail(CS_EINVAL, "NULL all_handles");
+  if (g.nprocs < 2) return fail(CS_EINVAL, "cs_ipc_import needs nprocs > 1");
+  rc = peer_import(g.peer, all_handles);
+  return rc ? fail(rc, "%s", peer_error()) : CS_OK;
+}
+
+int cs_gossip_step(float* params, const float* grads, float* psw, float lr, float momentum) {
+  int rc = check_bound();
+  if (rc) return rc;
+  rc = check_step_args(params, grads, psw);
+  if (rc) return rc;
+  const bool diag = g.diag != 0;
+  if (g.nprocs == 1) {
+    rc = enqueue_flat_step(params, grads, psw, lr, momentum, diag);
+  } else {
+    if (!g.peer.imported) return fail(CS_ENOTBOUND, "multi-GPU: cs_ipc_import has not been called");
+    PeerStepArgs pa;
+    pa.x = params; pa.m = g.mom; pa.g = grads; pa.psw = psw;
+    pa.ld = g.ld; pa.d = g.d; pa.nq = g.nq; pa.k = g.k;
+    pa.world = g.world; pa.n_loc = g.n_loc; pa.first = g.first; pa.rank = g.rank;
+    pa.nprocs = g.nprocs; pa.step = (uint32_t)g.step; pa.seed = g.seed;
+    pa.lr = lr; pa.mu = momentum;
+    pa.given = g.has_override ? g.d_given : nullptr;
+    pa.src = g.d_src; pa.dst = g.d_dst; pa.ord = g.d_ord; pa.err = g.d_err;
+    cudaEvent_t ev[2];
+    rc = next_event_pair(ev);
+    if (rc) return rc;
+    rc = peer_flat_step(g.peer, pa, g.stream, ev[0], ev[1]);
+    if (rc) return fail(rc, "%s", peer_error());
+  }
+  if (rc) return rc;
+  if (diag) g.diag_valid = (g.nprocs == 1);
+  g.step += 1;
+  return CS_OK;
+}
+
+int cs_gossip_step_host(float* params, const float* grads_host, float* psw, float lr,
+                        float momentum, double* diag_out) {
+  int rc = check_bound();
+  if (rc) return rc;
+  if (!grads_host || !diag_out) return fail(CS_EINVAL, "NULL grads_host/diag_out");
+  if (g.nprocs != 1) return fail(CS_EUNSUPPORTED, "cs_gossip_step_host is single-GPU");
+  const size_t bytes = sizeof(float) * (size_t)g.n_loc * (size_t)g.ld;
+  if (g.stage_bytes < bytes) {
+    if (g.d_stage) cudaFree(g.d_stage);
+    g.d_stage = nullptr;
+    CS_CUDA(cudaMalloc(&g.d_stage, bytes));
+    g.stage_bytes = bytes;
+  }
+  CS_CUDA(cudaMemcpyAsync(g.d_stage, grads_host, bytes, cudaMemcpyHostToDevice, g.stream));
+  rc = check_step_args(params, g.d_stage, psw);
+  if (rc) return rc;
+  rc = enqueue_flat_step(params, g.d_stage, psw, lr, momentum, true);
+  if (rc) return rc;
+  g.diag_valid = true;
+  g.step += 1;
+  CS_CUDA(cudaMemcpyAsync(diag_out, g.d_diag, 2 * sizeof(double), cudaMemcpyDeviceToHost, g.stream));
+  CS_CUDA(cudaStreamSynchronize(g.stream));
+  return poll_device_errors();
+}
+
+int cs_hier_step(float* params, float* grads, float* psw, float lr, float momentum) {
+  int rc = check_bound();
+  if (rc) return rc;
+  rc = check_step_args(params, grads, psw);
+  if (rc) return rc;
+  if (g.nprocs != 1)
+    return fail(CS_EUNSUPPORTED, "multi-GPU hierarchical step is not implemented in this build");
+  const bool diag = g.diag != 0;
+  const int L = g.groups, gs = g.world / g.groups;
+  TopoArgs t = topo_args(L, CS_TAG_HIER, psw, gs);
+  CS_CUDA(launch_topology(t, g.stream));
+  const int grid = local_grid_size(true, diag, g.d);
+  if (diag) {
+    rc = ensure_partials(grid);
+    if (rc) return rc;
+  }
+  LocalArgs a = local_args(params, grads, L, gs, lr, momentum);
+  cudaEvent_t ev[2];
+  rc = next_event_pair(ev);
+  if (rc) return rc;
+  if (ev[0]) CS_CUDA(cudaEventRecord(ev[0], g.stream));
+  CS_CUDA(launch_hier_local(a, diag, grid, g.stream));
+  if (ev[1]) CS_CUDA(cudaEventRecord(ev[1], g.stream));
+  if (diag) {
+    CS_CUDA(launch_diag_finalize(g.d_partials, grid, g.world, g.d_diag, g.stream));
+    g.diag_valid = true;
+  }
+  g.step += 1;
+  return CS_OK;
+}
+
+int cs_set_step(int64_t step) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (step < 0 || step >= (int64_t(1) << 32)) return fail(CS_EINVAL, "step outside [0, 2^32)");
+  g.step = step;
+  return CS_OK;
+}
+
+int cs_get_step(int64_t* step_out) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (!step_out) return fail(CS_EINVAL, "NULL step_out");
+  *step_out = g.step;
+  return CS_OK;
+}
+
+int cs_set_diag(int enable) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  g.diag = enable ? 1 : 0;
+  return CS_OK;
+}
+
+int cs_get_diag(double* cd_out, double* mean_out) {
+  int rc = check_bound();
+  if (rc) return rc;
+  if (!cd_out || !mean_out) return fail(CS_EINVAL, "NULL output");
+  if (!g.diag_valid) return fail(CS_EINVAL, "no step with diagnostics enabled yet");
+  double h[2];
+  CS_CUDA(cudaMemcpyAsync(h, g.d_diag, sizeof(h), cudaMemcpyDeviceToHost, g.stream));
+  CS_CUDA(cudaStreamSynchronize(g.stream));
+  rc = poll_device_errors();
+  if (rc) return rc;
+  *cd_out = h[0];
+  *mean_out = h[1];
+  return CS_OK;
+}
+
+int cs_sync(void) {
+  int rc = check_bound();
+  if (rc) return rc;
+  CS_CUDA(cudaStreamSynchronize(g.stream));
+  CS_CUDA(cudaGetLastError());
+  return poll_device_errors();
+}
+
+int cs_test_set_topology(const int32_t* src) {
+  int rc = check_bound();
+  if (rc) return rc;
+  if (src == nullptr) {
+    g.has_override = false;
+    return CS_OK;
+  }
+  rc = validate_derangements(src, g.world, g.k);
+  if (rc) return rc;
+  CS_CUDA(cudaStreamSynchronize(g.stream));
+  CS_CUDA(cudaMemcpy(g.d_given, src, sizeof(int32_t) * (size_t)g.k * g.world,
+                     cudaMemcpyHostToDevice));
+  g.has_override = true;
+  return CS_OK;
+}
+
+int cs_test_device_topology(int64_t step, int tag, int32_t* src_out) {
+  int rc = check_bound();
+  if (rc) return rc;
+  if (!src_out) return fail(CS_EINVAL, "NULL src_out");
+  if (step < 0 || step >= (int64_t(1) << 32)) return fail(CS_EINVAL, "step outside [0, 2^32)");
+  const int n = tag == CS_TAG_HIER ? g.groups : g.world;
+  TopoArgs t = topo_args(n, tag, nullptr, 1);
+  t.step = (uint32_t)step;
+  t.rw = nullptr;
+  t.inv_wsum = nullptr;
+  CS_CUDA(launch_topology(t, g.stream));
+  CS_CUDA(cudaMemcpyAsync(src_out, g.d_src, sizeof(int32_t) * (size_t)g.k * n,
+                          cudaMemcpyDeviceToHost, g.stream));
+  CS_CUDA(cudaStreamSynchronize(g.stream));
+  return poll_device_errors();
+}
+
+int cs_synth_fill(float* out, int64_t rows, int64_t d, int64_t ld, uint64_t seed, int tag,
+                  int64_t row0, float scale) {
+  if (!out) return fail(CS_EINVAL, "NULL out");
+  if (rows < 0 || d < 0 || ld < d || row0 < 0 || tag < 0)
+    return fail(CS_EINVAL, "bad synth shape");
+  if (rows == 0 || d == 0) return CS_OK;
+  CS_CUDA(launch_synth(out, rows, d, ld, seed, tag, row0, scale, g.bound ? g.stream : nullptr));
+  return CS_OK;
+}
+
+int cs_step_bytes(int64_t step, int hier, double* out) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (!g.bound) return fail(CS_ENOTBOUND, "cs_bind has not been called");
+  if (!out) return fail(CS_EINVAL, "NULL out");
+  const double d = (double)g.d;
+  std::vector<int64_t> b = host_bounds(g.d, g.k);
+  if (!hier) {
+    out[0] = 20.0 * g.n_loc * d;  // read x, m, g; write x', m'
+    std::vector<int32_t> src((size_t)g.k * g.world);
+    int rc = cs_topology(step, src.data());
+    if (rc) return rc;
+    double nvl = 0.0;
+    for (int s = 0; s < g.k; ++s)
+      for (int i = g.first; i < g.first + g.n_loc; ++i)
+        if (src[(size_t)s * g.world + i] / g.n_loc != g.rank) nvl += 4.0 * (double)(b[s + 1] - b[s]);
+    out[1] = nvl;
+  } else {
+    const int gs = g.world / g.groups;
+    const int L_loc = g.n_loc / gs > 0 ? g.n_loc / gs : 1;
+    // read members' g, leaders' x and m; write leaders' m and every member's x
+    out[0] = (4.0 * g.n_loc + 12.0 * L_loc + 4.0 * g.n_loc) * d;
+    out[1] = 0.0;
+  }
+  return CS_OK;
+}
+
+int cs_set_timing(int enable) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (g.bound) CS_CUDA(cudaStreamSynchronize(g.stream));
+  g.timing = enable != 0;
+  g.events_used = 0;
+  return CS_OK;
+}
+
+int cs_get_timing(double* total_ms_out, int64_t* launches_out) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (!total_ms_out || !launches_out) return fail(CS_EINVAL, "NULL output");
+  double total = 0.0;
+  for (size_t i = 0; i + 1 < g.events_used; i += 2) {
+    CS_CUDA(cudaEventSynchronize(g.events[i + 1]));
+    float ms = 0.f;
+    CS_CUDA(cudaEventElapsedTime(&ms, g.events[i], g.events[i + 1]));
+    total += ms;
+  }
+  *total_ms_out = total;
+  *launches_out = (int64_t)(g.events_used / 2);
+  return CS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// Internal declarations shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cs {
+
+constexpr int kMaxWorld = 1024;          // == CS_MAX_WORLD
+constexpr int kMaxAttempts = 10000;      // Alg. 2 restart cap (reading C-6)
+constexpr int kQuantum = 32;             // segment quantum (reading C-2)
+
+// Cycle-order table entries: worker index | flags.  For segment s the table
+// lists every worker once, cycle by cycle, each cycle in the order
+// c0, c1 = src(c0), c2 = src(c1), ...; so x'_{c_p} = (y_{c_p} + y_{c_{p+1}})/2 and
+// the last member of a cycle closes with its first.
+constexpr uint32_t kOrdStart = 1u << 30;
+constexpr uint32_t kOrdEnd = 1u << 31;
+constexpr uint32_t kOrdIdx = (1u << 30) - 1;
+
+// Device error flags (int[3]): [0] topology restart cap hit, [1] non-finite gradient,
+// [2] a cross-GPU wait timed out.
+enum { kErrTopology = 0, kErrDiverged = 1, kErrTimeout = 2, kNumErr = 3 };
+
+struct TopoArgs {
+  uint64_t seed;
+  uint32_t step;
+  int n;               // ranks in this topology (world, or #leaders)
+  int k;
+  int tag;
+  const int32_t* given;  // device [k][n] injected topology, or nullptr
+  int32_t* src;        // out [k][n]   receiver -> sender
+  int32_t* dst;        // out [k][n]   sender -> receiver (inverse)
+  uint32_t* ord;       // out [k][n]   cycle order (kOrd* flags)
+  float* psw;          // in/out [rows][k] push-sum weights (nullptr: skip)
+  int group_size;      // rows per topology rank (1 flat, |G| hierarchical)
+  double* rw;          // out [k][n] 1 / w'_{rank,s} in fp64 (diagnostics)
+  double* inv_wsum;    // out [k] 1 / sum over all rows of w'_{.,s}
+  int* err;
+};
+
+struct LocalArgs {
+  float* x;            // [rows][ld]
+  float* m;            // [rows][ld]
+  const float* g;      // [rows][ld]
+  int64_t ld;
+  int64_t d;
+  int n;               // ranks of the topology (world or #leaders)
+  int group_size;      // 1 for flat
+  int k;
+  int64_t nq;          // ceil(d / 32)
+  const uint32_t* ord;
+  const double* rw;
+  const double* inv_wsum;
+  float lr, mu, inv_group;
+  double* partials;    // [gridDim.x][2]
+  int* err;
+};
+
+cudaError_t launch_topology(const TopoArgs& a, cudaStream_t st);
+int host_alg2(uint64_t seed, uint32_t step, uint32_t seg, int n, int tag, int32_t* src);
+
+cudaError_t launch_gossip_local(const LocalArgs& a, bool diag, int grid, cudaStream_t st);
+cudaError_t launch_hier_local(const LocalArgs& a, bool diag, int grid, cudaStream_t st);
+cudaError_t launch_diag_finalize(const double* partials, int nparts, int n, double* out,
+                                 cudaStream_t st);
+cudaError_t launch_synth(float* out, int64_t rows, int64_t d, int64_t ld, uint64_t seed,
+                         int tag, int64_t row0, float scale, cudaStream_t st);
+int local_grid_size(bool hier, bool diag, int64_t d);
+
+}  // namespace cs
+
+namespace cs {
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+}  // namespace cs

@@ -1,0 +1,387 @@
+// Multi-GPU flat step over NVLink peer memory (configs 3 and 5).
+//
+// Workers are partitioned contiguously: worker w lives on GPU w / n_loc.  At step
+// t each GPU runs ONE persistent kernel (cooperative launch, so every CTA is
+// co-resident) over "tiles" — a segment-aligned range of columns for all its
+// n_loc local workers — visited in the same order on every GPU:
+//
+//   push  for each local worker i: m' and y_i (a3) from x, m, g; y_i[tile] is
+//         stored straight into the RECEIVER's inbox on the receiver's GPU
+//         (Alg.1 l.7 isend to send_to = dst_s(i)), and kept
+//         in shared memory; the first tile of a segment also pushes w_{i,s}.
+//         Then one flag per (tile, receiving worker) is set on the receiver's
+//         GPU with system-scope release (the irecv "completion", Alg.1 l.14).
+//   wait  for this GPU's own workers' flags of the same tile (acquire), i.e.
+//         Alg.1 l.14 "wait send and recv", per tile instead of per model.
+//   mix   x_i = (y_i + inbox_i) * 0.5, w_{i,s} = (w_{i,s} + wbox_{i,s}) * 0.5  (a5).
+//
+// Every CTA pushes tile q before it waits on tile q and all CTAs are resident,
+// so all waits of iteration q are satisfiable (no deadlock); many CTAs per SM
+// overlap one CTA's wait with the others' streaming, so the NVLink transfer
+// overlaps the local update tile by tile.
+//
+// The inbox ping-pongs on step parity; before pushing at epoch e a GPU waits
+// until every peer has finished epoch e-2 (the last reader of that parity) —
+// the "done" words each GPU writes into every peer's region at the end of a
+// step.  Flags and done words carry the monotone epoch, so nothing is reset.
+// Spins are bounded (~20 s of %globaltimer) and report CS_ETIMEOUT instead of
+// hanging the GPU.
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/crossover_sgd.h"
+#include "common.cuh"
+#include "peer.cuh"
+
+namespace cs {
+
+namespace {
+
+std::string g_peer_err;
+
+int perr(int code, const char* what, cudaError_t e) {
+  char buf[256];
+  snprintf(buf, sizeof(buf), "%s: %s", what, e == cudaSuccess ? "" : cudaGetErrorString(e));
+  g_peer_err = buf;
+  return code;
+}
+
+constexpr int kPeerThreads = 256;
+constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// wait until (int32)(*p - target) >= 0; returns false on timeout
+__device__ bool spin_until(const uint32_t* p, uint32_t target) {
+  if ((int32_t)(ld_acquire_sys(p) - target) >= 0) return true;
+  const uint64_t t0 = globaltimer();
+  while (true) {
+    if ((int32_t)(ld_acquire_sys(p) - target) >= 0) return true;
+    if (globaltimer() - t0 > kSpinLimitNs) return false;
+    __nanosleep(64);
+  }
+}
+
+struct PeerKernelArgs {
+  PeerStepArgs s;
+  char* const* peers;       // [nprocs] region bases
+  const int64_t* tiles;     // [n_tiles][2] (segment, start)
+  const int64_t* tile_end;  // [n_tiles]
+  int n_tiles;
+  int tile;
+  uint32_t epoch;           // this step's epoch (>= 1)
+  size_t off_inbox, off_wbox, off_flags, off_done, off_count;
+};
+
+__device__ __forceinline__ float4 mom4(float4 m, float4 g, float mu) {
+  return make_float4(__fadd_rn(__fmul_rn(mu, m.x), g.x), __fadd_rn(__fmul_rn(mu, m.y), g.y),
+                     __fadd_rn(__fmul_rn(mu, m.z), g.z), __fadd_rn(__fmul_rn(mu, m.w), g.w));
+}
+__device__ __forceinline__ float4 sgd4(float4 x, float4 m, float lr) {
+  return make_float4(__fsub_rn(x.x, __fmul_rn(lr, m.x)), __fsub_rn(x.y, __fmul_rn(lr, m.y)),
+                     __fsub_rn(x.z, __fmul_rn(lr, m.z)), __fsub_rn(x.w, __fmul_rn(lr, m.w)));
+}
+__device__ __forceinline__ float4 mean4(float4 a, float4 b) {
+  return make_float4(__fmul_rn(__fadd_rn(a.x, b.x), 0.5f), __fmul_rn(__fadd_rn(a.y, b.y), 0.5f),
+                     __fmul_rn(__fadd_rn(a.z, b.z), 0.5f), __fmul_rn(__fadd_rn(a.w, b.w), 0.5f));
+}
+__device__ __forceinline__ void st4(float* p, float4 v, int valid) {
+  if (valid == 4) {
+    *reinterpret_cast<float4*>(p) = v;
+  } else {
+    if (valid > 0) p[0] = v.x;
+    if (valid > 1) p[1] = v.y;
+    if (valid > 2) p[2] = v.z;
+  }
+}
+__device__ __forceinline__ bool nonfinite4(float4 g) {
+  const uint32_t e = 0x7f800000u;
+  return ((__float_as_uint(g.x) & e) == e) | ((__float_as_uint(g.y) & e) == e) |
+         ((__float_as_uint(g.z) & e) == e) | ((__float_as_uint(g.w) & e) == e);
+}
+
+__global__ void __launch_bounds__(kPeerThreads) k_gossip_peer(const PeerKernelArgs a) {
+  extern __shared__ float4 ybuf[];  // [n_loc][tile/4]
+  __shared__ int s_timeout;
+  const PeerStepArgs& s = a.s;
+  const int n_loc = s.n_loc;
+  const uint32_t e = a.epoch;
+  const int par = (int)(e & 1u);
+  char* mine = a.peers[s.rank];
+  const int64_t ld = s.ld;
+  const int tv = a.tile / 4;
+  bool bad = false;
+
+  if (threadIdx.x == 0) s_timeout = 0;
+  // ping-pong safety: every receiver finished epoch e-2, the last reader of this parity
+  if (threadIdx.x < s.nprocs && e >= 3) {
+    const uint32_t* done = reinterpret_cast<const uint32_t*>(mine + a.off_done);
+    if (!spin_until(done + threadIdx.x, e - 2)) atomicOr(&s_timeout, 1);
+  }
+  __syncthreads();
+
+  for (int u = blockIdx.x; u < a.n_tiles && !s_timeout; u += gridDim.x) {
+    const int seg = (int)a.tiles[2 * u];
+    const int64_t c0 = a.tiles[2 * u + 1];
+    const int64_t c1 = a.tile_end[u];
+    const bool first_tile = (u == 0) || (a.tiles[2 * (u - 1)] != seg);
+    const int nv = (int)((c1 - c0 + 3) >> 2);
+
+    // ---- push ------------------------------------------------------------------
+    for (int r = 0; r < n_loc; ++r) {
+      const int i = s.first + r;
+      const int recv = s.dst[(int64_t)seg * s.world + i];
+      const int rp = recv / n_loc, rl = recv - rp * n_loc;
+      float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) +
+                     ((int64_t)par * n_loc + rl) * ld;
+      const int64_t rowoff = (int64_t)r * ld;
+      for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        const int64_t j = c0 + 4 * (int64_t)v;
+        const int valid = (int)imin64(4, c1 - j);
+        const float4 cx = __ldcs(reinterpret_cast<const float4*>(s.x + rowoff + j));
+        const float4 cm = __ldcs(reinterpret_cast<const float4*>(s.m + rowoff + j));
+        const float4 cg = __ldcs(reinterpret_cast<const float4*>(s.g + rowoff + j));
+        bad |= nonfinite4(cg);
+        const float4 mn = mom4(cm, cg, s.mu);
+        const float4 y = sgd4(cx, mn, s.lr);
+        st4(s.m + rowoff + j, mn, valid);
+        st4(inbox + j, y, valid);
+        ybuf[r * tv + v] = y;
+      }
+      if (first_tile && threadIdx.x == 0) {
+        float* wbox = reinterpret_cast<float*>(a.peers[rp] + a.off_wbox) +
+                      ((int64_t)par * n_loc + rl) * s.k;
+        wbox[seg] = s.psw[(int64_t)r * s.k + seg];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < n_loc) {
+      const int i = s.first + threadIdx.x;
+      const int recv = s.dst[(int64_t)seg * s.world + i];
+      const int rp = recv / n_loc, rl = recv - rp * n_loc;
+      uint32_t* flag = reinterpret_cast<uint32_t*>(a.peers[rp] + a.off_flags) +
+                       (int64_t)u * n_loc + rl;
+      __threadfence_system();
+      st_release_sys(flag, e);
+    }
+
+    // ---- wait for this tile's inbound segments ----------------------------------
+    if (threadIdx.x < n_loc) {
+      const uint32_t* flag = reinterpret_cast<const uint32_t*>(mine + a.off_flags) +
+                             (int64_t)u * n_loc + threadIdx.x;
+      if (!spin_until(flag, e)) atomicOr(&s_timeout, 1);
+    }
+    __syncthreads();
+    if (s_timeout) break;
+
+    // ---- mix ------------------------------------------------------------------
+    for (int r = 0; r < n_loc; ++r) {
+      const float* inbox = reinterpret_cast<const float*>(mine + a.off_inbox) +
+                           ((int64_t)par * n_loc + r) * ld;
+      const int64_t rowoff = (int64_t)r * ld;
+      for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        const int64_t j = c0 + 4 * (int64_t)v;
+        const int valid = (int)imin64(4, c1 - j);
+        const float4 yin = __ldcg(reinterpret_cast<const float4*>(inbox + j));
+        st4(s.x + rowoff + j, mean4(ybuf[r * tv + v], yin), valid);
+      }
+      if (first_tile && threadIdx.x == 0) {
+        const float* wbox = reinterpret_cast<const float*>(mine + a.off_wbox) +
+                            ((int64_t)par * n_loc + r) * s.k;
+        float* w = s.psw + (int64_t)r * s.k + seg;
+        *w = __fmul_rn(__fadd_rn(*w, __ldcg(wbox + seg)), 0.5f);
+      }
+    }
+    __syncthreads();  // ybuf reuse
+  }
+
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(s.err + kErrDiverged, 1);
+  if (threadIdx.x == 0 && s_timeout) atomicOr(s.err + kErrTimeout, 1);
+
+  // ---- end of step: last CTA tells every peer this GPU finished epoch e ------------
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    uint32_t* count = reinterpret_cast<uint32_t*>(mine + a.off_count);
+    const uint32_t prev = atomicAdd(count, 1u);
+    if (prev + 1 == e * gridDim.x) {
+      __threadfence_system();
+      for (int p = 0; p < s.nprocs; ++p) {
+        uint32_t* done = reinterpret_cast<uint32_t*>(a.peers[p] + a.off_done) + s.rank;
+        st_release_sys(done, e);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+const char* peer_error() { return g_peer_err.c_str(); }
+
+int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs, int rank) {
+  p = PeerState();
+  p.nprocs = nprocs;
+  p.rank = rank;
+  p.n_loc = n_loc;
+  p.k = k;
+  p.ld = ld;
+  // tile: ~16 KB of y per CTA in shared memory
+  int tile = 4096 / (n_loc < 1 ? 1 : n_loc);
+  tile = (tile / kQuantum) * kQuantum;
+  if (tile < 128) tile = 128;
+  p.tile = tile;
+  // segment-aligned tiles
+  const int64_t nq = (d + kQuantum - 1) / kQuantum;
+  std::vector<int64_t> tiles, ends;
+  for (int s = 0; s < k; ++s) {
+    int64_t b0 = kQuantum * ((s * nq) / k);
+    int64_t b1 = (s + 1 == k) ? d : kQuantum * (((s + 1) * nq) / k);
+    if (b0 > d) b0 = d;
+    if (b1 > d) b1 = d;
+    for (int64_t c = b0; c < b1; c += tile) {
+      tiles.push_back(s);
+      tiles.push_back(c);
+      ends.push_back(c + tile < b1 ? c + tile : b1);
+    }
+  }
+  p.n_tiles = (int)ends.size();
+  p.off_inbox = 0;
+  p.off_wbox = align_up(p.off_inbox + sizeof(float) * 2 * (size_t)n_loc * ld, 256);
+  p.off_flags = align_up(p.off_wbox + sizeof(float) * 2 * (size_t)n_loc * k, 256);
+  p.off_done = align_up(p.off_flags + sizeof(uint32_t) * (size_t)p.n_tiles * n_loc, 256);
+  p.off_count = align_up(p.off_done + sizeof(uint32_t) * (size_t)nprocs, 256);
+  p.bytes = align_up(p.off_count + 256, 4096);
+  cudaError_t e = cudaMalloc(&p.base, p.bytes);
+  if (e != cudaSuccess) return perr(CS_ECUDA, "peer region cudaMalloc", e);
+  e = cudaMemset(p.base + p.off_flags, 0, p.bytes - p.off_flags);
+  if (e != cudaSuccess) return perr(CS_ECUDA, "peer region memset", e);
+  e = cudaMalloc(&p.d_tiles, sizeof(int64_t) * tiles.size());
+  if (e == cudaSuccess) e = cudaMalloc(&p.d_tile_end, sizeof(int64_t) * ends.size());
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p.d_tiles, tiles.data(), sizeof(int64_t) * tiles.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p.d_tile_end, ends.data(), sizeof(int64_t) * ends.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return perr(CS_ECUDA, "tile table", e);
+  const size_t smem = sizeof(float) * (size_t)n_loc * tile;
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(k_gossip_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return perr(CS_ECUDA, "smem attribute", e);
+  }
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gossip_peer, kPeerThreads, smem);
+  if (e != cudaSuccess || occ < 1) return perr(CS_ECUDA, "occupancy", e);
+  p.grid = sms * occ;
+  if (p.grid > p.n_tiles) p.grid = p.n_tiles;
+  p.peer_base.assign(nprocs, nullptr);
+  p.peer_base[rank] = p.base;
+  p.allocated = true;
+  return CS_OK;
+}
+
+void peer_release(PeerState& p) {
+  if (p.imported) {
+    for (int r = 0; r < p.nprocs; ++r)
+      if (r != p.rank && p.peer_base[r]) cudaIpcCloseMemHandle(p.peer_base[r]);
+  }
+  if (p.base) cudaFree(p.base);
+  if (p.d_peer_base) cudaFree(p.d_peer_base);
+  if (p.d_tiles) cudaFree(p.d_tiles);
+  if (p.d_tile_end) cudaFree(p.d_tile_end);
+  p = PeerState();
+}
+
+int peer_export(PeerState& p, char* handle_out) {
+  if (!p.allocated) return perr(CS_ENOTBOUND, "peer region not allocated", cudaSuccess);
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, p.base);
+  if (e != cudaSuccess) return perr(CS_ECUDA, "cudaIpcGetMemHandle", e);
+  static_assert(sizeof(cudaIpcMemHandle_t) == CS_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle_out, &h, sizeof(h));
+  return CS_OK;
+}
+
+int peer_import(PeerState& p, const char* all) {
+  if (!p.allocated) return perr(CS_ENOTBOUND, "peer region not allocated", cudaSuccess);
+  for (int r = 0; r < p.nprocs; ++r) {
+    if (r == p.rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, all + (size_t)r * CS_IPC_HANDLE_BYTES, sizeof(h));
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return perr(CS_ECUDA, "cudaIpcOpenMemHandle", e);
+    p.peer_base[r] = (char*)ptr;
+  }
+  cudaError_t e = cudaMalloc(&p.d_peer_base, sizeof(char*) * p.nprocs);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p.d_peer_base, p.peer_base.data(), sizeof(char*) * p.nprocs,
+                   cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return perr(CS_ECUDA, "peer table", e);
+  p.imported = true;
+  return CS_OK;
+}
+
+int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEvent_t ev0,
+                   cudaEvent_t ev1) {
+  TopoArgs t;
+  t.seed = a.seed;
+  t.step = a.step;
+  t.n = a.world;
+  t.k = a.k;
+  t.tag = CS_TAG_FLAT;
+  t.given = a.given;
+  t.src = a.src;
+  t.dst = a.dst;
+  t.ord = nullptr;
+  t.psw = nullptr;
+  t.group_size = 1;
+  t.rw = nullptr;
+  t.inv_wsum = nullptr;
+  t.err = a.err;
+  cudaError_t e = launch_topology(t, st);
+  if (e != cudaSuccess) return perr(CS_ECUDA, "topology launch", e);
+
+  PeerKernelArgs ka;
+  ka.s = a;
+  ka.peers = p.d_peer_base;
+  ka.tiles = p.d_tiles;
+  ka.tile_end = p.d_tile_end;
+  ka.n_tiles = p.n_tiles;
+  ka.tile = p.tile;
+  ka.epoch = ++p.epoch;
+  ka.off_inbox = p.off_inbox;
+  ka.off_wbox = p.off_wbox;
+  ka.off_flags = p.off_flags;
+  ka.off_done = p.off_done;
+  ka.off_count = p.off_count;
+  const size_t smem = sizeof(float) * (size_t)a.n_loc * p.tile;
+  void* args[] = {&ka};
+  if (ev0) cudaEventRecord(ev0, st);
+  e = cudaLaunchCooperativeKernel((const void*)k_gossip_peer, dim3(p.grid), dim3(kPeerThreads), args,
+                                  smem, st);
+  if (e != cudaSuccess) return perr(CS_ECUDA, "cooperative launch", e);
+  if (ev1) cudaEventRecord(ev1, st);
+  return CS_OK;
+}
+
+}  // namespace cs
