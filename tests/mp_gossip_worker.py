@@ -1,0 +1,91 @@
+"""torchrun worker for the multi-GPU parity test (tests/test_gpu_multi.py).
+
+Each rank holds n_loc workers (global ids rank*n_loc ..), steps through the
+C-ABI with segments exchanged over NVLink peer memory, and compares its rows on
+sampled columns with the oracle run for all workers on the same columns.
+Exit code 0 = parity; 1 = mismatch."""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import synth  # noqa: E402
+from oracle import topology as T  # noqa: E402
+
+import __graft_entry__ as entry  # noqa: E402
+
+entry.build()
+import paper_2012_15198_b200 as cs  # noqa: E402
+from gpu_util import OracleRun  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n-loc", type=int, required=True)
+    ap.add_argument("--d", type=int, required=True)
+    ap.add_argument("--k", type=int, required=True)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--full", action="store_true", help="compare every column (small d)")
+    a = ap.parse_args()
+    rank, ws, lr_ = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(lr_)
+    dev = torch.device("cuda", lr_)
+    dist.init_process_group("nccl", device_id=dev)
+    n_loc, d, k, seed = a.n_loc, a.d, a.k, a.seed
+    world = n_loc * ws
+    first = rank * n_loc
+    lr, mu = float(synth.DEFAULT_LR), float(synth.DEFAULT_MOMENTUM)
+    cs.cs_init(world, world, k, seed)
+    stream = torch.cuda.current_stream(dev)
+    x = torch.empty(n_loc, d, device=dev)
+    m = torch.zeros(n_loc, d, device=dev)
+    w = torch.ones(n_loc, k, device=dev)
+    B = world + 1
+    bank = torch.empty(B + n_loc, d, device=dev)
+    cs.cs_bind(m, d, d, rank, ws, stream)
+    cs.cs_synth_fill(x, n_loc, d, d, seed, synth.TAG_INIT, first, 1.0)
+    cs.cs_synth_fill(bank, B, d, d, seed, synth.TAG_GRAD, 0, float(synth.GRAD_SCALE))
+    torch.cuda.synchronize()
+    bank[B:] = bank[:n_loc]
+    torch.cuda.synchronize()
+    cs.setup_peers()
+
+    cols = np.arange(d) if a.full else synth.sample_columns(d, T.segment_bounds(d, k))
+    orc = OracleRun(world, d, k, seed, cols=cols)
+    idx = torch.from_numpy(cols).to(dev)
+    ok = True
+    for t in range(a.steps):
+        o = (t + first) % B
+        cs.cs_gossip_step(x, bank[o:o + n_loc], w, lr, mu)
+        orc.step(lr, mu)
+        cs.cs_sync()
+        xs = x.index_select(1, idx).cpu().numpy()
+        ms = m.index_select(1, idx).cpu().numpy()
+        rows = slice(first, first + n_loc)
+        if not (np.array_equal(xs, orc.x[rows]) and np.array_equal(ms, orc.m[rows])
+                and np.array_equal(w.cpu().numpy(), orc.w[rows])):
+            bad = np.argwhere(xs != orc.x[rows])
+            print(f"rank {rank} step {t}: mismatch at {bad[:5].tolist()} of {bad.shape[0]}", flush=True)
+            ok = False
+            break
+    okt = torch.tensor([1 if ok else 0], device=dev)
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(f"mp parity world={world} n_loc={n_loc} d={d} k={k} steps={a.steps}: "
+              f"{'OK' if okt.item() else 'FAIL'}", flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    cs.cs_finalize()
+    sys.exit(0 if okt.item() else 1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,45 @@
+"""-m gpu, >= 2 GPUs: the NVLink peer-memory path (one process per GPU) against
+the oracle, bit-exact on sampled (or all) columns.  Skipped on 1-GPU boxes; the
+world_size-2 host logic is covered on CPU by tests/test_multiproc_cpu.py."""
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def _run(nproc, *args, timeout=600):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "mp_gossip_worker.py"),
+           *[str(a) for a in args]]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    assert "OK" in p.stdout
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("n_loc,d,k,steps,full", [(1, 4099, 3, 6, True), (3, 50_001, 5, 5, True),
+                                                  (8, 200_000, 32, 4, True), (1, 1_000_003, 8, 8, True)])
+def test_two_gpu_parity(n_loc, d, k, steps, full):
+    args = ["--n-loc", n_loc, "--d", d, "--k", k, "--steps", steps]
+    if full:
+        args.append("--full")
+    _run(2, *args)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+def test_two_gpu_resnet50_sampled():
+    # BASELINE configs[2] layout (one worker per GPU, 25,557,032 fp32, k = 8)
+    _run(2, "--n-loc", 1, "--d", 25_557_032, "--k", 8, "--steps", 10)
+
+
+@pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
+@pytest.mark.parametrize("n_loc,d,k", [(1, 25_557_032, 8), (8, 1_000_000, 16)])
+def test_four_gpu_parity(n_loc, d, k):
+    _run(4, "--n-loc", n_loc, "--d", d, "--k", k, "--steps", 6)

@@ -28,6 +28,7 @@ LR, MU = float(synth.DEFAULT_LR), float(synth.DEFAULT_MOMENTUM)
 
 
 def _bind(n, d, k, seed, groups=None, ld=None):
+    ld = (d + 3) // 4 * 4 if ld is None else ld
     cs.cs_init(n, groups or n, k, seed)
     x, m, w, bank2 = device_state(cs, n, d, k, seed, ld=ld)
     cs.cs_bind(m, d, x.shape[1], 0, 1, torch.cuda.current_stream())
