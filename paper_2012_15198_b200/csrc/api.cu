@@ -64,9 +64,10 @@ struct Ctx {
   double* d_rw = nullptr;
   double* d_inv_wsum = nullptr;
   int* d_err = nullptr;
-  double* d_partials = nullptr;
-  int partials_cap = 0;
+  double* d_partials = nullptr;   // [local_max_grid()][2]
   double* d_diag = nullptr;
+  unsigned* d_counter = nullptr;  // CTA arrival counter of the fused kernels
+  int launches_per_step = 0;
   bool has_override = false;
 
   float* d_stage = nullptr;   // cs_gossip_step_host staging buffer
@@ -106,11 +107,11 @@ int next_event_pair(cudaEvent_t* ev) {
 void free_device() {
   auto f = [](void* p) { if (p) cudaFree(p); };
   f(g.d_bounds); f(g.d_src); f(g.d_dst); f(g.d_ord); f(g.d_given); f(g.d_rw);
-  f(g.d_inv_wsum); f(g.d_err); f(g.d_partials); f(g.d_diag); f(g.d_stage);
+  f(g.d_inv_wsum); f(g.d_err); f(g.d_partials); f(g.d_diag); f(g.d_stage); f(g.d_counter);
   g.d_bounds = nullptr; g.d_src = nullptr; g.d_dst = nullptr; g.d_ord = nullptr;
   g.d_given = nullptr; g.d_rw = nullptr; g.d_inv_wsum = nullptr; g.d_err = nullptr;
-  g.d_partials = nullptr; g.d_diag = nullptr; g.d_stage = nullptr;
-  g.partials_cap = 0; g.stage_bytes = 0;
+  g.d_partials = nullptr; g.d_diag = nullptr; g.d_stage = nullptr; g.d_counter = nullptr;
+  g.stage_bytes = 0;
   peer_release(g.peer);
 }
 
@@ -157,15 +158,6 @@ int poll_device_errors() {
   return CS_OK;
 }
 
-int ensure_partials(int grid) {
-  if (grid <= g.partials_cap) return CS_OK;
-  if (g.d_partials) cudaFree(g.d_partials);
-  g.d_partials = nullptr;
-  CS_CUDA(cudaMalloc(&g.d_partials, sizeof(double) * 2 * (size_t)grid));
-  g.partials_cap = grid;
-  return CS_OK;
-}
-
 TopoArgs topo_args(int n, int tag, float* psw, int group_size) {
   TopoArgs t;
   t.seed = g.seed;
@@ -185,7 +177,8 @@ TopoArgs topo_args(int n, int tag, float* psw, int group_size) {
   return t;
 }
 
-LocalArgs local_args(float* params, const float* grads, int n, int gs, float lr, float mu) {
+LocalArgs local_args(float* params, const float* grads, float* psw, int n, int gs, int tag,
+                     float lr, float mu) {
   LocalArgs a;
   a.x = params;
   a.m = g.mom;
@@ -196,13 +189,20 @@ LocalArgs local_args(float* params, const float* grads, int n, int gs, float lr,
   a.group_size = gs;
   a.k = g.k;
   a.nq = g.nq;
+  a.seed = g.seed;
+  a.step = (uint32_t)g.step;
+  a.tag = tag;
+  a.given = nullptr;
   a.ord = g.d_ord;
   a.rw = g.d_rw;
   a.inv_wsum = g.d_inv_wsum;
+  a.psw = psw;
   a.lr = lr;
   a.mu = mu;
   a.inv_group = 1.0f / (float)gs;
   a.partials = g.d_partials;
+  a.diag_out = g.d_diag;
+  a.counter = g.d_counter;
   a.err = g.d_err;
   return a;
 }
@@ -221,25 +221,28 @@ int validate_derangements(const int32_t* src, int n, int k) {
   return CS_OK;
 }
 
+// One flat step on one GPU.  Small topologies (n <= 64, k*n <= 2048) are built by
+// every CTA of the fused kernel itself (one launch per step); larger ones by
+// k_topology into global tables first.
 int enqueue_flat_step(float* params, const float* grads, float* psw, float lr, float mu,
                       bool diag) {
   const int n = g.world;
-  TopoArgs t = topo_args(n, CS_TAG_FLAT, psw, 1);
-  if (g.has_override) t.given = g.d_given;
-  CS_CUDA(launch_topology(t, g.stream));
-  const int grid = local_grid_size(false, diag, g.d);
-  if (diag) {
-    int rc = ensure_partials(grid);
-    if (rc) return rc;
+  const bool fused = fused_topology_ok(n, g.k);
+  LocalArgs a = local_args(params, grads, psw, n, 1, CS_TAG_FLAT, lr, mu);
+  if (fused) {
+    a.given = g.has_override ? g.d_given : nullptr;
+  } else {
+    TopoArgs t = topo_args(n, CS_TAG_FLAT, psw, 1);
+    if (g.has_override) t.given = g.d_given;
+    CS_CUDA(launch_topology(t, g.stream));
   }
-  LocalArgs a = local_args(params, grads, n, 1, lr, mu);
   cudaEvent_t ev[2];
   int rc = next_event_pair(ev);
   if (rc) return rc;
   if (ev[0]) CS_CUDA(cudaEventRecord(ev[0], g.stream));
-  CS_CUDA(launch_gossip_local(a, diag, grid, g.stream));
+  CS_CUDA(launch_gossip_local(a, diag, fused, g.stream, nullptr));
   if (ev[1]) CS_CUDA(cudaEventRecord(ev[1], g.stream));
-  if (diag) CS_CUDA(launch_diag_finalize(g.d_partials, grid, n, g.d_diag, g.stream));
+  g.launches_per_step = fused ? 1 : 2;
   return CS_OK;
 }
 
@@ -352,6 +355,9 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
   CS_CUDA(cudaMalloc(&g.d_err, sizeof(int) * kNumErr));
   CS_CUDA(cudaMemset(g.d_err, 0, sizeof(int) * kNumErr));
   CS_CUDA(cudaMalloc(&g.d_diag, sizeof(double) * 2));
+  CS_CUDA(cudaMalloc(&g.d_partials, sizeof(double) * 2 * (size_t)local_max_grid()));
+  CS_CUDA(cudaMalloc(&g.d_counter, sizeof(unsigned)));
+  CS_CUDA(cudaMemset(g.d_counter, 0, sizeof(unsigned)));
   if (nprocs > 1) {
     int rc = peer_alloc(g.peer, g.n_loc, d, ld, g.k, nprocs, proc_rank);
     if (rc) return fail(rc, "%s", peer_error());
@@ -450,24 +456,20 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
     return fail(CS_EUNSUPPORTED, "multi-GPU hierarchical step is not implemented in this build");
   const bool diag = g.diag != 0;
   const int L = g.groups, gs = g.world / g.groups;
-  TopoArgs t = topo_args(L, CS_TAG_HIER, psw, gs);
-  CS_CUDA(launch_topology(t, g.stream));
-  const int grid = local_grid_size(true, diag, g.d);
-  if (diag) {
-    rc = ensure_partials(grid);
-    if (rc) return rc;
+  const bool fused = fused_topology_ok(L, g.k);
+  LocalArgs a = local_args(params, grads, psw, L, gs, CS_TAG_HIER, lr, momentum);
+  if (!fused) {
+    TopoArgs t = topo_args(L, CS_TAG_HIER, psw, gs);
+    CS_CUDA(launch_topology(t, g.stream));
   }
-  LocalArgs a = local_args(params, grads, L, gs, lr, momentum);
   cudaEvent_t ev[2];
   rc = next_event_pair(ev);
   if (rc) return rc;
   if (ev[0]) CS_CUDA(cudaEventRecord(ev[0], g.stream));
-  CS_CUDA(launch_hier_local(a, diag, grid, g.stream));
+  CS_CUDA(launch_hier_local(a, diag, fused, g.stream, nullptr));
   if (ev[1]) CS_CUDA(cudaEventRecord(ev[1], g.stream));
-  if (diag) {
-    CS_CUDA(launch_diag_finalize(g.d_partials, grid, g.world, g.d_diag, g.stream));
-    g.diag_valid = true;
-  }
+  if (diag) g.diag_valid = true;
+  g.launches_per_step = fused ? 1 : 2;
   g.step += 1;
   return CS_OK;
 }

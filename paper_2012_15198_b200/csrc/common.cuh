@@ -44,28 +44,41 @@ struct LocalArgs {
   const float* g;      // [rows][ld]
   int64_t ld;
   int64_t d;
-  int n;               // ranks of the topology (world or #leaders)
-  int group_size;      // 1 for flat
+  int n;               // ranks of the topology (world, or #leaders when hierarchical)
+  int group_size;      // rows per rank: 1 flat, |G| hierarchical
   int k;
   int64_t nq;          // ceil(d / 32)
+  // fused topology (prologue builds the tables in shared memory)
+  uint64_t seed;
+  uint32_t step;
+  int tag;
+  const int32_t* given;  // injected [k][n] topology (tests) or nullptr
+  // precomputed tables (fallback when n > 64 or k*n is large; built by k_topology)
   const uint32_t* ord;
   const double* rw;
   const double* inv_wsum;
+  float* psw;          // [rows][k]; fused path mixes it (last CTA), fallback: k_topology did
   float lr, mu, inv_group;
   double* partials;    // [gridDim.x][2]
+  double* diag_out;    // [2] {CD, mean checksum}
+  unsigned* counter;   // CTA arrival counter (0 between launches)
   int* err;
 };
+
+constexpr int kFusedMaxN = 64;      // fused prologue: u64 availability mask
+constexpr int kFusedMaxKN = 2048;   // fused prologue: k*n table entries in shared memory
 
 cudaError_t launch_topology(const TopoArgs& a, cudaStream_t st);
 int host_alg2(uint64_t seed, uint32_t step, uint32_t seg, int n, int tag, int32_t* src);
 
-cudaError_t launch_gossip_local(const LocalArgs& a, bool diag, int grid, cudaStream_t st);
-cudaError_t launch_hier_local(const LocalArgs& a, bool diag, int grid, cudaStream_t st);
-cudaError_t launch_diag_finalize(const double* partials, int nparts, int n, double* out,
-                                 cudaStream_t st);
+bool fused_topology_ok(int n, int k);
+cudaError_t launch_gossip_local(const LocalArgs& a, bool diag, bool fused, cudaStream_t st,
+                                int* grid_out);
+cudaError_t launch_hier_local(const LocalArgs& a, bool diag, bool fused, cudaStream_t st,
+                              int* grid_out);
+int local_max_grid();
 cudaError_t launch_synth(float* out, int64_t rows, int64_t d, int64_t ld, uint64_t seed,
                          int tag, int64_t row0, float scale, cudaStream_t st);
-int local_grid_size(bool hier, bool diag, int64_t d);
 
 }  // namespace cs
 

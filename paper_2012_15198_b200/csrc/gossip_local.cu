@@ -1,25 +1,33 @@
 // Single-GPU hot path: every worker co-resident in this GPU's HBM (configs 1, 2;
 // the paper itself ran "multiple processes for each GPU").
 //
-// k_gossip_local fuses, per float4 column (4 consecutive parameters), for all n
-// workers:
+// ONE launch per step.  k_gossip_local fuses, per float4 column (4 consecutive
+// parameters), for all n workers:
+//   a2  (prologue, every CTA) the k per-segment topologies of this step — Alg. 2
+//       from the shared seed, PAPER.md:165-191 — and their cycle order, into
+//       shared memory (no communication, no separate topology kernel)
 //   a3  m_i <- fl(fl(mu*m_i) + g_i);  y_i <- fl(x_i - fl(lr*m_i))   (C-8, C-9)
 //   a4  receive y_{src_s(i)} — here an HBM row already in flight in this thread
 //   a5  x_i <- fl(fl(y_i + y_{src_s(i)}) * 0.5)                    (Alg.1 l.17)
-//   a6  (DIAG) fp64 shifted sums of z = x'/w' per column -> per-block partials
+//       and (epilogue, last CTA) psw_{i,s} <- (psw_{i,s} + psw_{src,s}) * 0.5
+//   a6  (DIAG) fp64 shifted sums of z = x'/w' per column -> per-block partials,
+//       reduced in a fixed order by the last CTA (deterministic)
 //
 // Column-owner cycle walk: the thread that owns column j visits the workers of
-// segment s(j) in the cycle order of src_s (k_topology), so y_{c_p} and
-// y_{c_{p+1}} = y_{src(c_p)} are both in registers when x'_{c_p} is written and
-// each of x, m, g is read exactly once and x, m written exactly once: the
-// algorithmic 20 B per parameter per worker, in place, with no ping-pong buffer
-// (every element is read by its owner before its owner writes it).
-// Loads of the next PF workers' rows are issued before the current row's
-// arithmetic (explicit register pipeline) to keep enough bytes in flight.
+// segment s(j) in the cycle order of src_s, so y_{c_p} and y_{c_{p+1}} =
+// y_{src(c_p)} are both in registers when x'_{c_p} is written; each of x, m, g
+// is read exactly once and x, m written exactly once: the algorithmic 20 B per
+// parameter per worker, in place, with no ping-pong buffer (every element is
+// read by its owner before its owner writes it).  The loads of the next PF
+// workers' rows are issued before the current row's arithmetic (register
+// pipeline) to keep enough bytes in flight per SM.
 //
 // All fp32 arithmetic uses __fmul_rn/__fadd_rn/__fsub_rn: never contracted to
 // FMA, so results are bit-identical to the oracle's separately rounded ops.
+#include <stdlib.h>
+
 #include "common.cuh"
+#include "philox.cuh"
 
 namespace cs {
 
@@ -54,14 +62,18 @@ __device__ __forceinline__ float4 pair_mean(float4 a, float4 b) {
                      __fmul_rn(__fadd_rn(a.z, b.z), 0.5f), __fmul_rn(__fadd_rn(a.w, b.w), 0.5f));
 }
 
+__device__ __forceinline__ float pair_mean1(float a, float b) {
+  return __fmul_rn(__fadd_rn(a, b), 0.5f);
+}
+
 __device__ __forceinline__ bool nonfinite4(float4 g) {
   const uint32_t e = 0x7f800000u;
   return ((__float_as_uint(g.x) & e) == e) | ((__float_as_uint(g.y) & e) == e) |
          ((__float_as_uint(g.z) & e) == e) | ((__float_as_uint(g.w) & e) == e);
 }
 
-// Per-column fp64 accumulators for the consensus diagnostics: shifted by the
-// first value c seen in the column so S2 - ... does not cancel near consensus.
+// Per-column fp64 accumulators for the consensus diagnostics, shifted by the
+// first value c seen in the column so the variance does not cancel near consensus.
 struct ColDiag {
   double c[4], s1[4], s2[4], xs[4];
   __device__ __forceinline__ void reset() {
@@ -81,7 +93,7 @@ struct ColDiag {
       xs[e] += mult * (double)xa[e];
     }
   }
-  // column j's contribution: sum_i (z_ij - zbar_j)^2 and zbar_j
+  // column j's contribution: sum_i (z_ij - zbar_j)^2 = S2 - 2(zbar-c)S1 + n(zbar-c)^2, and zbar_j
   __device__ __forceinline__ void finish(double inv_wsum, double n, int valid, double& dacc,
                                          double& zacc) const {
 #pragma unroll
@@ -120,13 +132,202 @@ __device__ __forceinline__ void block_reduce_store(double a, double b, double* o
   }
 }
 
+// Alg. 2 for one segment by one warp, n <= 64 (readings C-5..C-7):
+// lanes draw the Philox words of an attempt in parallel, lane 0 runs the
+// sequential roulette over a 64-bit availability mask, the warp restarts on a
+// dead end.  Same definition as host_alg2 / the oracle; different code.
+__device__ void warp_alg2_small(uint64_t seed, uint32_t step, int s, int n, int tag,
+                                uint32_t* u, int32_t* src, int* err) {
+  const int lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  const int nb = (n + 3) >> 2;
+  for (int attempt = 0; attempt < kMaxAttempts; ++attempt) {
+    if (lane < nb) {
+      U32x4 r = philox4x32_10((uint32_t)lane, (uint32_t)attempt | ((uint32_t)tag << 16), (uint32_t)s,
+                              step, k0, k1);
+      u[4 * lane] = r.v[0];
+      u[4 * lane + 1] = r.v[1];
+      u[4 * lane + 2] = r.v[2];
+      u[4 * lane + 3] = r.v[3];
+    }
+    __syncwarp();
+    int ok = 1;
+    if (lane == 0) {
+      uint64_t avail = (n == 64) ? ~0ull : ((1ull << n) - 1ull);
+      for (int i = 0; i < n; ++i) {
+        const uint64_t cand = avail & ~(1ull << i);        // zero diagonal + picked ranks
+        const uint32_t cnt = (uint32_t)__popcll(cand);
+        if (cnt == 0) { ok = 0; break; }                   // dead end -> restart (C-6)
+        const uint32_t c = roulette_index(u[i], cnt);      // C-7
+        const uint32_t lo = (uint32_t)cand, hi = (uint32_t)(cand >> 32);
+        const uint32_t plo = (uint32_t)__popc(lo);
+        const int bit = c < plo ? (int)__fns(lo, 0, (int)c + 1) : 32 + (int)__fns(hi, 0, (int)(c - plo) + 1);
+        src[i] = bit;
+        avail &= ~(1ull << bit);
+      }
+    }
+    ok = __shfl_sync(FULL, ok, 0);
+    __syncwarp();
+    if (ok) return;
+  }
+  if (lane == 0) {
+    atomicOr(err + kErrTopology, 1);
+    for (int i = 0; i < n; ++i) src[i] = (i + 1) % n;
+  }
+  __syncwarp();
+}
+
+// Shared-memory tables of the fused prologue.
+struct SmemTopo {
+  double* rw;       // [k][n]   1 / w'_{rank,s}  (DIAG)
+  double* iws;      // [k]      1 / sum_rows w'_{.,s}  (DIAG)
+  uint32_t* ord;    // [k][n]   cycle order
+  int32_t* src;     // [k][n]
+  float* wsn;       // [n][k]   psw snapshot of each rank's (leader) row
+  uint32_t* scratch;  // [warps][64] Philox words
+};
+
+__host__ __device__ inline size_t fused_smem_bytes(int n, int k, int warps, bool diag) {
+  size_t b = 0;
+  if (diag) b += sizeof(double) * ((size_t)k * n + k);
+  b += sizeof(uint32_t) * (size_t)k * n;  // ord
+  b += sizeof(int32_t) * (size_t)k * n;   // src
+  b += sizeof(float) * (size_t)n * k;     // wsn
+  b += sizeof(uint32_t) * 64 * warps;     // scratch
+  return b;
+}
+
+__device__ SmemTopo carve(unsigned char* base, int n, int k, bool diag) {
+  SmemTopo t;
+  size_t off = 0;
+  if (diag) {
+    t.rw = reinterpret_cast<double*>(base);
+    off += sizeof(double) * (size_t)k * n;
+    t.iws = reinterpret_cast<double*>(base + off);
+    off += sizeof(double) * k;
+  } else {
+    t.rw = nullptr;
+    t.iws = nullptr;
+  }
+  t.ord = reinterpret_cast<uint32_t*>(base + off);
+  off += sizeof(uint32_t) * (size_t)k * n;
+  t.src = reinterpret_cast<int32_t*>(base + off);
+  off += sizeof(int32_t) * (size_t)k * n;
+  t.wsn = reinterpret_cast<float*>(base + off);
+  off += sizeof(float) * (size_t)n * k;
+  t.scratch = reinterpret_cast<uint32_t*>(base + off);
+  return t;
+}
+
+// w'_{i,s} from the snapshot (n >= 2 mixes with the source; a single leader keeps its weight)
+__device__ __forceinline__ float mixed_weight(const SmemTopo& t, int n, int k, int s, int i) {
+  const float wi = t.wsn[i * k + s];
+  return n >= 2 ? pair_mean1(wi, t.wsn[t.src[s * n + i] * k + s]) : wi;
+}
+
+// Prologue of the fused kernels: every CTA builds this step's tables.
+template <bool DIAG>
+__device__ void build_topology_smem(const LocalArgs& a, const SmemTopo& t) {
+  const int n = a.n, k = a.k, gs = a.group_size;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int e = threadIdx.x; e < n * k; e += blockDim.x) {
+    const int i = e / k, s = e - i * k;
+    t.wsn[e] = a.psw[(int64_t)i * gs * k + s];
+  }
+  for (int s = wid; s < k; s += nwarps) {
+    int32_t* srow = t.src + s * n;
+    if (a.given != nullptr) {
+      for (int i = lane; i < n; i += 32) srow[i] = a.given[(int64_t)s * n + i];
+      __syncwarp();
+    } else if (n == 1) {
+      if (lane == 0) srow[0] = 0;
+      __syncwarp();
+    } else {
+      warp_alg2_small(a.seed, a.step, s, n, a.tag, t.scratch + 64 * wid, srow, a.err);
+    }
+    if (lane == 0) {  // cycle order: c0, src(c0), src(src(c0)), ...
+      uint64_t seen = 0;
+      int pos = 0;
+      for (int i0 = 0; i0 < n; ++i0) {
+        if ((seen >> i0) & 1ull) continue;
+        int p = i0;
+        uint32_t flag = kOrdStart;
+        do {
+          seen |= 1ull << p;
+          const int nx = srow[p];
+          t.ord[s * n + pos++] = (uint32_t)p | flag | (nx == i0 ? kOrdEnd : 0u);
+          flag = 0;
+          p = nx;
+        } while (p != i0);
+      }
+    }
+  }
+  __syncthreads();
+  if (DIAG) {
+    for (int e = threadIdx.x; e < n * k; e += blockDim.x) {
+      const int s = e / n, i = e - s * n;
+      t.rw[e] = 1.0 / (double)mixed_weight(t, n, k, s, i);
+    }
+    for (int s = threadIdx.x; s < k; s += blockDim.x) {
+      double sum = 0.0;
+      for (int i = 0; i < n; ++i) sum += (double)mixed_weight(t, n, k, s, i) * (double)gs;
+      t.iws[s] = 1.0 / sum;
+    }
+    __syncthreads();
+  }
+}
+
+// Epilogue: the last CTA to arrive writes the mixed push-sum weights (fused path)
+// and reduces the diagnostics partials in a fixed order.
+template <bool DIAG, bool FUSED>
+__device__ void finish_step(const LocalArgs& a, const SmemTopo& t, double dacc, double zacc) {
+  __shared__ int s_last;
+  if (DIAG) block_reduce_store(dacc, zacc, a.partials);
+  if (!DIAG && !FUSED) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(a.counter, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int n = a.n, k = a.k, gs = a.group_size;
+  if (FUSED) {
+    for (int e = threadIdx.x; e < n * k; e += blockDim.x) {
+      const int i = e / k, s = e - i * k;
+      const float wn = mixed_weight(t, n, k, s, i);
+      for (int r = 0; r < gs; ++r) a.psw[((int64_t)i * gs + r) * k + s] = wn;
+    }
+  }
+  if (DIAG && threadIdx.x < 32) {
+    double da = 0.0, za = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) {
+      da += __ldcg(a.partials + 2 * b);
+      za += __ldcg(a.partials + 2 * b + 1);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      da += __shfl_xor_sync(0xffffffffu, da, off);
+      za += __shfl_xor_sync(0xffffffffu, za, off);
+    }
+    if (threadIdx.x == 0) {
+      a.diag_out[0] = sqrt(fmax(da, 0.0) / ((double)n * gs));
+      a.diag_out[1] = za;
+    }
+  }
+  if (threadIdx.x == 0) *a.counter = 0u;
+}
+
 }  // namespace
 
 constexpr int kThreads = 256;
-constexpr int kPF = 2;  // rows in flight ahead of the one being computed
 
-template <bool DIAG>
+template <int PF, bool DIAG, bool FUSED>
 __global__ void __launch_bounds__(kThreads) k_gossip_local(const LocalArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = a.n;
   const int64_t ld = a.ld, d = a.d;
   const int64_t nvec = (d + 3) >> 2;
@@ -135,25 +336,31 @@ __global__ void __launch_bounds__(kThreads) k_gossip_local(const LocalArgs a) {
   double dacc = 0.0, zacc = 0.0;
   bool bad = false;
 
+  SmemTopo t = carve(smem_raw, n, a.k, DIAG && FUSED);
+  if (FUSED) build_topology_smem<DIAG>(a, t);
+  const uint32_t* ord_all = FUSED ? t.ord : a.ord;
+  const double* rw_all = FUSED ? t.rw : a.rw;
+  const double* iws_all = FUSED ? t.iws : a.inv_wsum;
+
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
     const int64_t j = v << 2;
     const int valid = (int)imin64(4, d - j);
-    // segment of column j (reading C-2): largest s with 32*floor(s*nq/k) <= j
+    // segment of column j (reading C-2): the largest s with 32*floor(s*nq/k) <= j
     const int64_t q = j >> 5;
     const int s = (int)imin64(a.k - 1, ((q + 1) * a.k - 1) / a.nq);
-    const uint32_t* ord = a.ord + (int64_t)s * n;
-    const double* rw = DIAG ? a.rw + (int64_t)s * n : nullptr;
+    const uint32_t* ord = ord_all + (int64_t)s * n;
+    const double* rw = DIAG ? rw_all + (int64_t)s * n : nullptr;
 
-    float4 bx[kPF], bm[kPF], bg[kPF];
-    uint32_t be[kPF];
+    float4 bx[PF], bm[PF], bg[PF];
+    uint32_t be[PF];
 #pragma unroll
-    for (int t = 0; t < kPF; ++t) {
-      if (t < n) {
-        be[t] = __ldg(ord + t);
-        const int64_t off = (int64_t)(be[t] & kOrdIdx) * ld + j;
-        bx[t] = ld_stream(a.x + off);
-        bm[t] = ld_stream(a.m + off);
-        bg[t] = ld_stream(a.g + off);
+    for (int u = 0; u < PF; ++u) {
+      if (u < n) {
+        be[u] = ord[u];
+        const int64_t off = (int64_t)(be[u] & kOrdIdx) * ld + j;
+        bx[u] = ld_stream(a.x + off);
+        bm[u] = ld_stream(a.m + off);
+        bg[u] = ld_stream(a.g + off);
       }
     }
     float4 yfirst = make_float4(0.f, 0.f, 0.f, 0.f), yprev = yfirst;
@@ -163,19 +370,19 @@ __global__ void __launch_bounds__(kThreads) k_gossip_local(const LocalArgs a) {
     if (DIAG) cd.reset();
     bool first_diag = true;
 
-    for (int p0 = 0; p0 < n; p0 += kPF) {
+    for (int p0 = 0; p0 < n; p0 += PF) {
 #pragma unroll
-      for (int t = 0; t < kPF; ++t) {
-        const int p = p0 + t;
+      for (int u = 0; u < PF; ++u) {
+        const int p = p0 + u;
         if (p < n) {
-          const float4 cx = bx[t], cm = bm[t], cg = bg[t];
-          const uint32_t e = be[t];
-          if (p + kPF < n) {  // refill this slot with the row kPF ahead
-            be[t] = __ldg(ord + p + kPF);
-            const int64_t off2 = (int64_t)(be[t] & kOrdIdx) * ld + j;
-            bx[t] = ld_stream(a.x + off2);
-            bm[t] = ld_stream(a.m + off2);
-            bg[t] = ld_stream(a.g + off2);
+          const float4 cx = bx[u], cm = bm[u], cg = bg[u];
+          const uint32_t e = be[u];
+          if (p + PF < n) {  // refill this slot with the row PF ahead
+            be[u] = ord[p + PF];
+            const int64_t off2 = (int64_t)(be[u] & kOrdIdx) * ld + j;
+            bx[u] = ld_stream(a.x + off2);
+            bm[u] = ld_stream(a.m + off2);
+            bg[u] = ld_stream(a.g + off2);
           }
           const uint32_t row = e & kOrdIdx;
           const int64_t off = (int64_t)row * ld + j;
@@ -201,10 +408,10 @@ __global__ void __launch_bounds__(kThreads) k_gossip_local(const LocalArgs a) {
         }
       }
     }
-    if (DIAG) cd.finish(a.inv_wsum[s], (double)n, valid, dacc, zacc);
+    if (DIAG) cd.finish(iws_all[s], (double)n, valid, dacc, zacc);
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.err + kErrDiverged, 1);
-  if (DIAG) block_reduce_store(dacc, zacc, a.partials);
+  finish_step<DIAG, FUSED>(a, t, dacc, zacc);
 }
 
 // Hierarchical step with every worker co-resident (§3.3):
@@ -212,8 +419,9 @@ __global__ void __launch_bounds__(kThreads) k_gossip_local(const LocalArgs a) {
 //   h2  leader: m <- mu*m + gbar, y <- x - lr*m; then the cycle walk over the
 //       leader topology mixes leaders' y (tag HIER); one leader: x' = y
 //   h3  x' written to every member row of the group (bitwise identical)
-template <bool DIAG>
+template <bool DIAG, bool FUSED>
 __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int L = a.n, gs = a.group_size;
   const int64_t ld = a.ld, d = a.d;
   const int64_t nvec = (d + 3) >> 2;
@@ -222,13 +430,19 @@ __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
   double dacc = 0.0, zacc = 0.0;
   bool bad = false;
 
+  SmemTopo t = carve(smem_raw, L, a.k, DIAG && FUSED);
+  if (FUSED) build_topology_smem<DIAG>(a, t);
+  const uint32_t* ord_all = FUSED ? t.ord : a.ord;
+  const double* rw_all = FUSED ? t.rw : a.rw;
+  const double* iws_all = FUSED ? t.iws : a.inv_wsum;
+
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
     const int64_t j = v << 2;
     const int valid = (int)imin64(4, d - j);
     const int64_t q = j >> 5;
     const int s = (int)imin64(a.k - 1, ((q + 1) * a.k - 1) / a.nq);
-    const uint32_t* ord = a.ord + (int64_t)s * L;
-    const double* rw = DIAG ? a.rw + (int64_t)s * L : nullptr;
+    const uint32_t* ord = ord_all + (int64_t)s * L;
+    const double* rw = DIAG ? rw_all + (int64_t)s * L : nullptr;
     float4 yfirst = make_float4(0.f, 0.f, 0.f, 0.f), yprev = yfirst;
     uint32_t prev_leader = 0;
     ColDiag cd;
@@ -236,7 +450,7 @@ __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
     bool first_diag = true;
 
     for (int p = 0; p < L; ++p) {
-      const uint32_t e = __ldg(ord + p);
+      const uint32_t e = ord[p];
       const uint32_t G = e & kOrdIdx;
       const int64_t lead_off = (int64_t)G * gs * ld + j;
       const float4 cx = ld_stream(a.x + lead_off);
@@ -256,7 +470,7 @@ __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
       st_stream(a.m + lead_off, mn, valid);
       if (L == 1) {
         for (int r = 0; r < gs; ++r) st_stream(a.x + lead_off + (int64_t)r * ld, y, valid);
-        if (DIAG) { cd.add(y, rw[G], true, (double)gs); }
+        if (DIAG) cd.add(y, rw[G], true, (double)gs);
         continue;
       }
       if (e & kOrdStart) {
@@ -275,35 +489,10 @@ __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
       yprev = y;
       prev_leader = G;
     }
-    if (DIAG) cd.finish(a.inv_wsum[s], (double)L * gs, valid, dacc, zacc);
+    if (DIAG) cd.finish(iws_all[s], (double)L * gs, valid, dacc, zacc);
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.err + kErrDiverged, 1);
-  if (DIAG) block_reduce_store(dacc, zacc, a.partials);
-}
-
-// Fixed-order reduction of the per-block partials -> {CD, mean checksum}.
-__global__ void __launch_bounds__(256) k_diag_finalize(const double* partials, int nparts, int n,
-                                                       double* out) {
-  __shared__ double sa[256], sb[256];
-  double a = 0.0, b = 0.0;
-  for (int i = threadIdx.x; i < nparts; i += blockDim.x) {
-    a += partials[2 * i];
-    b += partials[2 * i + 1];
-  }
-  sa[threadIdx.x] = a;
-  sb[threadIdx.x] = b;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) {
-      sa[threadIdx.x] += sa[threadIdx.x + w];
-      sb[threadIdx.x] += sb[threadIdx.x + w];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    out[0] = sqrt(fmax(sa[0], 0.0) / (double)n);
-    out[1] = sb[0];
-  }
+  finish_step<DIAG, FUSED>(a, t, dacc, zacc);
 }
 
 // Test/bench input generator (NOT the method): SplitMix64 counter hash of
@@ -325,41 +514,91 @@ __global__ void k_synth(float* out, int64_t rows, int64_t d, int64_t ld, uint64_
   }
 }
 
-static int g_num_sms = 0;
-static int g_occ[2][2] = {{0, 0}, {0, 0}};
+// ------------------------------------------------------------------ launch ----
 
-int local_grid_size(bool hier, bool diag, int64_t d) {
+namespace {
+
+int g_num_sms = 0;
+
+int num_sms() {
   if (g_num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ[0][0], k_gossip_local<false>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ[0][1], k_gossip_local<true>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ[1][0], k_hier_local<false>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_occ[1][1], k_hier_local<true>, kThreads, 0);
   }
-  const int64_t nvec = (d + 3) / 4;
+  return g_num_sms;
+}
+
+// Register-pipeline depth of the flat kernel (rows in flight ahead of the one
+// being computed).  CS_LOCAL_PF overrides it for tuning runs.
+int pipeline_depth() {
+  static int pf = 0;
+  if (pf == 0) {
+    const char* e = getenv("CS_LOCAL_PF");
+    pf = e ? atoi(e) : 2;
+    if (pf != 1 && pf != 2 && pf != 3 && pf != 4) pf = 2;
+  }
+  return pf;
+}
+
+template <typename K>
+cudaError_t launch_persistent(K kernel, const LocalArgs& a, size_t smem, cudaStream_t st,
+                              int* grid_out) {
+  cudaError_t e = cudaSuccess;
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (occ < 1) occ = 1;
+  const int64_t nvec = (a.d + 3) / 4;
   const int64_t need = (nvec + kThreads - 1) / kThreads;
-  int64_t cap = (int64_t)g_num_sms * (g_occ[hier][diag] > 0 ? g_occ[hier][diag] : 1);
-  return (int)(need < cap ? (need > 0 ? need : 1) : cap);
-}
-
-cudaError_t launch_gossip_local(const LocalArgs& a, bool diag, int grid, cudaStream_t st) {
-  if (diag) k_gossip_local<true><<<grid, kThreads, 0, st>>>(a);
-  else k_gossip_local<false><<<grid, kThreads, 0, st>>>(a);
+  const int64_t cap = (int64_t)num_sms() * occ;
+  const int grid = (int)(need < cap ? (need > 0 ? need : 1) : cap);
+  kernel<<<grid, kThreads, smem, st>>>(a);
+  if (grid_out) *grid_out = grid;
   return cudaGetLastError();
 }
 
-cudaError_t launch_hier_local(const LocalArgs& a, bool diag, int grid, cudaStream_t st) {
-  if (diag) k_hier_local<true><<<grid, kThreads, 0, st>>>(a);
-  else k_hier_local<false><<<grid, kThreads, 0, st>>>(a);
-  return cudaGetLastError();
+template <int PF>
+cudaError_t launch_flat_pf(const LocalArgs& a, bool diag, bool fused, size_t smem, cudaStream_t st,
+                           int* grid_out) {
+  if (fused) {
+    if (diag) return launch_persistent(k_gossip_local<PF, true, true>, a, smem, st, grid_out);
+    return launch_persistent(k_gossip_local<PF, false, true>, a, smem, st, grid_out);
+  }
+  if (diag) return launch_persistent(k_gossip_local<PF, true, false>, a, 0, st, grid_out);
+  return launch_persistent(k_gossip_local<PF, false, false>, a, 0, st, grid_out);
 }
 
-cudaError_t launch_diag_finalize(const double* partials, int nparts, int n, double* out,
-                                 cudaStream_t st) {
-  k_diag_finalize<<<1, 256, 0, st>>>(partials, nparts, n, out);
-  return cudaGetLastError();
+}  // namespace
+
+bool fused_topology_ok(int n, int k) { return n <= kFusedMaxN && (int64_t)n * k <= kFusedMaxKN; }
+
+int local_max_grid() { return num_sms() * 8; }
+
+cudaError_t launch_gossip_local(const LocalArgs& a, bool diag, bool fused, cudaStream_t st,
+                                int* grid_out) {
+  const size_t smem = fused ? fused_smem_bytes(a.n, a.k, kThreads / 32, diag) : 0;
+  switch (pipeline_depth()) {
+    case 1: return launch_flat_pf<1>(a, diag, fused, smem, st, grid_out);
+    case 3: return launch_flat_pf<3>(a, diag, fused, smem, st, grid_out);
+    case 4: return launch_flat_pf<4>(a, diag, fused, smem, st, grid_out);
+    default: return launch_flat_pf<2>(a, diag, fused, smem, st, grid_out);
+  }
+}
+
+cudaError_t launch_hier_local(const LocalArgs& a, bool diag, bool fused, cudaStream_t st,
+                              int* grid_out) {
+  const size_t smem = fused ? fused_smem_bytes(a.n, a.k, kThreads / 32, diag) : 0;
+  if (fused) {
+    if (diag) return launch_persistent(k_hier_local<true, true>, a, smem, st, grid_out);
+    return launch_persistent(k_hier_local<false, true>, a, smem, st, grid_out);
+  }
+  if (diag) return launch_persistent(k_hier_local<true, false>, a, 0, st, grid_out);
+  return launch_persistent(k_hier_local<false, false>, a, 0, st, grid_out);
 }
 
 cudaError_t launch_synth(float* out, int64_t rows, int64_t d, int64_t ld, uint64_t seed, int tag,
