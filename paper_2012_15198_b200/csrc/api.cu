@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -68,6 +69,12 @@ struct Ctx {
   double* d_diag = nullptr;
   unsigned* d_counter = nullptr;  // CTA arrival counter of the fused kernels
   int launches_per_step = 0;
+
+  // bulk-TMA single-GPU kernel (n <= 64): balanced segment-aligned tiles
+  bool use_tma = false;
+  TileDesc* d_tiles = nullptr;
+  int n_tiles = 0;
+  int tma_grid_plain = 0, tma_grid_diag = 0;
   bool has_override = false;
 
   float* d_stage = nullptr;   // cs_gossip_step_host staging buffer
@@ -107,10 +114,11 @@ int next_event_pair(cudaEvent_t* ev) {
 void free_device() {
   auto f = [](void* p) { if (p) cudaFree(p); };
   f(g.d_bounds); f(g.d_src); f(g.d_dst); f(g.d_ord); f(g.d_given); f(g.d_rw);
-  f(g.d_inv_wsum); f(g.d_err); f(g.d_partials); f(g.d_diag); f(g.d_stage); f(g.d_counter);
+  f(g.d_inv_wsum); f(g.d_err); f(g.d_partials); f(g.d_diag); f(g.d_stage); f(g.d_counter); f(g.d_tiles);
   g.d_bounds = nullptr; g.d_src = nullptr; g.d_dst = nullptr; g.d_ord = nullptr;
   g.d_given = nullptr; g.d_rw = nullptr; g.d_inv_wsum = nullptr; g.d_err = nullptr;
   g.d_partials = nullptr; g.d_diag = nullptr; g.d_stage = nullptr; g.d_counter = nullptr;
+  g.d_tiles = nullptr; g.n_tiles = 0; g.use_tma = false;
   g.stage_bytes = 0;
   peer_release(g.peer);
 }
@@ -204,6 +212,8 @@ LocalArgs local_args(float* params, const float* grads, float* psw, int n, int g
   a.diag_out = g.d_diag;
   a.counter = g.d_counter;
   a.err = g.d_err;
+  a.tiles = g.d_tiles;
+  a.n_tiles = g.n_tiles;
   return a;
 }
 
@@ -229,6 +239,17 @@ int enqueue_flat_step(float* params, const float* grads, float* psw, float lr, f
   const int n = g.world;
   const bool fused = fused_topology_ok(n, g.k);
   LocalArgs a = local_args(params, grads, psw, n, 1, CS_TAG_FLAT, lr, mu);
+  if (fused && g.use_tma) {
+    a.given = g.has_override ? g.d_given : nullptr;
+    cudaEvent_t ev[2];
+    int rc = next_event_pair(ev);
+    if (rc) return rc;
+    if (ev[0]) CS_CUDA(cudaEventRecord(ev[0], g.stream));
+    CS_CUDA(launch_gossip_tma(a, diag, diag ? g.tma_grid_diag : g.tma_grid_plain, g.stream));
+    if (ev[1]) CS_CUDA(cudaEventRecord(ev[1], g.stream));
+    g.launches_per_step = 1;
+    return CS_OK;
+  }
   if (fused) {
     a.given = g.has_override ? g.d_given : nullptr;
   } else {
@@ -358,6 +379,28 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
   CS_CUDA(cudaMalloc(&g.d_partials, sizeof(double) * 2 * (size_t)local_max_grid()));
   CS_CUDA(cudaMalloc(&g.d_counter, sizeof(unsigned)));
   CS_CUDA(cudaMemset(g.d_counter, 0, sizeof(unsigned)));
+  if (nprocs == 1 && fused_topology_ok(g.world, g.k)) {
+    const char* kern = getenv("CS_LOCAL_KERNEL");
+    g.use_tma = !(kern && strcmp(kern, "reg") == 0);
+  }
+  if (g.use_tma) {
+    g.tma_grid_plain = tma_grid(g.world, g.k, false);
+    g.tma_grid_diag = tma_grid(g.world, g.k, true);
+    CS_CUDA(cudaGetLastError());
+    const int T = tma_tile_len(d, g.tma_grid_plain);
+    std::vector<TileDesc> tiles;
+    for (int s = 0; s < g.k; ++s)
+      for (int64_t c = b[s]; c < b[s + 1]; c += T) {
+        TileDesc td;
+        td.c0 = c;
+        td.seg = s;
+        td.len = (int32_t)((c + T < b[s + 1] ? c + T : b[s + 1]) - c);
+        tiles.push_back(td);
+      }
+    g.n_tiles = (int)tiles.size();
+    CS_CUDA(cudaMalloc(&g.d_tiles, sizeof(TileDesc) * tiles.size()));
+    CS_CUDA(cudaMemcpy(g.d_tiles, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice));
+  }
   if (nprocs > 1) {
     int rc = peer_alloc(g.peer, g.n_loc, d, ld, g.k, nprocs, proc_rank);
     if (rc) return fail(rc, "%s", peer_error());

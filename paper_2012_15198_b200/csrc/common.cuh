@@ -38,6 +38,8 @@ struct TopoArgs {
   int* err;
 };
 
+struct TileDesc;
+
 struct LocalArgs {
   float* x;            // [rows][ld]
   float* m;            // [rows][ld]
@@ -63,7 +65,19 @@ struct LocalArgs {
   double* diag_out;    // [2] {CD, mean checksum}
   unsigned* counter;   // CTA arrival counter (0 between launches)
   int* err;
+  // bulk-TMA kernel: segment-aligned column tiles
+  const TileDesc* tiles;
+  int n_tiles;
 };
+
+// A column tile [c0, c0 + len) inside segment seg (len <= kTmaTileMax, c0 % 32 == 0).
+struct TileDesc {
+  int64_t c0;
+  int32_t seg;
+  int32_t len;
+};
+
+constexpr int kTmaTileMax = 2048;   // elements per row-tile (8 KB per array)
 
 constexpr int kFusedMaxN = 64;      // fused prologue: u64 availability mask
 constexpr int kFusedMaxKN = 2048;   // fused prologue: k*n table entries in shared memory
@@ -77,6 +91,10 @@ cudaError_t launch_gossip_local(const LocalArgs& a, bool diag, bool fused, cudaS
 cudaError_t launch_hier_local(const LocalArgs& a, bool diag, bool fused, cudaStream_t st,
                               int* grid_out);
 int local_max_grid();
+// bulk-TMA single-GPU kernel: grid size, and the balanced tile length for (d, grid)
+int tma_grid(int n, int k, bool diag);
+int tma_tile_len(int64_t d, int grid);
+cudaError_t launch_gossip_tma(const LocalArgs& a, bool diag, int grid, cudaStream_t st);
 cudaError_t launch_synth(float* out, int64_t rows, int64_t d, int64_t ld, uint64_t seed,
                          int tag, int64_t row0, float scale, cudaStream_t st);
 

@@ -327,7 +327,7 @@ constexpr int kThreads = 256;
 
 template <int PF, bool DIAG, bool FUSED>
 __global__ void __launch_bounds__(kThreads) k_gossip_local(const LocalArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int n = a.n;
   const int64_t ld = a.ld, d = a.d;
   const int64_t nvec = (d + 3) >> 2;
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kThreads) k_gossip_local(const LocalArgs a) {
 //   h3  x' written to every member row of the group (bitwise identical)
 template <bool DIAG, bool FUSED>
 __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int L = a.n, gs = a.group_size;
   const int64_t ld = a.ld, d = a.d;
   const int64_t nvec = (d + 3) >> 2;
@@ -493,6 +493,213 @@ __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.err + kErrDiverged, 1);
   finish_step<DIAG, FUSED>(a, t, dacc, zacc);
+}
+
+// ----------------------------------------------------------------------------
+// Bulk-TMA variant of the flat single-GPU step (the default for n <= 64).
+//
+// Same column-owner cycle walk, but the rows of a column tile (up to 2048
+// consecutive parameters of one segment) are staged in shared memory by 1-D
+// bulk TMA copies (cp.async.bulk ... mbarrier::complete_tx), 8 KB per array per
+// row, instead of per-thread 16-byte loads: every DRAM request is a long
+// contiguous burst.  Warp-specialised: warp 8 (one elected lane) is the
+// producer, walking the same (tile, cycle position) sequence as the consumers
+// and refilling a kStages-deep ring of {x, m, g} row-tiles; warps 0-7 consume,
+// each thread owning kVPT float4 columns of the tile, keeping y_first / y_prev
+// of its columns in registers and storing x', m' straight to HBM.
+// ----------------------------------------------------------------------------
+namespace {
+
+constexpr int kTmaConsumers = 256;
+constexpr int kTmaThreads = kTmaConsumers + 32;
+constexpr int kVPT = kTmaTileMax / (4 * kTmaConsumers);  // float4 columns per consumer thread
+constexpr int kStages = 4;
+constexpr size_t kStageBytes = 3ull * kTmaTileMax * sizeof(float);
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__host__ __device__ inline size_t tma_smem_bytes(int n, int k, bool diag) {
+  return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t) +
+         fused_smem_bytes(n, k, kTmaThreads / 32, diag);
+}
+
+}  // namespace
+
+template <bool DIAG>
+__global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stage_buf = reinterpret_cast<float*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  SmemTopo t = carve(reinterpret_cast<unsigned char*>(empty + kStages), a.n, a.k, DIAG);
+
+  const int n = a.n;
+  const int64_t ld = a.ld;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmaConsumers / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  build_topology_smem<DIAG>(a, t);  // ends with __syncthreads (also publishes the barriers)
+
+  double dacc = 0.0, zacc = 0.0;
+  if (warp == kTmaConsumers / 32) {
+    // ---------------- producer warp -------------------------------------------
+    uint32_t it = 0;
+    for (int u = blockIdx.x; u < a.n_tiles; u += gridDim.x) {
+      const TileDesc td = a.tiles[u];
+      const uint32_t bytes = (uint32_t)(((td.len + 3) & ~3) * sizeof(float));
+      const uint32_t* ord = t.ord + td.seg * n;
+      for (int p = 0; p < n; ++p, ++it) {
+        if (lane == 0) {
+          const int st = (int)(it % kStages);
+          mbar_wait(&empty[st], ((it / kStages) & 1u) ^ 1u);
+          const int64_t off = (int64_t)(ord[p] & kOrdIdx) * ld + td.c0;
+          float* buf = stage_buf + (size_t)st * 3 * kTmaTileMax;
+          mbar_arrive_expect_tx(&full[st], 3 * bytes);
+          bulk_g2s(buf, a.x + off, bytes, &full[st]);
+          bulk_g2s(buf + kTmaTileMax, a.m + off, bytes, &full[st]);
+          bulk_g2s(buf + 2 * kTmaTileMax, a.g + off, bytes, &full[st]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- consumer warps ------------------------------------------
+    const float mu = a.mu, lr = a.lr;
+    bool bad = false;
+    uint32_t it = 0;
+    for (int u = blockIdx.x; u < a.n_tiles; u += gridDim.x) {
+      const TileDesc td = a.tiles[u];
+      const uint32_t* ord = t.ord + td.seg * n;
+      const double* rw = DIAG ? t.rw + td.seg * n : nullptr;
+      float4 yfirst[kVPT], yprev[kVPT];
+      ColDiag cd[kVPT];
+      if (DIAG) {
+#pragma unroll
+        for (int c = 0; c < kVPT; ++c) cd[c].reset();
+      }
+      bool first_diag = true;
+      uint32_t prev_row = 0;
+      for (int p = 0; p < n; ++p, ++it) {
+        const int st = (int)(it % kStages);
+        mbar_wait(&full[st], (it / kStages) & 1u);
+        const float* buf = stage_buf + (size_t)st * 3 * kTmaTileMax;
+        const uint32_t e = ord[p];
+        const uint32_t row = e & kOrdIdx;
+#pragma unroll
+        for (int c = 0; c < kVPT; ++c) {
+          const int v = c * kTmaConsumers + threadIdx.x;       // float4 index in the tile
+          const int valid = td.len - 4 * v;
+          if (valid > 0) {
+            const int vv = valid < 4 ? valid : 4;
+            const float4 cx = reinterpret_cast<const float4*>(buf)[v];
+            const float4 cm = reinterpret_cast<const float4*>(buf + kTmaTileMax)[v];
+            const float4 cg = reinterpret_cast<const float4*>(buf + 2 * kTmaTileMax)[v];
+            bad |= nonfinite4(cg);
+            const float4 mn = momentum_update(cm, cg, mu);
+            const float4 y = sgd_apply(cx, mn, lr);
+            const int64_t j = td.c0 + 4 * v;
+            st_stream(a.m + (int64_t)row * ld + j, mn, vv);
+            if (e & kOrdStart) {
+              yfirst[c] = y;
+            } else {
+              const float4 xo = pair_mean(yprev[c], y);
+              st_stream(a.x + (int64_t)prev_row * ld + j, xo, vv);
+              if (DIAG) cd[c].add(xo, rw[prev_row], first_diag, 1.0);
+            }
+            if (e & kOrdEnd) {
+              const float4 xo = pair_mean(y, yfirst[c]);
+              st_stream(a.x + (int64_t)row * ld + j, xo, vv);
+              if (DIAG) cd[c].add(xo, rw[row], first_diag && (e & kOrdStart), 1.0);
+            }
+            yprev[c] = y;
+          }
+        }
+        if (DIAG && ((e & kOrdStart) == 0 || (e & kOrdEnd))) first_diag = false;
+        prev_row = row;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+      }
+      if (DIAG) {
+#pragma unroll
+        for (int c = 0; c < kVPT; ++c) {
+          const int v = c * kTmaConsumers + threadIdx.x;
+          const int valid = td.len - 4 * v;
+          if (valid > 0) cd[c].finish(t.iws[td.seg], (double)n, valid < 4 ? valid : 4, dacc, zacc);
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.err + kErrDiverged, 1);
+  }
+  finish_step<DIAG, true>(a, t, dacc, zacc);
+}
+
+int tma_grid(int n, int k, bool diag) {
+  const size_t smem = tma_smem_bytes(n, k, diag);
+  auto kern = diag ? k_gossip_tma<true> : k_gossip_tma<false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTmaThreads, smem);
+  if (occ < 1) occ = 1;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms * occ;
+}
+
+// Tile length (multiple of 32, <= kTmaTileMax) chosen so the number of tiles is
+// close to a multiple of the grid: the static round-robin schedule then leaves
+// almost no tail imbalance.
+int tma_tile_len(int64_t d, int grid) {
+  const int64_t nq = (d + kQuantum - 1) / kQuantum;
+  const int64_t per_wave = (int64_t)grid * (kTmaTileMax / kQuantum);   // quanta per full wave
+  const int64_t waves = (nq + per_wave - 1) / per_wave;
+  int64_t q = (nq + (int64_t)grid * waves - 1) / ((int64_t)grid * waves);
+  if (q < 1) q = 1;
+  if (q > kTmaTileMax / kQuantum) q = kTmaTileMax / kQuantum;
+  return (int)(q * kQuantum);
+}
+
+cudaError_t launch_gossip_tma(const LocalArgs& a, bool diag, int grid, cudaStream_t st) {
+  const size_t smem = tma_smem_bytes(a.n, a.k, diag);
+  if (diag) k_gossip_tma<true><<<grid, kTmaThreads, smem, st>>>(a);
+  else k_gossip_tma<false><<<grid, kTmaThreads, smem, st>>>(a);
+  return cudaGetLastError();
 }
 
 // Test/bench input generator (NOT the method): SplitMix64 counter hash of
