@@ -218,6 +218,10 @@ int cs_step_bytes(int64_t step, int hier, double* out);
 int cs_set_timing(int enable);
 int cs_get_timing(double* total_ms_out, int64_t* launches_out);
 
+/* Name of the hot kernel the most recent step launched (static string, "" before
+ * the first step) and the number of library kernel launches that step issued. */
+const char* cs_kernel_info(int* launches_per_step_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,6 +31,7 @@ from ._lib import (  # noqa: F401
     cs_set_step,
     cs_set_timing,
     cs_get_timing,
+    cs_kernel_info,
     cs_set_stream,
     cs_step_bytes,
     cs_sync,

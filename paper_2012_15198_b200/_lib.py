@@ -62,6 +62,7 @@ _SIGS = {
     "cs_step_bytes": (_c_int, [_c_i64, _c_int, _vp]),
     "cs_set_timing": (_c_int, [_c_int]),
     "cs_get_timing": (_c_int, [_vp, _vp]),
+    "cs_kernel_info": (ctypes.c_char_p, [_vp]),
 }
 
 for _name, (_res, _args) in _SIGS.items():
@@ -243,3 +244,9 @@ def cs_get_timing() -> tuple[float, int]:
     ms, n = ctypes.c_double(0.0), ctypes.c_int64(0)
     _check(lib.cs_get_timing(ctypes.byref(ms), ctypes.byref(n)), "cs_get_timing")
     return ms.value, n.value
+
+
+def cs_kernel_info() -> tuple[str, int]:
+    n = ctypes.c_int(0)
+    name = lib.cs_kernel_info(ctypes.byref(n))
+    return name.decode(), n.value

@@ -69,6 +69,7 @@ struct Ctx {
   double* d_diag = nullptr;
   unsigned* d_counter = nullptr;  // CTA arrival counter of the fused kernels
   int launches_per_step = 0;
+  const char* hot_kernel = "";
 
   // bulk-TMA single-GPU kernel (n <= 64): balanced segment-aligned tiles
   bool use_tma = false;
@@ -248,6 +249,7 @@ int enqueue_flat_step(float* params, const float* grads, float* psw, float lr, f
     CS_CUDA(launch_gossip_tma(a, diag, diag ? g.tma_grid_diag : g.tma_grid_plain, g.stream));
     if (ev[1]) CS_CUDA(cudaEventRecord(ev[1], g.stream));
     g.launches_per_step = 1;
+    g.hot_kernel = "k_gossip_tma";
     return CS_OK;
   }
   if (fused) {
@@ -264,6 +266,7 @@ int enqueue_flat_step(float* params, const float* grads, float* psw, float lr, f
   CS_CUDA(launch_gossip_local(a, diag, fused, g.stream, nullptr));
   if (ev[1]) CS_CUDA(cudaEventRecord(ev[1], g.stream));
   g.launches_per_step = fused ? 1 : 2;
+  g.hot_kernel = "k_gossip_local";
   return CS_OK;
 }
 
@@ -458,6 +461,8 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
     if (rc) return rc;
     rc = peer_flat_step(g.peer, pa, g.stream, ev[0], ev[1]);
     if (rc) return fail(rc, "%s", peer_error());
+    g.launches_per_step = 2;
+    g.hot_kernel = "k_gossip_peer";
   }
   if (rc) return rc;
   if (diag) g.diag_valid = (g.nprocs == 1);
@@ -513,6 +518,7 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
   if (ev[1]) CS_CUDA(cudaEventRecord(ev[1], g.stream));
   if (diag) g.diag_valid = true;
   g.launches_per_step = fused ? 1 : 2;
+  g.hot_kernel = "k_hier_local";
   g.step += 1;
   return CS_OK;
 }
@@ -650,6 +656,11 @@ int cs_get_timing(double* total_ms_out, int64_t* launches_out) {
   *total_ms_out = total;
   *launches_out = (int64_t)(g.events_used / 2);
   return CS_OK;
+}
+
+const char* cs_kernel_info(int* launches_per_step_out) {
+  if (launches_per_step_out) *launches_per_step_out = g.launches_per_step;
+  return g.hot_kernel;
 }
 
 }  // extern "C"
