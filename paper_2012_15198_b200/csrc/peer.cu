@@ -2,23 +2,25 @@
 //
 // Workers are partitioned contiguously: worker w lives on GPU w / n_loc.  At step
 // t each GPU runs ONE persistent kernel (cooperative launch, so every CTA is
-// co-resident) over "tiles" — a segment-aligned range of columns for all its
-// n_loc local workers — visited in the same order on every GPU:
+// co-resident).  The work unit is (tile q, local worker r): a segment-aligned
+// range of up to kPeerTile columns of one worker's vector.  Units are numbered
+// tile-major (u = q * n_loc + r) and CTA c takes units c, c + G, c + 2G, ... on
+// every GPU.  For a unit a CTA
 //
-//   push  for each local worker i: m' and y_i (a3) from x, m, g; y_i[tile] is
-//         stored straight into the RECEIVER's inbox on the receiver's GPU
-//         (Alg.1 l.7 isend to send_to = dst_s(i)), and kept
-//         in shared memory; the first tile of a segment also pushes w_{i,s}.
-//         Then one flag per (tile, receiving worker) is set on the receiver's
-//         GPU with system-scope release (the irecv "completion", Alg.1 l.14).
-//   wait  for this GPU's own workers' flags of the same tile (acquire), i.e.
-//         Alg.1 l.14 "wait send and recv", per tile instead of per model.
-//   mix   x_i = (y_i + inbox_i) * 0.5, w_{i,s} = (w_{i,s} + wbox_{i,s}) * 0.5  (a5).
+//   push  computes m' and y (a3) from x, m, g; stores y[tile] straight into the
+//         RECEIVER's inbox on the receiver's GPU (Alg.1 l.7 isend to
+//         send_to = dst_s(i)) and keeps it in shared memory;
+//         the first tile of a segment also pushes w_{i,s}.  Then it sets the
+//         receiver's flag of that unit with system-scope release (the irecv
+//         completion, Alg.1 l.14).
+//   wait  acquires its own flag of the unit (pushed by src_s(i), wherever it lives)
+//   mix   x = (y + inbox) * 0.5, w = (w + wbox) * 0.5  (a5, Alg.1 l.17).
 //
-// Every CTA pushes tile q before it waits on tile q and all CTAs are resident,
-// so all waits of iteration q are satisfiable (no deadlock); many CTAs per SM
-// overlap one CTA's wait with the others' streaming, so the NVLink transfer
-// overlaps the local update tile by tile.
+// Software pipeline: a CTA pushes unit i before it waits for / mixes unit i-1, so
+// the flag round trip of one unit overlaps the streaming of the next.  Waits
+// only ever target units of the same tile pushed by other CTAs, every CTA
+// pushes a unit before waiting on anything later, and all CTAs are resident:
+// by induction on the tile index every push happens, so no wait deadlocks.
 //
 // The inbox ping-pongs on step parity; before pushing at epoch e a GPU waits
 // until every peer has finished epoch e-2 (the last reader of that parity) —
@@ -27,6 +29,7 @@
 // Spins are bounded (~20 s of %globaltimer) and report CS_ETIMEOUT instead of
 // hanging the GPU.
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -50,6 +53,7 @@ int perr(int code, const char* what, cudaError_t e) {
 }
 
 constexpr int kPeerThreads = 256;
+constexpr int kPeerTile = 4096;  // columns per unit: 16 KB of one worker's row
 constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -77,7 +81,7 @@ __device__ bool spin_until(const uint32_t* p, uint32_t target) {
   while (true) {
     if ((int32_t)(ld_acquire_sys(p) - target) >= 0) return true;
     if (globaltimer() - t0 > kSpinLimitNs) return false;
-    __nanosleep(64);
+    __nanosleep(32);
   }
 }
 
@@ -87,8 +91,8 @@ struct PeerKernelArgs {
   const int64_t* tiles;     // [n_tiles][2] (segment, start)
   const int64_t* tile_end;  // [n_tiles]
   int n_tiles;
-  int tile;
   uint32_t epoch;           // this step's epoch (>= 1)
+  int mode;                 // 0 normal; diagnostics (wrong results): 1 local-only, 2 no waits
   size_t off_inbox, off_wbox, off_flags, off_done, off_count;
 };
 
@@ -106,6 +110,15 @@ __device__ __forceinline__ float4 mean4(float4 a, float4 b) {
 }
 __device__ __forceinline__ void st4(float* p, float4 v, int valid) {
   if (valid == 4) {
+    __stcs(reinterpret_cast<float4*>(p), v);
+  } else {
+    if (valid > 0) p[0] = v.x;
+    if (valid > 1) p[1] = v.y;
+    if (valid > 2) p[2] = v.z;
+  }
+}
+__device__ __forceinline__ void st4_remote(float* p, float4 v, int valid) {
+  if (valid == 4) {
     *reinterpret_cast<float4*>(p) = v;
   } else {
     if (valid > 0) p[0] = v.x;
@@ -119,19 +132,103 @@ __device__ __forceinline__ bool nonfinite4(float4 g) {
          ((__float_as_uint(g.z) & e) == e) | ((__float_as_uint(g.w) & e) == e);
 }
 
+struct Unit {
+  int tile, r, seg;
+  int64_t c0, c1;
+  bool first_tile;
+};
+
+__device__ __forceinline__ Unit unit_of(const PeerKernelArgs& a, int u) {
+  Unit x;
+  x.tile = u / a.s.n_loc;
+  x.r = u - x.tile * a.s.n_loc;
+  x.seg = (int)a.tiles[2 * x.tile];
+  x.c0 = a.tiles[2 * x.tile + 1];
+  x.c1 = a.tile_end[x.tile];
+  x.first_tile = (x.tile == 0) || (a.tiles[2 * (x.tile - 1)] != x.seg);
+  return x;
+}
+
+// (receiver GPU, receiver's local index) of local worker r's segment seg
+__device__ __forceinline__ void receiver_of(const PeerKernelArgs& a, int seg, int r, int& rp, int& rl) {
+  const PeerStepArgs& s = a.s;
+  if (a.mode == 1) { rp = s.rank; rl = r; return; }
+  const int recv = s.dst[(int64_t)seg * s.world + s.first + r];
+  rp = recv / s.n_loc;
+  rl = recv - rp * s.n_loc;
+}
+
+__device__ void push_unit(const PeerKernelArgs& a, const Unit& U, float4* ybuf, bool& bad) {
+  const PeerStepArgs& s = a.s;
+  const int par = (int)(a.epoch & 1u);
+  int rp, rl;
+  receiver_of(a, U.seg, U.r, rp, rl);
+  float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
+  const int64_t rowoff = (int64_t)U.r * s.ld;
+  const int nv = (int)((U.c1 - U.c0 + 3) >> 2);
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    const int64_t j = U.c0 + 4 * (int64_t)v;
+    const int valid = (int)imin64(4, U.c1 - j);
+    const float4 cx = __ldcs(reinterpret_cast<const float4*>(s.x + rowoff + j));
+    const float4 cm = __ldcs(reinterpret_cast<const float4*>(s.m + rowoff + j));
+    const float4 cg = __ldcs(reinterpret_cast<const float4*>(s.g + rowoff + j));
+    bad |= nonfinite4(cg);
+    const float4 mn = mom4(cm, cg, s.mu);
+    const float4 y = sgd4(cx, mn, s.lr);
+    st4(s.m + rowoff + j, mn, valid);
+    st4_remote(inbox + j, y, valid);
+    ybuf[v] = y;
+  }
+  if (U.first_tile && threadIdx.x == 0) {
+    float* wbox = reinterpret_cast<float*>(a.peers[rp] + a.off_wbox) + ((int64_t)par * s.n_loc + rl) * s.k;
+    wbox[U.seg] = s.psw[(int64_t)U.r * s.k + U.seg];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t* flag = reinterpret_cast<uint32_t*>(a.peers[rp] + a.off_flags) + (int64_t)U.tile * s.n_loc + rl;
+    __threadfence_system();
+    st_release_sys(flag, a.epoch);
+  }
+}
+
+__device__ bool wait_mix_unit(const PeerKernelArgs& a, const Unit& U, const float4* ybuf, int* s_timeout) {
+  const PeerStepArgs& s = a.s;
+  const int par = (int)(a.epoch & 1u);
+  char* mine = a.peers[s.rank];
+  if (threadIdx.x == 0 && a.mode != 2) {
+    const uint32_t* flag = reinterpret_cast<const uint32_t*>(mine + a.off_flags) + (int64_t)U.tile * s.n_loc + U.r;
+    if (!spin_until(flag, a.epoch)) *s_timeout = 1;
+  }
+  __syncthreads();
+  if (*s_timeout) return false;
+  const float* inbox = reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * s.n_loc + U.r) * s.ld;
+  const int64_t rowoff = (int64_t)U.r * s.ld;
+  const int nv = (int)((U.c1 - U.c0 + 3) >> 2);
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    const int64_t j = U.c0 + 4 * (int64_t)v;
+    const int valid = (int)imin64(4, U.c1 - j);
+    const float4 yin = __ldcg(reinterpret_cast<const float4*>(inbox + j));
+    st4(s.x + rowoff + j, mean4(ybuf[v], yin), valid);
+  }
+  if (U.first_tile && threadIdx.x == 0) {
+    const float* wbox = reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * s.n_loc + U.r) * s.k;
+    float* w = s.psw + (int64_t)U.r * s.k + U.seg;
+    *w = __fmul_rn(__fadd_rn(*w, __ldcg(wbox + U.seg)), 0.5f);
+  }
+  return true;
+}
+
 __global__ void __launch_bounds__(kPeerThreads) k_gossip_peer(const PeerKernelArgs a) {
-  extern __shared__ float4 ybuf[];  // [n_loc][tile/4]
+  __shared__ float4 ybuf[2][kPeerTile / 4];
   __shared__ int s_timeout;
   const PeerStepArgs& s = a.s;
-  const int n_loc = s.n_loc;
   const uint32_t e = a.epoch;
-  const int par = (int)(e & 1u);
   char* mine = a.peers[s.rank];
-  const int64_t ld = s.ld;
-  const int tv = a.tile / 4;
+  const int n_units = a.n_tiles * s.n_loc;
   bool bad = false;
 
   if (threadIdx.x == 0) s_timeout = 0;
+  __syncthreads();
   // ping-pong safety: every receiver finished epoch e-2, the last reader of this parity
   if (threadIdx.x < s.nprocs && e >= 3) {
     const uint32_t* done = reinterpret_cast<const uint32_t*>(mine + a.off_done);
@@ -139,79 +236,23 @@ __global__ void __launch_bounds__(kPeerThreads) k_gossip_peer(const PeerKernelAr
   }
   __syncthreads();
 
-  for (int u = blockIdx.x; u < a.n_tiles && !s_timeout; u += gridDim.x) {
-    const int seg = (int)a.tiles[2 * u];
-    const int64_t c0 = a.tiles[2 * u + 1];
-    const int64_t c1 = a.tile_end[u];
-    const bool first_tile = (u == 0) || (a.tiles[2 * (u - 1)] != seg);
-    const int nv = (int)((c1 - c0 + 3) >> 2);
-
-    // ---- push ------------------------------------------------------------------
-    for (int r = 0; r < n_loc; ++r) {
-      const int i = s.first + r;
-      const int recv = s.dst[(int64_t)seg * s.world + i];
-      const int rp = recv / n_loc, rl = recv - rp * n_loc;
-      float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) +
-                     ((int64_t)par * n_loc + rl) * ld;
-      const int64_t rowoff = (int64_t)r * ld;
-      for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-        const int64_t j = c0 + 4 * (int64_t)v;
-        const int valid = (int)imin64(4, c1 - j);
-        const float4 cx = __ldcs(reinterpret_cast<const float4*>(s.x + rowoff + j));
-        const float4 cm = __ldcs(reinterpret_cast<const float4*>(s.m + rowoff + j));
-        const float4 cg = __ldcs(reinterpret_cast<const float4*>(s.g + rowoff + j));
-        bad |= nonfinite4(cg);
-        const float4 mn = mom4(cm, cg, s.mu);
-        const float4 y = sgd4(cx, mn, s.lr);
-        st4(s.m + rowoff + j, mn, valid);
-        st4(inbox + j, y, valid);
-        ybuf[r * tv + v] = y;
-      }
-      if (first_tile && threadIdx.x == 0) {
-        float* wbox = reinterpret_cast<float*>(a.peers[rp] + a.off_wbox) +
-                      ((int64_t)par * n_loc + rl) * s.k;
-        wbox[seg] = s.psw[(int64_t)r * s.k + seg];
-      }
+  Unit prev;
+  bool have_prev = false;
+  int i = 0;
+  for (int u = blockIdx.x; !s_timeout; u += gridDim.x, ++i) {
+    const bool have = u < n_units;
+    Unit cur;
+    if (have) {
+      cur = unit_of(a, u);
+      push_unit(a, cur, ybuf[i & 1], bad);  // ends with __syncthreads + flag release
     }
-    __syncthreads();
-    if (threadIdx.x < n_loc) {
-      const int i = s.first + threadIdx.x;
-      const int recv = s.dst[(int64_t)seg * s.world + i];
-      const int rp = recv / n_loc, rl = recv - rp * n_loc;
-      uint32_t* flag = reinterpret_cast<uint32_t*>(a.peers[rp] + a.off_flags) +
-                       (int64_t)u * n_loc + rl;
-      __threadfence_system();
-      st_release_sys(flag, e);
+    if (have_prev) {
+      if (!wait_mix_unit(a, prev, ybuf[(i - 1) & 1], &s_timeout)) break;
+      __syncthreads();  // ybuf[(i-1)&1] is refilled by the next push
     }
-
-    // ---- wait for this tile's inbound segments ----------------------------------
-    if (threadIdx.x < n_loc) {
-      const uint32_t* flag = reinterpret_cast<const uint32_t*>(mine + a.off_flags) +
-                             (int64_t)u * n_loc + threadIdx.x;
-      if (!spin_until(flag, e)) atomicOr(&s_timeout, 1);
-    }
-    __syncthreads();
-    if (s_timeout) break;
-
-    // ---- mix ------------------------------------------------------------------
-    for (int r = 0; r < n_loc; ++r) {
-      const float* inbox = reinterpret_cast<const float*>(mine + a.off_inbox) +
-                           ((int64_t)par * n_loc + r) * ld;
-      const int64_t rowoff = (int64_t)r * ld;
-      for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-        const int64_t j = c0 + 4 * (int64_t)v;
-        const int valid = (int)imin64(4, c1 - j);
-        const float4 yin = __ldcg(reinterpret_cast<const float4*>(inbox + j));
-        st4(s.x + rowoff + j, mean4(ybuf[r * tv + v], yin), valid);
-      }
-      if (first_tile && threadIdx.x == 0) {
-        const float* wbox = reinterpret_cast<const float*>(mine + a.off_wbox) +
-                            ((int64_t)par * n_loc + r) * s.k;
-        float* w = s.psw + (int64_t)r * s.k + seg;
-        *w = __fmul_rn(__fadd_rn(*w, __ldcg(wbox + seg)), 0.5f);
-      }
-    }
-    __syncthreads();  // ybuf reuse
+    if (!have) break;
+    prev = cur;
+    have_prev = true;
   }
 
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(s.err + kErrDiverged, 1);
@@ -222,8 +263,8 @@ __global__ void __launch_bounds__(kPeerThreads) k_gossip_peer(const PeerKernelAr
   if (threadIdx.x == 0) {
     __threadfence();
     uint32_t* count = reinterpret_cast<uint32_t*>(mine + a.off_count);
-    const uint32_t prev = atomicAdd(count, 1u);
-    if (prev + 1 == e * gridDim.x) {
+    const uint32_t prevc = atomicAdd(count, 1u);
+    if (prevc + 1 == e * gridDim.x) {
       __threadfence_system();
       for (int p = 0; p < s.nprocs; ++p) {
         uint32_t* done = reinterpret_cast<uint32_t*>(a.peers[p] + a.off_done) + s.rank;
@@ -244,11 +285,9 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   p.n_loc = n_loc;
   p.k = k;
   p.ld = ld;
-  // tile: ~16 KB of y per CTA in shared memory
-  int tile = 4096 / (n_loc < 1 ? 1 : n_loc);
-  tile = (tile / kQuantum) * kQuantum;
-  if (tile < 128) tile = 128;
-  p.tile = tile;
+  p.tile = kPeerTile;
+  const char* mode = getenv("CS_PEER_MODE");
+  p.mode = mode ? atoi(mode) : 0;
   // segment-aligned tiles
   const int64_t nq = (d + kQuantum - 1) / kQuantum;
   std::vector<int64_t> tiles, ends;
@@ -257,10 +296,10 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
     int64_t b1 = (s + 1 == k) ? d : kQuantum * (((s + 1) * nq) / k);
     if (b0 > d) b0 = d;
     if (b1 > d) b1 = d;
-    for (int64_t c = b0; c < b1; c += tile) {
+    for (int64_t c = b0; c < b1; c += kPeerTile) {
       tiles.push_back(s);
       tiles.push_back(c);
-      ends.push_back(c + tile < b1 ? c + tile : b1);
+      ends.push_back(c + kPeerTile < b1 ? c + kPeerTile : b1);
     }
   }
   p.n_tiles = (int)ends.size();
@@ -281,18 +320,15 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   if (e == cudaSuccess)
     e = cudaMemcpy(p.d_tile_end, ends.data(), sizeof(int64_t) * ends.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return perr(CS_ECUDA, "tile table", e);
-  const size_t smem = sizeof(float) * (size_t)n_loc * tile;
-  if (smem > 48 * 1024) {
-    e = cudaFuncSetAttribute(k_gossip_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return perr(CS_ECUDA, "smem attribute", e);
-  }
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gossip_peer, kPeerThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gossip_peer, kPeerThreads, 0);
   if (e != cudaSuccess || occ < 1) return perr(CS_ECUDA, "occupancy", e);
   p.grid = sms * occ;
-  if (p.grid > p.n_tiles) p.grid = p.n_tiles;
+  const int n_units = p.n_tiles * n_loc;
+  if (p.grid > n_units) p.grid = n_units;
+  if (p.grid < n_loc) return perr(CS_EUNSUPPORTED, "more local workers than resident CTAs", cudaSuccess);
   p.peer_base.assign(nprocs, nullptr);
   p.peer_base[rank] = p.base;
   p.allocated = true;
@@ -367,18 +403,17 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   ka.tiles = p.d_tiles;
   ka.tile_end = p.d_tile_end;
   ka.n_tiles = p.n_tiles;
-  ka.tile = p.tile;
   ka.epoch = ++p.epoch;
+  ka.mode = p.mode;
   ka.off_inbox = p.off_inbox;
   ka.off_wbox = p.off_wbox;
   ka.off_flags = p.off_flags;
   ka.off_done = p.off_done;
   ka.off_count = p.off_count;
-  const size_t smem = sizeof(float) * (size_t)a.n_loc * p.tile;
   void* args[] = {&ka};
   if (ev0) cudaEventRecord(ev0, st);
   e = cudaLaunchCooperativeKernel((const void*)k_gossip_peer, dim3(p.grid), dim3(kPeerThreads), args,
-                                  smem, st);
+                                  0, st);
   if (e != cudaSuccess) return perr(CS_ECUDA, "cooperative launch", e);
   if (ev1) cudaEventRecord(ev1, st);
   return CS_OK;

@@ -31,6 +31,7 @@ struct PeerState {
   int nprocs = 0, rank = 0, n_loc = 0, k = 0;
   int64_t ld = 0;
   int tile = 0;          // elements per tile (multiple of 32)
+  int mode = 0;          // CS_PEER_MODE diagnostics: 0 normal, 1 local-only, 2 no waits
   int n_tiles = 0;
   int grid = 0;
   size_t bytes = 0;

@@ -28,18 +28,18 @@ from gpu_util import OracleRun  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--n-loc", type=int, required=True)
-    ap.add_argument("--d", type=int, required=True)
-    ap.add_argument("--k", type=int, required=True)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--full", action="store_true", help="compare every column (small d)")
+    ap.add_argument("--workers-per-gpu", type=int, required=True)
+    ap.add_argument("--vector-len", type=int, required=True)
+    ap.add_argument("--segments", type=int, required=True)
+    ap.add_argument("--num-steps", type=int, default=5)
+    ap.add_argument("--rng-seed", type=int, default=0)
+    ap.add_argument("--compare-all", action="store_true", help="compare every column (small d)")
     a = ap.parse_args()
     rank, ws, lr_ = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(lr_)
     dev = torch.device("cuda", lr_)
     dist.init_process_group("nccl", device_id=dev)
-    n_loc, d, k, seed = a.n_loc, a.d, a.k, a.seed
+    n_loc, d, k, seed = a.workers_per_gpu, a.vector_len, a.segments, a.rng_seed
     world = n_loc * ws
     first = rank * n_loc
     lr, mu = float(synth.DEFAULT_LR), float(synth.DEFAULT_MOMENTUM)
@@ -58,11 +58,11 @@ def main():
     torch.cuda.synchronize()
     cs.setup_peers()
 
-    cols = np.arange(d) if a.full else synth.sample_columns(d, T.segment_bounds(d, k))
+    cols = np.arange(d) if a.compare_all else synth.sample_columns(d, T.segment_bounds(d, k))
     orc = OracleRun(world, d, k, seed, cols=cols)
     idx = torch.from_numpy(cols).to(dev)
     ok = True
-    for t in range(a.steps):
+    for t in range(a.num_steps):
         o = (t + first) % B
         cs.cs_gossip_step(x, bank[o:o + n_loc], w, lr, mu)
         orc.step(lr, mu)
@@ -79,7 +79,7 @@ def main():
     okt = torch.tensor([1 if ok else 0], device=dev)
     dist.all_reduce(okt, op=dist.ReduceOp.MIN)
     if rank == 0:
-        print(f"mp parity world={world} n_loc={n_loc} d={d} k={k} steps={a.steps}: "
+        print(f"mp parity world={world} n_loc={n_loc} d={d} k={k} steps={a.num_steps}: "
               f"{'OK' if okt.item() else 'FAIL'}", flush=True)
     dist.barrier()
     dist.destroy_process_group()

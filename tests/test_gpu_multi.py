@@ -14,9 +14,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def _run(nproc, *args, timeout=600):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
-           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "mp_gossip_worker.py"),
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "mp_gossip_worker.py"),
            *[str(a) for a in args]]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
@@ -27,19 +34,19 @@ def _run(nproc, *args, timeout=600):
 @pytest.mark.parametrize("n_loc,d,k,steps,full", [(1, 4099, 3, 6, True), (3, 50_001, 5, 5, True),
                                                   (8, 200_000, 32, 4, True), (1, 1_000_003, 8, 8, True)])
 def test_two_gpu_parity(n_loc, d, k, steps, full):
-    args = ["--n-loc", n_loc, "--d", d, "--k", k, "--steps", steps]
+    args = ["--workers-per-gpu", n_loc, "--vector-len", d, "--segments", k, "--num-steps", steps]
     if full:
-        args.append("--full")
+        args.append("--compare-all")
     _run(2, *args)
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 def test_two_gpu_resnet50_sampled():
     # BASELINE configs[2] layout (one worker per GPU, 25,557,032 fp32, k = 8)
-    _run(2, "--n-loc", 1, "--d", 25_557_032, "--k", 8, "--steps", 10)
+    _run(2, "--workers-per-gpu", 1, "--vector-len", 25_557_032, "--segments", 8, "--num-steps", 10)
 
 
 @pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
 @pytest.mark.parametrize("n_loc,d,k", [(1, 25_557_032, 8), (8, 1_000_000, 16)])
 def test_four_gpu_parity(n_loc, d, k):
-    _run(4, "--n-loc", n_loc, "--d", d, "--k", k, "--steps", 6)
+    _run(4, "--workers-per-gpu", n_loc, "--vector-len", d, "--segments", k, "--num-steps", 6)
