@@ -214,6 +214,8 @@ def main():
     ap.add_argument("--cpu-cols", type=int, default=1_000_000)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--path", default="auto", choices=["auto", "reg", "tma", "peer"],
+                    help="library kernel path (cs_set_path); peer with 1 GPU = single-GPU emulation")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -250,6 +252,7 @@ def main():
     B = world + 1
 
     cs.cs_init(world, world, k, seed)
+    cs.cs_set_path({"auto": 0, "reg": 1, "tma": 2, "peer": 3}[args.path])
     stream = torch.cuda.Stream(dev)
     with torch.cuda.stream(stream):
         x = torch.empty(n_loc, d, device=dev)
@@ -325,7 +328,8 @@ def main():
             o = (tt + first) % B
             return host_bank[o:o + n_loc]
 
-        if world_size == 1:
+        host_api = world_size == 1 and args.path != "peer"
+        if host_api:
             cs.cs_gossip_step_host(x, hgrads(t), w, lr, mu)     # warm the staging buffer
             t += 1
             e0 = time.perf_counter()
@@ -368,7 +372,7 @@ def main():
         e2e = {"value": 4.0 * world * d / (ems / esteps * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": esteps,
                "ms_per_step": ems / esteps, "wall_s": wall,
-               "api": "cs_gossip_step_host" if world_size == 1 else "H2D copy + cs_gossip_step + psw D2H"}
+               "api": "cs_gossip_step_host" if host_api else "H2D copy + cs_gossip_step + psw D2H"}
         del host_bank
 
     # ---- roofline of the hot kernel --------------------------------------------------
@@ -377,7 +381,8 @@ def main():
     hbm_per_launch = hbm_b / args.steps
     hbm_ach = hbm_per_launch / avg_kern_s / 1e9
     roof_hbm = {"bound": "hbm", "achieved": hbm_ach, "peak": hpeak, "unit": "GB/s", "frac": hbm_ach / hpeak,
-                "traffic": ncu_traffic(args.config if world_size == 1 else f"{args.config}@{world_size}"),
+                "traffic": ncu_traffic(f"{args.config}" + ("" if args.path == "auto" else f":{args.path}")
+                                       + ("" if world_size == 1 else f"@{world_size}")),
                 "peak_source": hpeak_src, "kernel": hot_kernel,
                 "algorithmic_bytes_per_launch": hbm_per_launch, "bytes_formula": "20 B x n_loc x d",
                 "avg_kernel_us": avg_kern_s * 1e6, "launches_timed": kern_launches}

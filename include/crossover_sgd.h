@@ -121,6 +121,22 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
 /* Change the stream later steps are enqueued on. */
 int cs_set_stream(void* stream);
 
+/* Kernel path for later cs_bind calls (default CS_PATH_AUTO):
+ *   CS_PATH_AUTO   nprocs > 1: CS_PATH_PEER; else CS_PATH_TMA when world <= 64 and
+ *                  k*world <= 2048, otherwise CS_PATH_REG
+ *   CS_PATH_REG    single-GPU column-owner kernel with register pipelining
+ *   CS_PATH_TMA    single-GPU column-owner kernel with bulk-TMA row-tile staging
+ *   CS_PATH_PEER   exchange-through-inbox kernel of the multi-GPU path; with
+ *                  nprocs == 1 every receiver is local (single-GPU emulation of the
+ *                  multi-GPU protocol, used by tests and profiling)
+ * All paths compute bit-identical results.  Errors: CS_ENOTINIT, CS_EINVAL,
+ * CS_EUNSUPPORTED (TMA requested for a topology it does not cover). */
+#define CS_PATH_AUTO 0
+#define CS_PATH_REG  1
+#define CS_PATH_TMA  2
+#define CS_PATH_PEER 3
+int cs_set_path(int path);
+
 /* Multi-GPU (nprocs > 1): export this process's peer-visible exchange region
  * (allocated by cs_bind) as a CUDA IPC handle (CS_IPC_HANDLE_BYTES bytes into
  * handle_out).  The caller all-gathers the handles (e.g. over torch.distributed)

@@ -26,6 +26,7 @@ CS_QUANTUM = 32
 CS_IPC_HANDLE_BYTES = 64
 CS_TAG_FLAT = 0
 CS_TAG_HIER = 1
+CS_PATH_AUTO, CS_PATH_REG, CS_PATH_TMA, CS_PATH_PEER = 0, 1, 2, 3
 
 STATUS = {
     0: "CS_OK", -1: "CS_EINVAL_WORLD", -2: "CS_EINVAL_GROUPS", -3: "CS_EINVAL_SEGMENTS",
@@ -46,6 +47,7 @@ _SIGS = {
     "cs_topology_hier": (_c_int, [_c_i64, _vp]),
     "cs_bind": (_c_int, [_vp, _c_i64, _c_i64, _c_int, _c_int, _vp]),
     "cs_set_stream": (_c_int, [_vp]),
+    "cs_set_path": (_c_int, [_c_int]),
     "cs_ipc_export": (_c_int, [_vp]),
     "cs_ipc_import": (_c_int, [_vp]),
     "cs_gossip_step": (_c_int, [_vp, _vp, _vp, _c_f, _c_f]),
@@ -250,3 +252,7 @@ def cs_kernel_info() -> tuple[str, int]:
     n = ctypes.c_int(0)
     name = lib.cs_kernel_info(ctypes.byref(n))
     return name.decode(), n.value
+
+
+def cs_set_path(path: int) -> None:
+    _check(lib.cs_set_path(path), "cs_set_path")

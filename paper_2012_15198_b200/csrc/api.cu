@@ -72,7 +72,9 @@ struct Ctx {
   const char* hot_kernel = "";
 
   // bulk-TMA single-GPU kernel (n <= 64): balanced segment-aligned tiles
+  int path = CS_PATH_AUTO;     // requested by cs_set_path (applies at the next cs_bind)
   bool use_tma = false;
+  bool use_peer = false;
   TileDesc* d_tiles = nullptr;
   int n_tiles = 0;
   int tma_grid_plain = 0, tma_grid_diag = 0;
@@ -382,10 +384,10 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
   CS_CUDA(cudaMalloc(&g.d_partials, sizeof(double) * 2 * (size_t)local_max_grid()));
   CS_CUDA(cudaMalloc(&g.d_counter, sizeof(unsigned)));
   CS_CUDA(cudaMemset(g.d_counter, 0, sizeof(unsigned)));
-  if (nprocs == 1 && fused_topology_ok(g.world, g.k)) {
-    const char* kern = getenv("CS_LOCAL_KERNEL");
-    g.use_tma = !(kern && strcmp(kern, "reg") == 0);
-  }
+  g.use_peer = nprocs > 1 || g.path == CS_PATH_PEER;
+  if (g.path == CS_PATH_TMA && !fused_topology_ok(g.world, g.k))
+    return fail(CS_EUNSUPPORTED, "CS_PATH_TMA needs world <= 64 and k*world <= 2048");
+  g.use_tma = !g.use_peer && g.path != CS_PATH_REG && fused_topology_ok(g.world, g.k);
   if (g.use_tma) {
     g.tma_grid_plain = tma_grid(g.world, g.k, false);
     g.tma_grid_diag = tma_grid(g.world, g.k, true);
@@ -404,12 +406,23 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
     CS_CUDA(cudaMalloc(&g.d_tiles, sizeof(TileDesc) * tiles.size()));
     CS_CUDA(cudaMemcpy(g.d_tiles, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice));
   }
-  if (nprocs > 1) {
+  if (g.use_peer) {
     int rc = peer_alloc(g.peer, g.n_loc, d, ld, g.k, nprocs, proc_rank);
     if (rc) return fail(rc, "%s", peer_error());
+    if (nprocs == 1) {  // single-GPU emulation: the only peer is this GPU
+      rc = peer_import_self(g.peer);
+      if (rc) return fail(rc, "%s", peer_error());
+    }
   }
   g.bound = true;
   g.diag_valid = false;
+  return CS_OK;
+}
+
+int cs_set_path(int path) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (path < CS_PATH_AUTO || path > CS_PATH_PEER) return fail(CS_EINVAL, "unknown path %d", path);
+  g.path = path;
   return CS_OK;
 }
 
@@ -444,9 +457,10 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
   rc = check_step_args(params, grads, psw);
   if (rc) return rc;
   const bool diag = g.diag != 0;
-  if (g.nprocs == 1) {
+  if (!g.use_peer) {
     rc = enqueue_flat_step(params, grads, psw, lr, momentum, diag);
   } else {
+    if (diag) return fail(CS_EUNSUPPORTED, "diagnostics are not implemented on the peer-exchange path");
     if (!g.peer.imported) return fail(CS_ENOTBOUND, "multi-GPU: cs_ipc_import has not been called");
     PeerStepArgs pa;
     pa.x = params; pa.m = g.mom; pa.g = grads; pa.psw = psw;
@@ -465,7 +479,7 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
     g.hot_kernel = "k_gossip_peer";
   }
   if (rc) return rc;
-  if (diag) g.diag_valid = (g.nprocs == 1);
+  if (diag) g.diag_valid = true;
   g.step += 1;
   return CS_OK;
 }
@@ -475,7 +489,7 @@ int cs_gossip_step_host(float* params, const float* grads_host, float* psw, floa
   int rc = check_bound();
   if (rc) return rc;
   if (!grads_host || !diag_out) return fail(CS_EINVAL, "NULL grads_host/diag_out");
-  if (g.nprocs != 1) return fail(CS_EUNSUPPORTED, "cs_gossip_step_host is single-GPU");
+  if (g.use_peer) return fail(CS_EUNSUPPORTED, "cs_gossip_step_host is single-GPU (local paths)");
   const size_t bytes = sizeof(float) * (size_t)g.n_loc * (size_t)g.ld;
   if (g.stage_bytes < bytes) {
     if (g.d_stage) cudaFree(g.d_stage);

@@ -377,6 +377,16 @@ int peer_import(PeerState& p, const char* all) {
   return CS_OK;
 }
 
+int peer_import_self(PeerState& p) {
+  if (!p.allocated) return perr(CS_ENOTBOUND, "peer region not allocated", cudaSuccess);
+  cudaError_t e = cudaMalloc(&p.d_peer_base, sizeof(char*) * p.nprocs);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p.d_peer_base, p.peer_base.data(), sizeof(char*) * p.nprocs, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return perr(CS_ECUDA, "peer table", e);
+  p.imported = true;
+  return CS_OK;
+}
+
 int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEvent_t ev0,
                    cudaEvent_t ev1) {
   TopoArgs t;

@@ -48,6 +48,7 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
 void peer_release(PeerState& p);
 int peer_export(PeerState& p, char* handle_out);
 int peer_import(PeerState& p, const char* all_handles);
+int peer_import_self(PeerState& p);  // nprocs == 1: the only peer is this GPU
 int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEvent_t ev0,
                    cudaEvent_t ev1);
 const char* peer_error();

@@ -27,9 +27,11 @@ from gpu_util import OracleRun, device, device_state, grads_view, rel_norm_err  
 LR, MU = float(synth.DEFAULT_LR), float(synth.DEFAULT_MOMENTUM)
 
 
-def _bind(n, d, k, seed, groups=None, ld=None):
+def _bind(n, d, k, seed, groups=None, ld=None, path=None):
     ld = (d + 3) // 4 * 4 if ld is None else ld
     cs.cs_init(n, groups or n, k, seed)
+    if path is not None:
+        cs.cs_set_path(path)
     x, m, w, bank2 = device_state(cs, n, d, k, seed, ld=ld)
     cs.cs_bind(m, d, x.shape[1], 0, 1, torch.cuda.current_stream())
     return x, m, w, bank2
@@ -291,3 +293,54 @@ def test_resume_via_set_step():
         cs.cs_gossip_step(snap[0], grads_view(bank2, n, t), snap[2], LR, MU)
     cs.cs_sync()
     assert torch.equal(snap[0], ref)
+
+
+# ---- every kernel path is bit-identical to the oracle ---------------------------------
+
+PATHS = {"reg": 1, "tma": 2, "peer": 3}
+
+
+@pytest.mark.parametrize("path", ["reg", "tma", "peer"])
+@pytest.mark.parametrize("n,d,k,ld", [(2, 7, 1, 8), (3, 4099, 3, 4100), (8, 100_003, 4, 100_004),
+                                      (16, 65_536, 8, 65_536), (5, 12_345, 5, 12_348)])
+def test_each_path_bitwise(path, n, d, k, ld):
+    x, m, w, bank2 = _bind(n, d, k, 17, ld=ld, path=PATHS[path])
+    x[:, d:] = 3.0
+    orc = OracleRun(n, d, k, 17)
+    for t in range(4):
+        cs.cs_gossip_step(x, grads_view(bank2, n, t), w, LR, MU)
+        orc.step(LR, MU)
+    cs.cs_sync()
+    name, _ = cs.cs_kernel_info()
+    assert name == {"reg": "k_gossip_local", "tma": "k_gossip_tma", "peer": "k_gossip_peer"}[path]
+    xg = x.cpu().numpy()
+    assert np.array_equal(xg[:, :d], orc.x)
+    assert np.array_equal(m.cpu().numpy()[:, :d], orc.m)
+    assert np.array_equal(w.cpu().numpy(), orc.w)
+    assert np.all(xg[:, d:] == 3.0)
+
+
+def test_peer_path_single_gpu_resnet50_pair_sampled():
+    # the multi-GPU exchange protocol (inbox push, per-unit flags, epochs) with both
+    # workers of BASELINE configs[2] co-resident: 2 x 25,557,032, k = 8, 10 steps
+    n, d, k = 2, 25_557_032, 8
+    x, m, w, bank2 = _bind(n, d, k, 0, path=PATHS["peer"])
+    cols = synth.sample_columns(d, T.segment_bounds(d, k))
+    orc = OracleRun(n, d, k, 0, cols=cols)
+    idx = torch.from_numpy(cols).cuda()
+    for t in range(10):
+        cs.cs_gossip_step(x, grads_view(bank2, n, t), w, LR, MU)
+        orc.step(LR, MU)
+    cs.cs_sync()
+    assert np.array_equal(x.index_select(1, idx).cpu().numpy(), orc.x)
+    assert np.array_equal(m.index_select(1, idx).cpu().numpy(), orc.m)
+    assert np.array_equal(w.cpu().numpy(), orc.w)
+
+
+def test_peer_path_rejects_diagnostics():
+    x, m, w, bank2 = _bind(4, 1024, 2, 1, path=PATHS["peer"])
+    cs.cs_set_diag(True)
+    with pytest.raises(cs.CSError) as e:
+        cs.cs_gossip_step(x, grads_view(bank2, 4, 0), w, LR, MU)
+    assert e.value.code == -12
+    cs.cs_set_diag(False)
