@@ -208,6 +208,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None, choices=sorted(WORKLOADS))
     ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--workers-per-gpu", type=int, default=None)
     ap.add_argument("--d", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -243,6 +244,9 @@ def main():
     n_loc, d, k, desc = WORKLOADS[args.config]
     d = args.d or d
     k = args.k or k
+    if args.workers_per_gpu:
+        n_loc = args.workers_per_gpu
+        desc += f" [{n_loc} workers per GPU]"
     world = n_loc * world_size
     if world < 2:
         raise SystemExit(f"config {args.config} needs >= 2 workers in total")

@@ -45,14 +45,15 @@ def main():
     lr, mu = float(synth.DEFAULT_LR), float(synth.DEFAULT_MOMENTUM)
     cs.cs_init(world, world, k, seed)
     stream = torch.cuda.current_stream(dev)
-    x = torch.empty(n_loc, d, device=dev)
-    m = torch.zeros(n_loc, d, device=dev)
+    ld = (d + 3) // 4 * 4
+    x = torch.zeros(n_loc, ld, device=dev)
+    m = torch.zeros(n_loc, ld, device=dev)
     w = torch.ones(n_loc, k, device=dev)
     B = world + 1
-    bank = torch.empty(B + n_loc, d, device=dev)
-    cs.cs_bind(m, d, d, rank, ws, stream)
-    cs.cs_synth_fill(x, n_loc, d, d, seed, synth.TAG_INIT, first, 1.0)
-    cs.cs_synth_fill(bank, B, d, d, seed, synth.TAG_GRAD, 0, float(synth.GRAD_SCALE))
+    bank = torch.zeros(B + n_loc, ld, device=dev)
+    cs.cs_bind(m, d, ld, rank, ws, stream)
+    cs.cs_synth_fill(x, n_loc, d, ld, seed, synth.TAG_INIT, first, 1.0)
+    cs.cs_synth_fill(bank, B, d, ld, seed, synth.TAG_GRAD, 0, float(synth.GRAD_SCALE))
     torch.cuda.synchronize()
     bank[B:] = bank[:n_loc]
     torch.cuda.synchronize()
