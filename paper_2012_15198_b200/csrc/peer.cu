@@ -5,22 +5,28 @@
 // co-resident).  The work unit is (tile q, local worker r): a segment-aligned
 // range of up to kPeerTile columns of one worker's vector.  Units are numbered
 // tile-major (u = q * n_loc + r) and CTA c takes units c, c + G, c + 2G, ... on
-// every GPU.  For a unit a CTA
+// every GPU.
 //
-//   push  computes m' and y (a3) from x, m, g; stores y[tile] straight into the
-//         RECEIVER's inbox on the receiver's GPU (Alg.1 l.7 isend to
-//         send_to = dst_s(i)) and keeps it in shared memory;
-//         the first tile of a segment also pushes w_{i,s}.  Then it sets the
-//         receiver's flag of that unit with system-scope release (the irecv
-//         completion, Alg.1 l.14).
-//   wait  acquires its own flag of the unit (pushed by src_s(i), wherever it lives)
-//   mix   x = (y + inbox) * 0.5, w = (w + wbox) * 0.5  (a5, Alg.1 l.17).
+// Warp-specialised CTA (8 compute warps + 1 signal warp), all hand-offs through
+// shared-memory mbarriers so no compute warp ever waits on a system fence:
 //
-// Software pipeline: a CTA pushes unit i before it waits for / mixes unit i-1, so
-// the flag round trip of one unit overlaps the streaming of the next.  Waits
-// only ever target units of the same tile pushed by other CTAs, every CTA
-// pushes a unit before waiting on anything later, and all CTAs are resident:
-// by induction on the tile index every push happens, so no wait deadlocks.
+//   compute, unit i   push: m', y from x, m, g (a3); m' -> HBM; y -> the
+//                     RECEIVER's inbox on the receiver's GPU (NVLink store; Alg.1
+//                     l.7 isend to send_to = dst_s(i)) and -> a
+//                     shared-memory ring slot; the first tile of a segment also
+//                     pushes w_{i,s}; then arrive `pushed[slot]`.
+//   compute, unit i-L mix: wait `ready[slot]`, x = (y + inbox) * 0.5 and
+//                     w = (w + wbox) * 0.5 (a5, Alg.1 l.17).
+//   signal warp       for each pushed unit: st.release.sys of the receiver's flag
+//                     (the irecv completion, Alg.1 l.14); for each released unit
+//                     whose own inbound flag is set (ld.acquire.sys): arrive
+//                     `ready[slot]`.  It polls both queues, never blocking one on
+//                     the other.
+//
+// Deadlock freedom: pushes never wait on another GPU (only on this CTA's own
+// mix of unit i+1-S, whose data is pushed by another CTA's unit of an earlier
+// tile), all CTAs are resident, and every GPU visits tiles in the same order;
+// by induction on the tile index every push is eventually issued.
 //
 // The inbox ping-pongs on step parity; before pushing at epoch e a GPU waits
 // until every peer has finished epoch e-2 (the last reader of that parity) —
@@ -38,6 +44,7 @@
 #include "../../include/crossover_sgd.h"
 #include "common.cuh"
 #include "peer.cuh"
+#include "ptx.cuh"
 
 namespace cs {
 
@@ -52,35 +59,23 @@ int perr(int code, const char* what, cudaError_t e) {
   return code;
 }
 
-constexpr int kPeerThreads = 256;
-constexpr int kPeerTile = 4096;  // columns per unit: 16 KB of one worker's row
+constexpr int kCompute = 256;                 // 8 compute warps
+constexpr int kPeerThreads = kCompute + 32;   // + 1 signal warp
+constexpr int kPeerTile = 4096;               // columns per unit: 16 KB of one worker's row
+constexpr int kLag = 2;                       // mix trails push by kLag units
+constexpr int kSlots = kLag + 1;              // y ring slots
+constexpr size_t kPeerSmem = sizeof(float) * kSlots * kPeerTile;
 constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ uint64_t globaltimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
 // wait until (int32)(*p - target) >= 0; returns false on timeout
 __device__ bool spin_until(const uint32_t* p, uint32_t target) {
-  if ((int32_t)(ld_acquire_sys(p) - target) >= 0) return true;
-  const uint64_t t0 = globaltimer();
+  if ((int32_t)(ptx::ld_acquire_sys(p) - target) >= 0) return true;
+  const uint64_t t0 = ptx::globaltimer();
   while (true) {
-    if ((int32_t)(ld_acquire_sys(p) - target) >= 0) return true;
-    if (globaltimer() - t0 > kSpinLimitNs) return false;
+    if ((int32_t)(ptx::ld_acquire_sys(p) - target) >= 0) return true;
+    if (ptx::globaltimer() - t0 > kSpinLimitNs) return false;
     __nanosleep(32);
   }
 }
@@ -158,7 +153,9 @@ __device__ __forceinline__ void receiver_of(const PeerKernelArgs& a, int seg, in
   rl = recv - rp * s.n_loc;
 }
 
-__device__ void push_unit(const PeerKernelArgs& a, const Unit& U, float4* ybuf, bool& bad) {
+// compute warps: a3 + push of one unit into ybuf (tid in [0, kCompute))
+__device__ __forceinline__ void push_unit(const PeerKernelArgs& a, const Unit& U, float4* ybuf, int tid,
+                                          bool& bad) {
   const PeerStepArgs& s = a.s;
   const int par = (int)(a.epoch & 1u);
   int rp, rl;
@@ -166,68 +163,88 @@ __device__ void push_unit(const PeerKernelArgs& a, const Unit& U, float4* ybuf, 
   float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
   const int64_t rowoff = (int64_t)U.r * s.ld;
   const int nv = (int)((U.c1 - U.c0 + 3) >> 2);
-  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-    const int64_t j = U.c0 + 4 * (int64_t)v;
-    const int valid = (int)imin64(4, U.c1 - j);
-    const float4 cx = __ldcs(reinterpret_cast<const float4*>(s.x + rowoff + j));
-    const float4 cm = __ldcs(reinterpret_cast<const float4*>(s.m + rowoff + j));
-    const float4 cg = __ldcs(reinterpret_cast<const float4*>(s.g + rowoff + j));
-    bad |= nonfinite4(cg);
-    const float4 mn = mom4(cm, cg, s.mu);
-    const float4 y = sgd4(cx, mn, s.lr);
-    st4(s.m + rowoff + j, mn, valid);
-    st4_remote(inbox + j, y, valid);
-    ybuf[v] = y;
+  constexpr int kPer = kPeerTile / 4 / kCompute;
+  float4 cx[kPer], cm[kPer], cg[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {  // issue every load of the unit first
+    const int v = tid + q * kCompute;
+    if (v < nv) {
+      const int64_t j = U.c0 + 4 * (int64_t)v;
+      cx[q] = __ldcs(reinterpret_cast<const float4*>(s.x + rowoff + j));
+      cm[q] = __ldcs(reinterpret_cast<const float4*>(s.m + rowoff + j));
+      cg[q] = __ldcs(reinterpret_cast<const float4*>(s.g + rowoff + j));
+    }
   }
-  if (U.first_tile && threadIdx.x == 0) {
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int v = tid + q * kCompute;
+    if (v < nv) {
+      const int64_t j = U.c0 + 4 * (int64_t)v;
+      const int valid = (int)imin64(4, U.c1 - j);
+      bad |= nonfinite4(cg[q]);
+      const float4 mn = mom4(cm[q], cg[q], s.mu);
+      const float4 y = sgd4(cx[q], mn, s.lr);
+      st4(s.m + rowoff + j, mn, valid);
+      st4_remote(inbox + j, y, valid);
+      ybuf[v] = y;
+    }
+  }
+  if (U.first_tile && tid == 0) {
     float* wbox = reinterpret_cast<float*>(a.peers[rp] + a.off_wbox) + ((int64_t)par * s.n_loc + rl) * s.k;
     wbox[U.seg] = s.psw[(int64_t)U.r * s.k + U.seg];
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t* flag = reinterpret_cast<uint32_t*>(a.peers[rp] + a.off_flags) + (int64_t)U.tile * s.n_loc + rl;
-    __threadfence_system();
-    st_release_sys(flag, a.epoch);
-  }
 }
 
-__device__ bool wait_mix_unit(const PeerKernelArgs& a, const Unit& U, const float4* ybuf, int* s_timeout) {
+// compute warps: a5 for one unit whose inbound segment tile has been acquired
+__device__ __forceinline__ void mix_unit(const PeerKernelArgs& a, const Unit& U, const float4* ybuf, int tid) {
   const PeerStepArgs& s = a.s;
   const int par = (int)(a.epoch & 1u);
   char* mine = a.peers[s.rank];
-  if (threadIdx.x == 0 && a.mode != 2) {
-    const uint32_t* flag = reinterpret_cast<const uint32_t*>(mine + a.off_flags) + (int64_t)U.tile * s.n_loc + U.r;
-    if (!spin_until(flag, a.epoch)) *s_timeout = 1;
-  }
-  __syncthreads();
-  if (*s_timeout) return false;
   const float* inbox = reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * s.n_loc + U.r) * s.ld;
   const int64_t rowoff = (int64_t)U.r * s.ld;
   const int nv = (int)((U.c1 - U.c0 + 3) >> 2);
-  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-    const int64_t j = U.c0 + 4 * (int64_t)v;
-    const int valid = (int)imin64(4, U.c1 - j);
-    const float4 yin = __ldcg(reinterpret_cast<const float4*>(inbox + j));
-    st4(s.x + rowoff + j, mean4(ybuf[v], yin), valid);
+  constexpr int kPer = kPeerTile / 4 / kCompute;
+  float4 yin[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int v = tid + q * kCompute;
+    if (v < nv) yin[q] = __ldcg(reinterpret_cast<const float4*>(inbox + U.c0 + 4 * (int64_t)v));
   }
-  if (U.first_tile && threadIdx.x == 0) {
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int v = tid + q * kCompute;
+    if (v < nv) {
+      const int64_t j = U.c0 + 4 * (int64_t)v;
+      st4(s.x + rowoff + j, mean4(ybuf[v], yin[q]), (int)imin64(4, U.c1 - j));
+    }
+  }
+  if (U.first_tile && tid == 0) {
     const float* wbox = reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * s.n_loc + U.r) * s.k;
     float* w = s.psw + (int64_t)U.r * s.k + U.seg;
     *w = __fmul_rn(__fadd_rn(*w, __ldcg(wbox + U.seg)), 0.5f);
   }
-  return true;
 }
 
-__global__ void __launch_bounds__(kPeerThreads) k_gossip_peer(const PeerKernelArgs a) {
-  __shared__ float4 ybuf[2][kPeerTile / 4];
+__global__ void __launch_bounds__(kPeerThreads, 2) k_gossip_peer(const PeerKernelArgs a) {
+  extern __shared__ float4 ybuf_ring[];  // [kSlots][kPeerTile / 4]
+  __shared__ uint64_t pushed[kSlots], ready[kSlots];
   __shared__ int s_timeout;
   const PeerStepArgs& s = a.s;
   const uint32_t e = a.epoch;
   char* mine = a.peers[s.rank];
   const int n_units = a.n_tiles * s.n_loc;
-  bool bad = false;
+  const int G = gridDim.x;
+  const int n_my = blockIdx.x < n_units ? (n_units - blockIdx.x + G - 1) / G : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  if (threadIdx.x == 0) s_timeout = 0;
+  if (threadIdx.x == 0) {
+    s_timeout = 0;
+    for (int i = 0; i < kSlots; ++i) {
+      ptx::mbar_init(&pushed[i], kCompute / 32);
+      ptx::mbar_init(&ready[i], 1);
+    }
+    ptx::mbar_fence_init();
+  }
   __syncthreads();
   // ping-pong safety: every receiver finished epoch e-2, the last reader of this parity
   if (threadIdx.x < s.nprocs && e >= 3) {
@@ -236,30 +253,76 @@ __global__ void __launch_bounds__(kPeerThreads) k_gossip_peer(const PeerKernelAr
   }
   __syncthreads();
 
-  Unit prev;
-  bool have_prev = false;
-  int i = 0;
-  for (int u = blockIdx.x; !s_timeout; u += gridDim.x, ++i) {
-    const bool have = u < n_units;
-    Unit cur;
-    if (have) {
-      cur = unit_of(a, u);
-      push_unit(a, cur, ybuf[i & 1], bad);  // ends with __syncthreads + flag release
+  if (warp < kCompute / 32) {
+    // ---------------- compute warps ---------------------------------------------
+    bool bad = false;
+    const int tid = threadIdx.x;
+    volatile int* timeout = &s_timeout;
+    for (int i = 0; i < n_my + kLag && !*timeout; ++i) {
+      if (i < n_my) {
+        const Unit U = unit_of(a, blockIdx.x + i * G);
+        push_unit(a, U, ybuf_ring + (i % kSlots) * (kPeerTile / 4), tid, bad);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&pushed[i % kSlots]);
+      }
+      if (i >= kLag) {
+        const int j = i - kLag;
+        if (a.mode != 2) {
+          // the signal warp gives up (and sets s_timeout) after its spin bound
+          while (!ptx::mbar_try(&ready[j % kSlots], (uint32_t)((j / kSlots) & 1)) && !*timeout) {
+          }
+        }
+        if (*timeout) break;
+        mix_unit(a, unit_of(a, blockIdx.x + j * G), ybuf_ring + (j % kSlots) * (kPeerTile / 4), tid);
+      }
     }
-    if (have_prev) {
-      if (!wait_mix_unit(a, prev, ybuf[(i - 1) & 1], &s_timeout)) break;
-      __syncthreads();  // ybuf[(i-1)&1] is refilled by the next push
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(s.err + kErrDiverged, 1);
+  } else {
+    // ---------------- signal warp -----------------------------------------------
+    if (lane == 0) {
+      int nrel = 0, nacq = 0;
+      uint64_t t0 = 0;
+      while (nacq < n_my) {
+        bool progress = false;
+        while (nrel < n_my && ptx::mbar_test(&pushed[nrel % kSlots], (uint32_t)((nrel / kSlots) & 1))) {
+          const Unit U = unit_of(a, blockIdx.x + nrel * G);
+          int rp, rl;
+          receiver_of(a, U.seg, U.r, rp, rl);
+          uint32_t* flag = reinterpret_cast<uint32_t*>(a.peers[rp] + a.off_flags) + (int64_t)U.tile * s.n_loc + rl;
+          ptx::st_release_sys(flag, e);
+          ++nrel;
+          progress = true;
+        }
+        if (nacq < nrel) {
+          const Unit U = unit_of(a, blockIdx.x + nacq * G);
+          const uint32_t* flag =
+              reinterpret_cast<const uint32_t*>(mine + a.off_flags) + (int64_t)U.tile * s.n_loc + U.r;
+          if (a.mode == 2 || (int32_t)(ptx::ld_acquire_sys(flag) - e) >= 0) {
+            ptx::mbar_arrive(&ready[nacq % kSlots]);
+            ++nacq;
+            progress = true;
+          }
+        }
+        if (progress) {
+          t0 = 0;
+        } else {
+          const uint64_t now = ptx::globaltimer();
+          if (t0 == 0) t0 = now;
+          if (now - t0 > kSpinLimitNs) {  // give up: the compute warps poll s_timeout
+            *(volatile int*)&s_timeout = 1;
+            break;
+          }
+          __nanosleep(20);
+        }
+      }
     }
-    if (!have) break;
-    prev = cur;
-    have_prev = true;
+    __syncwarp();
   }
 
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(s.err + kErrDiverged, 1);
+  __syncthreads();
   if (threadIdx.x == 0 && s_timeout) atomicOr(s.err + kErrTimeout, 1);
 
   // ---- end of step: last CTA tells every peer this GPU finished epoch e ------------
-  __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     uint32_t* count = reinterpret_cast<uint32_t*>(mine + a.off_count);
@@ -268,7 +331,7 @@ __global__ void __launch_bounds__(kPeerThreads) k_gossip_peer(const PeerKernelAr
       __threadfence_system();
       for (int p = 0; p < s.nprocs; ++p) {
         uint32_t* done = reinterpret_cast<uint32_t*>(a.peers[p] + a.off_done) + s.rank;
-        st_release_sys(done, e);
+        ptx::st_release_sys(done, e);
       }
     }
   }
@@ -323,7 +386,9 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gossip_peer, kPeerThreads, 0);
+  e = cudaFuncSetAttribute(k_gossip_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPeerSmem);
+  if (e != cudaSuccess) return perr(CS_ECUDA, "smem attribute", e);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gossip_peer, kPeerThreads, kPeerSmem);
   if (e != cudaSuccess || occ < 1) return perr(CS_ECUDA, "occupancy", e);
   p.grid = sms * occ;
   const int n_units = p.n_tiles * n_loc;
@@ -423,7 +488,7 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   void* args[] = {&ka};
   if (ev0) cudaEventRecord(ev0, st);
   e = cudaLaunchCooperativeKernel((const void*)k_gossip_peer, dim3(p.grid), dim3(kPeerThreads), args,
-                                  0, st);
+                                  kPeerSmem, st);
   if (e != cudaSuccess) return perr(CS_ECUDA, "cooperative launch", e);
   if (ev1) cudaEventRecord(ev1, st);
   return CS_OK;
