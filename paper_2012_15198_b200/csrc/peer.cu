@@ -2,31 +2,32 @@
 //
 // Workers are partitioned contiguously: worker w lives on GPU w / n_loc.  At step
 // t each GPU runs ONE persistent kernel (cooperative launch, so every CTA is
-// co-resident).  The work unit is (tile q, local worker r): a segment-aligned
-// range of up to kPeerTile columns of one worker's vector.  Units are numbered
-// tile-major (u = q * n_loc + r) and CTA c takes units c, c + G, c + 2G, ... on
-// every GPU.
+// co-resident; one CTA per SM).  The work unit is (tile q, local worker r): a
+// segment-aligned range of up to kPeerTile columns of one worker's vector.
+// Units are numbered tile-major (u = q * n_loc + r) and CTA c takes units
+// c, c + G, c + 2G, ... on every GPU.
 //
-// Warp-specialised CTA (8 compute warps + 1 signal warp), all hand-offs through
-// shared-memory mbarriers so no compute warp ever waits on a system fence:
+// Warp-specialised CTA, every hand-off through shared-memory mbarriers:
 //
-//   compute, unit i   push: m', y from x, m, g (a3); m' -> HBM; y -> the
-//                     RECEIVER's inbox on the receiver's GPU (NVLink store; Alg.1
-//                     l.7 isend to send_to = dst_s(i)) and -> a
-//                     shared-memory ring slot; the first tile of a segment also
-//                     pushes w_{i,s}; then arrive `pushed[slot]`.
-//   compute, unit i-L mix: wait `ready[slot]`, x = (y + inbox) * 0.5 and
-//                     w = (w + wbox) * 0.5 (a5, Alg.1 l.17).
-//   signal warp       for each pushed unit: st.release.sys of the receiver's flag
-//                     (the irecv completion, Alg.1 l.14); for each released unit
-//                     whose own inbound flag is set (ld.acquire.sys): arrive
-//                     `ready[slot]`.  It polls both queues, never blocking one on
-//                     the other.
+//   load warp      bulk-TMA of x, m, g row-tiles of the next units into a
+//                  kStagesA-deep ring (cp.async.bulk, 8 KB per array per unit).
+//   compute warps  unit i, push: m', y (a3) from the staged tiles; m' -> HBM;
+//                  y -> the RECEIVER's inbox on the receiver's GPU (NVLink store;
+//                  Alg.1 l.7 isend to send_to = dst_s(i)) and
+//                  -> a y ring slot; first tile of a segment also pushes w_{i,s}.
+//                  unit i-kLag, mix: x = (y + inbox) * 0.5, w = (w + wbox) * 0.5
+//                  (a5, Alg.1 l.17), the inbox tile already staged in smem.
+//   signal warp    for each pushed unit: st.release.sys of the receiver's flag
+//                  (the irecv completion, Alg.1 l.14); for each released unit
+//                  whose own inbound flag is set (ld.acquire.sys): bulk-TMA the
+//                  inbox tile into the B ring.  It polls both queues, never
+//                  blocking one on the other.
 //
-// Deadlock freedom: pushes never wait on another GPU (only on this CTA's own
-// mix of unit i+1-S, whose data is pushed by another CTA's unit of an earlier
-// tile), all CTAs are resident, and every GPU visits tiles in the same order;
-// by induction on the tile index every push is eventually issued.
+// Deadlock freedom: a push never waits on another GPU; a mix of unit j waits
+// for the push of unit j on its source GPU, which is a unit of the same tile;
+// every CTA holds at most one unit per tile (G >= n_loc) and visits tiles in
+// increasing order on every GPU, all CTAs are resident, so by induction on the
+// tile index every push is eventually issued.
 //
 // The inbox ping-pongs on step parity; before pushing at epoch e a GPU waits
 // until every peer has finished epoch e-2 (the last reader of that parity) —
@@ -59,12 +60,16 @@ int perr(int code, const char* what, cudaError_t e) {
   return code;
 }
 
-constexpr int kCompute = 256;                 // 8 compute warps
-constexpr int kPeerThreads = kCompute + 32;   // + 1 signal warp
-constexpr int kPeerTile = 4096;               // columns per unit: 16 KB of one worker's row
-constexpr int kLag = 2;                       // mix trails push by kLag units
-constexpr int kSlots = kLag + 1;              // y ring slots
-constexpr size_t kPeerSmem = sizeof(float) * kSlots * kPeerTile;
+constexpr int kCompute = 256;                   // 8 compute warps
+constexpr int kPeerThreads = kCompute + 64;     // + load warp + signal warp
+constexpr int kPeerTile = 2048;                 // columns per unit: 8 KB of one worker's row
+constexpr int kPer = kPeerTile / 4 / kCompute;  // float4 per compute thread per array
+constexpr int kStagesA = 4;                     // x, m, g ring depth (units)
+constexpr int kLag = 3;                         // mix trails push by kLag units
+constexpr int kSlotsY = kLag + 1;               // y ring slots
+constexpr int kStagesB = 4;                     // inbox ring depth (units)
+constexpr size_t kTileBytes = sizeof(float) * kPeerTile;
+constexpr size_t kPeerSmem = kTileBytes * (3 * kStagesA + kSlotsY + kStagesB);
 constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -153,96 +158,41 @@ __device__ __forceinline__ void receiver_of(const PeerKernelArgs& a, int seg, in
   rl = recv - rp * s.n_loc;
 }
 
-// compute warps: a3 + push of one unit into ybuf (tid in [0, kCompute))
-__device__ __forceinline__ void push_unit(const PeerKernelArgs& a, const Unit& U, float4* ybuf, int tid,
-                                          bool& bad) {
-  const PeerStepArgs& s = a.s;
-  const int par = (int)(a.epoch & 1u);
-  int rp, rl;
-  receiver_of(a, U.seg, U.r, rp, rl);
-  float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
-  const int64_t rowoff = (int64_t)U.r * s.ld;
-  const int nv = (int)((U.c1 - U.c0 + 3) >> 2);
-  constexpr int kPer = kPeerTile / 4 / kCompute;
-  float4 cx[kPer], cm[kPer], cg[kPer];
-#pragma unroll
-  for (int q = 0; q < kPer; ++q) {  // issue every load of the unit first
-    const int v = tid + q * kCompute;
-    if (v < nv) {
-      const int64_t j = U.c0 + 4 * (int64_t)v;
-      cx[q] = __ldcs(reinterpret_cast<const float4*>(s.x + rowoff + j));
-      cm[q] = __ldcs(reinterpret_cast<const float4*>(s.m + rowoff + j));
-      cg[q] = __ldcs(reinterpret_cast<const float4*>(s.g + rowoff + j));
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    const int v = tid + q * kCompute;
-    if (v < nv) {
-      const int64_t j = U.c0 + 4 * (int64_t)v;
-      const int valid = (int)imin64(4, U.c1 - j);
-      bad |= nonfinite4(cg[q]);
-      const float4 mn = mom4(cm[q], cg[q], s.mu);
-      const float4 y = sgd4(cx[q], mn, s.lr);
-      st4(s.m + rowoff + j, mn, valid);
-      st4_remote(inbox + j, y, valid);
-      ybuf[v] = y;
-    }
-  }
-  if (U.first_tile && tid == 0) {
-    float* wbox = reinterpret_cast<float*>(a.peers[rp] + a.off_wbox) + ((int64_t)par * s.n_loc + rl) * s.k;
-    wbox[U.seg] = s.psw[(int64_t)U.r * s.k + U.seg];
-  }
+__device__ __forceinline__ uint32_t tile_bytes(const Unit& U) {
+  return (uint32_t)((((U.c1 - U.c0) + 3) & ~int64_t(3)) * (int64_t)sizeof(float));
 }
 
-// compute warps: a5 for one unit whose inbound segment tile has been acquired
-__device__ __forceinline__ void mix_unit(const PeerKernelArgs& a, const Unit& U, const float4* ybuf, int tid) {
-  const PeerStepArgs& s = a.s;
-  const int par = (int)(a.epoch & 1u);
-  char* mine = a.peers[s.rank];
-  const float* inbox = reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * s.n_loc + U.r) * s.ld;
-  const int64_t rowoff = (int64_t)U.r * s.ld;
-  const int nv = (int)((U.c1 - U.c0 + 3) >> 2);
-  constexpr int kPer = kPeerTile / 4 / kCompute;
-  float4 yin[kPer];
-#pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    const int v = tid + q * kCompute;
-    if (v < nv) yin[q] = __ldcg(reinterpret_cast<const float4*>(inbox + U.c0 + 4 * (int64_t)v));
-  }
-#pragma unroll
-  for (int q = 0; q < kPer; ++q) {
-    const int v = tid + q * kCompute;
-    if (v < nv) {
-      const int64_t j = U.c0 + 4 * (int64_t)v;
-      st4(s.x + rowoff + j, mean4(ybuf[v], yin[q]), (int)imin64(4, U.c1 - j));
-    }
-  }
-  if (U.first_tile && tid == 0) {
-    const float* wbox = reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * s.n_loc + U.r) * s.k;
-    float* w = s.psw + (int64_t)U.r * s.k + U.seg;
-    *w = __fmul_rn(__fadd_rn(*w, __ldcg(wbox + U.seg)), 0.5f);
-  }
-}
-
-__global__ void __launch_bounds__(kPeerThreads, 2) k_gossip_peer(const PeerKernelArgs a) {
-  extern __shared__ float4 ybuf_ring[];  // [kSlots][kPeerTile / 4]
-  __shared__ uint64_t pushed[kSlots], ready[kSlots];
+__global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKernelArgs a) {
+  extern __shared__ __align__(128) float smem_f[];
+  float* ringA = smem_f;                                   // [kStagesA][3][kPeerTile]
+  float* ringY = ringA + (size_t)kStagesA * 3 * kPeerTile; // [kSlotsY][kPeerTile]
+  float* ringB = ringY + (size_t)kSlotsY * kPeerTile;      // [kStagesB][kPeerTile]
+  __shared__ uint64_t a_full[kStagesA], a_empty[kStagesA];
+  __shared__ uint64_t b_full[kStagesB], b_empty[kStagesB];
+  __shared__ uint64_t pushed[kSlotsY];
   __shared__ int s_timeout;
+
   const PeerStepArgs& s = a.s;
   const uint32_t e = a.epoch;
+  const int par = (int)(e & 1u);
   char* mine = a.peers[s.rank];
   const int n_units = a.n_tiles * s.n_loc;
   const int G = gridDim.x;
   const int n_my = blockIdx.x < n_units ? (n_units - blockIdx.x + G - 1) / G : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  volatile int* timeout = &s_timeout;
 
   if (threadIdx.x == 0) {
     s_timeout = 0;
-    for (int i = 0; i < kSlots; ++i) {
-      ptx::mbar_init(&pushed[i], kCompute / 32);
-      ptx::mbar_init(&ready[i], 1);
+    for (int i = 0; i < kStagesA; ++i) {
+      ptx::mbar_init(&a_full[i], 1);
+      ptx::mbar_init(&a_empty[i], kCompute / 32);
     }
+    for (int i = 0; i < kStagesB; ++i) {
+      ptx::mbar_init(&b_full[i], 1);
+      ptx::mbar_init(&b_empty[i], kCompute / 32);
+    }
+    for (int i = 0; i < kSlotsY; ++i) ptx::mbar_init(&pushed[i], kCompute / 32);
     ptx::mbar_fence_init();
   }
   __syncthreads();
@@ -257,34 +207,105 @@ __global__ void __launch_bounds__(kPeerThreads, 2) k_gossip_peer(const PeerKerne
     // ---------------- compute warps ---------------------------------------------
     bool bad = false;
     const int tid = threadIdx.x;
-    volatile int* timeout = &s_timeout;
     for (int i = 0; i < n_my + kLag && !*timeout; ++i) {
-      if (i < n_my) {
+      if (i < n_my) {  // push unit i
         const Unit U = unit_of(a, blockIdx.x + i * G);
-        push_unit(a, U, ybuf_ring + (i % kSlots) * (kPeerTile / 4), tid, bad);
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&pushed[i % kSlots]);
-      }
-      if (i >= kLag) {
-        const int j = i - kLag;
-        if (a.mode != 2) {
-          // the signal warp gives up (and sets s_timeout) after its spin bound
-          while (!ptx::mbar_try(&ready[j % kSlots], (uint32_t)((j / kSlots) & 1)) && !*timeout) {
-          }
+        const int st = i % kStagesA;
+        while (!ptx::mbar_try(&a_full[st], (uint32_t)((i / kStagesA) & 1)) && !*timeout) {
         }
         if (*timeout) break;
-        mix_unit(a, unit_of(a, blockIdx.x + j * G), ybuf_ring + (j % kSlots) * (kPeerTile / 4), tid);
+        const float* bx = ringA + (size_t)st * 3 * kPeerTile;
+        float4* yslot = reinterpret_cast<float4*>(ringY + (size_t)(i % kSlotsY) * kPeerTile);
+        int rp, rl;
+        receiver_of(a, U.seg, U.r, rp, rl);
+        float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
+        const int64_t rowoff = (int64_t)U.r * s.ld;
+        const int len = (int)(U.c1 - U.c0);
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+          const int v = tid + q * kCompute;
+          const int valid = len - 4 * v;
+          if (valid > 0) {
+            const int vv = valid < 4 ? valid : 4;
+            const float4 cx = reinterpret_cast<const float4*>(bx)[v];
+            const float4 cm = reinterpret_cast<const float4*>(bx + kPeerTile)[v];
+            const float4 cg = reinterpret_cast<const float4*>(bx + 2 * kPeerTile)[v];
+            bad |= nonfinite4(cg);
+            const float4 mn = mom4(cm, cg, s.mu);
+            const float4 y = sgd4(cx, mn, s.lr);
+            const int64_t j = U.c0 + 4 * (int64_t)v;
+            st4(s.m + rowoff + j, mn, vv);
+            st4_remote(inbox + j, y, vv);
+            yslot[v] = y;
+          }
+        }
+        if (U.first_tile && tid == 0) {
+          float* wbox = reinterpret_cast<float*>(a.peers[rp] + a.off_wbox) + ((int64_t)par * s.n_loc + rl) * s.k;
+          wbox[U.seg] = s.psw[(int64_t)U.r * s.k + U.seg];
+        }
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive(&a_empty[st]);
+          ptx::mbar_arrive(&pushed[i % kSlotsY]);
+        }
+      }
+      if (i >= kLag) {  // mix unit j
+        const int j = i - kLag;
+        const Unit U = unit_of(a, blockIdx.x + j * G);
+        const int sb = j % kStagesB;
+        while (!ptx::mbar_try(&b_full[sb], (uint32_t)((j / kStagesB) & 1)) && !*timeout) {
+        }
+        if (*timeout) break;
+        const float4* yslot = reinterpret_cast<const float4*>(ringY + (size_t)(j % kSlotsY) * kPeerTile);
+        const float4* yin = reinterpret_cast<const float4*>(ringB + (size_t)sb * kPeerTile);
+        const int64_t rowoff = (int64_t)U.r * s.ld;
+        const int len = (int)(U.c1 - U.c0);
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+          const int v = tid + q * kCompute;
+          const int valid = len - 4 * v;
+          if (valid > 0) {
+            const int64_t jj = U.c0 + 4 * (int64_t)v;
+            st4(s.x + rowoff + jj, mean4(yslot[v], yin[v]), valid < 4 ? valid : 4);
+          }
+        }
+        if (U.first_tile && tid == 0) {
+          const float* wbox = reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * s.n_loc + U.r) * s.k;
+          float* w = s.psw + (int64_t)U.r * s.k + U.seg;
+          *w = __fmul_rn(__fadd_rn(*w, __ldcg(wbox + U.seg)), 0.5f);
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&b_empty[sb]);
       }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(s.err + kErrDiverged, 1);
+  } else if (warp == kCompute / 32) {
+    // ---------------- load warp: x, m, g tiles ahead -------------------------------
+    if (lane == 0) {
+      for (int i = 0; i < n_my && !*timeout; ++i) {
+        const Unit U = unit_of(a, blockIdx.x + i * G);
+        const int st = i % kStagesA;
+        while (!ptx::mbar_try(&a_empty[st], (uint32_t)(((i / kStagesA) & 1) ^ 1)) && !*timeout) {
+        }
+        if (*timeout) break;
+        const uint32_t bytes = tile_bytes(U);
+        const int64_t off = (int64_t)U.r * s.ld + U.c0;
+        float* buf = ringA + (size_t)st * 3 * kPeerTile;
+        ptx::mbar_arrive_expect_tx(&a_full[st], 3 * bytes);
+        ptx::bulk_g2s(buf, s.x + off, bytes, &a_full[st]);
+        ptx::bulk_g2s(buf + kPeerTile, s.m + off, bytes, &a_full[st]);
+        ptx::bulk_g2s(buf + 2 * kPeerTile, s.g + off, bytes, &a_full[st]);
+      }
+    }
+    __syncwarp();
   } else {
-    // ---------------- signal warp -----------------------------------------------
+    // ---------------- signal warp: flags out, flags in, inbox tiles ---------------
     if (lane == 0) {
       int nrel = 0, nacq = 0;
       uint64_t t0 = 0;
       while (nacq < n_my) {
         bool progress = false;
-        while (nrel < n_my && ptx::mbar_test(&pushed[nrel % kSlots], (uint32_t)((nrel / kSlots) & 1))) {
+        while (nrel < n_my && ptx::mbar_test(&pushed[nrel % kSlotsY], (uint32_t)((nrel / kSlotsY) & 1))) {
           const Unit U = unit_of(a, blockIdx.x + nrel * G);
           int rp, rl;
           receiver_of(a, U.seg, U.r, rp, rl);
@@ -297,8 +318,15 @@ __global__ void __launch_bounds__(kPeerThreads, 2) k_gossip_peer(const PeerKerne
           const Unit U = unit_of(a, blockIdx.x + nacq * G);
           const uint32_t* flag =
               reinterpret_cast<const uint32_t*>(mine + a.off_flags) + (int64_t)U.tile * s.n_loc + U.r;
-          if (a.mode == 2 || (int32_t)(ptx::ld_acquire_sys(flag) - e) >= 0) {
-            ptx::mbar_arrive(&ready[nacq % kSlots]);
+          const int sb = nacq % kStagesB;
+          if ((a.mode == 2 || (int32_t)(ptx::ld_acquire_sys(flag) - e) >= 0) &&
+              ptx::mbar_test(&b_empty[sb], (uint32_t)(((nacq / kStagesB) & 1) ^ 1))) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired data -> TMA reads
+            const uint32_t bytes = tile_bytes(U);
+            const float* src = reinterpret_cast<const float*>(mine + a.off_inbox) +
+                               ((int64_t)par * s.n_loc + U.r) * s.ld + U.c0;
+            ptx::mbar_arrive_expect_tx(&b_full[sb], bytes);
+            ptx::bulk_g2s(ringB + (size_t)sb * kPeerTile, src, bytes, &b_full[sb]);
             ++nacq;
             progress = true;
           }
@@ -308,8 +336,8 @@ __global__ void __launch_bounds__(kPeerThreads, 2) k_gossip_peer(const PeerKerne
         } else {
           const uint64_t now = ptx::globaltimer();
           if (t0 == 0) t0 = now;
-          if (now - t0 > kSpinLimitNs) {  // give up: the compute warps poll s_timeout
-            *(volatile int*)&s_timeout = 1;
+          if (now - t0 > kSpinLimitNs) {  // give up: the other warps poll s_timeout
+            *timeout = 1;
             break;
           }
           __nanosleep(20);
@@ -374,7 +402,7 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   p.bytes = align_up(p.off_count + 256, 4096);
   cudaError_t e = cudaMalloc(&p.base, p.bytes);
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region cudaMalloc", e);
-  e = cudaMemset(p.base + p.off_flags, 0, p.bytes - p.off_flags);
+  e = cudaMemset(p.base, 0, p.bytes);  // inbox padding is read by 16-byte-rounded bulk copies
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region memset", e);
   e = cudaMalloc(&p.d_tiles, sizeof(int64_t) * tiles.size());
   if (e == cudaSuccess) e = cudaMalloc(&p.d_tile_end, sizeof(int64_t) * ends.size());
