@@ -17,11 +17,16 @@
 //                  -> a y ring slot; first tile of a segment also pushes w_{i,s}.
 //                  unit i-kLag, mix: x = (y + inbox) * 0.5, w = (w + wbox) * 0.5
 //                  (a5, Alg.1 l.17), the inbox tile already staged in smem.
-//   signal warp    for each pushed unit: st.release.sys of the receiver's flag
-//                  (the irecv completion, Alg.1 l.14); for each released unit
-//                  whose own inbound flag is set (ld.acquire.sys): bulk-TMA the
-//                  inbox tile into the B ring.  It polls both queues, never
-//                  blocking one on the other.
+//   signal warp    releases the receivers' flags of every pushed unit (the irecv
+//                  completion, Alg.1 l.14) — one fence.acq_rel.sys per batch of
+//                  pushed units, then relaxed flag stores; polls its own inbound
+//                  flags relaxed and, after one fence per batch, bulk-TMAs the
+//                  inbox tiles into the B ring.  It never blocks one queue on the
+//                  other.
+//
+// All unit metadata (segment bounds, first tile of each segment, receivers of
+// the local workers) lives in shared memory, so the single-lane producer and
+// signal loops issue no dependent global loads.
 //
 // Deadlock freedom: a push never waits on another GPU; a mix of unit j waits
 // for the push of unit j on its source GPU, which is a unit of the same tile;
@@ -69,10 +74,17 @@ constexpr int kLag = 3;                         // mix trails push by kLag units
 constexpr int kSlotsY = kLag + 1;               // y ring slots
 constexpr int kStagesB = 4;                     // inbox ring depth (units)
 constexpr size_t kTileBytes = sizeof(float) * kPeerTile;
-constexpr size_t kPeerSmem = kTileBytes * (3 * kStagesA + kSlotsY + kStagesB);
+constexpr size_t kRingBytes = kTileBytes * (3 * kStagesA + kSlotsY + kStagesB);
+constexpr int kMaxDstSmem = 4096;               // receivers table in smem when k*n_loc <= this
 constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+size_t peer_smem_bytes(int k, int n_loc) {
+  size_t b = kRingBytes + sizeof(int64_t) * (k + 1) + sizeof(int32_t) * (k + 1);
+  if ((int64_t)k * n_loc <= kMaxDstSmem) b += sizeof(int32_t) * (size_t)k * n_loc;
+  return align_up(b, 16);
+}
 
 // wait until (int32)(*p - target) >= 0; returns false on timeout
 __device__ bool spin_until(const uint32_t* p, uint32_t target) {
@@ -88,8 +100,8 @@ __device__ bool spin_until(const uint32_t* p, uint32_t target) {
 struct PeerKernelArgs {
   PeerStepArgs s;
   char* const* peers;       // [nprocs] region bases
-  const int64_t* tiles;     // [n_tiles][2] (segment, start)
-  const int64_t* tile_end;  // [n_tiles]
+  const int64_t* bounds;    // [k+1] segment bounds
+  const int32_t* seg_t0;    // [k+1] first tile of each segment (seg_t0[k] = n_tiles)
   int n_tiles;
   uint32_t epoch;           // this step's epoch (>= 1)
   int mode;                 // 0 normal; diagnostics (wrong results): 1 local-only, 2 no waits
@@ -132,35 +144,45 @@ __device__ __forceinline__ bool nonfinite4(float4 g) {
          ((__float_as_uint(g.z) & e) == e) | ((__float_as_uint(g.w) & e) == e);
 }
 
+// Shared-memory unit metadata and a per-role monotone cursor over segments.
+struct Meta {
+  const int64_t* bnd;   // [k+1]
+  const int32_t* t0;    // [k+1]
+  const int32_t* dstl;  // [k][n_loc] global receiver of local worker r in segment s (or global table)
+  bool dst_global;
+};
+
 struct Unit {
-  int tile, r, seg;
-  int64_t c0, c1;
+  int tile, r, seg, len;
+  int64_t c0;
   bool first_tile;
 };
 
-__device__ __forceinline__ Unit unit_of(const PeerKernelArgs& a, int u) {
+__device__ __forceinline__ Unit unit_at(const PeerKernelArgs& a, const Meta& M, int u, int& cursor) {
   Unit x;
   x.tile = u / a.s.n_loc;
   x.r = u - x.tile * a.s.n_loc;
-  x.seg = (int)a.tiles[2 * x.tile];
-  x.c0 = a.tiles[2 * x.tile + 1];
-  x.c1 = a.tile_end[x.tile];
-  x.first_tile = (x.tile == 0) || (a.tiles[2 * (x.tile - 1)] != x.seg);
+  while (M.t0[cursor + 1] <= x.tile) ++cursor;
+  x.seg = cursor;
+  const int64_t c0 = M.bnd[cursor] + (int64_t)(x.tile - M.t0[cursor]) * kPeerTile;
+  const int64_t c1 = c0 + kPeerTile < M.bnd[cursor + 1] ? c0 + kPeerTile : M.bnd[cursor + 1];
+  x.c0 = c0;
+  x.len = (int)(c1 - c0);
+  x.first_tile = x.tile == M.t0[cursor];
   return x;
 }
 
 // (receiver GPU, receiver's local index) of local worker r's segment seg
-__device__ __forceinline__ void receiver_of(const PeerKernelArgs& a, int seg, int r, int& rp, int& rl) {
+__device__ __forceinline__ void receiver_of(const PeerKernelArgs& a, const Meta& M, int seg, int r, int& rp,
+                                            int& rl) {
   const PeerStepArgs& s = a.s;
   if (a.mode == 1) { rp = s.rank; rl = r; return; }
-  const int recv = s.dst[(int64_t)seg * s.world + s.first + r];
+  const int recv = M.dst_global ? s.dst[(int64_t)seg * s.world + s.first + r] : M.dstl[seg * s.n_loc + r];
   rp = recv / s.n_loc;
   rl = recv - rp * s.n_loc;
 }
 
-__device__ __forceinline__ uint32_t tile_bytes(const Unit& U) {
-  return (uint32_t)((((U.c1 - U.c0) + 3) & ~int64_t(3)) * (int64_t)sizeof(float));
-}
+__device__ __forceinline__ uint32_t tile_bytes(const Unit& U) { return (uint32_t)(((U.len + 3) & ~3) * 4); }
 
 __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKernelArgs a) {
   extern __shared__ __align__(128) float smem_f[];
@@ -182,6 +204,24 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   volatile int* timeout = &s_timeout;
 
+  // ---- metadata into shared memory --------------------------------------------------
+  int64_t* bnd = reinterpret_cast<int64_t*>(ringB + (size_t)kStagesB * kPeerTile);
+  int32_t* t0 = reinterpret_cast<int32_t*>(bnd + s.k + 1);
+  int32_t* dstl = t0 + s.k + 1;
+  Meta M;
+  M.bnd = bnd;
+  M.t0 = t0;
+  M.dstl = dstl;
+  M.dst_global = (int64_t)s.k * s.n_loc > kMaxDstSmem;
+  for (int i = threadIdx.x; i <= s.k; i += blockDim.x) {
+    bnd[i] = a.bounds[i];
+    t0[i] = a.seg_t0[i];
+  }
+  if (!M.dst_global)
+    for (int i = threadIdx.x; i < s.k * s.n_loc; i += blockDim.x) {
+      const int sg = i / s.n_loc, r = i - sg * s.n_loc;
+      dstl[i] = s.dst[(int64_t)sg * s.world + s.first + r];
+    }
   if (threadIdx.x == 0) {
     s_timeout = 0;
     for (int i = 0; i < kStagesA; ++i) {
@@ -207,9 +247,10 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
     // ---------------- compute warps ---------------------------------------------
     bool bad = false;
     const int tid = threadIdx.x;
+    int cur_push = 0, cur_mix = 0;
     for (int i = 0; i < n_my + kLag && !*timeout; ++i) {
       if (i < n_my) {  // push unit i
-        const Unit U = unit_of(a, blockIdx.x + i * G);
+        const Unit U = unit_at(a, M, blockIdx.x + i * G, cur_push);
         const int st = i % kStagesA;
         while (!ptx::mbar_try(&a_full[st], (uint32_t)((i / kStagesA) & 1)) && !*timeout) {
         }
@@ -217,14 +258,13 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
         const float* bx = ringA + (size_t)st * 3 * kPeerTile;
         float4* yslot = reinterpret_cast<float4*>(ringY + (size_t)(i % kSlotsY) * kPeerTile);
         int rp, rl;
-        receiver_of(a, U.seg, U.r, rp, rl);
+        receiver_of(a, M, U.seg, U.r, rp, rl);
         float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
         const int64_t rowoff = (int64_t)U.r * s.ld;
-        const int len = (int)(U.c1 - U.c0);
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
           const int v = tid + q * kCompute;
-          const int valid = len - 4 * v;
+          const int valid = U.len - 4 * v;
           if (valid > 0) {
             const int vv = valid < 4 ? valid : 4;
             const float4 cx = reinterpret_cast<const float4*>(bx)[v];
@@ -251,7 +291,7 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
       }
       if (i >= kLag) {  // mix unit j
         const int j = i - kLag;
-        const Unit U = unit_of(a, blockIdx.x + j * G);
+        const Unit U = unit_at(a, M, blockIdx.x + j * G, cur_mix);
         const int sb = j % kStagesB;
         while (!ptx::mbar_try(&b_full[sb], (uint32_t)((j / kStagesB) & 1)) && !*timeout) {
         }
@@ -259,11 +299,10 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
         const float4* yslot = reinterpret_cast<const float4*>(ringY + (size_t)(j % kSlotsY) * kPeerTile);
         const float4* yin = reinterpret_cast<const float4*>(ringB + (size_t)sb * kPeerTile);
         const int64_t rowoff = (int64_t)U.r * s.ld;
-        const int len = (int)(U.c1 - U.c0);
 #pragma unroll
         for (int q = 0; q < kPer; ++q) {
           const int v = tid + q * kCompute;
-          const int valid = len - 4 * v;
+          const int valid = U.len - 4 * v;
           if (valid > 0) {
             const int64_t jj = U.c0 + 4 * (int64_t)v;
             st4(s.x + rowoff + jj, mean4(yslot[v], yin[v]), valid < 4 ? valid : 4);
@@ -282,8 +321,9 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
   } else if (warp == kCompute / 32) {
     // ---------------- load warp: x, m, g tiles ahead -------------------------------
     if (lane == 0) {
+      int cur = 0;
       for (int i = 0; i < n_my && !*timeout; ++i) {
-        const Unit U = unit_of(a, blockIdx.x + i * G);
+        const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
         const int st = i % kStagesA;
         while (!ptx::mbar_try(&a_empty[st], (uint32_t)(((i / kStagesA) & 1) ^ 1)) && !*timeout) {
         }
@@ -301,46 +341,63 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
   } else {
     // ---------------- signal warp: flags out, flags in, inbox tiles ---------------
     if (lane == 0) {
-      int nrel = 0, nacq = 0;
-      uint64_t t0 = 0;
+      int nrel = 0, nacq = 0, cur_rel = 0, cur_acq = 0;
+      uint64_t tstall = 0;
       while (nacq < n_my) {
         bool progress = false;
-        while (nrel < n_my && ptx::mbar_test(&pushed[nrel % kSlotsY], (uint32_t)((nrel / kSlotsY) & 1))) {
-          const Unit U = unit_of(a, blockIdx.x + nrel * G);
-          int rp, rl;
-          receiver_of(a, U.seg, U.r, rp, rl);
-          uint32_t* flag = reinterpret_cast<uint32_t*>(a.peers[rp] + a.off_flags) + (int64_t)U.tile * s.n_loc + rl;
-          ptx::st_release_sys(flag, e);
-          ++nrel;
+        // release every unit the compute warps have pushed: one system fence per batch
+        int cnt = 0;
+        while (nrel + cnt < n_my && cnt < kSlotsY &&
+               ptx::mbar_test(&pushed[(nrel + cnt) % kSlotsY], (uint32_t)(((nrel + cnt) / kSlotsY) & 1)))
+          ++cnt;
+        if (cnt > 0) {
+          ptx::fence_acq_rel_sys();
+          for (int c = 0; c < cnt; ++c) {
+            const Unit U = unit_at(a, M, blockIdx.x + (nrel + c) * G, cur_rel);
+            int rp, rl;
+            receiver_of(a, M, U.seg, U.r, rp, rl);
+            uint32_t* flag =
+                reinterpret_cast<uint32_t*>(a.peers[rp] + a.off_flags) + (int64_t)U.tile * s.n_loc + rl;
+            ptx::st_relaxed_sys(flag, e);
+          }
+          nrel += cnt;
           progress = true;
         }
-        if (nacq < nrel) {
-          const Unit U = unit_of(a, blockIdx.x + nacq * G);
+        // acquire inbound units whose flag is set and whose B slot is free: one fence per batch
+        int got = 0;
+        int cur_probe = cur_acq;
+        while (nacq + got < nrel && got < kStagesB &&
+               ptx::mbar_test(&b_empty[(nacq + got) % kStagesB], (uint32_t)((((nacq + got) / kStagesB) & 1) ^ 1))) {
+          const Unit U = unit_at(a, M, blockIdx.x + (nacq + got) * G, cur_probe);
           const uint32_t* flag =
               reinterpret_cast<const uint32_t*>(mine + a.off_flags) + (int64_t)U.tile * s.n_loc + U.r;
-          const int sb = nacq % kStagesB;
-          if ((a.mode == 2 || (int32_t)(ptx::ld_acquire_sys(flag) - e) >= 0) &&
-              ptx::mbar_test(&b_empty[sb], (uint32_t)(((nacq / kStagesB) & 1) ^ 1))) {
-            asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired data -> TMA reads
+          if (a.mode != 2 && (int32_t)(ptx::ld_relaxed_sys(flag) - e) < 0) break;
+          ++got;
+        }
+        if (got > 0) {
+          ptx::fence_acq_rel_sys();
+          ptx::fence_proxy_async_global();
+          for (int c = 0; c < got; ++c) {
+            const Unit U = unit_at(a, M, blockIdx.x + (nacq + c) * G, cur_acq);
+            const int sb = (nacq + c) % kStagesB;
             const uint32_t bytes = tile_bytes(U);
             const float* src = reinterpret_cast<const float*>(mine + a.off_inbox) +
                                ((int64_t)par * s.n_loc + U.r) * s.ld + U.c0;
             ptx::mbar_arrive_expect_tx(&b_full[sb], bytes);
             ptx::bulk_g2s(ringB + (size_t)sb * kPeerTile, src, bytes, &b_full[sb]);
-            ++nacq;
-            progress = true;
           }
+          nacq += got;
+          progress = true;
         }
         if (progress) {
-          t0 = 0;
+          tstall = 0;
         } else {
           const uint64_t now = ptx::globaltimer();
-          if (t0 == 0) t0 = now;
-          if (now - t0 > kSpinLimitNs) {  // give up: the other warps poll s_timeout
+          if (tstall == 0) tstall = now;
+          if (now - tstall > kSpinLimitNs) {  // give up: the other warps poll s_timeout
             *timeout = 1;
             break;
           }
-          __nanosleep(20);
         }
       }
     }
@@ -379,21 +436,21 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   p.tile = kPeerTile;
   const char* mode = getenv("CS_PEER_MODE");
   p.mode = mode ? atoi(mode) : 0;
-  // segment-aligned tiles
+  // segment bounds (reading C-2) and segment-aligned tiles
   const int64_t nq = (d + kQuantum - 1) / kQuantum;
-  std::vector<int64_t> tiles, ends;
-  for (int s = 0; s < k; ++s) {
-    int64_t b0 = kQuantum * ((s * nq) / k);
-    int64_t b1 = (s + 1 == k) ? d : kQuantum * (((s + 1) * nq) / k);
-    if (b0 > d) b0 = d;
-    if (b1 > d) b1 = d;
-    for (int64_t c = b0; c < b1; c += kPeerTile) {
-      tiles.push_back(s);
-      tiles.push_back(c);
-      ends.push_back(c + kPeerTile < b1 ? c + kPeerTile : b1);
-    }
+  std::vector<int64_t> bounds(k + 1);
+  std::vector<int32_t> seg_t0(k + 1);
+  int n_tiles = 0;
+  for (int s = 0; s <= k; ++s) {
+    int64_t b = (s == k) ? d : kQuantum * ((s * nq) / k);
+    bounds[s] = b < d ? b : d;
   }
-  p.n_tiles = (int)ends.size();
+  for (int s = 0; s < k; ++s) {
+    seg_t0[s] = n_tiles;
+    n_tiles += (int)((bounds[s + 1] - bounds[s] + kPeerTile - 1) / kPeerTile);
+  }
+  seg_t0[k] = n_tiles;
+  p.n_tiles = n_tiles;
   p.off_inbox = 0;
   p.off_wbox = align_up(p.off_inbox + sizeof(float) * 2 * (size_t)n_loc * ld, 256);
   p.off_flags = align_up(p.off_wbox + sizeof(float) * 2 * (size_t)n_loc * k, 256);
@@ -404,19 +461,20 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region cudaMalloc", e);
   e = cudaMemset(p.base, 0, p.bytes);  // inbox padding is read by 16-byte-rounded bulk copies
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region memset", e);
-  e = cudaMalloc(&p.d_tiles, sizeof(int64_t) * tiles.size());
-  if (e == cudaSuccess) e = cudaMalloc(&p.d_tile_end, sizeof(int64_t) * ends.size());
+  e = cudaMalloc(&p.d_bounds, sizeof(int64_t) * (k + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&p.d_seg_t0, sizeof(int32_t) * (k + 1));
   if (e == cudaSuccess)
-    e = cudaMemcpy(p.d_tiles, tiles.data(), sizeof(int64_t) * tiles.size(), cudaMemcpyHostToDevice);
+    e = cudaMemcpy(p.d_bounds, bounds.data(), sizeof(int64_t) * (k + 1), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
-    e = cudaMemcpy(p.d_tile_end, ends.data(), sizeof(int64_t) * ends.size(), cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) return perr(CS_ECUDA, "tile table", e);
+    e = cudaMemcpy(p.d_seg_t0, seg_t0.data(), sizeof(int32_t) * (k + 1), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return perr(CS_ECUDA, "tile tables", e);
+  const size_t smem = peer_smem_bytes(k, n_loc);
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaFuncSetAttribute(k_gossip_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPeerSmem);
+  e = cudaFuncSetAttribute(k_gossip_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return perr(CS_ECUDA, "smem attribute", e);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gossip_peer, kPeerThreads, kPeerSmem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gossip_peer, kPeerThreads, smem);
   if (e != cudaSuccess || occ < 1) return perr(CS_ECUDA, "occupancy", e);
   p.grid = sms * occ;
   const int n_units = p.n_tiles * n_loc;
@@ -437,6 +495,8 @@ void peer_release(PeerState& p) {
   if (p.d_peer_base) cudaFree(p.d_peer_base);
   if (p.d_tiles) cudaFree(p.d_tiles);
   if (p.d_tile_end) cudaFree(p.d_tile_end);
+  if (p.d_bounds) cudaFree(p.d_bounds);
+  if (p.d_seg_t0) cudaFree(p.d_seg_t0);
   p = PeerState();
 }
 
@@ -503,8 +563,8 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   PeerKernelArgs ka;
   ka.s = a;
   ka.peers = p.d_peer_base;
-  ka.tiles = p.d_tiles;
-  ka.tile_end = p.d_tile_end;
+  ka.bounds = p.d_bounds;
+  ka.seg_t0 = p.d_seg_t0;
   ka.n_tiles = p.n_tiles;
   ka.epoch = ++p.epoch;
   ka.mode = p.mode;
@@ -516,7 +576,7 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   void* args[] = {&ka};
   if (ev0) cudaEventRecord(ev0, st);
   e = cudaLaunchCooperativeKernel((const void*)k_gossip_peer, dim3(p.grid), dim3(kPeerThreads), args,
-                                  kPeerSmem, st);
+                                  peer_smem_bytes(a.k, a.n_loc), st);
   if (e != cudaSuccess) return perr(CS_ECUDA, "cooperative launch", e);
   if (ev1) cudaEventRecord(ev1, st);
   return CS_OK;

@@ -41,6 +41,8 @@ struct PeerState {
   char** d_peer_base = nullptr;         // device copy
   int64_t* d_tiles = nullptr;           // [n_tiles][2]: (segment, start column), end implied
   int64_t* d_tile_end = nullptr;        // [n_tiles]
+  int64_t* d_bounds = nullptr;          // [k+1] segment bounds
+  int32_t* d_seg_t0 = nullptr;          // [k+1] first tile index of each segment
   uint32_t epoch = 0;                   // multi-GPU steps issued since bind
 };
 
