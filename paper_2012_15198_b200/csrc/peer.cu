@@ -2,42 +2,35 @@
 //
 // Workers are partitioned contiguously: worker w lives on GPU w / n_loc.  At step
 // t each GPU runs ONE persistent kernel (cooperative launch, so every CTA is
-// co-resident; one CTA per SM).  The work unit is (tile q, local worker r): a
-// segment-aligned range of up to kPeerTile columns of one worker's vector.
-// Units are numbered tile-major (u = q * n_loc + r) and CTA c takes units
-// c, c + G, c + 2G, ... on every GPU.
+// co-resident).  The work unit is (tile q, local worker r): a segment-aligned
+// range of up to kPeerTile columns of one worker's vector, numbered tile-major
+// (u = q * n_loc + r); CTA c takes units c, c + G, c + 2G, ... on every GPU.
+// The units are cut into W "waves" of ~64 MB of traffic, the same on every GPU.
 //
-// Warp-specialised CTA, every hand-off through shared-memory mbarriers:
+// Per CTA, wave-pipelined:
 //
-//   load warp      bulk-TMA of x, m, g row-tiles of the next units into a
-//                  kStagesA-deep ring (cp.async.bulk, 8 KB per array per unit).
-//   compute warps  unit i, push: m', y (a3) from the staged tiles; m' -> HBM;
-//                  y -> the RECEIVER's inbox on the receiver's GPU (NVLink store;
-//                  Alg.1 l.7 isend to send_to = dst_s(i)) and
-//                  -> a y ring slot; first tile of a segment also pushes w_{i,s}.
-//                  unit i-kLag, mix: x = (y + inbox) * 0.5, w = (w + wbox) * 0.5
-//                  (a5, Alg.1 l.17), the inbox tile already staged in smem.
-//   signal warp    releases the receivers' flags of every pushed unit (the irecv
-//                  completion, Alg.1 l.14) — one fence.acq_rel.sys per batch of
-//                  pushed units, then relaxed flag stores; polls its own inbound
-//                  flags relaxed and, after one fence per batch, bulk-TMAs the
-//                  inbox tiles into the B ring.  It never blocks one queue on the
-//                  other.
+//   push wave w   for each of its units: m', y from x, m, g (a3), the tiles
+//                 streamed into shared memory by a bulk-TMA load warp; m' -> HBM;
+//                 y -> x (kept in L2 for the mix) and -> the RECEIVER's inbox on
+//                 the receiver's GPU (NVLink store; Alg.1 l.7 isend to
+//                 send_to = dst_s(i)); the first tile of a
+//                 segment also pushes w_{i,s}.  Then ONE fence.acq_rel.sys and a
+//                 red.add on every GPU's arrival counter of wave w (the irecv
+//                 completion, Alg.1 l.14, for a whole wave at once).
+//   mix wave w-1  wait until this GPU's counter of wave w-1 has every CTA of every
+//                 GPU (Alg.1 l.12-14 "wait send and recv"), then
+//                 x = (y + inbox) * 0.5, w = (w + wbox) * 0.5 (a5, Alg.1 l.17);
+//                 y and inbox of a wave are still L2-resident, so the effective
+//                 HBM traffic stays near the 28 B/param of a fused pass.
 //
-// All unit metadata (segment bounds, first tile of each segment, receivers of
-// the local workers) lives in shared memory, so the single-lane producer and
-// signal loops issue no dependent global loads.
-//
-// Deadlock freedom: a push never waits on another GPU; a mix of unit j waits
-// for the push of unit j on its source GPU, which is a unit of the same tile;
-// every CTA holds at most one unit per tile (G >= n_loc) and visits tiles in
-// increasing order on every GPU, all CTAs are resident, so by induction on the
-// tile index every push is eventually issued.
+// Deadlock freedom: pushes never wait on another GPU; to push wave w a CTA has
+// mixed wave w-2, which needs every CTA's push of wave w-2; all CTAs are
+// resident, so by induction on w every wave completes.
 //
 // The inbox ping-pongs on step parity; before pushing at epoch e a GPU waits
 // until every peer has finished epoch e-2 (the last reader of that parity) —
 // the "done" words each GPU writes into every peer's region at the end of a
-// step.  Flags and done words carry the monotone epoch, so nothing is reset.
+// step.  Counters and done words carry the monotone epoch, so nothing is reset.
 // Spins are bounded (~20 s of %globaltimer) and report CS_ETIMEOUT instead of
 // hanging the GPU.
 #include <stdio.h>
@@ -66,16 +59,14 @@ int perr(int code, const char* what, cudaError_t e) {
 }
 
 constexpr int kCompute = 256;                   // 8 compute warps
-constexpr int kPeerThreads = kCompute + 64;     // + load warp + signal warp
+constexpr int kPeerThreads = kCompute + 32;     // + bulk-TMA load warp
 constexpr int kPeerTile = 2048;                 // columns per unit: 8 KB of one worker's row
 constexpr int kPer = kPeerTile / 4 / kCompute;  // float4 per compute thread per array
 constexpr int kStagesA = 4;                     // x, m, g ring depth (units)
-constexpr int kLag = 3;                         // mix trails push by kLag units
-constexpr int kSlotsY = kLag + 1;               // y ring slots
-constexpr int kStagesB = 4;                     // inbox ring depth (units)
 constexpr size_t kTileBytes = sizeof(float) * kPeerTile;
-constexpr size_t kRingBytes = kTileBytes * (3 * kStagesA + kSlotsY + kStagesB);
-constexpr int kMaxDstSmem = 4096;               // receivers table in smem when k*n_loc <= this
+constexpr size_t kRingBytes = kTileBytes * 3 * kStagesA;
+constexpr int kMaxDstSmem = 2048;               // receivers table in smem when k*n_loc <= this
+constexpr double kWaveBytes = 64.0 * 1024 * 1024;
 constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -86,15 +77,17 @@ size_t peer_smem_bytes(int k, int n_loc) {
   return align_up(b, 16);
 }
 
-// wait until (int32)(*p - target) >= 0; returns false on timeout
-__device__ bool spin_until(const uint32_t* p, uint32_t target) {
-  if ((int32_t)(ptx::ld_acquire_sys(p) - target) >= 0) return true;
-  const uint64_t t0 = ptx::globaltimer();
-  while (true) {
-    if ((int32_t)(ptx::ld_acquire_sys(p) - target) >= 0) return true;
-    if (ptx::globaltimer() - t0 > kSpinLimitNs) return false;
+// wait until (int32)(*p - target) >= 0 polling relaxed, then acquire; false on timeout
+__device__ bool wait_acquire(const uint32_t* p, uint32_t target) {
+  uint64_t t0 = 0;
+  while ((int32_t)(ptx::ld_relaxed_sys(p) - target) < 0) {
+    const uint64_t now = ptx::globaltimer();
+    if (t0 == 0) t0 = now;
+    if (now - t0 > kSpinLimitNs) return false;
     __nanosleep(32);
   }
+  ptx::fence_acq_rel_sys();
+  return true;
 }
 
 struct PeerKernelArgs {
@@ -103,9 +96,10 @@ struct PeerKernelArgs {
   const int64_t* bounds;    // [k+1] segment bounds
   const int32_t* seg_t0;    // [k+1] first tile of each segment (seg_t0[k] = n_tiles)
   int n_tiles;
+  int waves;
   uint32_t epoch;           // this step's epoch (>= 1)
   int mode;                 // 0 normal; diagnostics (wrong results): 1 local-only, 2 no waits
-  size_t off_inbox, off_wbox, off_flags, off_done, off_count;
+  size_t off_inbox, off_wbox, off_wave, off_done, off_count;
 };
 
 __device__ __forceinline__ float4 mom4(float4 m, float4 g, float mu) {
@@ -120,7 +114,8 @@ __device__ __forceinline__ float4 mean4(float4 a, float4 b) {
   return make_float4(__fmul_rn(__fadd_rn(a.x, b.x), 0.5f), __fmul_rn(__fadd_rn(a.y, b.y), 0.5f),
                      __fmul_rn(__fadd_rn(a.z, b.z), 0.5f), __fmul_rn(__fadd_rn(a.w, b.w), 0.5f));
 }
-__device__ __forceinline__ void st4(float* p, float4 v, int valid) {
+// streaming store (evict-first): for data not read again this step
+__device__ __forceinline__ void st4_cs(float* p, float4 v, int valid) {
   if (valid == 4) {
     __stcs(reinterpret_cast<float4*>(p), v);
   } else {
@@ -129,7 +124,8 @@ __device__ __forceinline__ void st4(float* p, float4 v, int valid) {
     if (valid > 2) p[2] = v.z;
   }
 }
-__device__ __forceinline__ void st4_remote(float* p, float4 v, int valid) {
+// default-policy store: y (read back by the mix while still in L2), remote inbox
+__device__ __forceinline__ void st4(float* p, float4 v, int valid) {
   if (valid == 4) {
     *reinterpret_cast<float4*>(p) = v;
   } else {
@@ -148,7 +144,7 @@ __device__ __forceinline__ bool nonfinite4(float4 g) {
 struct Meta {
   const int64_t* bnd;   // [k+1]
   const int32_t* t0;    // [k+1]
-  const int32_t* dstl;  // [k][n_loc] global receiver of local worker r in segment s (or global table)
+  const int32_t* dstl;  // [k][n_loc] global receiver of local worker r in segment s
   bool dst_global;
 };
 
@@ -182,16 +178,14 @@ __device__ __forceinline__ void receiver_of(const PeerKernelArgs& a, const Meta&
   rl = recv - rp * s.n_loc;
 }
 
-__device__ __forceinline__ uint32_t tile_bytes(const Unit& U) { return (uint32_t)(((U.len + 3) & ~3) * 4); }
+__device__ __forceinline__ int wave_of(int u, int n_units, int waves) {
+  return (int)(((int64_t)u * waves) / n_units);
+}
 
-__global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKernelArgs a) {
+__global__ void __launch_bounds__(kPeerThreads, 2) k_gossip_peer(const PeerKernelArgs a) {
   extern __shared__ __align__(128) float smem_f[];
-  float* ringA = smem_f;                                   // [kStagesA][3][kPeerTile]
-  float* ringY = ringA + (size_t)kStagesA * 3 * kPeerTile; // [kSlotsY][kPeerTile]
-  float* ringB = ringY + (size_t)kSlotsY * kPeerTile;      // [kStagesB][kPeerTile]
+  float* ringA = smem_f;  // [kStagesA][3][kPeerTile]
   __shared__ uint64_t a_full[kStagesA], a_empty[kStagesA];
-  __shared__ uint64_t b_full[kStagesB], b_empty[kStagesB];
-  __shared__ uint64_t pushed[kSlotsY];
   __shared__ int s_timeout;
 
   const PeerStepArgs& s = a.s;
@@ -200,12 +194,13 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
   char* mine = a.peers[s.rank];
   const int n_units = a.n_tiles * s.n_loc;
   const int G = gridDim.x;
+  const int W = a.waves;
   const int n_my = blockIdx.x < n_units ? (n_units - blockIdx.x + G - 1) / G : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   volatile int* timeout = &s_timeout;
 
   // ---- metadata into shared memory --------------------------------------------------
-  int64_t* bnd = reinterpret_cast<int64_t*>(ringB + (size_t)kStagesB * kPeerTile);
+  int64_t* bnd = reinterpret_cast<int64_t*>(ringA + (size_t)kStagesA * 3 * kPeerTile);
   int32_t* t0 = reinterpret_cast<int32_t*>(bnd + s.k + 1);
   int32_t* dstl = t0 + s.k + 1;
   Meta M;
@@ -228,18 +223,13 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
       ptx::mbar_init(&a_full[i], 1);
       ptx::mbar_init(&a_empty[i], kCompute / 32);
     }
-    for (int i = 0; i < kStagesB; ++i) {
-      ptx::mbar_init(&b_full[i], 1);
-      ptx::mbar_init(&b_empty[i], kCompute / 32);
-    }
-    for (int i = 0; i < kSlotsY; ++i) ptx::mbar_init(&pushed[i], kCompute / 32);
     ptx::mbar_fence_init();
   }
   __syncthreads();
   // ping-pong safety: every receiver finished epoch e-2, the last reader of this parity
   if (threadIdx.x < s.nprocs && e >= 3) {
     const uint32_t* done = reinterpret_cast<const uint32_t*>(mine + a.off_done);
-    if (!spin_until(done + threadIdx.x, e - 2)) atomicOr(&s_timeout, 1);
+    if (!wait_acquire(done + threadIdx.x, e - 2)) atomicOr(&s_timeout, 1);
   }
   __syncthreads();
 
@@ -247,79 +237,103 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
     // ---------------- compute warps ---------------------------------------------
     bool bad = false;
     const int tid = threadIdx.x;
-    int cur_push = 0, cur_mix = 0;
-    for (int i = 0; i < n_my + kLag && !*timeout; ++i) {
-      if (i < n_my) {  // push unit i
-        const Unit U = unit_at(a, M, blockIdx.x + i * G, cur_push);
-        const int st = i % kStagesA;
-        while (!ptx::mbar_try(&a_full[st], (uint32_t)((i / kStagesA) & 1)) && !*timeout) {
-        }
-        if (*timeout) break;
-        const float* bx = ringA + (size_t)st * 3 * kPeerTile;
-        float4* yslot = reinterpret_cast<float4*>(ringY + (size_t)(i % kSlotsY) * kPeerTile);
-        int rp, rl;
-        receiver_of(a, M, U.seg, U.r, rp, rl);
-        float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
-        const int64_t rowoff = (int64_t)U.r * s.ld;
-#pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-          const int v = tid + q * kCompute;
-          const int valid = U.len - 4 * v;
-          if (valid > 0) {
-            const int vv = valid < 4 ? valid : 4;
-            const float4 cx = reinterpret_cast<const float4*>(bx)[v];
-            const float4 cm = reinterpret_cast<const float4*>(bx + kPeerTile)[v];
-            const float4 cg = reinterpret_cast<const float4*>(bx + 2 * kPeerTile)[v];
-            bad |= nonfinite4(cg);
-            const float4 mn = mom4(cm, cg, s.mu);
-            const float4 y = sgd4(cx, mn, s.lr);
-            const int64_t j = U.c0 + 4 * (int64_t)v;
-            st4(s.m + rowoff + j, mn, vv);
-            st4_remote(inbox + j, y, vv);
-            yslot[v] = y;
+    const uint32_t expect = e * (uint32_t)G * (uint32_t)s.nprocs;  // arrivals per wave, cumulative
+    int ip = 0, cur_push = 0;  // push cursor (unit index i of this CTA)
+    int im = 0, cur_mix = 0;   // mix cursor
+    for (int w = 0; w <= W && !*timeout; ++w) {
+      if (w < W) {
+        // ---- push every unit of wave w
+        for (; ip < n_my && wave_of(blockIdx.x + ip * G, n_units, W) == w; ++ip) {
+          const Unit U = unit_at(a, M, blockIdx.x + ip * G, cur_push);
+          const int st = ip % kStagesA;
+          while (!ptx::mbar_try(&a_full[st], (uint32_t)((ip / kStagesA) & 1)) && !*timeout) {
           }
+          if (*timeout) break;
+          const float* bx = ringA + (size_t)st * 3 * kPeerTile;
+          int rp, rl;
+          receiver_of(a, M, U.seg, U.r, rp, rl);
+          float* inbox =
+              reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
+          const int64_t rowoff = (int64_t)U.r * s.ld;
+#pragma unroll
+          for (int q = 0; q < kPer; ++q) {
+            const int v = tid + q * kCompute;
+            const int valid = U.len - 4 * v;
+            if (valid > 0) {
+              const int vv = valid < 4 ? valid : 4;
+              const float4 cx = reinterpret_cast<const float4*>(bx)[v];
+              const float4 cm = reinterpret_cast<const float4*>(bx + kPeerTile)[v];
+              const float4 cg = reinterpret_cast<const float4*>(bx + 2 * kPeerTile)[v];
+              bad |= nonfinite4(cg);
+              const float4 mn = mom4(cm, cg, s.mu);
+              const float4 y = sgd4(cx, mn, s.lr);
+              const int64_t j = U.c0 + 4 * (int64_t)v;
+              st4_cs(s.m + rowoff + j, mn, vv);
+              st4(s.x + rowoff + j, y, vv);  // y, read back by this thread's mix
+              st4(inbox + j, y, vv);         // NVLink push
+            }
+          }
+          if (U.first_tile && tid == 0) {
+            float* wbox =
+                reinterpret_cast<float*>(a.peers[rp] + a.off_wbox) + ((int64_t)par * s.n_loc + rl) * s.k;
+            wbox[U.seg] = s.psw[(int64_t)U.r * s.k + U.seg];
+          }
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&a_empty[st]);
         }
-        if (U.first_tile && tid == 0) {
-          float* wbox = reinterpret_cast<float*>(a.peers[rp] + a.off_wbox) + ((int64_t)par * s.n_loc + rl) * s.k;
-          wbox[U.seg] = s.psw[(int64_t)U.r * s.k + U.seg];
-        }
-        __syncwarp();
-        if (lane == 0) {
-          ptx::mbar_arrive(&a_empty[st]);
-          ptx::mbar_arrive(&pushed[i % kSlotsY]);
+        // ---- release wave w to every GPU: one system fence for the whole wave
+        ptx::named_bar_sync(1, kCompute);
+        if (tid < s.nprocs) {  // lanes of warp 0: one fence instruction, then the arrivals
+          ptx::fence_acq_rel_sys();
+          uint32_t* cnt = reinterpret_cast<uint32_t*>(a.peers[tid] + a.off_wave) + w;
+          ptx::red_add_relaxed_sys(cnt, 1u);
         }
       }
-      if (i >= kLag) {  // mix unit j
-        const int j = i - kLag;
-        const Unit U = unit_at(a, M, blockIdx.x + j * G, cur_mix);
-        const int sb = j % kStagesB;
-        while (!ptx::mbar_try(&b_full[sb], (uint32_t)((j / kStagesB) & 1)) && !*timeout) {
+      if (w >= 1) {
+        // ---- mix every unit of wave w-1
+        const int v = w - 1;
+        if (tid == 0 && a.mode != 2) {
+          const uint32_t* cnt = reinterpret_cast<const uint32_t*>(mine + a.off_wave) + v;
+          if (!wait_acquire(cnt, expect)) *timeout = 1;
         }
+        ptx::named_bar_sync(1, kCompute);
         if (*timeout) break;
-        const float4* yslot = reinterpret_cast<const float4*>(ringY + (size_t)(j % kSlotsY) * kPeerTile);
-        const float4* yin = reinterpret_cast<const float4*>(ringB + (size_t)sb * kPeerTile);
-        const int64_t rowoff = (int64_t)U.r * s.ld;
+        for (; im < n_my && wave_of(blockIdx.x + im * G, n_units, W) == v; ++im) {
+          const Unit U = unit_at(a, M, blockIdx.x + im * G, cur_mix);
+          const float* inbox =
+              reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * s.n_loc + U.r) * s.ld;
+          const int64_t rowoff = (int64_t)U.r * s.ld;
+          float4 yo[kPer], yi[kPer];
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-          const int v = tid + q * kCompute;
-          const int valid = U.len - 4 * v;
-          if (valid > 0) {
-            const int64_t jj = U.c0 + 4 * (int64_t)v;
-            st4(s.x + rowoff + jj, mean4(yslot[v], yin[v]), valid < 4 ? valid : 4);
+          for (int q = 0; q < kPer; ++q) {
+            const int vv = tid + q * kCompute;
+            if (U.len - 4 * vv > 0) {
+              const int64_t j = U.c0 + 4 * (int64_t)vv;
+              yo[q] = *reinterpret_cast<const float4*>(s.x + rowoff + j);
+              yi[q] = __ldcg(reinterpret_cast<const float4*>(inbox + j));
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kPer; ++q) {
+            const int vv = tid + q * kCompute;
+            const int valid = U.len - 4 * vv;
+            if (valid > 0) {
+              const int64_t j = U.c0 + 4 * (int64_t)vv;
+              st4_cs(s.x + rowoff + j, mean4(yo[q], yi[q]), valid < 4 ? valid : 4);
+            }
+          }
+          if (U.first_tile && tid == 0) {
+            const float* wbox =
+                reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * s.n_loc + U.r) * s.k;
+            float* wp = s.psw + (int64_t)U.r * s.k + U.seg;
+            *wp = __fmul_rn(__fadd_rn(*wp, __ldcg(wbox + U.seg)), 0.5f);
           }
         }
-        if (U.first_tile && tid == 0) {
-          const float* wbox = reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * s.n_loc + U.r) * s.k;
-          float* w = s.psw + (int64_t)U.r * s.k + U.seg;
-          *w = __fmul_rn(__fadd_rn(*w, __ldcg(wbox + U.seg)), 0.5f);
-        }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&b_empty[sb]);
       }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(s.err + kErrDiverged, 1);
-  } else if (warp == kCompute / 32) {
-    // ---------------- load warp: x, m, g tiles ahead -------------------------------
+  } else {
+    // ---------------- load warp: x, m, g tiles of the next units ---------------------
     if (lane == 0) {
       int cur = 0;
       for (int i = 0; i < n_my && !*timeout; ++i) {
@@ -328,77 +342,13 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
         while (!ptx::mbar_try(&a_empty[st], (uint32_t)(((i / kStagesA) & 1) ^ 1)) && !*timeout) {
         }
         if (*timeout) break;
-        const uint32_t bytes = tile_bytes(U);
+        const uint32_t bytes = (uint32_t)(((U.len + 3) & ~3) * 4);
         const int64_t off = (int64_t)U.r * s.ld + U.c0;
         float* buf = ringA + (size_t)st * 3 * kPeerTile;
         ptx::mbar_arrive_expect_tx(&a_full[st], 3 * bytes);
         ptx::bulk_g2s(buf, s.x + off, bytes, &a_full[st]);
         ptx::bulk_g2s(buf + kPeerTile, s.m + off, bytes, &a_full[st]);
         ptx::bulk_g2s(buf + 2 * kPeerTile, s.g + off, bytes, &a_full[st]);
-      }
-    }
-    __syncwarp();
-  } else {
-    // ---------------- signal warp: flags out, flags in, inbox tiles ---------------
-    if (lane == 0) {
-      int nrel = 0, nacq = 0, cur_rel = 0, cur_acq = 0;
-      uint64_t tstall = 0;
-      while (nacq < n_my) {
-        bool progress = false;
-        // release every unit the compute warps have pushed: one system fence per batch
-        int cnt = 0;
-        while (nrel + cnt < n_my && cnt < kSlotsY &&
-               ptx::mbar_test(&pushed[(nrel + cnt) % kSlotsY], (uint32_t)(((nrel + cnt) / kSlotsY) & 1)))
-          ++cnt;
-        if (cnt > 0) {
-          ptx::fence_acq_rel_sys();
-          for (int c = 0; c < cnt; ++c) {
-            const Unit U = unit_at(a, M, blockIdx.x + (nrel + c) * G, cur_rel);
-            int rp, rl;
-            receiver_of(a, M, U.seg, U.r, rp, rl);
-            uint32_t* flag =
-                reinterpret_cast<uint32_t*>(a.peers[rp] + a.off_flags) + (int64_t)U.tile * s.n_loc + rl;
-            ptx::st_relaxed_sys(flag, e);
-          }
-          nrel += cnt;
-          progress = true;
-        }
-        // acquire inbound units whose flag is set and whose B slot is free: one fence per batch
-        int got = 0;
-        int cur_probe = cur_acq;
-        while (nacq + got < nrel && got < kStagesB &&
-               ptx::mbar_test(&b_empty[(nacq + got) % kStagesB], (uint32_t)((((nacq + got) / kStagesB) & 1) ^ 1))) {
-          const Unit U = unit_at(a, M, blockIdx.x + (nacq + got) * G, cur_probe);
-          const uint32_t* flag =
-              reinterpret_cast<const uint32_t*>(mine + a.off_flags) + (int64_t)U.tile * s.n_loc + U.r;
-          if (a.mode != 2 && (int32_t)(ptx::ld_relaxed_sys(flag) - e) < 0) break;
-          ++got;
-        }
-        if (got > 0) {
-          ptx::fence_acq_rel_sys();
-          ptx::fence_proxy_async_global();
-          for (int c = 0; c < got; ++c) {
-            const Unit U = unit_at(a, M, blockIdx.x + (nacq + c) * G, cur_acq);
-            const int sb = (nacq + c) % kStagesB;
-            const uint32_t bytes = tile_bytes(U);
-            const float* src = reinterpret_cast<const float*>(mine + a.off_inbox) +
-                               ((int64_t)par * s.n_loc + U.r) * s.ld + U.c0;
-            ptx::mbar_arrive_expect_tx(&b_full[sb], bytes);
-            ptx::bulk_g2s(ringB + (size_t)sb * kPeerTile, src, bytes, &b_full[sb]);
-          }
-          nacq += got;
-          progress = true;
-        }
-        if (progress) {
-          tstall = 0;
-        } else {
-          const uint64_t now = ptx::globaltimer();
-          if (tstall == 0) tstall = now;
-          if (now - tstall > kSpinLimitNs) {  // give up: the other warps poll s_timeout
-            *timeout = 1;
-            break;
-          }
-        }
       }
     }
     __syncwarp();
@@ -451,15 +401,22 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   }
   seg_t0[k] = n_tiles;
   p.n_tiles = n_tiles;
+  // waves of ~kWaveBytes of this GPU's traffic (28 B per parameter per local worker)
+  const double bytes = 28.0 * (double)n_loc * (double)d;
+  int waves = (int)(bytes / kWaveBytes + 0.999);
+  if (waves < 2) waves = 2;
+  if (waves > 1024) waves = 1024;
+  p.waves = waves;
   p.off_inbox = 0;
   p.off_wbox = align_up(p.off_inbox + sizeof(float) * 2 * (size_t)n_loc * ld, 256);
-  p.off_flags = align_up(p.off_wbox + sizeof(float) * 2 * (size_t)n_loc * k, 256);
-  p.off_done = align_up(p.off_flags + sizeof(uint32_t) * (size_t)p.n_tiles * n_loc, 256);
+  p.off_wave = align_up(p.off_wbox + sizeof(float) * 2 * (size_t)n_loc * k, 256);
+  p.off_done = align_up(p.off_wave + sizeof(uint32_t) * (size_t)waves, 256);
   p.off_count = align_up(p.off_done + sizeof(uint32_t) * (size_t)nprocs, 256);
+  p.off_flags = p.off_count;  // unused by this protocol
   p.bytes = align_up(p.off_count + 256, 4096);
   cudaError_t e = cudaMalloc(&p.base, p.bytes);
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region cudaMalloc", e);
-  e = cudaMemset(p.base, 0, p.bytes);  // inbox padding is read by 16-byte-rounded bulk copies
+  e = cudaMemset(p.base, 0, p.bytes);
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region memset", e);
   e = cudaMalloc(&p.d_bounds, sizeof(int64_t) * (k + 1));
   if (e == cudaSuccess) e = cudaMalloc(&p.d_seg_t0, sizeof(int32_t) * (k + 1));
@@ -479,7 +436,6 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   p.grid = sms * occ;
   const int n_units = p.n_tiles * n_loc;
   if (p.grid > n_units) p.grid = n_units;
-  if (p.grid < n_loc) return perr(CS_EUNSUPPORTED, "more local workers than resident CTAs", cudaSuccess);
   p.peer_base.assign(nprocs, nullptr);
   p.peer_base[rank] = p.base;
   p.allocated = true;
@@ -566,11 +522,12 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   ka.bounds = p.d_bounds;
   ka.seg_t0 = p.d_seg_t0;
   ka.n_tiles = p.n_tiles;
+  ka.waves = p.waves;
   ka.epoch = ++p.epoch;
   ka.mode = p.mode;
   ka.off_inbox = p.off_inbox;
   ka.off_wbox = p.off_wbox;
-  ka.off_flags = p.off_flags;
+  ka.off_wave = p.off_wave;
   ka.off_done = p.off_done;
   ka.off_count = p.off_count;
   void* args[] = {&ka};

@@ -32,6 +32,8 @@ struct PeerState {
   int64_t ld = 0;
   int tile = 0;          // elements per tile (multiple of 32)
   int mode = 0;          // CS_PEER_MODE diagnostics: 0 normal, 1 local-only, 2 no waits
+  int waves = 0;         // push/mix waves per step
+  size_t off_wave = 0;   // per-wave arrival counters [waves]
   int n_tiles = 0;
   int grid = 0;
   size_t bytes = 0;
