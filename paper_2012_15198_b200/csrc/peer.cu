@@ -5,27 +5,28 @@
 // co-resident).  The work unit is (tile q, local worker r): a segment-aligned
 // range of up to kPeerTile columns of one worker's vector, numbered tile-major
 // (u = q * n_loc + r); CTA c takes units c, c + G, c + 2G, ... on every GPU.
-// The units are cut into W "waves" of ~64 MB of traffic, the same on every GPU.
+// Units are cut into waves of exactly G*m units (m per CTA, G*m a multiple of
+// n_loc so a tile never straddles two waves), the same on every GPU.
 //
-// Per CTA, wave-pipelined:
+// Warp-specialised CTA:
 //
-//   push wave w   for each of its units: m', y from x, m, g (a3), the tiles
-//                 streamed into shared memory by a bulk-TMA load warp; m' -> HBM;
-//                 y -> x (kept in L2 for the mix) and -> the RECEIVER's inbox on
-//                 the receiver's GPU (NVLink store; Alg.1 l.7 isend to
+//   load warp     bulk-TMA of the x, m, g row-tiles of the next units into a
+//                 kStagesA-deep shared-memory ring.
+//   push warps    wave w: for each unit, m', y from the staged tiles (a3); m' ->
+//                 HBM; y -> x (kept in L2 for the mix) and -> the RECEIVER's
+//                 inbox on the receiver's GPU (NVLink store; Alg.1 l.7 isend to
 //                 send_to = dst_s(i)); the first tile of a
-//                 segment also pushes w_{i,s}.  Then ONE fence.acq_rel.sys and a
+//                 segment also pushes w_{i,s}.  Then one fence.acq_rel.sys and a
 //                 red.add on every GPU's arrival counter of wave w (the irecv
 //                 completion, Alg.1 l.14, for a whole wave at once).
-//   mix wave w-1  wait until this GPU's counter of wave w-1 has every CTA of every
-//                 GPU (Alg.1 l.12-14 "wait send and recv"), then
-//                 x = (y + inbox) * 0.5, w = (w + wbox) * 0.5 (a5, Alg.1 l.17);
-//                 y and inbox of a wave are still L2-resident, so the effective
-//                 HBM traffic stays near the 28 B/param of a fused pass.
+//   mix warps     wave w: wait until this GPU's counter of wave w has every CTA
+//                 of every GPU (Alg.1 l.12-14 "wait send and recv"), then
+//                 x = (y + inbox) * 0.5, w = (w + wbox) * 0.5 (a5, Alg.1 l.17).
+//                 y and inbox of a wave are still L2-resident.
 //
-// Deadlock freedom: pushes never wait on another GPU; to push wave w a CTA has
-// mixed wave w-2, which needs every CTA's push of wave w-2; all CTAs are
-// resident, so by induction on w every wave completes.
+// The NVLink-bound pushes of wave w overlap the HBM-bound mixes of earlier
+// waves.  Deadlock freedom: push warps never wait on another GPU (only on their
+// own TMA ring), mix warps only wait for pushes, and all CTAs are resident.
 //
 // The inbox ping-pongs on step parity; before pushing at epoch e a GPU waits
 // until every peer has finished epoch e-2 (the last reader of that parity) —
@@ -58,16 +59,17 @@ int perr(int code, const char* what, cudaError_t e) {
   return code;
 }
 
-constexpr int kCompute = 256;                   // 8 compute warps
-constexpr int kPeerThreads = kCompute + 32;     // + bulk-TMA load warp
+constexpr int kGroup = 128;                     // threads per warp group (push / mix)
+constexpr int kPeerThreads = 2 * kGroup + 32;   // push warps, mix warps, bulk-TMA load warp
 constexpr int kPeerTile = 2048;                 // columns per unit: 8 KB of one worker's row
-constexpr int kPer = kPeerTile / 4 / kCompute;  // float4 per compute thread per array
+constexpr int kPer = kPeerTile / 4 / kGroup;    // float4 per thread per array
 constexpr int kStagesA = 4;                     // x, m, g ring depth (units)
 constexpr size_t kTileBytes = sizeof(float) * kPeerTile;
 constexpr size_t kRingBytes = kTileBytes * 3 * kStagesA;
 constexpr int kMaxDstSmem = 2048;               // receivers table in smem when k*n_loc <= this
-constexpr double kWaveBytes = 64.0 * 1024 * 1024;
+constexpr double kWaveBytes = 48.0 * 1024 * 1024;
 constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
+constexpr int kBarPush = 1, kBarMix = 2;        // named barrier ids
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -97,6 +99,7 @@ struct PeerKernelArgs {
   const int32_t* seg_t0;    // [k+1] first tile of each segment (seg_t0[k] = n_tiles)
   int n_tiles;
   int waves;
+  int per_wave;             // m: units per CTA per wave
   uint32_t epoch;           // this step's epoch (>= 1)
   int mode;                 // 0 normal; diagnostics (wrong results): 1 local-only, 2 no waits
   size_t off_inbox, off_wbox, off_wave, off_done, off_count;
@@ -114,7 +117,7 @@ __device__ __forceinline__ float4 mean4(float4 a, float4 b) {
   return make_float4(__fmul_rn(__fadd_rn(a.x, b.x), 0.5f), __fmul_rn(__fadd_rn(a.y, b.y), 0.5f),
                      __fmul_rn(__fadd_rn(a.z, b.z), 0.5f), __fmul_rn(__fadd_rn(a.w, b.w), 0.5f));
 }
-// streaming store (evict-first): for data not read again this step
+// streaming store (evict-first): data not read again this step
 __device__ __forceinline__ void st4_cs(float* p, float4 v, int valid) {
   if (valid == 4) {
     __stcs(reinterpret_cast<float4*>(p), v);
@@ -178,11 +181,7 @@ __device__ __forceinline__ void receiver_of(const PeerKernelArgs& a, const Meta&
   rl = recv - rp * s.n_loc;
 }
 
-__device__ __forceinline__ int wave_of(int u, int n_units, int waves) {
-  return (int)(((int64_t)u * waves) / n_units);
-}
-
-__global__ void __launch_bounds__(kPeerThreads, 2) k_gossip_peer(const PeerKernelArgs a) {
+__global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKernelArgs a) {
   extern __shared__ __align__(128) float smem_f[];
   float* ringA = smem_f;  // [kStagesA][3][kPeerTile]
   __shared__ uint64_t a_full[kStagesA], a_empty[kStagesA];
@@ -194,7 +193,7 @@ __global__ void __launch_bounds__(kPeerThreads, 2) k_gossip_peer(const PeerKerne
   char* mine = a.peers[s.rank];
   const int n_units = a.n_tiles * s.n_loc;
   const int G = gridDim.x;
-  const int W = a.waves;
+  const int W = a.waves, m_per = a.per_wave;
   const int n_my = blockIdx.x < n_units ? (n_units - blockIdx.x + G - 1) / G : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   volatile int* timeout = &s_timeout;
@@ -221,7 +220,7 @@ __global__ void __launch_bounds__(kPeerThreads, 2) k_gossip_peer(const PeerKerne
     s_timeout = 0;
     for (int i = 0; i < kStagesA; ++i) {
       ptx::mbar_init(&a_full[i], 1);
-      ptx::mbar_init(&a_empty[i], kCompute / 32);
+      ptx::mbar_init(&a_empty[i], kGroup / 32);
     }
     ptx::mbar_fence_init();
   }
@@ -233,105 +232,103 @@ __global__ void __launch_bounds__(kPeerThreads, 2) k_gossip_peer(const PeerKerne
   }
   __syncthreads();
 
-  if (warp < kCompute / 32) {
-    // ---------------- compute warps ---------------------------------------------
+  if (warp < kGroup / 32) {
+    // ---------------- push warps ------------------------------------------------
     bool bad = false;
     const int tid = threadIdx.x;
-    const uint32_t expect = e * (uint32_t)G * (uint32_t)s.nprocs;  // arrivals per wave, cumulative
-    int ip = 0, cur_push = 0;  // push cursor (unit index i of this CTA)
-    int im = 0, cur_mix = 0;   // mix cursor
-    for (int w = 0; w <= W && !*timeout; ++w) {
-      if (w < W) {
-        // ---- push every unit of wave w
-        for (; ip < n_my && wave_of(blockIdx.x + ip * G, n_units, W) == w; ++ip) {
-          const Unit U = unit_at(a, M, blockIdx.x + ip * G, cur_push);
-          const int st = ip % kStagesA;
-          while (!ptx::mbar_try(&a_full[st], (uint32_t)((ip / kStagesA) & 1)) && !*timeout) {
-          }
-          if (*timeout) break;
-          const float* bx = ringA + (size_t)st * 3 * kPeerTile;
-          int rp, rl;
-          receiver_of(a, M, U.seg, U.r, rp, rl);
-          float* inbox =
-              reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
-          const int64_t rowoff = (int64_t)U.r * s.ld;
-#pragma unroll
-          for (int q = 0; q < kPer; ++q) {
-            const int v = tid + q * kCompute;
-            const int valid = U.len - 4 * v;
-            if (valid > 0) {
-              const int vv = valid < 4 ? valid : 4;
-              const float4 cx = reinterpret_cast<const float4*>(bx)[v];
-              const float4 cm = reinterpret_cast<const float4*>(bx + kPeerTile)[v];
-              const float4 cg = reinterpret_cast<const float4*>(bx + 2 * kPeerTile)[v];
-              bad |= nonfinite4(cg);
-              const float4 mn = mom4(cm, cg, s.mu);
-              const float4 y = sgd4(cx, mn, s.lr);
-              const int64_t j = U.c0 + 4 * (int64_t)v;
-              st4_cs(s.m + rowoff + j, mn, vv);
-              st4(s.x + rowoff + j, y, vv);  // y, read back by this thread's mix
-              st4(inbox + j, y, vv);         // NVLink push
-            }
-          }
-          if (U.first_tile && tid == 0) {
-            float* wbox =
-                reinterpret_cast<float*>(a.peers[rp] + a.off_wbox) + ((int64_t)par * s.n_loc + rl) * s.k;
-            wbox[U.seg] = s.psw[(int64_t)U.r * s.k + U.seg];
-          }
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&a_empty[st]);
+    int cur = 0;
+    for (int w = 0; w < W; ++w) {
+      const int i_end = (w + 1) * m_per < n_my ? (w + 1) * m_per : n_my;
+      for (int i = w * m_per; i < i_end && !*timeout; ++i) {
+        const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
+        const int st = i % kStagesA;
+        while (!ptx::mbar_try(&a_full[st], (uint32_t)((i / kStagesA) & 1)) && !*timeout) {
         }
-        // ---- release wave w to every GPU: one system fence for the whole wave
-        ptx::named_bar_sync(1, kCompute);
-        if (tid < s.nprocs) {  // lanes of warp 0: one fence instruction, then the arrivals
-          ptx::fence_acq_rel_sys();
-          uint32_t* cnt = reinterpret_cast<uint32_t*>(a.peers[tid] + a.off_wave) + w;
-          ptx::red_add_relaxed_sys(cnt, 1u);
-        }
-      }
-      if (w >= 1) {
-        // ---- mix every unit of wave w-1
-        const int v = w - 1;
-        if (tid == 0 && a.mode != 2) {
-          const uint32_t* cnt = reinterpret_cast<const uint32_t*>(mine + a.off_wave) + v;
-          if (!wait_acquire(cnt, expect)) *timeout = 1;
-        }
-        ptx::named_bar_sync(1, kCompute);
         if (*timeout) break;
-        for (; im < n_my && wave_of(blockIdx.x + im * G, n_units, W) == v; ++im) {
-          const Unit U = unit_at(a, M, blockIdx.x + im * G, cur_mix);
-          const float* inbox =
-              reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * s.n_loc + U.r) * s.ld;
-          const int64_t rowoff = (int64_t)U.r * s.ld;
-          float4 yo[kPer], yi[kPer];
+        const float* bx = ringA + (size_t)st * 3 * kPeerTile;
+        int rp, rl;
+        receiver_of(a, M, U.seg, U.r, rp, rl);
+        float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
+        const int64_t rowoff = (int64_t)U.r * s.ld;
 #pragma unroll
-          for (int q = 0; q < kPer; ++q) {
-            const int vv = tid + q * kCompute;
-            if (U.len - 4 * vv > 0) {
-              const int64_t j = U.c0 + 4 * (int64_t)vv;
-              yo[q] = *reinterpret_cast<const float4*>(s.x + rowoff + j);
-              yi[q] = __ldcg(reinterpret_cast<const float4*>(inbox + j));
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < kPer; ++q) {
-            const int vv = tid + q * kCompute;
-            const int valid = U.len - 4 * vv;
-            if (valid > 0) {
-              const int64_t j = U.c0 + 4 * (int64_t)vv;
-              st4_cs(s.x + rowoff + j, mean4(yo[q], yi[q]), valid < 4 ? valid : 4);
-            }
-          }
-          if (U.first_tile && tid == 0) {
-            const float* wbox =
-                reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * s.n_loc + U.r) * s.k;
-            float* wp = s.psw + (int64_t)U.r * s.k + U.seg;
-            *wp = __fmul_rn(__fadd_rn(*wp, __ldcg(wbox + U.seg)), 0.5f);
+        for (int q = 0; q < kPer; ++q) {
+          const int v = tid + q * kGroup;
+          const int valid = U.len - 4 * v;
+          if (valid > 0) {
+            const int vv = valid < 4 ? valid : 4;
+            const float4 cx = reinterpret_cast<const float4*>(bx)[v];
+            const float4 cm = reinterpret_cast<const float4*>(bx + kPeerTile)[v];
+            const float4 cg = reinterpret_cast<const float4*>(bx + 2 * kPeerTile)[v];
+            bad |= nonfinite4(cg);
+            const float4 mn = mom4(cm, cg, s.mu);
+            const float4 y = sgd4(cx, mn, s.lr);
+            const int64_t j = U.c0 + 4 * (int64_t)v;
+            st4_cs(s.m + rowoff + j, mn, vv);
+            st4(s.x + rowoff + j, y, vv);  // y, read back by the mix warps from L2
+            st4(inbox + j, y, vv);         // NVLink push
           }
         }
+        if (U.first_tile && tid == 0) {
+          float* wbox = reinterpret_cast<float*>(a.peers[rp] + a.off_wbox) + ((int64_t)par * s.n_loc + rl) * s.k;
+          wbox[U.seg] = s.psw[(int64_t)U.r * s.k + U.seg];
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&a_empty[st]);
+      }
+      // release wave w to every GPU: one system fence for the whole wave
+      ptx::named_bar_sync(kBarPush, kGroup);
+      if (tid < s.nprocs) {  // lanes of warp 0: one fence instruction, then the arrivals
+        ptx::fence_acq_rel_sys();
+        uint32_t* cnt = reinterpret_cast<uint32_t*>(a.peers[tid] + a.off_wave) + w;
+        ptx::red_add_relaxed_sys(cnt, 1u);
       }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(s.err + kErrDiverged, 1);
+  } else if (warp < 2 * kGroup / 32) {
+    // ---------------- mix warps -------------------------------------------------
+    const int tid = threadIdx.x - kGroup;
+    const uint32_t expect = e * (uint32_t)G * (uint32_t)s.nprocs;  // arrivals per wave, cumulative
+    int cur = 0;
+    for (int w = 0; w < W; ++w) {
+      if (tid == 0 && a.mode != 2) {
+        const uint32_t* cnt = reinterpret_cast<const uint32_t*>(mine + a.off_wave) + w;
+        if (!wait_acquire(cnt, expect)) *timeout = 1;
+      }
+      ptx::named_bar_sync(kBarMix, kGroup);
+      if (*timeout) break;
+      const int i_end = (w + 1) * m_per < n_my ? (w + 1) * m_per : n_my;
+      for (int i = w * m_per; i < i_end; ++i) {
+        const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
+        const float* inbox =
+            reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * s.n_loc + U.r) * s.ld;
+        const int64_t rowoff = (int64_t)U.r * s.ld;
+        float4 yo[kPer], yi[kPer];
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+          const int vv = tid + q * kGroup;
+          if (U.len - 4 * vv > 0) {
+            const int64_t j = U.c0 + 4 * (int64_t)vv;
+            yo[q] = __ldcg(reinterpret_cast<const float4*>(s.x + rowoff + j));
+            yi[q] = __ldcg(reinterpret_cast<const float4*>(inbox + j));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+          const int vv = tid + q * kGroup;
+          const int valid = U.len - 4 * vv;
+          if (valid > 0) {
+            const int64_t j = U.c0 + 4 * (int64_t)vv;
+            st4_cs(s.x + rowoff + j, mean4(yo[q], yi[q]), valid < 4 ? valid : 4);
+          }
+        }
+        if (U.first_tile && tid == 0) {
+          const float* wbox =
+              reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * s.n_loc + U.r) * s.k;
+          float* wp = s.psw + (int64_t)U.r * s.k + U.seg;
+          *wp = __fmul_rn(__fadd_rn(*wp, __ldcg(wbox + U.seg)), 0.5f);
+        }
+      }
+    }
   } else {
     // ---------------- load warp: x, m, g tiles of the next units ---------------------
     if (lane == 0) {
@@ -372,6 +369,15 @@ __global__ void __launch_bounds__(kPeerThreads, 2) k_gossip_peer(const PeerKerne
   }
 }
 
+int gcd_int(int a, int b) {
+  while (b) {
+    const int t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
 }  // namespace
 
 const char* peer_error() { return g_peer_err.c_str(); }
@@ -401,20 +407,35 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   }
   seg_t0[k] = n_tiles;
   p.n_tiles = n_tiles;
-  // waves of ~kWaveBytes of this GPU's traffic (28 B per parameter per local worker)
-  const double bytes = 28.0 * (double)n_loc * (double)d;
-  int waves = (int)(bytes / kWaveBytes + 0.999);
-  if (waves < 2) waves = 2;
-  if (waves > 1024) waves = 1024;
-  p.waves = waves;
+
+  const size_t smem = peer_smem_bytes(k, n_loc);
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaFuncSetAttribute(k_gossip_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return perr(CS_ECUDA, "smem attribute", e);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gossip_peer, kPeerThreads, smem);
+  if (e != cudaSuccess || occ < 1) return perr(CS_ECUDA, "occupancy", e);
+  p.grid = sms * occ;
+  const int n_units = p.n_tiles * n_loc;
+  if (p.grid > n_units) p.grid = n_units;
+  // waves of G*m units, G*m a multiple of n_loc (tiles never straddle waves), ~kWaveBytes each
+  const int step_m = n_loc / gcd_int(p.grid, n_loc);
+  const double unit_bytes = 28.0 * kPeerTile;
+  int m = (int)(kWaveBytes / unit_bytes / p.grid + 0.5);
+  if (m < 1) m = 1;
+  m = (m + step_m - 1) / step_m * step_m;
+  p.per_wave = m;
+  p.waves = (n_units + p.grid * m - 1) / (p.grid * m);
+
   p.off_inbox = 0;
   p.off_wbox = align_up(p.off_inbox + sizeof(float) * 2 * (size_t)n_loc * ld, 256);
   p.off_wave = align_up(p.off_wbox + sizeof(float) * 2 * (size_t)n_loc * k, 256);
-  p.off_done = align_up(p.off_wave + sizeof(uint32_t) * (size_t)waves, 256);
+  p.off_done = align_up(p.off_wave + sizeof(uint32_t) * (size_t)p.waves, 256);
   p.off_count = align_up(p.off_done + sizeof(uint32_t) * (size_t)nprocs, 256);
   p.off_flags = p.off_count;  // unused by this protocol
   p.bytes = align_up(p.off_count + 256, 4096);
-  cudaError_t e = cudaMalloc(&p.base, p.bytes);
+  e = cudaMalloc(&p.base, p.bytes);
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region cudaMalloc", e);
   e = cudaMemset(p.base, 0, p.bytes);
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region memset", e);
@@ -425,17 +446,6 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   if (e == cudaSuccess)
     e = cudaMemcpy(p.d_seg_t0, seg_t0.data(), sizeof(int32_t) * (k + 1), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return perr(CS_ECUDA, "tile tables", e);
-  const size_t smem = peer_smem_bytes(k, n_loc);
-  int dev = 0, sms = 0, occ = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaFuncSetAttribute(k_gossip_peer, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return perr(CS_ECUDA, "smem attribute", e);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gossip_peer, kPeerThreads, smem);
-  if (e != cudaSuccess || occ < 1) return perr(CS_ECUDA, "occupancy", e);
-  p.grid = sms * occ;
-  const int n_units = p.n_tiles * n_loc;
-  if (p.grid > n_units) p.grid = n_units;
   p.peer_base.assign(nprocs, nullptr);
   p.peer_base[rank] = p.base;
   p.allocated = true;
@@ -523,6 +533,7 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   ka.seg_t0 = p.d_seg_t0;
   ka.n_tiles = p.n_tiles;
   ka.waves = p.waves;
+  ka.per_wave = p.per_wave;
   ka.epoch = ++p.epoch;
   ka.mode = p.mode;
   ka.off_inbox = p.off_inbox;

@@ -33,6 +33,7 @@ struct PeerState {
   int tile = 0;          // elements per tile (multiple of 32)
   int mode = 0;          // CS_PEER_MODE diagnostics: 0 normal, 1 local-only, 2 no waits
   int waves = 0;         // push/mix waves per step
+  int per_wave = 0;      // units per CTA per wave
   size_t off_wave = 0;   // per-wave arrival counters [waves]
   int n_tiles = 0;
   int grid = 0;
