@@ -60,14 +60,15 @@ int perr(int code, const char* what, cudaError_t e) {
 }
 
 constexpr int kGroup = 128;                     // threads per warp group (push / mix)
-constexpr int kPeerThreads = 2 * kGroup + 32;   // push warps, mix warps, bulk-TMA load warp
+constexpr int kPeerThreads = 2 * kGroup + 64;   // push warps, mix warps, load warp, release warp
+constexpr int kWaveSlots = 8;                   // wave hand-off ring (push warps -> release warp)
 constexpr int kPeerTile = 2048;                 // columns per unit: 8 KB of one worker's row
 constexpr int kPer = kPeerTile / 4 / kGroup;    // float4 per thread per array
 constexpr int kStagesA = 4;                     // x, m, g ring depth (units)
 constexpr size_t kTileBytes = sizeof(float) * kPeerTile;
 constexpr size_t kRingBytes = kTileBytes * 3 * kStagesA;
 constexpr int kMaxDstSmem = 2048;               // receivers table in smem when k*n_loc <= this
-constexpr double kWaveBytes = 48.0 * 1024 * 1024;
+constexpr double kWaveBytes = 24.0 * 1024 * 1024;
 constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
 constexpr int kBarPush = 1, kBarMix = 2;        // named barrier ids
 
@@ -185,7 +186,8 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
   extern __shared__ __align__(128) float smem_f[];
   float* ringA = smem_f;  // [kStagesA][3][kPeerTile]
   __shared__ uint64_t a_full[kStagesA], a_empty[kStagesA];
-  __shared__ int s_timeout;
+  __shared__ uint64_t wave_done[kWaveSlots];
+  __shared__ int s_timeout, s_released;
 
   const PeerStepArgs& s = a.s;
   const uint32_t e = a.epoch;
@@ -218,10 +220,12 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
     }
   if (threadIdx.x == 0) {
     s_timeout = 0;
+    s_released = 0;
     for (int i = 0; i < kStagesA; ++i) {
       ptx::mbar_init(&a_full[i], 1);
       ptx::mbar_init(&a_empty[i], kGroup / 32);
     }
+    for (int i = 0; i < kWaveSlots; ++i) ptx::mbar_init(&wave_done[i], kGroup / 32);
     ptx::mbar_fence_init();
   }
   __syncthreads();
@@ -275,12 +279,13 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&a_empty[st]);
       }
-      // release wave w to every GPU: one system fence for the whole wave
-      ptx::named_bar_sync(kBarPush, kGroup);
-      if (tid < s.nprocs) {  // lanes of warp 0: one fence instruction, then the arrivals
-        ptx::fence_acq_rel_sys();
-        uint32_t* cnt = reinterpret_cast<uint32_t*>(a.peers[tid] + a.off_wave) + w;
-        ptx::red_add_relaxed_sys(cnt, 1u);
+      // hand wave w to the release warp (it fences once and signals every GPU)
+      __syncwarp();
+      if (lane == 0) {
+        volatile int* released = &s_released;
+        while (*released <= w - kWaveSlots && !*timeout) {
+        }
+        ptx::mbar_arrive(&wave_done[w % kWaveSlots]);
       }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(s.err + kErrDiverged, 1);
@@ -297,41 +302,70 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
       ptx::named_bar_sync(kBarMix, kGroup);
       if (*timeout) break;
       const int i_end = (w + 1) * m_per < n_my ? (w + 1) * m_per : n_my;
-      for (int i = w * m_per; i < i_end; ++i) {
-        const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
-        const float* inbox =
-            reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * s.n_loc + U.r) * s.ld;
-        const int64_t rowoff = (int64_t)U.r * s.ld;
-        float4 yo[kPer], yi[kPer];
+      for (int i = w * m_per; i < i_end; i += 2) {  // two units per pass: 4*kPer loads in flight
+        Unit U[2];
+        bool have[2];
+        float4 yo[2][kPer], yi[2][kPer];
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-          const int vv = tid + q * kGroup;
-          if (U.len - 4 * vv > 0) {
-            const int64_t j = U.c0 + 4 * (int64_t)vv;
-            yo[q] = __ldcg(reinterpret_cast<const float4*>(s.x + rowoff + j));
-            yi[q] = __ldcg(reinterpret_cast<const float4*>(inbox + j));
+        for (int h = 0; h < 2; ++h) {
+          have[h] = i + h < i_end;
+          if (!have[h]) continue;
+          U[h] = unit_at(a, M, blockIdx.x + (i + h) * G, cur);
+          const float* inbox =
+              reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * s.n_loc + U[h].r) * s.ld;
+          const int64_t rowoff = (int64_t)U[h].r * s.ld;
+#pragma unroll
+          for (int q = 0; q < kPer; ++q) {
+            const int vv = tid + q * kGroup;
+            if (U[h].len - 4 * vv > 0) {
+              const int64_t j = U[h].c0 + 4 * (int64_t)vv;
+              yo[h][q] = __ldcg(reinterpret_cast<const float4*>(s.x + rowoff + j));
+              yi[h][q] = __ldcg(reinterpret_cast<const float4*>(inbox + j));
+            }
           }
         }
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-          const int vv = tid + q * kGroup;
-          const int valid = U.len - 4 * vv;
-          if (valid > 0) {
-            const int64_t j = U.c0 + 4 * (int64_t)vv;
-            st4_cs(s.x + rowoff + j, mean4(yo[q], yi[q]), valid < 4 ? valid : 4);
+        for (int h = 0; h < 2; ++h) {
+          if (!have[h]) continue;
+          const int64_t rowoff = (int64_t)U[h].r * s.ld;
+#pragma unroll
+          for (int q = 0; q < kPer; ++q) {
+            const int vv = tid + q * kGroup;
+            const int valid = U[h].len - 4 * vv;
+            if (valid > 0) {
+              const int64_t j = U[h].c0 + 4 * (int64_t)vv;
+              st4_cs(s.x + rowoff + j, mean4(yo[h][q], yi[h][q]), valid < 4 ? valid : 4);
+            }
           }
-        }
-        if (U.first_tile && tid == 0) {
-          const float* wbox =
-              reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * s.n_loc + U.r) * s.k;
-          float* wp = s.psw + (int64_t)U.r * s.k + U.seg;
-          *wp = __fmul_rn(__fadd_rn(*wp, __ldcg(wbox + U.seg)), 0.5f);
+          if (U[h].first_tile && tid == 0) {
+            const float* wbox =
+                reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * s.n_loc + U[h].r) * s.k;
+            float* wp = s.psw + (int64_t)U[h].r * s.k + U[h].seg;
+            *wp = __fmul_rn(__fadd_rn(*wp, __ldcg(wbox + U[h].seg)), 0.5f);
+          }
         }
       }
+    }
+  } else if (warp == 2 * kGroup / 32 + 1) {
+    // ---------------- release warp: one fence per wave, then every GPU's counter -------
+    for (int w = 0; w < W; ++w) {
+      if (lane == 0)
+        while (!ptx::mbar_try(&wave_done[w % kWaveSlots], (uint32_t)((w / kWaveSlots) & 1)) && !*timeout) {
+        }
+      __syncwarp();
+      if (*timeout) break;
+      if (lane < s.nprocs) {  // one fence instruction for the warp, then the arrivals
+        ptx::fence_acq_rel_sys();
+        uint32_t* cnt = reinterpret_cast<uint32_t*>(a.peers[lane] + a.off_wave) + w;
+        ptx::red_add_relaxed_sys(cnt, 1u);
+      }
+      __syncwarp();
+      if (lane == 0) *(volatile int*)&s_released = w + 1;
     }
   } else {
     // ---------------- load warp: x, m, g tiles of the next units ---------------------
     if (lane == 0) {
+      const uint64_t pol = ptx::policy_evict_first();
       int cur = 0;
       for (int i = 0; i < n_my && !*timeout; ++i) {
         const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
@@ -343,9 +377,9 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
         const int64_t off = (int64_t)U.r * s.ld + U.c0;
         float* buf = ringA + (size_t)st * 3 * kPeerTile;
         ptx::mbar_arrive_expect_tx(&a_full[st], 3 * bytes);
-        ptx::bulk_g2s(buf, s.x + off, bytes, &a_full[st]);
-        ptx::bulk_g2s(buf + kPeerTile, s.m + off, bytes, &a_full[st]);
-        ptx::bulk_g2s(buf + 2 * kPeerTile, s.g + off, bytes, &a_full[st]);
+        ptx::bulk_g2s_hint(buf, s.x + off, bytes, &a_full[st], pol);
+        ptx::bulk_g2s_hint(buf + kPeerTile, s.m + off, bytes, &a_full[st], pol);
+        ptx::bulk_g2s_hint(buf + 2 * kPeerTile, s.g + off, bytes, &a_full[st], pol);
       }
     }
     __syncwarp();
