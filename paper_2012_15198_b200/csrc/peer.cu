@@ -70,7 +70,7 @@ constexpr size_t kRingBytes = kTileBytes * 3 * kStagesA;
 constexpr int kMaxDstSmem = 2048;               // receivers table in smem when k*n_loc <= this
 constexpr double kWaveBytes = 24.0 * 1024 * 1024;
 constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
-constexpr int kBarPush = 1, kBarMix = 2;        // named barrier ids
+constexpr int kBarMix = 2;                      // named barrier id of the mix warps
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
