@@ -103,6 +103,7 @@ struct PeerKernelArgs {
   int per_wave;             // m: units per CTA per wave
   uint32_t epoch;           // this step's epoch (>= 1)
   int mode;                 // 0 normal; diagnostics (wrong results): 1 local-only, 2 no waits
+  int hint;                 // L2 evict-first policy on the x, m, g bulk loads
   size_t off_inbox, off_wbox, off_wave, off_done, off_count;
 };
 
@@ -377,9 +378,15 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
         const int64_t off = (int64_t)U.r * s.ld + U.c0;
         float* buf = ringA + (size_t)st * 3 * kPeerTile;
         ptx::mbar_arrive_expect_tx(&a_full[st], 3 * bytes);
-        ptx::bulk_g2s_hint(buf, s.x + off, bytes, &a_full[st], pol);
-        ptx::bulk_g2s_hint(buf + kPeerTile, s.m + off, bytes, &a_full[st], pol);
-        ptx::bulk_g2s_hint(buf + 2 * kPeerTile, s.g + off, bytes, &a_full[st], pol);
+        if (a.hint) {
+          ptx::bulk_g2s_hint(buf, s.x + off, bytes, &a_full[st], pol);
+          ptx::bulk_g2s_hint(buf + kPeerTile, s.m + off, bytes, &a_full[st], pol);
+          ptx::bulk_g2s_hint(buf + 2 * kPeerTile, s.g + off, bytes, &a_full[st], pol);
+        } else {
+          ptx::bulk_g2s(buf, s.x + off, bytes, &a_full[st]);
+          ptx::bulk_g2s(buf + kPeerTile, s.m + off, bytes, &a_full[st]);
+          ptx::bulk_g2s(buf + 2 * kPeerTile, s.g + off, bytes, &a_full[st]);
+        }
       }
     }
     __syncwarp();
@@ -456,7 +463,9 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   // waves of G*m units, G*m a multiple of n_loc (tiles never straddle waves), ~kWaveBytes each
   const int step_m = n_loc / gcd_int(p.grid, n_loc);
   const double unit_bytes = 28.0 * kPeerTile;
-  int m = (int)(kWaveBytes / unit_bytes / p.grid + 0.5);
+  const char* wmb = getenv("CS_PEER_WAVE_MB");  // tuning knob
+  const double wave_bytes = wmb ? atof(wmb) * 1024 * 1024 : kWaveBytes;
+  int m = (int)(wave_bytes / unit_bytes / p.grid + 0.5);
   if (m < 1) m = 1;
   m = (m + step_m - 1) / step_m * step_m;
   p.per_wave = m;
@@ -569,7 +578,8 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   ka.waves = p.waves;
   ka.per_wave = p.per_wave;
   ka.epoch = ++p.epoch;
-  ka.mode = p.mode;
+  ka.mode = p.mode & 3;
+  ka.hint = (p.mode & 4) ? 0 : 1;
   ka.off_inbox = p.off_inbox;
   ka.off_wbox = p.off_wbox;
   ka.off_wave = p.off_wave;
