@@ -410,6 +410,208 @@ __global__ void __launch_bounds__(kPeerThreads, 1) k_gossip_peer(const PeerKerne
   }
 }
 
+// ---------------------------------------------------------------------------
+// Two-kernel schedule (algo 2): a pure streaming push kernel, then a streaming
+// mix kernel.  No per-tile or per-wave synchronisation at all: one
+// system-scope signal per GPU per kernel.
+//
+//   k_peer_push  per unit (tile, local worker): bulk-TMA x, m, g -> m', y (a3);
+//                m' -> HBM, y -> x (local), y -> the receiver's inbox (NVLink,
+//                Alg.1 l.7); w_{i,s} -> the receiver's wbox.  The last CTA to
+//                finish publishes push_done[rank] = e to every GPU (Alg.1 l.14).
+//   k_peer_mix   waits until every GPU published push_done = e, then
+//                x = (y + inbox) * 0.5, w = (w + wbox) * 0.5 (a5, Alg.1 l.17);
+//                the last CTA publishes done[rank] = e (ping-pong safety).
+// ---------------------------------------------------------------------------
+constexpr int kPushCompute = 256;
+constexpr int kPushThreads = kPushCompute + 32;
+constexpr int kPushPer = kPeerTile / 4 / kPushCompute;
+
+struct PushMixArgs {
+  PeerKernelArgs k;
+  size_t off_pdone, off_pcount;
+};
+
+__global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PushMixArgs pa) {
+  const PeerKernelArgs& a = pa.k;
+  extern __shared__ __align__(128) float smem_f[];
+  float* ringA = smem_f;
+  __shared__ uint64_t a_full[kStagesA], a_empty[kStagesA];
+  __shared__ int s_timeout;
+  const PeerStepArgs& s = a.s;
+  const uint32_t e = a.epoch;
+  const int par = (int)(e & 1u);
+  char* mine = a.peers[s.rank];
+  const int n_units = a.n_tiles * s.n_loc;
+  const int G = gridDim.x;
+  const int n_my = blockIdx.x < n_units ? (n_units - blockIdx.x + G - 1) / G : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  volatile int* timeout = &s_timeout;
+
+  int64_t* bnd = reinterpret_cast<int64_t*>(ringA + (size_t)kStagesA * 3 * kPeerTile);
+  int32_t* t0 = reinterpret_cast<int32_t*>(bnd + s.k + 1);
+  int32_t* dstl = t0 + s.k + 1;
+  Meta M;
+  M.bnd = bnd;
+  M.t0 = t0;
+  M.dstl = dstl;
+  M.dst_global = (int64_t)s.k * s.n_loc > kMaxDstSmem;
+  for (int i = threadIdx.x; i <= s.k; i += blockDim.x) {
+    bnd[i] = a.bounds[i];
+    t0[i] = a.seg_t0[i];
+  }
+  if (!M.dst_global)
+    for (int i = threadIdx.x; i < s.k * s.n_loc; i += blockDim.x) {
+      const int sg = i / s.n_loc, r = i - sg * s.n_loc;
+      dstl[i] = s.dst[(int64_t)sg * s.world + s.first + r];
+    }
+  if (threadIdx.x == 0) {
+    s_timeout = 0;
+    for (int i = 0; i < kStagesA; ++i) {
+      ptx::mbar_init(&a_full[i], 1);
+      ptx::mbar_init(&a_empty[i], kPushCompute / 32);
+    }
+    ptx::mbar_fence_init();
+  }
+  __syncthreads();
+  // ping-pong safety: every receiver finished mixing epoch e-2 (last reader of this parity)
+  if (threadIdx.x < s.nprocs && e >= 3) {
+    const uint32_t* done = reinterpret_cast<const uint32_t*>(mine + a.off_done);
+    if (!wait_acquire(done + threadIdx.x, e - 2)) atomicOr(&s_timeout, 1);
+  }
+  __syncthreads();
+
+  if (warp < kPushCompute / 32) {
+    bool bad = false;
+    const int tid = threadIdx.x;
+    int cur = 0;
+    for (int i = 0; i < n_my && !*timeout; ++i) {
+      const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
+      const int st = i % kStagesA;
+      ptx::mbar_wait(&a_full[st], (uint32_t)((i / kStagesA) & 1));
+      const float* bx = ringA + (size_t)st * 3 * kPeerTile;
+      int rp, rl;
+      receiver_of(a, M, U.seg, U.r, rp, rl);
+      float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
+      const int64_t rowoff = (int64_t)U.r * s.ld;
+#pragma unroll
+      for (int q = 0; q < kPushPer; ++q) {
+        const int v = tid + q * kPushCompute;
+        const int valid = U.len - 4 * v;
+        if (valid > 0) {
+          const int vv = valid < 4 ? valid : 4;
+          const float4 cx = reinterpret_cast<const float4*>(bx)[v];
+          const float4 cm = reinterpret_cast<const float4*>(bx + kPeerTile)[v];
+          const float4 cg = reinterpret_cast<const float4*>(bx + 2 * kPeerTile)[v];
+          bad |= nonfinite4(cg);
+          const float4 mn = mom4(cm, cg, s.mu);
+          const float4 y = sgd4(cx, mn, s.lr);
+          const int64_t j = U.c0 + 4 * (int64_t)v;
+          st4_cs(s.m + rowoff + j, mn, vv);
+          st4(s.x + rowoff + j, y, vv);
+          st4(inbox + j, y, vv);
+        }
+      }
+      if (U.first_tile && tid == 0) {
+        float* wbox = reinterpret_cast<float*>(a.peers[rp] + a.off_wbox) + ((int64_t)par * s.n_loc + rl) * s.k;
+        wbox[U.seg] = s.psw[(int64_t)U.r * s.k + U.seg];
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&a_empty[st]);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(s.err + kErrDiverged, 1);
+  } else if (lane == 0) {
+    int cur = 0;
+    for (int i = 0; i < n_my; ++i) {
+      const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
+      const int st = i % kStagesA;
+      ptx::mbar_wait(&a_empty[st], (uint32_t)(((i / kStagesA) & 1) ^ 1));
+      const uint32_t bytes = (uint32_t)(((U.len + 3) & ~3) * 4);
+      const int64_t off = (int64_t)U.r * s.ld + U.c0;
+      float* buf = ringA + (size_t)st * 3 * kPeerTile;
+      ptx::mbar_arrive_expect_tx(&a_full[st], 3 * bytes);
+      ptx::bulk_g2s(buf, s.x + off, bytes, &a_full[st]);
+      ptx::bulk_g2s(buf + kPeerTile, s.m + off, bytes, &a_full[st]);
+      ptx::bulk_g2s(buf + 2 * kPeerTile, s.g + off, bytes, &a_full[st]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_timeout) atomicOr(s.err + kErrTimeout, 1);
+    __threadfence();
+    uint32_t* count = reinterpret_cast<uint32_t*>(mine + pa.off_pcount);
+    const uint32_t prevc = atomicAdd(count, 1u);
+    if (prevc + 1 == e * gridDim.x) {  // every CTA's pushes are issued: publish them
+      __threadfence_system();
+      for (int p = 0; p < s.nprocs; ++p)
+        ptx::st_release_sys(reinterpret_cast<uint32_t*>(a.peers[p] + pa.off_pdone) + s.rank, e);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_peer_mix(const PushMixArgs pa) {
+  const PeerKernelArgs& a = pa.k;
+  const PeerStepArgs& s = a.s;
+  const uint32_t e = a.epoch;
+  const int par = (int)(e & 1u);
+  char* mine = a.peers[s.rank];
+  __shared__ int s_timeout;
+  if (threadIdx.x == 0) s_timeout = 0;
+  __syncthreads();
+  if (threadIdx.x < s.nprocs && a.mode != 2) {
+    const uint32_t* pd = reinterpret_cast<const uint32_t*>(mine + pa.off_pdone);
+    if (!wait_acquire(pd + threadIdx.x, e)) atomicOr(&s_timeout, 1);
+  }
+  __syncthreads();
+  if (!s_timeout) {
+    const int64_t nv = (s.d + 3) >> 2;
+    const int64_t total = nv * s.n_loc;
+    const float* inbox0 = reinterpret_cast<const float*>(mine + a.off_inbox) + (int64_t)par * s.n_loc * s.ld;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < total; base += 2 * stride) {
+      float4 yo[2], yi[2];
+      int64_t off[2];
+      int valid[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t idx = base + h * stride;
+        valid[h] = 0;
+        if (idx < total) {
+          const int64_t r = idx / nv, v = idx - r * nv;
+          const int64_t j = 4 * v;
+          valid[h] = (int)imin64(4, s.d - j);
+          off[h] = r * s.ld + j;
+          yo[h] = __ldcs(reinterpret_cast<const float4*>(s.x + off[h]));
+          yi[h] = __ldcs(reinterpret_cast<const float4*>(inbox0 + off[h]));
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (valid[h] > 0) st4_cs(s.x + off[h], mean4(yo[h], yi[h]), valid[h]);
+    }
+    if (blockIdx.x == 0) {
+      for (int i = threadIdx.x; i < s.n_loc * s.k; i += blockDim.x) {
+        const int r = i / s.k, sg = i - r * s.k;
+        const float* wbox = reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * s.n_loc + r) * s.k;
+        float* wp = s.psw + (int64_t)r * s.k + sg;
+        *wp = __fmul_rn(__fadd_rn(*wp, __ldcg(wbox + sg)), 0.5f);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_timeout) atomicOr(s.err + kErrTimeout, 1);
+    __threadfence();
+    uint32_t* count = reinterpret_cast<uint32_t*>(mine + a.off_count);
+    const uint32_t prevc = atomicAdd(count, 1u);
+    if (prevc + 1 == e * gridDim.x) {
+      __threadfence_system();
+      for (int p = 0; p < s.nprocs; ++p)
+        ptx::st_release_sys(reinterpret_cast<uint32_t*>(a.peers[p] + a.off_done) + s.rank, e);
+    }
+  }
+}
+
 int gcd_int(int a, int b) {
   while (b) {
     const int t = a % b;
@@ -476,8 +678,22 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   p.off_wave = align_up(p.off_wbox + sizeof(float) * 2 * (size_t)n_loc * k, 256);
   p.off_done = align_up(p.off_wave + sizeof(uint32_t) * (size_t)p.waves, 256);
   p.off_count = align_up(p.off_done + sizeof(uint32_t) * (size_t)nprocs, 256);
+  p.off_pdone = align_up(p.off_count + 256, 256);
+  p.off_pcount = align_up(p.off_pdone + sizeof(uint32_t) * (size_t)nprocs, 256);
   p.off_flags = p.off_count;  // unused by this protocol
-  p.bytes = align_up(p.off_count + 256, 4096);
+  p.bytes = align_up(p.off_pcount + 256, 4096);
+  const char* algo = getenv("CS_PEER_ALGO");
+  p.algo = algo ? atoi(algo) : 0;
+  {
+    int occ_push = 0, occ_mix = 0;
+    e = cudaFuncSetAttribute(k_peer_push, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_push, k_peer_push, kPushThreads, smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_mix, k_peer_mix, 256, 0);
+    if (e != cudaSuccess || occ_push < 1 || occ_mix < 1) return perr(CS_ECUDA, "push/mix occupancy", e);
+    p.grid_push = sms * occ_push;
+    if (p.grid_push > n_units) p.grid_push = n_units;
+    p.grid_mix = sms * occ_mix;
+  }
   e = cudaMalloc(&p.base, p.bytes);
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region cudaMalloc", e);
   e = cudaMemset(p.base, 0, p.bytes);
@@ -585,6 +801,19 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   ka.off_wave = p.off_wave;
   ka.off_done = p.off_done;
   ka.off_count = p.off_count;
+  if (p.algo == 2) {
+    PushMixArgs pm;
+    pm.k = ka;
+    pm.off_pdone = p.off_pdone;
+    pm.off_pcount = p.off_pcount;
+    if (ev0) cudaEventRecord(ev0, st);
+    k_peer_push<<<p.grid_push, kPushThreads, peer_smem_bytes(a.k, a.n_loc), st>>>(pm);
+    k_peer_mix<<<p.grid_mix, 256, 0, st>>>(pm);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return perr(CS_ECUDA, "push/mix launch", e);
+    if (ev1) cudaEventRecord(ev1, st);
+    return CS_OK;
+  }
   void* args[] = {&ka};
   if (ev0) cudaEventRecord(ev0, st);
   e = cudaLaunchCooperativeKernel((const void*)k_gossip_peer, dim3(p.grid), dim3(kPeerThreads), args,

@@ -34,6 +34,10 @@ struct PeerState {
   int mode = 0;          // CS_PEER_MODE diagnostics: 0 normal, 1 local-only, 2 no waits
   int waves = 0;         // push/mix waves per step
   int per_wave = 0;      // units per CTA per wave
+  int algo = 0;          // 0: fused wave kernel; 2: push kernel + mix kernel
+  int grid_push = 0, grid_mix = 0;
+  size_t off_pdone = 0;  // [nprocs] push-complete epochs (two-kernel schedule)
+  size_t off_pcount = 0; // push-kernel CTA arrival counter
   size_t off_wave = 0;   // per-wave arrival counters [waves]
   int n_tiles = 0;
   int grid = 0;
