@@ -432,6 +432,8 @@ struct PushMixArgs {
   size_t off_pdone, off_pcount;
 };
 
+// PULL: y goes only to this GPU's own exchange buffer; receivers pull it in k_peer_mix_pull.
+template <bool PULL>
 __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PushMixArgs pa) {
   const PeerKernelArgs& a = pa.k;
   extern __shared__ __align__(128) float smem_f[];
@@ -492,7 +494,8 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PushMixArgs
       const float* bx = ringA + (size_t)st * 3 * kPeerTile;
       int rp, rl;
       receiver_of(a, M, U.seg, U.r, rp, rl);
-      float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
+      float* inbox = PULL ? reinterpret_cast<float*>(mine + a.off_inbox) + ((int64_t)par * s.n_loc + U.r) * s.ld
+                          : reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
       const int64_t rowoff = (int64_t)U.r * s.ld;
 #pragma unroll
       for (int q = 0; q < kPushPer; ++q) {
@@ -508,8 +511,8 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PushMixArgs
           const float4 y = sgd4(cx, mn, s.lr);
           const int64_t j = U.c0 + 4 * (int64_t)v;
           st4_cs(s.m + rowoff + j, mn, vv);
-          st4(s.x + rowoff + j, y, vv);
-          st4(inbox + j, y, vv);
+          if (!PULL) st4(s.x + rowoff + j, y, vv);
+          st4(inbox + j, y, vv);  // PULL: own exchange buffer; else the receiver's inbox (NVLink)
         }
       }
       if (U.first_tile && tid == 0) {
@@ -583,6 +586,75 @@ __global__ void __launch_bounds__(256) k_peer_mix(const PushMixArgs pa) {
           off[h] = r * s.ld + j;
           yo[h] = __ldcs(reinterpret_cast<const float4*>(s.x + off[h]));
           yi[h] = __ldcs(reinterpret_cast<const float4*>(inbox0 + off[h]));
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (valid[h] > 0) st4_cs(s.x + off[h], mean4(yo[h], yi[h]), valid[h]);
+    }
+    if (blockIdx.x == 0) {
+      for (int i = threadIdx.x; i < s.n_loc * s.k; i += blockDim.x) {
+        const int r = i / s.k, sg = i - r * s.k;
+        const float* wbox = reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * s.n_loc + r) * s.k;
+        float* wp = s.psw + (int64_t)r * s.k + sg;
+        *wp = __fmul_rn(__fadd_rn(*wp, __ldcg(wbox + sg)), 0.5f);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_timeout) atomicOr(s.err + kErrTimeout, 1);
+    __threadfence();
+    uint32_t* count = reinterpret_cast<uint32_t*>(mine + a.off_count);
+    const uint32_t prevc = atomicAdd(count, 1u);
+    if (prevc + 1 == e * gridDim.x) {
+      __threadfence_system();
+      for (int p = 0; p < s.nprocs; ++p)
+        ptx::st_release_sys(reinterpret_cast<uint32_t*>(a.peers[p] + a.off_done) + s.rank, e);
+    }
+  }
+}
+
+// Pull variant of the mix: x_i = (y_i + y_{src_s(i)}) * 0.5 with y_src read straight
+// from the source GPU's exchange buffer over NVLink (128-bit peer loads).
+__global__ void __launch_bounds__(256) k_peer_mix_pull(const PushMixArgs pa) {
+  const PeerKernelArgs& a = pa.k;
+  const PeerStepArgs& s = a.s;
+  const uint32_t e = a.epoch;
+  const int par = (int)(e & 1u);
+  char* mine = a.peers[s.rank];
+  __shared__ int s_timeout;
+  if (threadIdx.x == 0) s_timeout = 0;
+  __syncthreads();
+  if (threadIdx.x < s.nprocs && a.mode != 2) {
+    const uint32_t* pd = reinterpret_cast<const uint32_t*>(mine + pa.off_pdone);
+    if (!wait_acquire(pd + threadIdx.x, e)) atomicOr(&s_timeout, 1);
+  }
+  __syncthreads();
+  if (!s_timeout) {
+    const int64_t nv = (s.d + 3) >> 2;
+    const int64_t total = nv * s.n_loc;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < total; base += 2 * stride) {
+      float4 yo[2], yi[2];
+      int64_t off[2];
+      int valid[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t idx = base + h * stride;
+        valid[h] = 0;
+        if (idx < total) {
+          const int64_t r = idx / nv, v = idx - r * nv;
+          const int64_t j = 4 * v;
+          const int64_t q = j >> 5;
+          const int seg = (int)imin64(s.k - 1, ((q + 1) * s.k - 1) / s.nq);
+          const int src = s.src[(int64_t)seg * s.world + s.first + (int)r];
+          const int sp = src / s.n_loc, sl = src - sp * s.n_loc;
+          valid[h] = (int)imin64(4, s.d - j);
+          off[h] = r * s.ld + j;
+          yo[h] = __ldcs(reinterpret_cast<const float4*>(mine + a.off_inbox) + (((int64_t)par * s.n_loc + r) * s.ld + j) / 4);
+          yi[h] = __ldcg(reinterpret_cast<const float4*>(a.peers[sp] + a.off_inbox) +
+                         (((int64_t)par * s.n_loc + sl) * s.ld + j) / 4);
         }
       }
 #pragma unroll
@@ -686,8 +758,11 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   p.algo = algo ? atoi(algo) : 0;
   {
     int occ_push = 0, occ_mix = 0;
-    e = cudaFuncSetAttribute(k_peer_push, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_push, k_peer_push, kPushThreads, smem);
+    e = cudaFuncSetAttribute(k_peer_push<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_peer_push<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_push, k_peer_push<false>, kPushThreads, smem);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_mix, k_peer_mix, 256, 0);
     if (e != cudaSuccess || occ_push < 1 || occ_mix < 1) return perr(CS_ECUDA, "push/mix occupancy", e);
     p.grid_push = sms * occ_push;
@@ -801,17 +876,22 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   ka.off_wave = p.off_wave;
   ka.off_done = p.off_done;
   ka.off_count = p.off_count;
-  if (p.algo == 2) {
+  if (p.algo == 2 || p.algo == 3) {
+    const bool pull = p.algo == 3;
     PushMixArgs pm;
     pm.k = ka;
     pm.off_pdone = p.off_pdone;
     pm.off_pcount = p.off_pcount;
+    static const bool time_push_only = getenv("CS_PEER_TIME_PUSH") != nullptr;  // tuning knob
     if (ev0) cudaEventRecord(ev0, st);
-    k_peer_push<<<p.grid_push, kPushThreads, peer_smem_bytes(a.k, a.n_loc), st>>>(pm);
-    k_peer_mix<<<p.grid_mix, 256, 0, st>>>(pm);
+    if (pull) k_peer_push<true><<<p.grid_push, kPushThreads, peer_smem_bytes(a.k, a.n_loc), st>>>(pm);
+    else k_peer_push<false><<<p.grid_push, kPushThreads, peer_smem_bytes(a.k, a.n_loc), st>>>(pm);
+    if (ev1 && time_push_only) cudaEventRecord(ev1, st);
+    if (pull) k_peer_mix_pull<<<p.grid_mix, 256, 0, st>>>(pm);
+    else k_peer_mix<<<p.grid_mix, 256, 0, st>>>(pm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return perr(CS_ECUDA, "push/mix launch", e);
-    if (ev1) cudaEventRecord(ev1, st);
+    if (ev1 && !time_push_only) cudaEventRecord(ev1, st);
     return CS_OK;
   }
   void* args[] = {&ka};
