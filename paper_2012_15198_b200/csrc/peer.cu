@@ -615,6 +615,169 @@ __global__ void __launch_bounds__(256) k_peer_mix(const PushMixArgs pa) {
   }
 }
 
+// Push kernel with the NVLink transfer handed to the TMA engine (algo 4): compute
+// warps write y into a shared-memory ring as well as into x; a store warp issues
+// one 1-D bulk copy (cp.async.bulk.global.shared::cta) of each 8 KB y tile into
+// the receiver's inbox, so the load/store units only carry the local traffic.
+constexpr int kTStagesA = 3, kTSlotsY = 3;
+constexpr int kTPushThreads = kPushCompute + 64;  // compute warps, load warp, store warp
+constexpr size_t kTRingBytes = kTileBytes * (3 * kTStagesA + kTSlotsY);
+
+size_t push_tma_smem_bytes(int k, int n_loc) {
+  size_t b = kTRingBytes + sizeof(int64_t) * (k + 1) + sizeof(int32_t) * (k + 1);
+  if ((int64_t)k * n_loc <= kMaxDstSmem) b += sizeof(int32_t) * (size_t)k * n_loc;
+  return align_up(b, 16);
+}
+
+__global__ void __launch_bounds__(kTPushThreads, 2) k_peer_push_tma(const PushMixArgs pa) {
+  const PeerKernelArgs& a = pa.k;
+  extern __shared__ __align__(128) float smem_f[];
+  float* ringA = smem_f;                                      // [kTStagesA][3][kPeerTile]
+  float* ringY = ringA + (size_t)kTStagesA * 3 * kPeerTile;   // [kTSlotsY][kPeerTile]
+  __shared__ uint64_t a_full[kTStagesA], a_empty[kTStagesA], y_full[kTSlotsY], y_empty[kTSlotsY];
+  __shared__ int s_timeout;
+  const PeerStepArgs& s = a.s;
+  const uint32_t e = a.epoch;
+  const int par = (int)(e & 1u);
+  char* mine = a.peers[s.rank];
+  const int n_units = a.n_tiles * s.n_loc;
+  const int G = gridDim.x;
+  const int n_my = blockIdx.x < n_units ? (n_units - blockIdx.x + G - 1) / G : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  volatile int* timeout = &s_timeout;
+
+  int64_t* bnd = reinterpret_cast<int64_t*>(ringY + (size_t)kTSlotsY * kPeerTile);
+  int32_t* t0 = reinterpret_cast<int32_t*>(bnd + s.k + 1);
+  int32_t* dstl = t0 + s.k + 1;
+  Meta M;
+  M.bnd = bnd;
+  M.t0 = t0;
+  M.dstl = dstl;
+  M.dst_global = (int64_t)s.k * s.n_loc > kMaxDstSmem;
+  for (int i = threadIdx.x; i <= s.k; i += blockDim.x) {
+    bnd[i] = a.bounds[i];
+    t0[i] = a.seg_t0[i];
+  }
+  if (!M.dst_global)
+    for (int i = threadIdx.x; i < s.k * s.n_loc; i += blockDim.x) {
+      const int sg = i / s.n_loc, r = i - sg * s.n_loc;
+      dstl[i] = s.dst[(int64_t)sg * s.world + s.first + r];
+    }
+  if (threadIdx.x == 0) {
+    s_timeout = 0;
+    for (int i = 0; i < kTStagesA; ++i) {
+      ptx::mbar_init(&a_full[i], 1);
+      ptx::mbar_init(&a_empty[i], kPushCompute / 32);
+    }
+    for (int i = 0; i < kTSlotsY; ++i) {
+      ptx::mbar_init(&y_full[i], kPushCompute / 32);
+      ptx::mbar_init(&y_empty[i], 1);
+    }
+    ptx::mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x < s.nprocs && e >= 3) {
+    const uint32_t* done = reinterpret_cast<const uint32_t*>(mine + a.off_done);
+    if (!wait_acquire(done + threadIdx.x, e - 2)) atomicOr(&s_timeout, 1);
+  }
+  __syncthreads();
+
+  if (warp < kPushCompute / 32) {
+    bool bad = false;
+    const int tid = threadIdx.x;
+    int cur = 0;
+    for (int i = 0; i < n_my && !*timeout; ++i) {
+      const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
+      const int st = i % kTStagesA, sy = i % kTSlotsY;
+      ptx::mbar_wait(&a_full[st], (uint32_t)((i / kTStagesA) & 1));
+      ptx::mbar_wait(&y_empty[sy], (uint32_t)(((i / kTSlotsY) & 1) ^ 1));
+      const float* bx = ringA + (size_t)st * 3 * kPeerTile;
+      float4* yt = reinterpret_cast<float4*>(ringY + (size_t)sy * kPeerTile);
+      const int64_t rowoff = (int64_t)U.r * s.ld;
+#pragma unroll
+      for (int q = 0; q < kPushPer; ++q) {
+        const int v = tid + q * kPushCompute;
+        const int valid = U.len - 4 * v;
+        if (valid > 0) {
+          const int vv = valid < 4 ? valid : 4;
+          const float4 cx = reinterpret_cast<const float4*>(bx)[v];
+          const float4 cm = reinterpret_cast<const float4*>(bx + kPeerTile)[v];
+          const float4 cg = reinterpret_cast<const float4*>(bx + 2 * kPeerTile)[v];
+          bad |= nonfinite4(cg);
+          const float4 mn = mom4(cm, cg, s.mu);
+          const float4 y = sgd4(cx, mn, s.lr);
+          const int64_t j = U.c0 + 4 * (int64_t)v;
+          st4_cs(s.m + rowoff + j, mn, vv);
+          st4(s.x + rowoff + j, y, vv);
+          yt[v] = y;
+        }
+      }
+      if (U.first_tile && tid == 0) {
+        int rp, rl;
+        receiver_of(a, M, U.seg, U.r, rp, rl);
+        float* wbox = reinterpret_cast<float*>(a.peers[rp] + a.off_wbox) + ((int64_t)par * s.n_loc + rl) * s.k;
+        wbox[U.seg] = s.psw[(int64_t)U.r * s.k + U.seg];
+      }
+      ptx::fence_proxy_async_shared();  // y tile -> the TMA engine's reads
+      __syncwarp();
+      if (lane == 0) {
+        ptx::mbar_arrive(&a_empty[st]);
+        ptx::mbar_arrive(&y_full[sy]);
+      }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(s.err + kErrDiverged, 1);
+  } else if (warp == kPushCompute / 32) {
+    if (lane == 0) {  // load warp
+      int cur = 0;
+      for (int i = 0; i < n_my; ++i) {
+        const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
+        const int st = i % kTStagesA;
+        ptx::mbar_wait(&a_empty[st], (uint32_t)(((i / kTStagesA) & 1) ^ 1));
+        const uint32_t bytes = (uint32_t)(((U.len + 3) & ~3) * 4);
+        const int64_t off = (int64_t)U.r * s.ld + U.c0;
+        float* buf = ringA + (size_t)st * 3 * kPeerTile;
+        ptx::mbar_arrive_expect_tx(&a_full[st], 3 * bytes);
+        ptx::bulk_g2s(buf, s.x + off, bytes, &a_full[st]);
+        ptx::bulk_g2s(buf + kPeerTile, s.m + off, bytes, &a_full[st]);
+        ptx::bulk_g2s(buf + 2 * kPeerTile, s.g + off, bytes, &a_full[st]);
+      }
+    }
+    __syncwarp();
+  } else {
+    if (lane == 0) {  // store warp: y tiles -> receivers' inboxes over NVLink
+      int cur = 0;
+      for (int i = 0; i < n_my; ++i) {
+        const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
+        const int sy = i % kTSlotsY;
+        ptx::mbar_wait(&y_full[sy], (uint32_t)((i / kTSlotsY) & 1));
+        int rp, rl;
+        receiver_of(a, M, U.seg, U.r, rp, rl);
+        float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
+        ptx::bulk_s2g(inbox + U.c0, ringY + (size_t)sy * kPeerTile, (uint32_t)(((U.len + 3) & ~3) * 4));
+        ptx::bulk_commit();
+        ptx::bulk_wait_read<1>();  // groups up to i-1 have read their tiles
+        if (i >= 1) ptx::mbar_arrive(&y_empty[(i - 1) % kTSlotsY]);
+      }
+      ptx::bulk_wait_all();  // every y tile has landed in its receiver's inbox
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      if (n_my >= 1) ptx::mbar_arrive(&y_empty[(n_my - 1) % kTSlotsY]);
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_timeout) atomicOr(s.err + kErrTimeout, 1);
+    __threadfence();
+    uint32_t* count = reinterpret_cast<uint32_t*>(mine + pa.off_pcount);
+    const uint32_t prevc = atomicAdd(count, 1u);
+    if (prevc + 1 == e * gridDim.x) {  // every CTA's pushes have landed: publish them
+      __threadfence_system();
+      for (int p = 0; p < s.nprocs; ++p)
+        ptx::st_release_sys(reinterpret_cast<uint32_t*>(a.peers[p] + pa.off_pdone) + s.rank, e);
+    }
+  }
+}
+
 // Pull variant of the mix: x_i = (y_i + y_{src_s(i)}) * 0.5 with y_src read straight
 // from the source GPU's exchange buffer over NVLink (128-bit peer loads).
 __global__ void __launch_bounds__(256) k_peer_mix_pull(const PushMixArgs pa) {
@@ -765,6 +928,13 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_push, k_peer_push<false>, kPushThreads, smem);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_mix, k_peer_mix, 256, 0);
     if (e != cudaSuccess || occ_push < 1 || occ_mix < 1) return perr(CS_ECUDA, "push/mix occupancy", e);
+    if (p.algo == 4) {  // TMA-store push kernel has its own footprint
+      const size_t smem_t = push_tma_smem_bytes(k, n_loc);
+      e = cudaFuncSetAttribute(k_peer_push_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t);
+      if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_push, k_peer_push_tma, kTPushThreads, smem_t);
+      if (e != cudaSuccess || occ_push < 1) return perr(CS_ECUDA, "push-tma occupancy", e);
+    }
     p.grid_push = sms * occ_push;
     if (p.grid_push > n_units) p.grid_push = n_units;
     p.grid_mix = sms * occ_mix;
@@ -876,7 +1046,7 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   ka.off_wave = p.off_wave;
   ka.off_done = p.off_done;
   ka.off_count = p.off_count;
-  if (p.algo == 2 || p.algo == 3) {
+  if (p.algo == 2 || p.algo == 3 || p.algo == 4) {
     const bool pull = p.algo == 3;
     PushMixArgs pm;
     pm.k = ka;
@@ -884,7 +1054,8 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     pm.off_pcount = p.off_pcount;
     static const bool time_push_only = getenv("CS_PEER_TIME_PUSH") != nullptr;  // tuning knob
     if (ev0) cudaEventRecord(ev0, st);
-    if (pull) k_peer_push<true><<<p.grid_push, kPushThreads, peer_smem_bytes(a.k, a.n_loc), st>>>(pm);
+    if (p.algo == 4) k_peer_push_tma<<<p.grid_push, kTPushThreads, push_tma_smem_bytes(a.k, a.n_loc), st>>>(pm);
+    else if (pull) k_peer_push<true><<<p.grid_push, kPushThreads, peer_smem_bytes(a.k, a.n_loc), st>>>(pm);
     else k_peer_push<false><<<p.grid_push, kPushThreads, peer_smem_bytes(a.k, a.n_loc), st>>>(pm);
     if (ev1 && time_push_only) cudaEventRecord(ev1, st);
     if (pull) k_peer_mix_pull<<<p.grid_mix, 256, 0, st>>>(pm);
