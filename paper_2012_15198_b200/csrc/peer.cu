@@ -778,6 +778,222 @@ __global__ void __launch_bounds__(kTPushThreads, 2) k_peer_push_tma(const PushMi
   }
 }
 
+// Fused push + mix (algo 5): k_peer_push_tma plus 4 mix warps.  Units are cut into
+// W waves of m units per CTA (G*m a multiple of n_loc: a tile never straddles two
+// waves).  After the last bulk store of wave w has completed, the store warp
+// fences once and adds 1 to wave w's arrival counter on every GPU; the mix warps
+// mix wave w once its counter holds every CTA of every GPU, overlapping the
+// NVLink-bound pushes of later waves.
+constexpr int kMixWarps = 4;
+constexpr int kFThreads = kPushCompute + 64 + 32 * kMixWarps;
+
+__global__ void __launch_bounds__(kFThreads, 1) k_peer_fused(const PushMixArgs pa) {
+  const PeerKernelArgs& a = pa.k;
+  extern __shared__ __align__(128) float smem_f[];
+  float* ringA = smem_f;
+  float* ringY = ringA + (size_t)kTStagesA * 3 * kPeerTile;
+  __shared__ uint64_t a_full[kTStagesA], a_empty[kTStagesA], y_full[kTSlotsY], y_empty[kTSlotsY];
+  __shared__ int s_timeout;
+  const PeerStepArgs& s = a.s;
+  const uint32_t e = a.epoch;
+  const int par = (int)(e & 1u);
+  char* mine = a.peers[s.rank];
+  const int n_units = a.n_tiles * s.n_loc;
+  const int G = gridDim.x;
+  const int W = a.waves, m_per = a.per_wave;
+  const int n_my = blockIdx.x < n_units ? (n_units - blockIdx.x + G - 1) / G : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  volatile int* timeout = &s_timeout;
+
+  int64_t* bnd = reinterpret_cast<int64_t*>(ringY + (size_t)kTSlotsY * kPeerTile);
+  int32_t* t0 = reinterpret_cast<int32_t*>(bnd + s.k + 1);
+  int32_t* dstl = t0 + s.k + 1;
+  Meta M;
+  M.bnd = bnd;
+  M.t0 = t0;
+  M.dstl = dstl;
+  M.dst_global = (int64_t)s.k * s.n_loc > kMaxDstSmem;
+  for (int i = threadIdx.x; i <= s.k; i += blockDim.x) {
+    bnd[i] = a.bounds[i];
+    t0[i] = a.seg_t0[i];
+  }
+  if (!M.dst_global)
+    for (int i = threadIdx.x; i < s.k * s.n_loc; i += blockDim.x) {
+      const int sg = i / s.n_loc, r = i - sg * s.n_loc;
+      dstl[i] = s.dst[(int64_t)sg * s.world + s.first + r];
+    }
+  if (threadIdx.x == 0) {
+    s_timeout = 0;
+    for (int i = 0; i < kTStagesA; ++i) {
+      ptx::mbar_init(&a_full[i], 1);
+      ptx::mbar_init(&a_empty[i], kPushCompute / 32);
+    }
+    for (int i = 0; i < kTSlotsY; ++i) {
+      ptx::mbar_init(&y_full[i], kPushCompute / 32);
+      ptx::mbar_init(&y_empty[i], 1);
+    }
+    ptx::mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x < s.nprocs && e >= 3) {
+    const uint32_t* done = reinterpret_cast<const uint32_t*>(mine + a.off_done);
+    if (!wait_acquire(done + threadIdx.x, e - 2)) atomicOr(&s_timeout, 1);
+  }
+  __syncthreads();
+
+  constexpr int kLoadWarp = kPushCompute / 32, kStoreWarp = kLoadWarp + 1, kMix0 = kStoreWarp + 1;
+  if (warp < kLoadWarp) {
+    // ---------------- compute warps: m', y; y -> x and the y ring --------------------
+    bool bad = false;
+    const int tid = threadIdx.x;
+    int cur = 0;
+    for (int i = 0; i < n_my && !*timeout; ++i) {
+      const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
+      const int st = i % kTStagesA, sy = i % kTSlotsY;
+      ptx::mbar_wait(&a_full[st], (uint32_t)((i / kTStagesA) & 1));
+      ptx::mbar_wait(&y_empty[sy], (uint32_t)(((i / kTSlotsY) & 1) ^ 1));
+      const float* bx = ringA + (size_t)st * 3 * kPeerTile;
+      float4* yt = reinterpret_cast<float4*>(ringY + (size_t)sy * kPeerTile);
+      const int64_t rowoff = (int64_t)U.r * s.ld;
+#pragma unroll
+      for (int q = 0; q < kPushPer; ++q) {
+        const int v = tid + q * kPushCompute;
+        const int valid = U.len - 4 * v;
+        if (valid > 0) {
+          const int vv = valid < 4 ? valid : 4;
+          const float4 cx = reinterpret_cast<const float4*>(bx)[v];
+          const float4 cm = reinterpret_cast<const float4*>(bx + kPeerTile)[v];
+          const float4 cg = reinterpret_cast<const float4*>(bx + 2 * kPeerTile)[v];
+          bad |= nonfinite4(cg);
+          const float4 mn = mom4(cm, cg, s.mu);
+          const float4 y = sgd4(cx, mn, s.lr);
+          const int64_t j = U.c0 + 4 * (int64_t)v;
+          st4_cs(s.m + rowoff + j, mn, vv);
+          st4(s.x + rowoff + j, y, vv);
+          yt[v] = y;
+        }
+      }
+      if (U.first_tile && tid == 0) {
+        int rp, rl;
+        receiver_of(a, M, U.seg, U.r, rp, rl);
+        float* wbox = reinterpret_cast<float*>(a.peers[rp] + a.off_wbox) + ((int64_t)par * s.n_loc + rl) * s.k;
+        wbox[U.seg] = s.psw[(int64_t)U.r * s.k + U.seg];
+      }
+      ptx::fence_proxy_async_shared();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::mbar_arrive(&a_empty[st]);
+        ptx::mbar_arrive(&y_full[sy]);
+      }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(s.err + kErrDiverged, 1);
+  } else if (warp == kLoadWarp) {
+    if (lane == 0) {
+      int cur = 0;
+      for (int i = 0; i < n_my; ++i) {
+        const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
+        const int st = i % kTStagesA;
+        ptx::mbar_wait(&a_empty[st], (uint32_t)(((i / kTStagesA) & 1) ^ 1));
+        const uint32_t bytes = (uint32_t)(((U.len + 3) & ~3) * 4);
+        const int64_t off = (int64_t)U.r * s.ld + U.c0;
+        float* buf = ringA + (size_t)st * 3 * kPeerTile;
+        ptx::mbar_arrive_expect_tx(&a_full[st], 3 * bytes);
+        ptx::bulk_g2s(buf, s.x + off, bytes, &a_full[st]);
+        ptx::bulk_g2s(buf + kPeerTile, s.m + off, bytes, &a_full[st]);
+        ptx::bulk_g2s(buf + 2 * kPeerTile, s.g + off, bytes, &a_full[st]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == kStoreWarp) {
+    // ---------------- store warp: y tiles -> inboxes; release each finished wave -----
+    if (lane == 0) {
+      int cur = 0, i = 0, rel = 0;  // rel: next unit whose y slot goes back to the compute warps
+      for (int w = 0; w < W; ++w) {
+        const int i_end = (w + 1) * m_per < n_my ? (w + 1) * m_per : n_my;
+        for (; i < i_end; ++i) {
+          const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
+          const int sy = i % kTSlotsY;
+          ptx::mbar_wait(&y_full[sy], (uint32_t)((i / kTSlotsY) & 1));
+          int rp, rl;
+          receiver_of(a, M, U.seg, U.r, rp, rl);
+          float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
+          ptx::bulk_s2g(inbox + U.c0, ringY + (size_t)sy * kPeerTile, (uint32_t)(((U.len + 3) & ~3) * 4));
+          ptx::bulk_commit();
+          ptx::bulk_wait_read<1>();  // groups of units < i have read their tiles
+          for (; rel < i; ++rel) ptx::mbar_arrive(&y_empty[rel % kTSlotsY]);
+        }
+        ptx::bulk_wait_all();  // wave w's tiles have landed
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        for (; rel < i; ++rel) ptx::mbar_arrive(&y_empty[rel % kTSlotsY]);
+        // the compute warps' x stores of this wave are ordered by y_full (acquire.cta) + the fence below
+        ptx::fence_acq_rel_sys();
+        for (int p = 0; p < s.nprocs; ++p)
+          ptx::red_add_relaxed_sys(reinterpret_cast<uint32_t*>(a.peers[p] + a.off_wave) + w, 1u);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- mix warps: wave w once every GPU has pushed it ------------------
+    const int tid = threadIdx.x - 32 * kMix0;
+    constexpr int kMixThreads = 32 * kMixWarps;
+    constexpr int kMixPer = kPeerTile / 4 / kMixThreads;
+    const uint32_t expect = e * (uint32_t)G * (uint32_t)s.nprocs;
+    int cur = 0;
+    for (int w = 0; w < W; ++w) {
+      if (tid == 0 && a.mode != 2) {
+        const uint32_t* cnt = reinterpret_cast<const uint32_t*>(mine + a.off_wave) + w;
+        if (!wait_acquire(cnt, expect)) *timeout = 1;
+      }
+      ptx::named_bar_sync(kBarMix, kMixThreads);
+      if (*timeout) break;
+      const int i_end = (w + 1) * m_per < n_my ? (w + 1) * m_per : n_my;
+      for (int i = w * m_per; i < i_end; ++i) {
+        const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
+        const float* inbox =
+            reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * s.n_loc + U.r) * s.ld;
+        const int64_t rowoff = (int64_t)U.r * s.ld;
+        float4 yo[kMixPer], yi[kMixPer];
+#pragma unroll
+        for (int q = 0; q < kMixPer; ++q) {
+          const int vv = tid + q * kMixThreads;
+          if (U.len - 4 * vv > 0) {
+            const int64_t j = U.c0 + 4 * (int64_t)vv;
+            yo[q] = __ldcg(reinterpret_cast<const float4*>(s.x + rowoff + j));
+            yi[q] = __ldcg(reinterpret_cast<const float4*>(inbox + j));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kMixPer; ++q) {
+          const int vv = tid + q * kMixThreads;
+          const int valid = U.len - 4 * vv;
+          if (valid > 0) {
+            const int64_t j = U.c0 + 4 * (int64_t)vv;
+            st4_cs(s.x + rowoff + j, mean4(yo[q], yi[q]), valid < 4 ? valid : 4);
+          }
+        }
+        if (U.first_tile && tid == 0) {
+          const float* wbox =
+              reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * s.n_loc + U.r) * s.k;
+          float* wp = s.psw + (int64_t)U.r * s.k + U.seg;
+          *wp = __fmul_rn(__fadd_rn(*wp, __ldcg(wbox + U.seg)), 0.5f);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_timeout) atomicOr(s.err + kErrTimeout, 1);
+    __threadfence();
+    uint32_t* count = reinterpret_cast<uint32_t*>(mine + a.off_count);
+    const uint32_t prevc = atomicAdd(count, 1u);
+    if (prevc + 1 == e * gridDim.x) {
+      __threadfence_system();
+      for (int p = 0; p < s.nprocs; ++p)
+        ptx::st_release_sys(reinterpret_cast<uint32_t*>(a.peers[p] + a.off_done) + s.rank, e);
+    }
+  }
+}
+
 // Pull variant of the mix: x_i = (y_i + y_{src_s(i)}) * 0.5 with y_src read straight
 // from the source GPU's exchange buffer over NVLink (128-bit peer loads).
 __global__ void __launch_bounds__(256) k_peer_mix_pull(const PushMixArgs pa) {
@@ -897,6 +1113,17 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   p.grid = sms * occ;
   const int n_units = p.n_tiles * n_loc;
   if (p.grid > n_units) p.grid = n_units;
+  const char* algo = getenv("CS_PEER_ALGO");
+  p.algo = algo ? atoi(algo) : 0;
+  if (p.algo == 5) {  // fused push+mix kernel: its own grid defines the waves
+    const size_t smem_f = push_tma_smem_bytes(k, n_loc);
+    int occ_f = 0;
+    e = cudaFuncSetAttribute(k_peer_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, k_peer_fused, kFThreads, smem_f);
+    if (e != cudaSuccess || occ_f < 1) return perr(CS_ECUDA, "fused occupancy", e);
+    p.grid = sms * occ_f;
+    if (p.grid > n_units) p.grid = n_units;
+  }
   // waves of G*m units, G*m a multiple of n_loc (tiles never straddle waves), ~kWaveBytes each
   const int step_m = n_loc / gcd_int(p.grid, n_loc);
   const double unit_bytes = 28.0 * kPeerTile;
@@ -917,8 +1144,6 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   p.off_pcount = align_up(p.off_pdone + sizeof(uint32_t) * (size_t)nprocs, 256);
   p.off_flags = p.off_count;  // unused by this protocol
   p.bytes = align_up(p.off_pcount + 256, 4096);
-  const char* algo = getenv("CS_PEER_ALGO");
-  p.algo = algo ? atoi(algo) : 0;
   {
     int occ_push = 0, occ_mix = 0;
     e = cudaFuncSetAttribute(k_peer_push<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1046,6 +1271,18 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   ka.off_wave = p.off_wave;
   ka.off_done = p.off_done;
   ka.off_count = p.off_count;
+  if (p.algo == 5) {
+    PushMixArgs pm;
+    pm.k = ka;
+    pm.off_pdone = p.off_pdone;
+    pm.off_pcount = p.off_pcount;
+    if (ev0) cudaEventRecord(ev0, st);
+    k_peer_fused<<<p.grid, kFThreads, push_tma_smem_bytes(a.k, a.n_loc), st>>>(pm);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return perr(CS_ECUDA, "fused launch", e);
+    if (ev1) cudaEventRecord(ev1, st);
+    return CS_OK;
+  }
   if (p.algo == 2 || p.algo == 3 || p.algo == 4) {
     const bool pull = p.algo == 3;
     PushMixArgs pm;
