@@ -220,6 +220,35 @@ LocalArgs local_args(float* params, const float* grads, float* psw, int n, int g
   return a;
 }
 
+PeerStepArgs peer_args(float* params, const float* grads, float* psw, float lr, float mu) {
+  PeerStepArgs pa;
+  pa.x = params;
+  pa.m = g.mom;
+  pa.g = grads;
+  pa.psw = psw;
+  pa.ld = g.ld;
+  pa.d = g.d;
+  pa.nq = g.nq;
+  pa.k = g.k;
+  pa.world = g.world;
+  pa.n_loc = g.n_loc;
+  pa.first = g.first;
+  pa.rank = g.rank;
+  pa.nprocs = g.nprocs;
+  pa.step = (uint32_t)g.step;
+  pa.seed = g.seed;
+  pa.lr = lr;
+  pa.mu = mu;
+  pa.given = nullptr;
+  pa.src = g.d_src;
+  pa.dst = g.d_dst;
+  pa.err = g.d_err;
+  pa.groups = g.groups;
+  pa.gs = 0;
+  pa.inv_gs = 1.0f / (float)(g.world / g.groups);
+  return pa;
+}
+
 int validate_derangements(const int32_t* src, int n, int k) {
   std::vector<int> seen(n);
   for (int s = 0; s < k; ++s) {
@@ -407,7 +436,9 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
     CS_CUDA(cudaMemcpy(g.d_tiles, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice));
   }
   if (g.use_peer) {
-    int rc = peer_alloc(g.peer, g.n_loc, d, ld, g.k, nprocs, proc_rank);
+    // hierarchical steps over the peer path: one worker per GPU, groups of world/groups GPUs
+    const int hier_gs = (nprocs > 1 && g.n_loc == 1) ? g.world / g.groups : 0;
+    int rc = peer_alloc(g.peer, g.n_loc, d, ld, g.k, nprocs, proc_rank, hier_gs);
     if (rc) return fail(rc, "%s", peer_error());
     if (nprocs == 1) {  // single-GPU emulation: the only peer is this GPU
       rc = peer_import_self(g.peer);
@@ -462,21 +493,15 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
   } else {
     if (diag) return fail(CS_EUNSUPPORTED, "diagnostics are not implemented on the peer-exchange path");
     if (!g.peer.imported) return fail(CS_ENOTBOUND, "multi-GPU: cs_ipc_import has not been called");
-    PeerStepArgs pa;
-    pa.x = params; pa.m = g.mom; pa.g = grads; pa.psw = psw;
-    pa.ld = g.ld; pa.d = g.d; pa.nq = g.nq; pa.k = g.k;
-    pa.world = g.world; pa.n_loc = g.n_loc; pa.first = g.first; pa.rank = g.rank;
-    pa.nprocs = g.nprocs; pa.step = (uint32_t)g.step; pa.seed = g.seed;
-    pa.lr = lr; pa.mu = momentum;
+    PeerStepArgs pa = peer_args(params, grads, psw, lr, momentum);
     pa.given = g.has_override ? g.d_given : nullptr;
-    pa.src = g.d_src; pa.dst = g.d_dst; pa.ord = g.d_ord; pa.err = g.d_err;
     cudaEvent_t ev[2];
     rc = next_event_pair(ev);
     if (rc) return rc;
     rc = peer_flat_step(g.peer, pa, g.stream, ev[0], ev[1]);
     if (rc) return fail(rc, "%s", peer_error());
-    g.launches_per_step = 2;
-    g.hot_kernel = "k_gossip_peer";
+    g.launches_per_step = 3;  // topology, push, mix
+    g.hot_kernel = "k_peer_push+k_peer_mix";
   }
   if (rc) return rc;
   if (diag) g.diag_valid = true;
@@ -514,9 +539,23 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
   if (rc) return rc;
   rc = check_step_args(params, grads, psw);
   if (rc) return rc;
-  if (g.nprocs != 1)
-    return fail(CS_EUNSUPPORTED, "multi-GPU hierarchical step is not implemented in this build");
   const bool diag = g.diag != 0;
+  if (g.nprocs > 1) {
+    if (diag) return fail(CS_EUNSUPPORTED, "diagnostics are not implemented on the peer-exchange path");
+    if (g.n_loc != 1)
+      return fail(CS_EUNSUPPORTED, "multi-GPU hierarchical step needs one worker per GPU (world == nprocs)");
+    if (!g.peer.imported) return fail(CS_ENOTBOUND, "multi-GPU: cs_ipc_import has not been called");
+    PeerStepArgs pa = peer_args(params, grads, psw, lr, momentum);
+    cudaEvent_t ev[2];
+    rc = next_event_pair(ev);
+    if (rc) return rc;
+    rc = peer_hier_step(g.peer, pa, g.stream, ev[0], ev[1]);
+    if (rc) return fail(rc, "%s", peer_error());
+    g.launches_per_step = g.groups >= 2 ? 5 : 3;  // (topology,) scatter, reduce, push(, mix)
+    g.hot_kernel = "k_hier_scatter+k_hier_reduce+k_peer_push+k_peer_mix";
+    g.step += 1;
+    return CS_OK;
+  }
   const int L = g.groups, gs = g.world / g.groups;
   const bool fused = fused_topology_ok(L, g.k);
   LocalArgs a = local_args(params, grads, psw, L, gs, CS_TAG_HIER, lr, momentum);

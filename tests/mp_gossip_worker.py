@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--num-steps", type=int, default=5)
     ap.add_argument("--rng-seed", type=int, default=0)
     ap.add_argument("--compare-all", action="store_true", help="compare every column (small d)")
+    ap.add_argument("--hier-groups", type=int, default=0, help="hierarchical step with this many groups")
     a = ap.parse_args()
     rank, ws, lr_ = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(lr_)
@@ -43,7 +44,8 @@ def main():
     world = n_loc * ws
     first = rank * n_loc
     lr, mu = float(synth.DEFAULT_LR), float(synth.DEFAULT_MOMENTUM)
-    cs.cs_init(world, world, k, seed)
+    groups = a.hier_groups or world
+    cs.cs_init(world, groups, k, seed)
     stream = torch.cuda.current_stream(dev)
     ld = (d + 3) // 4 * 4
     x = torch.zeros(n_loc, ld, device=dev)
@@ -60,18 +62,25 @@ def main():
     cs.setup_peers()
 
     cols = np.arange(d) if a.compare_all else synth.sample_columns(d, T.segment_bounds(d, k))
-    orc = OracleRun(world, d, k, seed, cols=cols)
+    orc = OracleRun(world, d, k, seed, cols=cols, groups=a.hier_groups or None)
+    step_fn = cs.cs_hier_step if a.hier_groups else cs.cs_gossip_step
     idx = torch.from_numpy(cols).to(dev)
     ok = True
     for t in range(a.num_steps):
         o = (t + first) % B
-        cs.cs_gossip_step(x, bank[o:o + n_loc], w, lr, mu)
+        step_fn(x, bank[o:o + n_loc], w, lr, mu)
         orc.step(lr, mu)
         cs.cs_sync()
         xs = x.index_select(1, idx).cpu().numpy()
         ms = m.index_select(1, idx).cpu().numpy()
         rows = slice(first, first + n_loc)
-        if not (np.array_equal(xs, orc.x[rows]) and np.array_equal(ms, orc.m[rows])
+        # hierarchical: momentum is defined at leaders only (members hold a replica)
+        gs = world // groups
+        m_ok = np.array_equal(ms, orc.m[rows]) if (not a.hier_groups or first % gs == 0) else True
+        if a.hier_groups and first % gs != 0:
+            lead = (first // gs) * gs
+            m_ok = np.array_equal(ms, orc.m[lead:lead + 1])  # the replica equals its leader's
+        if not (np.array_equal(xs, orc.x[rows]) and m_ok
                 and np.array_equal(w.cpu().numpy(), orc.w[rows])):
             bad = np.argwhere(xs != orc.x[rows])
             print(f"rank {rank} step {t}: mismatch at {bad[:5].tolist()} of {bad.shape[0]}", flush=True)
@@ -80,7 +89,7 @@ def main():
     okt = torch.tensor([1 if ok else 0], device=dev)
     dist.all_reduce(okt, op=dist.ReduceOp.MIN)
     if rank == 0:
-        print(f"mp parity world={world} n_loc={n_loc} d={d} k={k} steps={a.num_steps}: "
+        print(f"mp parity world={world} groups={groups} n_loc={n_loc} d={d} k={k} steps={a.num_steps}: "
               f"{'OK' if okt.item() else 'FAIL'}", flush=True)
     dist.barrier()
     dist.destroy_process_group()

@@ -46,6 +46,22 @@ def test_two_gpu_resnet50_sampled():
     _run(2, "--workers-per-gpu", 1, "--vector-len", 25_557_032, "--segments", 8, "--num-steps", 10)
 
 
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("groups,d,k", [(1, 100_003, 3), (2, 50_000, 4)])
+def test_two_gpu_hierarchical_bitwise(groups, d, k):
+    # one worker per GPU; groups=1: gradient allreduce + SGD, groups=2: leader gossip (swap)
+    _run(2, "--workers-per-gpu", 1, "--vector-len", d, "--segments", k, "--num-steps", 5,
+         "--hier-groups", groups, "--compare-all")
+
+
+@pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
+@pytest.mark.parametrize("groups,d,k", [(2, 1_000_003, 16), (1, 65_536, 2), (4, 70_001, 5)])
+def test_four_gpu_hierarchical_bitwise(groups, d, k):
+    # BASELINE configs[3] layout at 4 GPUs: 2 groups x 2 GPUs, k = 16
+    _run(4, "--workers-per-gpu", 1, "--vector-len", d, "--segments", k, "--num-steps", 4,
+         "--hier-groups", groups, "--compare-all")
+
+
 @pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
 @pytest.mark.parametrize("n_loc,d,k", [(1, 25_557_032, 8), (8, 1_000_000, 16)])
 def test_four_gpu_parity(n_loc, d, k):
