@@ -580,6 +580,7 @@ int cs_set_step(int64_t step) {
   if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
   if (step < 0 || step >= (int64_t(1) << 32)) return fail(CS_EINVAL, "step outside [0, 2^32)");
   g.step = step;
+  g.peer.need_sync = true;  // resumed state: re-replicate leaders to members on the next hier step
   return CS_OK;
 }
 

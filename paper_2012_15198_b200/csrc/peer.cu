@@ -513,6 +513,67 @@ __global__ void __launch_bounds__(kHierThreads) k_hier_reduce(const HierArgs h) 
   }
 }
 
+// Replica sync (first hierarchical step after bind / set_step): the leader copies its
+// x, m and psw into every member's sync buffers and publishes d3; members wait for it
+// and take the copy.  Afterwards the members are exact replicas of their leader, which
+// is what "the gossiped model parameter of the leader node propagates to other
+// workers" leaves them as after every step.
+struct SyncArgs {
+  HierArgs h;
+  float* x;
+  float* m;
+  float* psw;
+  int64_t ld;
+  int k;
+  uint32_t c3_target;
+  size_t off_xsync, off_msync, off_wsync, off_d3, off_c3;
+};
+
+__global__ void __launch_bounds__(kHierThreads) k_hier_sync(const SyncArgs sa) {
+  const HierArgs& h = sa.h;
+  const int grp = h.rank / h.gs, member = h.rank - grp * h.gs, gbase = grp * h.gs;
+  char* mine = h.peers[h.rank];
+  const int64_t nv = (h.d + 3) / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (member == 0) {
+    for (int c = 1; c < h.gs; ++c) {
+      char* dst = h.peers[gbase + c];
+      for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
+        const int64_t j = 4 * v;
+        const int valid = (int)imin64(4, h.d - j);
+        st4(reinterpret_cast<float*>(dst + sa.off_xsync) + j, ld4_valid(sa.x + j, valid), valid);
+        st4(reinterpret_cast<float*>(dst + sa.off_msync) + j, ld4_valid(sa.m + j, valid), valid);
+      }
+      if (blockIdx.x == 0)
+        for (int s = threadIdx.x; s < sa.k; s += blockDim.x)
+          reinterpret_cast<float*>(dst + sa.off_wsync)[s] = sa.psw[s];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      publish_when_last(h.peers, mine, sa.off_c3, sa.off_d3, h.rank, gbase, h.gs, h.epoch, sa.c3_target);
+  } else {
+    __shared__ int s_timeout;
+    if (threadIdx.x == 0) {
+      s_timeout = 0;
+      if (!wait_acquire(reinterpret_cast<const uint32_t*>(mine + sa.off_d3) + gbase, h.epoch)) s_timeout = 1;
+    }
+    __syncthreads();
+    if (s_timeout) {
+      if (threadIdx.x == 0) atomicOr(h.err + kErrTimeout, 1);
+      return;
+    }
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
+      const int64_t j = 4 * v;
+      const int valid = (int)imin64(4, h.d - j);
+      st4(sa.x + j, ld4_valid(reinterpret_cast<const float*>(mine + sa.off_xsync) + j, valid), valid);
+      st4(sa.m + j, ld4_valid(reinterpret_cast<const float*>(mine + sa.off_msync) + j, valid), valid);
+    }
+    if (blockIdx.x == 0)
+      for (int s = threadIdx.x; s < sa.k; s += blockDim.x)
+        sa.psw[s] = __ldcg(reinterpret_cast<const float*>(mine + sa.off_wsync) + s);
+  }
+}
+
 }  // namespace
 
 const char* peer_error() { return g_peer_err.c_str(); }
@@ -550,6 +611,10 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
     p.off_gbox = off;
     p.off_gbar = align_up(p.off_gbox + sizeof(float) * (size_t)gs * p.chunk, 256);
     off = align_up(p.off_gbar + sizeof(float) * (size_t)(ld > gs * p.chunk ? ld : gs * p.chunk), 256);
+    p.off_xsync = off;
+    p.off_msync = align_up(p.off_xsync + sizeof(float) * (size_t)ld, 256);
+    p.off_wsync = align_up(p.off_msync + sizeof(float) * (size_t)ld, 256);
+    off = align_up(p.off_wsync + sizeof(float) * (size_t)k, 256);
   }
   auto flags = [&](size_t& o) {
     o = off;
@@ -559,11 +624,13 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   flags(p.off_pdone);
   flags(p.off_d1);
   flags(p.off_d2);
+  flags(p.off_d3);
   p.off_count = off;
   p.off_pcount = off + 64;
   p.off_c1 = off + 128;
   p.off_c2 = off + 192;
-  p.bytes = align_up(off + 256, 4096);
+  p.off_c3 = off + 256;
+  p.bytes = align_up(off + 320, 4096);
   cudaError_t e = cudaMalloc(&p.base, p.bytes);
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region cudaMalloc", e);
   e = cudaMemset(p.base, 0, p.bytes);  // inbox padding is read by 16-byte-rounded bulk copies
@@ -739,6 +806,23 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   b.gs = p.gs;
   PeerKernelArgs ka = kernel_args(p, b, epoch, !exchange);
   if (ev0) cudaEventRecord(ev0, st);
+  if (p.need_sync && p.gs > 1) {  // members become exact replicas of their leader
+    SyncArgs sa;
+    sa.h = h;
+    sa.x = a.x;
+    sa.m = a.m;
+    sa.psw = a.psw;
+    sa.ld = a.ld;
+    sa.k = a.k;
+    sa.c3_target = (p.tot_c3 += (uint32_t)p.grid_hier);
+    sa.off_xsync = p.off_xsync;
+    sa.off_msync = p.off_msync;
+    sa.off_wsync = p.off_wsync;
+    sa.off_d3 = p.off_d3;
+    sa.off_c3 = p.off_c3;
+    k_hier_sync<<<p.grid_hier, kHierThreads, 0, st>>>(sa);
+  }
+  p.need_sync = false;
   const int64_t scatter_v = p.chunk / 4 * p.gs;
   int gsc = (int)((scatter_v + kHierThreads - 1) / kHierThreads);
   if (gsc > p.grid_hier) gsc = p.grid_hier;

@@ -43,6 +43,9 @@ struct PeerState {
   size_t off_pdone = 0, off_pcount = 0;                  // push-complete epochs, push arrivals
   size_t off_gbox = 0, off_gbar = 0;                     // hierarchical gradient buffers
   size_t off_d1 = 0, off_c1 = 0, off_d2 = 0, off_c2 = 0; // hierarchical phase epochs / arrivals
+  size_t off_xsync = 0, off_msync = 0, off_wsync = 0;    // leader -> member replica sync buffers
+  size_t off_d3 = 0, off_c3 = 0;
+  bool need_sync = true;   // next hierarchical step first copies each leader's state to its members
   char* base = nullptr;                 // this GPU's region
   std::vector<char*> peer_base;         // mapped regions of every rank (own at [rank])
   char** d_peer_base = nullptr;         // device copy
@@ -50,7 +53,7 @@ struct PeerState {
   int32_t* d_seg_t0 = nullptr;          // [k+1] first tile index of each segment
   uint32_t epoch = 0;                   // multi-GPU steps issued since bind
   // running totals of CTAs launched against each arrival counter (kernel targets)
-  uint32_t tot_count = 0, tot_pcount = 0, tot_c1 = 0, tot_c2 = 0;
+  uint32_t tot_count = 0, tot_pcount = 0, tot_c1 = 0, tot_c2 = 0, tot_c3 = 0;
 };
 
 // gs: GPUs per hierarchical group when a hierarchical step is possible (one worker

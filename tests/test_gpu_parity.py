@@ -312,7 +312,7 @@ def test_each_path_bitwise(path, n, d, k, ld):
         orc.step(LR, MU)
     cs.cs_sync()
     name, _ = cs.cs_kernel_info()
-    assert name == {"reg": "k_gossip_local", "tma": "k_gossip_tma", "peer": "k_gossip_peer"}[path]
+    assert name == {"reg": "k_gossip_local", "tma": "k_gossip_tma", "peer": "k_peer_push+k_peer_mix"}[path]
     xg = x.cpu().numpy()
     assert np.array_equal(xg[:, :d], orc.x)
     assert np.array_equal(m.cpu().numpy()[:, :d], orc.m)
