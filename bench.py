@@ -44,6 +44,8 @@ WORKLOADS = {
     "c1": (8, 1_000_000, 4, "8 workers x 1M fp32, k=4 (BASELINE configs[0])"),
     "c2": (16, 11_689_512, 8, "16 workers x ResNet-18-sized 11,689,512 fp32, k=8 (BASELINE configs[1])"),
     "c3": (1, 25_557_032, 8, "1 worker/GPU x ResNet-50-sized 25,557,032 fp32, k=8 (BASELINE configs[2])"),
+    "c4": (1, 25_557_032, 16, "hierarchical: 1 worker/GPU, groups of 4 GPUs (or all GPUs if fewer), "
+                              "ResNet-50-sized 25,557,032 fp32, k=16 (BASELINE configs[3])"),
     "c5": (8, 25_557_032, 8, "8 workers/GPU x ResNet-50-sized 25,557,032 fp32 (BASELINE configs[4])"),
 }
 
@@ -255,7 +257,10 @@ def main():
     first = rank * n_loc
     B = world + 1
 
-    cs.cs_init(world, world, k, seed)
+    hier = args.config == "c4"
+    groups = max(1, world // 4) if hier else world
+    cs.cs_init(world, groups, k, seed)
+    step_fn = cs.cs_hier_step if hier else cs.cs_gossip_step
     cs.cs_set_path({"auto": 0, "reg": 1, "tma": 2, "peer": 3}[args.path])
     stream = torch.cuda.Stream(dev)
     with torch.cuda.stream(stream):
@@ -282,7 +287,7 @@ def main():
 
     t = 0
     for _ in range(args.warmup):
-        cs.cs_gossip_step(x, grads(t), w, lr, mu)
+        step_fn(x, grads(t), w, lr, mu)
         t += 1
     cs.cs_sync()
     barrier()
@@ -291,7 +296,7 @@ def main():
     hbm_b, nvl_b = 0.0, 0.0
     nvl_max = []
     for s in range(t, t + args.steps):
-        hb, nb = cs.cs_step_bytes(s, False)
+        hb, nb = cs.cs_step_bytes(s, hier)
         hbm_b += hb
         nvl_max.append(nb)
     cs.cs_set_timing(True)
@@ -301,7 +306,7 @@ def main():
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            cs.cs_gossip_step(x, grads(t), w, lr, mu)
+            step_fn(x, grads(t), w, lr, mu)
             t += 1
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -359,7 +364,7 @@ def main():
             with torch.cuda.stream(stream):
                 for _ in range(esteps):
                     stage.copy_(hgrads(t), non_blocking=True)
-                    cs.cs_gossip_step(x, stage, w, lr, mu)
+                    step_fn(x, stage, w, lr, mu)
                     wout.copy_(w, non_blocking=True)
                     stream.synchronize()
                     t += 1

@@ -679,12 +679,20 @@ int cs_step_bytes(int64_t step, int hier, double* out) {
       for (int i = g.first; i < g.first + g.n_loc; ++i)
         if (src[(size_t)s * g.world + i] / g.n_loc != g.rank) nvl += 4.0 * (double)(b[s + 1] - b[s]);
     out[1] = nvl;
-  } else {
+  } else if (g.nprocs == 1) {
     const int gs = g.world / g.groups;
     const int L_loc = g.n_loc / gs > 0 ? g.n_loc / gs : 1;
     // read members' g, leaders' x and m; write leaders' m and every member's x
     out[0] = (4.0 * g.n_loc + 12.0 * L_loc + 4.0 * g.n_loc) * d;
     out[1] = 0.0;
+  } else {
+    // one worker per GPU: the group mean needs every member's g (reduce-scatter +
+    // all-gather, (gs-1)/gs of 4 B each way), then the leader exchange (4 B per
+    // parameter when there are >= 2 groups); HBM as a flat step on the group mean
+    const int gs = g.world / g.groups;
+    const double frac = (double)(gs - 1) / (double)gs;
+    out[0] = 20.0 * d;
+    out[1] = 2.0 * 4.0 * frac * d + (g.groups >= 2 ? 4.0 * d : 0.0);
   }
   return CS_OK;
 }
