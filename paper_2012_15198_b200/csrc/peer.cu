@@ -54,6 +54,7 @@
 #include "common.cuh"
 #include "peer.cuh"
 #include "ptx.cuh"
+#include "topo_device.cuh"
 
 namespace cs {
 
@@ -85,8 +86,11 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 size_t push_smem_bytes(int k, int n_loc) {
   size_t b = kRingBytes + sizeof(int64_t) * (k + 1) + sizeof(int32_t) * (k + 1);
   if ((int64_t)k * n_loc <= kMaxRecvSmem) b += sizeof(int32_t) * (size_t)k * n_loc;
+  b += sizeof(uint32_t) * 128 * (kPushThreads / 32);  // per-warp Alg. 2 scratch
   return align_up(b, 16);
 }
+
+bool fused_topo_ok(int ntop, int k, int n_loc) { return ntop <= 64 && (int64_t)k * n_loc <= kMaxRecvSmem; }
 
 // wait until (int32)(*p - target) >= 0 polling relaxed, then acquire; false on timeout
 __device__ bool wait_acquire(const uint32_t* p, uint32_t target) {
@@ -127,6 +131,7 @@ struct PeerKernelArgs {
   uint32_t done_target;     // arrival targets (see publish_when_last)
   uint32_t pdone_target;
   int final_only;           // hierarchical with one group: x = y, no exchange
+  int fused_topo;           // draw the topology in the push prologue (<= 64 ranks)
   size_t off_inbox, off_wbox, off_done, off_count, off_pdone, off_pcount, off_d2;
 };
 
@@ -255,11 +260,38 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
     bnd[i] = a.bounds[i];
     t0[i] = a.seg_t0[i];
   }
-  if (!M.recv_global && !a.final_only)
-    for (int i = threadIdx.x; i < s.k * s.n_loc; i += blockDim.x) {
-      const int sg = i / s.n_loc, r = i - sg * s.n_loc;
-      recv[i] = receiver_worker(s, sg, r);
+  if (!M.recv_global && !a.final_only) {
+    if (a.fused_topo) {
+      // draw this step's topologies here (Alg. 2): one warp per segment,
+      // then keep only where this GPU's workers send (send_to, Alg.1 l.6)
+      const int ntop = s.gs > 0 ? s.groups : s.world;
+      const int nwarps = blockDim.x >> 5;
+      uint32_t* u = reinterpret_cast<uint32_t*>(recv + s.k * s.n_loc) + warp * 128;
+      int32_t* srow = reinterpret_cast<int32_t*>(u + 64);
+      for (int sg = warp; sg < s.k; sg += nwarps) {
+        if (s.given != nullptr) {
+          for (int i = lane; i < ntop; i += 32) srow[i] = s.given[(int64_t)sg * ntop + i];
+          __syncwarp();
+        } else {
+          warp_alg2_small(s.seed, s.step, sg, ntop, s.gs > 0 ? CS_TAG_HIER : CS_TAG_FLAT, u, srow, s.err);
+        }
+        for (int r = lane; r < s.n_loc; r += 32) {
+          const int grp = s.gs > 0 ? s.rank / s.gs : 0;
+          const int target = s.gs > 0 ? grp : s.first + r;
+          int to = 0;
+          for (int jj = 0; jj < ntop; ++jj)
+            if (srow[jj] == target) to = jj;
+          recv[sg * s.n_loc + r] = s.gs > 0 ? to * s.gs + (s.rank - grp * s.gs) : to;
+        }
+        __syncwarp();
+      }
+    } else {
+      for (int i = threadIdx.x; i < s.k * s.n_loc; i += blockDim.x) {
+        const int sg = i / s.n_loc, r = i - sg * s.n_loc;
+        recv[i] = receiver_worker(s, sg, r);
+      }
     }
+  }
   if (threadIdx.x == 0) {
     s_timeout = 0;
     for (int i = 0; i < kStagesA; ++i) {
@@ -406,12 +438,13 @@ __global__ void __launch_bounds__(kMixThreads) k_peer_mix(const PeerKernelArgs a
     const int64_t total = nv * s.n_loc;
     const float* inbox0 = reinterpret_cast<const float*>(mine + a.off_inbox) + (int64_t)par * s.n_loc * s.ld;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < total; base += 2 * stride) {
-      float4 yo[2], yi[2];
-      int64_t off[2];
-      int valid[2];
+    constexpr int U = 4;  // float4 pairs in flight per thread
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < total; base += U * stride) {
+      float4 yo[U], yi[U];
+      int64_t off[U];
+      int valid[U];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < U; ++h) {
         const int64_t idx = base + h * stride;
         valid[h] = 0;
         if (idx < total) {
@@ -424,7 +457,7 @@ __global__ void __launch_bounds__(kMixThreads) k_peer_mix(const PeerKernelArgs a
         }
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+      for (int h = 0; h < U; ++h)
         if (valid[h] > 0) st4_cs(s.x + off[h], mean4(yo[h], yi[h]), valid[h]);
     }
     if (blockIdx.x == 0) {
@@ -719,6 +752,7 @@ PeerKernelArgs kernel_args(const PeerState& p, const PeerStepArgs& a, uint32_t e
   ka.n_tiles = p.n_tiles;
   ka.epoch = epoch;
   ka.final_only = final_only ? 1 : 0;
+  ka.fused_topo = fused_topo_ok(a.gs > 0 ? a.groups : a.world, a.k, a.n_loc) ? 1 : 0;
   ka.off_inbox = p.off_inbox;
   ka.off_wbox = p.off_wbox;
   ka.off_done = p.off_done;
@@ -766,7 +800,8 @@ int launch_push_mix(PeerState& p, PeerKernelArgs ka, cudaStream_t st) {
 
 int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEvent_t ev0,
                    cudaEvent_t ev1) {
-  int rc = launch_topology_for(a, a.world, CS_TAG_FLAT, st);
+  int rc = CS_OK;
+  if (!fused_topo_ok(a.world, a.k, a.n_loc)) rc = launch_topology_for(a, a.world, CS_TAG_FLAT, st);
   if (rc) return rc;
   PeerKernelArgs ka = kernel_args(p, a, ++p.epoch, false);
   ka.s.gs = 0;
@@ -780,7 +815,7 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
                    cudaEvent_t ev1) {
   if (p.gs <= 0 || a.n_loc != 1) return perr(CS_EUNSUPPORTED, "multi-GPU hierarchical step needs one worker per GPU", cudaSuccess);
   const bool exchange = a.groups >= 2;
-  if (exchange) {
+  if (exchange && !fused_topo_ok(a.groups, a.k, a.n_loc)) {
     int rc = launch_topology_for(a, a.groups, CS_TAG_HIER, st);
     if (rc) return rc;
   }
