@@ -260,38 +260,6 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
     bnd[i] = a.bounds[i];
     t0[i] = a.seg_t0[i];
   }
-  if (!M.recv_global && !a.final_only) {
-    if (a.fused_topo) {
-      // draw this step's topologies here (Alg. 2): one warp per segment,
-      // then keep only where this GPU's workers send (send_to, Alg.1 l.6)
-      const int ntop = s.gs > 0 ? s.groups : s.world;
-      const int nwarps = blockDim.x >> 5;
-      uint32_t* u = reinterpret_cast<uint32_t*>(recv + s.k * s.n_loc) + warp * 128;
-      int32_t* srow = reinterpret_cast<int32_t*>(u + 64);
-      for (int sg = warp; sg < s.k; sg += nwarps) {
-        if (s.given != nullptr) {
-          for (int i = lane; i < ntop; i += 32) srow[i] = s.given[(int64_t)sg * ntop + i];
-          __syncwarp();
-        } else {
-          warp_alg2_small(s.seed, s.step, sg, ntop, s.gs > 0 ? CS_TAG_HIER : CS_TAG_FLAT, u, srow, s.err);
-        }
-        for (int r = lane; r < s.n_loc; r += 32) {
-          const int grp = s.gs > 0 ? s.rank / s.gs : 0;
-          const int target = s.gs > 0 ? grp : s.first + r;
-          int to = 0;
-          for (int jj = 0; jj < ntop; ++jj)
-            if (srow[jj] == target) to = jj;
-          recv[sg * s.n_loc + r] = s.gs > 0 ? to * s.gs + (s.rank - grp * s.gs) : to;
-        }
-        __syncwarp();
-      }
-    } else {
-      for (int i = threadIdx.x; i < s.k * s.n_loc; i += blockDim.x) {
-        const int sg = i / s.n_loc, r = i - sg * s.n_loc;
-        recv[i] = receiver_worker(s, sg, r);
-      }
-    }
-  }
   if (threadIdx.x == 0) {
     s_timeout = 0;
     for (int i = 0; i < kStagesA; ++i) {
@@ -305,18 +273,58 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
     ptx::mbar_fence_init();
   }
   __syncthreads();
-  // ping-pong safety: every GPU finished its mix of epoch e-2, the last reader of this parity
-  if (threadIdx.x < s.nprocs && e >= 3) {
-    const uint32_t* done = reinterpret_cast<const uint32_t*>(mine + a.off_done);
-    if (!wait_acquire(done + threadIdx.x, e - 2)) atomicOr(&s_timeout, 1);
+  constexpr int kLoadWarp = kCompute / 32;
+  if (warp == kLoadWarp) {
+    // the load warp starts streaming at once; hierarchical: it is the only reader of the
+    // group mean (gbar), so it alone waits for it to be complete on this GPU
+    if (s.gs > 0 && lane < s.gs) {
+      const uint32_t* d2 = reinterpret_cast<const uint32_t*>(mine + a.off_d2);
+      const int gbase = (s.rank / s.gs) * s.gs;
+      if (!wait_acquire(d2 + gbase + lane, e)) atomicOr(&s_timeout, 1);
+    }
+    __syncwarp();
+  } else {
+    // meanwhile the other warps draw the receivers table ...
+    const int gw = warp < kLoadWarp ? warp : warp - 1, nw = (kPushThreads >> 5) - 1;
+    if (!M.recv_global && !a.final_only) {
+      if (a.fused_topo) {
+        // this step's topologies (Alg. 2): one warp per segment, then
+        // keep only where this GPU's workers send (send_to, Alg.1 l.6)
+        const int ntop = s.gs > 0 ? s.groups : s.world;
+        uint32_t* u = reinterpret_cast<uint32_t*>(recv + s.k * s.n_loc) + gw * 128;
+        int32_t* srow = reinterpret_cast<int32_t*>(u + 64);
+        for (int sg = gw; sg < s.k; sg += nw) {
+          if (s.given != nullptr) {
+            for (int i = lane; i < ntop; i += 32) srow[i] = s.given[(int64_t)sg * ntop + i];
+            __syncwarp();
+          } else {
+            warp_alg2_small(s.seed, s.step, sg, ntop, s.gs > 0 ? CS_TAG_HIER : CS_TAG_FLAT, u, srow, s.err);
+          }
+          for (int r = lane; r < s.n_loc; r += 32) {
+            const int grp = s.gs > 0 ? s.rank / s.gs : 0;
+            const int target = s.gs > 0 ? grp : s.first + r;
+            int to = 0;
+            for (int jj = 0; jj < ntop; ++jj)
+              if (srow[jj] == target) to = jj;
+            recv[sg * s.n_loc + r] = s.gs > 0 ? to * s.gs + (s.rank - grp * s.gs) : to;
+          }
+          __syncwarp();
+        }
+      } else {
+        for (int i = gw * 32 + lane; i < s.k * s.n_loc; i += nw * 32) {
+          const int sg = i / s.n_loc, r = i - sg * s.n_loc;
+          recv[i] = receiver_worker(s, sg, r);
+        }
+      }
+    }
+    // ... and make sure every GPU finished its mix of epoch e-2 (the last reader of the
+    // inbox parity this step writes) before anything is pushed
+    if (threadIdx.x < s.nprocs && e >= 3) {
+      const uint32_t* done = reinterpret_cast<const uint32_t*>(mine + a.off_done);
+      if (!wait_acquire(done + threadIdx.x, e - 2)) atomicOr(&s_timeout, 1);
+    }
+    ptx::named_bar_sync(1, kPushThreads - 32);
   }
-  // hierarchical: the group's mean gradient (gbar) is complete on this GPU
-  if (s.gs > 0 && threadIdx.x < s.gs) {
-    const uint32_t* d2 = reinterpret_cast<const uint32_t*>(mine + a.off_d2);
-    const int gbase = (s.rank / s.gs) * s.gs;
-    if (!wait_acquire(d2 + gbase + threadIdx.x, e)) atomicOr(&s_timeout, 1);
-  }
-  __syncthreads();
 
   if (warp < kCompute / 32) {
     // ---------------- compute warps: m', y; y -> x and the y ring --------------------
