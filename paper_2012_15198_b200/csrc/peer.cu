@@ -109,15 +109,19 @@ __device__ bool wait_acquire(const uint32_t* p, uint32_t target) {
 // the CTA that brings it to `target` (the host's running total of CTAs launched
 // against that counter, so launches of any grid size may interleave) publishes
 // `epoch` at word [rank] of `flag_off` on the GPUs [first, first + count).
+// (`copies` flag arrays `stride` bytes apart are published: every piece of a step
+// that had nothing to exchange.)
 __device__ void publish_when_last(char* const* peers, char* mine, size_t count_off, size_t flag_off, int rank,
-                                  int first, int count, uint32_t epoch, uint32_t target) {
+                                  int first, int count, uint32_t epoch, uint32_t target, int copies = 1,
+                                  size_t stride = 0) {
   __threadfence();
   uint32_t* cnt = reinterpret_cast<uint32_t*>(mine + count_off);
   const uint32_t prev = atomicAdd(cnt, 1u);
   if (prev + 1 == target) {
     __threadfence_system();
-    for (int p = first; p < first + count; ++p)
-      ptx::st_release_sys(reinterpret_cast<uint32_t*>(peers[p] + flag_off) + rank, epoch);
+    for (int c = 0; c < copies; ++c)
+      for (int p = first; p < first + count; ++p)
+        ptx::st_release_sys(reinterpret_cast<uint32_t*>(peers[p] + flag_off + c * stride) + rank, epoch);
   }
 }
 
@@ -127,6 +131,10 @@ struct PeerKernelArgs {
   const int64_t* bounds;    // [k+1] segment bounds
   const int32_t* seg_t0;    // [k+1] first tile of each segment (seg_t0[k] = n_tiles)
   int n_tiles;
+  int tile_lo, tile_hi;     // this launch's piece of the step: tiles [tile_lo, tile_hi)
+  int pieces;               // pieces per step and the stride of their flag arrays
+  size_t flag_stride;
+  int64_t col_lo, col_hi;   // ... = columns [col_lo, col_hi)
   uint32_t epoch;           // this step's epoch (>= 1)
   uint32_t done_target;     // arrival targets (see publish_when_last)
   uint32_t pdone_target;
@@ -242,7 +250,8 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
   const uint32_t e = a.epoch;
   const int par = (int)(e & 1u);
   char* mine = a.peers[s.rank];
-  const int n_units = a.n_tiles * s.n_loc;
+  const int u_lo = a.tile_lo * s.n_loc;
+  const int n_units = (a.tile_hi - a.tile_lo) * s.n_loc;
   const int G = gridDim.x;
   const int n_my = blockIdx.x < n_units ? (n_units - blockIdx.x + G - 1) / G : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -332,7 +341,7 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
     const int tid = threadIdx.x;
     int cur = 0;
     for (int i = 0; i < n_my && !*timeout; ++i) {
-      const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
+      const Unit U = unit_at(a, M, u_lo + blockIdx.x + i * G, cur);
       const int st = i % kStagesA, sy = i % kSlotsY;
       ptx::mbar_wait(&a_full[st], (uint32_t)((i / kStagesA) & 1));
       if (!a.final_only) ptx::mbar_wait(&y_empty[sy], (uint32_t)(((i / kSlotsY) & 1) ^ 1));
@@ -383,7 +392,7 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
       ptx::fence_proxy_async_global();  // acquired gbar (hierarchical) -> bulk-copy reads
       int cur = 0;
       for (int i = 0; i < n_my && !*timeout; ++i) {
-        const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
+        const Unit U = unit_at(a, M, u_lo + blockIdx.x + i * G, cur);
         const int st = i % kStagesA;
         ptx::mbar_wait(&a_empty[st], (uint32_t)(((i / kStagesA) & 1) ^ 1));
         const uint32_t bytes = (uint32_t)(((U.len + 3) & ~3) * 4);
@@ -401,7 +410,7 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
     if (lane == 0) {
       int cur = 0;
       for (int i = 0; i < n_my && !*timeout; ++i) {
-        const Unit U = unit_at(a, M, blockIdx.x + i * G, cur);
+        const Unit U = unit_at(a, M, u_lo + blockIdx.x + i * G, cur);
         const int sy = i % kSlotsY;
         ptx::mbar_wait(&y_full[sy], (uint32_t)((i / kSlotsY) & 1));
         int rp, rl;
@@ -421,8 +430,9 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
   __syncthreads();
   if (threadIdx.x == 0) {
     if (s_timeout) atomicOr(s.err + kErrTimeout, 1);
-    if (a.final_only)  // nothing to exchange: this step is complete
-      publish_when_last(a.peers, mine, a.off_count, a.off_done, s.rank, 0, s.nprocs, e, a.done_target);
+    if (a.final_only)  // nothing to exchange: this step is complete, for every piece
+      publish_when_last(a.peers, mine, a.off_count, a.off_done, s.rank, 0, s.nprocs, e, a.done_target,
+                        a.pieces, a.flag_stride);
     else  // every CTA's pushes have landed: publish them
       publish_when_last(a.peers, mine, a.off_pcount, a.off_pdone, s.rank, 0, s.nprocs, e, a.pdone_target);
   }
@@ -442,7 +452,7 @@ __global__ void __launch_bounds__(kMixThreads) k_peer_mix(const PeerKernelArgs a
   }
   __syncthreads();
   if (!s_timeout) {
-    const int64_t nv = (s.d + 3) >> 2;
+    const int64_t nv = (a.col_hi - a.col_lo + 3) >> 2;
     const int64_t total = nv * s.n_loc;
     const float* inbox0 = reinterpret_cast<const float*>(mine + a.off_inbox) + (int64_t)par * s.n_loc * s.ld;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -457,8 +467,8 @@ __global__ void __launch_bounds__(kMixThreads) k_peer_mix(const PeerKernelArgs a
         valid[h] = 0;
         if (idx < total) {
           const int64_t r = idx / nv, v = idx - r * nv;
-          const int64_t j = 4 * v;
-          valid[h] = (int)imin64(4, s.d - j);
+          const int64_t j = a.col_lo + 4 * v;
+          valid[h] = (int)imin64(4, a.col_hi - j);
           off[h] = r * s.ld + j;
           yo[h] = __ldcs(reinterpret_cast<const float4*>(s.x + off[h]));
           yi[h] = __ldcs(reinterpret_cast<const float4*>(inbox0 + off[h]));
@@ -468,9 +478,10 @@ __global__ void __launch_bounds__(kMixThreads) k_peer_mix(const PeerKernelArgs a
       for (int h = 0; h < U; ++h)
         if (valid[h] > 0) st4_cs(s.x + off[h], mean4(yo[h], yi[h]), valid[h]);
     }
-    if (blockIdx.x == 0) {
+    if (blockIdx.x == 0) {  // weights of the segments whose first tile is in this piece
       for (int i = threadIdx.x; i < s.n_loc * s.k; i += blockDim.x) {
         const int r = i / s.k, sg = i - r * s.k;
+        if (a.seg_t0[sg] < a.tile_lo || a.seg_t0[sg] >= a.tile_hi) continue;
         const float* wbox = reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * s.n_loc + r) * s.k;
         float* wp = s.psw + (int64_t)r * s.k + sg;
         *wp = __fmul_rn(__fadd_rn(*wp, __ldcg(wbox + sg)), 0.5f);
@@ -643,6 +654,8 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   }
   seg_t0[k] = n_tiles;
   p.n_tiles = n_tiles;
+  p.h_bounds = bounds;
+  p.h_seg_t0 = seg_t0;
   if (gs > 0) p.chunk = ((d + gs - 1) / gs + 3) / 4 * 4;
 
   p.off_inbox = 0;
@@ -661,17 +674,21 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
     o = off;
     off = align_up(off + sizeof(uint32_t) * (size_t)nprocs, 256);
   };
-  flags(p.off_done);
-  flags(p.off_pdone);
+  p.flag_stride = align_up(sizeof(uint32_t) * (size_t)nprocs, 256);
+  p.off_done = off;
+  off += PeerState::kMaxPieces * p.flag_stride;
+  p.off_pdone = off;
+  off += PeerState::kMaxPieces * p.flag_stride;
   flags(p.off_d1);
   flags(p.off_d2);
   flags(p.off_d3);
-  p.off_count = off;
-  p.off_pcount = off + 64;
-  p.off_c1 = off + 128;
-  p.off_c2 = off + 192;
-  p.off_c3 = off + 256;
-  p.bytes = align_up(off + 320, 4096);
+  p.off_count = off;                           // [kMaxPieces] counters, 64 B apart
+  p.off_pcount = off + 64 * PeerState::kMaxPieces;
+  off += 2 * 64 * PeerState::kMaxPieces;
+  p.off_c1 = off;
+  p.off_c2 = off + 64;
+  p.off_c3 = off + 128;
+  p.bytes = align_up(off + 192, 4096);
   cudaError_t e = cudaMalloc(&p.base, p.bytes);
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region cudaMalloc", e);
   e = cudaMemset(p.base, 0, p.bytes);  // inbox padding is read by 16-byte-rounded bulk copies
@@ -697,6 +714,26 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   p.grid_push = sms * occ_push < n_units ? sms * occ_push : n_units;
   p.grid_mix = sms * occ_mix;
   p.grid_hier = sms * occ_h;
+  // pieces: enough units per piece for every push CTA to pipeline a few (CS_PEER_PIECES overrides)
+  {
+    int P = n_units / (4 * p.grid_push);
+    const char* env = getenv("CS_PEER_PIECES");
+    if (env) P = atoi(env);
+    if (P < 1) P = 1;
+    if (P > 4 && !env) P = 4;
+    if (P > PeerState::kMaxPieces) P = PeerState::kMaxPieces;
+    if (P > p.n_tiles) P = p.n_tiles;
+    p.pieces = P;
+    p.piece_tile.resize(P + 1);
+    for (int q = 0; q <= P; ++q) p.piece_tile[q] = (int)((int64_t)q * p.n_tiles / P);
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    e = cudaStreamCreateWithPriority(&p.aux, cudaStreamNonBlocking, hi);
+    for (int q = 0; q < PeerState::kMaxPieces && e == cudaSuccess; ++q)
+      e = cudaEventCreateWithFlags(&p.ev_push[q], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.ev_mix, cudaEventDisableTiming);
+    if (e != cudaSuccess) return perr(CS_ECUDA, "aux stream / events", e);
+  }
   p.peer_base.assign(nprocs, nullptr);
   p.peer_base[rank] = p.base;
   p.allocated = true;
@@ -712,6 +749,13 @@ void peer_release(PeerState& p) {
   if (p.d_peer_base) cudaFree(p.d_peer_base);
   if (p.d_bounds) cudaFree(p.d_bounds);
   if (p.d_seg_t0) cudaFree(p.d_seg_t0);
+  if (p.aux) {
+    cudaStreamSynchronize(p.aux);
+    cudaStreamDestroy(p.aux);
+  }
+  for (int q = 0; q < PeerState::kMaxPieces; ++q)
+    if (p.ev_push[q]) cudaEventDestroy(p.ev_push[q]);
+  if (p.ev_mix) cudaEventDestroy(p.ev_mix);
   p = PeerState();
 }
 
@@ -763,6 +807,8 @@ PeerKernelArgs kernel_args(const PeerState& p, const PeerStepArgs& a, uint32_t e
   ka.fused_topo = fused_topo_ok(a.gs > 0 ? a.groups : a.world, a.k, a.n_loc) ? 1 : 0;
   ka.off_inbox = p.off_inbox;
   ka.off_wbox = p.off_wbox;
+  ka.pieces = p.pieces;
+  ka.flag_stride = p.flag_stride;
   ka.off_done = p.off_done;
   ka.off_count = p.off_count;
   ka.off_pdone = p.off_pdone;
@@ -791,15 +837,50 @@ int launch_topology_for(const PeerStepArgs& a, int n, int tag, cudaStream_t st) 
   return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "topology launch", e);
 }
 
-int launch_push_mix(PeerState& p, PeerKernelArgs ka, cudaStream_t st) {
-  if (ka.final_only) {
-    ka.done_target = (p.tot_count += (uint32_t)p.grid_push);
-  } else {
-    ka.pdone_target = (p.tot_pcount += (uint32_t)p.grid_push);
-    ka.done_target = (p.tot_count += (uint32_t)p.grid_mix);
+int64_t tile_col(const PeerState& p, int t) {
+  if (t >= p.n_tiles) return p.d;
+  int sg = 0;
+  while (p.h_seg_t0[sg + 1] <= t) ++sg;
+  return p.h_bounds[sg] + (int64_t)(t - p.h_seg_t0[sg]) * kPeerTile;
+}
+
+// push(q) on the caller's stream; mix(q) on the aux stream after push(q), so push(q+1)
+// overlaps mix(q); the caller's stream finally waits for the last mix.
+int launch_push_mix(PeerState& p, const PeerKernelArgs& ka, cudaStream_t st) {
+  const int P = ka.final_only ? 1 : p.pieces;
+  for (int q = 0; q < P; ++q) {
+    PeerKernelArgs kq = ka;
+    kq.tile_lo = P == 1 ? 0 : p.piece_tile[q];
+    kq.tile_hi = P == 1 ? p.n_tiles : p.piece_tile[q + 1];
+    kq.col_lo = tile_col(p, kq.tile_lo);
+    kq.col_hi = tile_col(p, kq.tile_hi);
+    kq.off_done = p.off_done + q * p.flag_stride;
+    kq.off_pdone = p.off_pdone + q * p.flag_stride;
+    kq.off_count = p.off_count + 64 * q;
+    kq.off_pcount = p.off_pcount + 64 * q;
+    const int units = (kq.tile_hi - kq.tile_lo) * ka.s.n_loc;
+    const int grid = p.grid_push < units ? p.grid_push : (units > 0 ? units : 1);
+    const size_t smem = push_smem_bytes(ka.s.k, ka.s.n_loc);
+    if (ka.final_only) {
+      kq.done_target = (p.tot_count[q] += (uint32_t)grid);
+      k_peer_push<<<grid, kPushThreads, smem, st>>>(kq);
+      continue;
+    }
+    kq.pdone_target = (p.tot_pcount[q] += (uint32_t)grid);
+    kq.done_target = (p.tot_count[q] += (uint32_t)p.grid_mix);
+    k_peer_push<<<grid, kPushThreads, smem, st>>>(kq);
+    if (P == 1) {
+      k_peer_mix<<<p.grid_mix, kMixThreads, 0, st>>>(kq);
+    } else {
+      cudaEventRecord(p.ev_push[q], st);
+      cudaStreamWaitEvent(p.aux, p.ev_push[q], 0);
+      k_peer_mix<<<p.grid_mix, kMixThreads, 0, p.aux>>>(kq);
+    }
   }
-  k_peer_push<<<p.grid_push, kPushThreads, push_smem_bytes(ka.s.k, ka.s.n_loc), st>>>(ka);
-  if (!ka.final_only) k_peer_mix<<<p.grid_mix, kMixThreads, 0, st>>>(ka);
+  if (P > 1) {
+    cudaEventRecord(p.ev_mix, p.aux);
+    cudaStreamWaitEvent(st, p.ev_mix, 0);
+  }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "push/mix launch", e);
 }

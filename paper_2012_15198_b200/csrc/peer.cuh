@@ -52,8 +52,22 @@ struct PeerState {
   int64_t* d_bounds = nullptr;          // [k+1] segment bounds
   int32_t* d_seg_t0 = nullptr;          // [k+1] first tile index of each segment
   uint32_t epoch = 0;                   // multi-GPU steps issued since bind
+  // The tiles of a step are cut into `pieces` contiguous ranges; push(p + 1) on the
+  // caller's stream overlaps mix(p) on `aux`.  Each piece has its own done / push-done
+  // flags ([nprocs] words at off_done / off_pdone + p * flag_stride) and arrival
+  // counters (off_count / off_pcount + 64 p).
+  static constexpr int kMaxPieces = 8;
+  int pieces = 1;
+  std::vector<int> piece_tile;          // [pieces + 1] tile boundaries
+  std::vector<int64_t> h_bounds;        // host copies of the segment bounds / first tiles
+  std::vector<int32_t> h_seg_t0;
+  size_t flag_stride = 0;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_push[kMaxPieces] = {};
+  cudaEvent_t ev_mix = nullptr;
   // running totals of CTAs launched against each arrival counter (kernel targets)
-  uint32_t tot_count = 0, tot_pcount = 0, tot_c1 = 0, tot_c2 = 0, tot_c3 = 0;
+  uint32_t tot_count[kMaxPieces] = {}, tot_pcount[kMaxPieces] = {};
+  uint32_t tot_c1 = 0, tot_c2 = 0, tot_c3 = 0;
 };
 
 // gs: GPUs per hierarchical group when a hierarchical step is possible (one worker

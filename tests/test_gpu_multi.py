@@ -21,11 +21,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _run(nproc, *args, timeout=600):
+def _run(nproc, *args, timeout=600, env=None):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "mp_gossip_worker.py"),
            *[str(a) for a in args]]
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT,
+                       env={**os.environ, **(env or {})})
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
     assert "OK" in p.stdout
 
@@ -44,6 +45,16 @@ def test_two_gpu_parity(n_loc, d, k, steps, full):
 def test_two_gpu_resnet50_sampled():
     # BASELINE configs[2] layout (one worker per GPU, 25,557,032 fp32, k = 8)
     _run(2, "--workers-per-gpu", 1, "--vector-len", 25_557_032, "--segments", 8, "--num-steps", 10)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("pieces", [3, 8])
+def test_two_gpu_pieces_bitwise(pieces):
+    # push(p+1) / mix(p) overlap across the caller's and the aux stream, across GPUs
+    _run(2, "--workers-per-gpu", 2, "--vector-len", 300_001, "--segments", 6, "--num-steps", 5,
+         "--compare-all", env={"CS_PEER_PIECES": str(pieces)})
+    _run(2, "--workers-per-gpu", 1, "--vector-len", 200_000, "--segments", 4, "--num-steps", 4,
+         "--hier-groups", 2, "--compare-all", env={"CS_PEER_PIECES": str(pieces)})
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")

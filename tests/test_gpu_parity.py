@@ -320,6 +320,22 @@ def test_each_path_bitwise(path, n, d, k, ld):
     assert np.all(xg[:, d:] == 3.0)
 
 
+@pytest.mark.parametrize("pieces", [2, 3, 8])
+def test_peer_path_pieces_bitwise(pieces, monkeypatch):
+    # the step cut into pieces: push(p+1) on the caller's stream overlaps mix(p) on the aux stream
+    monkeypatch.setenv("CS_PEER_PIECES", str(pieces))
+    n, d, k = 3, 70_003, 5
+    x, m, w, bank2 = _bind(n, d, k, 23, path=PATHS["peer"])
+    orc = OracleRun(n, d, k, 23)
+    for t in range(5):
+        cs.cs_gossip_step(x, grads_view(bank2, n, t), w, LR, MU)
+        orc.step(LR, MU)
+    cs.cs_sync()
+    assert np.array_equal(x.cpu().numpy()[:, :d], orc.x)
+    assert np.array_equal(m.cpu().numpy()[:, :d], orc.m)
+    assert np.array_equal(w.cpu().numpy(), orc.w)
+
+
 def test_peer_path_single_gpu_resnet50_pair_sampled():
     # the multi-GPU exchange protocol (inbox push, per-unit flags, epochs) with both
     # workers of BASELINE configs[2] co-resident: 2 x 25,557,032, k = 8, 10 steps
