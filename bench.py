@@ -398,14 +398,20 @@ def main():
     if world_size == 1:
         roofline = roof_hbm
     else:
+        # the step is bound by whichever resource needs longer for its algorithmic bytes
         nvl_per_launch = nvl_b_max / args.steps
         nvl_ach = nvl_per_launch / avg_kern_s / 1e9
-        roofline = {"bound": "nvlink", "achieved": nvl_ach, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+        roof_nvl = {"bound": "nvlink", "achieved": nvl_ach, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
                     "frac": nvl_ach / NVLINK_PEER_GBS, "traffic": None,
                     "peak_source": "measured peer copy per direction (B200_PROFILING.md; 900 nominal)",
-                    "kernel": "k_gossip_peer", "algorithmic_bytes_per_launch": nvl_per_launch,
-                    "bytes_formula": "4 B x remote-sourced segment elements, most-loaded GPU",
-                    "avg_kernel_us": avg_kern_s * 1e6, "launches_timed": kern_launches, "hbm": roof_hbm}
+                    "kernel": hot_kernel, "algorithmic_bytes_per_launch": nvl_per_launch,
+                    "bytes_formula": "4 B x remote-sourced segment elements (exact from the topology), "
+                                     "most-loaded GPU; hierarchical adds the in-group reduce-scatter + all-gather",
+                    "avg_kernel_us": avg_kern_s * 1e6, "launches_timed": kern_launches}
+        t_nvl = nvl_per_launch / (NVLINK_PEER_GBS * 1e9)
+        t_hbm = hbm_per_launch / (hpeak * 1e9)
+        roofline = dict(roof_nvl if t_nvl >= t_hbm else roof_hbm)
+        roofline["other"] = roof_hbm if t_nvl >= t_hbm else roof_nvl
 
     cpu = None
     if rank == 0 and world_size == 1 and not args.no_cpu:

@@ -714,13 +714,14 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   p.grid_push = sms * occ_push < n_units ? sms * occ_push : n_units;
   p.grid_mix = sms * occ_mix;
   p.grid_hier = sms * occ_h;
-  // pieces: enough units per piece for every push CTA to pipeline a few (CS_PEER_PIECES overrides)
+  // pieces per step (CS_PEER_PIECES)
   {
-    int P = n_units / (4 * p.grid_push);
+    // default 1: measured on 2 B200s (c3), 2 and 3 pieces cost more in repeated push
+    // prologues and tails than the mix overlap recovers
+    int P = 1;
     const char* env = getenv("CS_PEER_PIECES");
     if (env) P = atoi(env);
     if (P < 1) P = 1;
-    if (P > 4 && !env) P = 4;
     if (P > PeerState::kMaxPieces) P = PeerState::kMaxPieces;
     if (P > p.n_tiles) P = p.n_tiles;
     p.pieces = P;
