@@ -500,8 +500,9 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
     if (rc) return rc;
     rc = peer_flat_step(g.peer, pa, g.stream, ev[0], ev[1]);
     if (rc) return fail(rc, "%s", peer_error());
-    g.launches_per_step = 3;  // topology, push, mix
-    g.hot_kernel = "k_peer_push+k_peer_mix";
+    const bool fused_topo = g.world <= 64;  // the topology is drawn inside the first kernel
+    g.launches_per_step = fused_topo ? 2 : 3;
+    g.hot_kernel = g.peer.use_hybrid ? "k_hyb_walk+k_hyb_tail" : "k_peer_push+k_peer_mix";
   }
   if (rc) return rc;
   if (diag) g.diag_valid = true;

@@ -155,6 +155,7 @@ __device__ __forceinline__ float4 mean4(float4 a, float4 b) {
   return make_float4(__fmul_rn(__fadd_rn(a.x, b.x), 0.5f), __fmul_rn(__fadd_rn(a.y, b.y), 0.5f),
                      __fmul_rn(__fadd_rn(a.z, b.z), 0.5f), __fmul_rn(__fadd_rn(a.w, b.w), 0.5f));
 }
+__device__ __forceinline__ float pair_mean1(float a, float b) { return __fmul_rn(__fadd_rn(a, b), 0.5f); }
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
 }
@@ -626,6 +627,329 @@ __global__ void __launch_bounds__(kHierThreads) k_hier_sync(const SyncArgs sa) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Hybrid flat step for several workers per GPU (configs 2 at N > 1 and 5).
+//
+// Restricted to this GPU's workers, each segment's permutation splits into local
+// cycles and local chains c0 -> c1 = src(c0) -> ... -> cm, where dst(c0) and
+// src(cm) are on other GPUs.  k_hyb_walk is the single-GPU bulk-TMA cycle walk
+// (k_gossip_tma) over that structure: cycles are mixed in registers as on one
+// GPU; a chain's head additionally stores its y into the inbox of dst(c0) over
+// NVLink, and a chain's tail keeps its y in x.  k_hyb_tail then finishes only
+// the tails, x = (y + inbox) * 0.5, once every GPU's heads have landed.  HBM
+// per parameter: 20 B + 16 B x (fraction of remote-sourced workers), against
+// 36 B for the push/mix pair.
+constexpr int kHCons = 256;
+constexpr int kHThreads = kHCons + 32;
+constexpr int kHVPT = kTmaTileMax / (4 * kHCons);
+constexpr int kHStages = 4;
+constexpr size_t kHStageBytes = 3ull * kTmaTileMax * sizeof(float);
+constexpr uint32_t kHStart = 1u << 31, kHEnd = 1u << 30, kHHead = 1u << 29, kHTail = 1u << 28;
+constexpr uint32_t kHIdx = (1u << 28) - 1;
+constexpr int kHMaxTable = 2048;  // k * n_loc
+
+size_t hyb_smem_bytes(int k, int n_loc) {
+  return kHStages * kHStageBytes + sizeof(uint32_t) * 2 * (size_t)k * n_loc +
+         sizeof(uint32_t) * 192 * (kHThreads / 32);
+}
+
+struct HybArgs {
+  float* x;
+  float* m;
+  const float* g;
+  float* psw;
+  int64_t ld, d, nq;
+  int k, world, n_loc, first, rank, nprocs;
+  uint64_t seed;
+  uint32_t step;
+  const int32_t* given;     // injected topology [k][world] or nullptr
+  const int32_t* src_tbl;   // k_topology output [k][world] when !fused
+  int fused;
+  float lr, mu;
+  const TileDesc* tiles;
+  int n_tiles;
+  char* const* peers;
+  size_t off_inbox, off_wbox, off_done, off_pdone, off_count, off_pcount, flag_stride;
+  int pieces;
+  uint32_t epoch, pdone_target, done_target;
+  uint8_t* tail_tbl;        // [k][n_loc]: 1 = the worker's segment source is remote
+  int* err;
+};
+
+__global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stage_buf = reinterpret_cast<float*>(smem_raw);
+  uint32_t* ord = reinterpret_cast<uint32_t*>(smem_raw + kHStages * kHStageBytes);  // [k][n_loc]
+  int32_t* head_dst = reinterpret_cast<int32_t*>(ord + a.k * a.n_loc);             // [k][n_loc]
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(head_dst + a.k * a.n_loc);         // [warps][192]
+  __shared__ uint64_t full[kHStages], empty[kHStages];
+  __shared__ int s_timeout;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_loc = a.n_loc, first = a.first;
+  const int par = (int)(a.epoch & 1u);
+  char* mine = a.peers[a.rank];
+  volatile int* timeout = &s_timeout;
+
+  if (threadIdx.x == 0) {
+    s_timeout = 0;
+    for (int s = 0; s < kHStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], kHCons / 32);
+    }
+    ptx::mbar_fence_init();
+  }
+  // ---- this step's topology, restricted to this GPU's workers (Alg. 2)
+  {
+    uint32_t* u = scratch + warp * 192;
+    int32_t* srow = reinterpret_cast<int32_t*>(u + 64);   // [<= 64] when fused
+    int32_t* dstl = reinterpret_cast<int32_t*>(u + 128);  // [n_loc] dst of local workers
+    const int nw = blockDim.x >> 5;
+    for (int sg = warp; sg < a.k; sg += nw) {
+      const int32_t* row;
+      if (a.given != nullptr) {
+        row = a.given + (int64_t)sg * a.world;
+      } else if (a.fused) {
+        warp_alg2_small(a.seed, a.step, sg, a.world, CS_TAG_FLAT, u, srow, a.err);
+        row = srow;
+      } else {
+        row = a.src_tbl + (int64_t)sg * a.world;
+      }
+      __syncwarp();
+      for (int jj = lane; jj < a.world; jj += 32) {  // inverse on the local range: dst
+        const int v = row[jj];
+        if (v >= first && v < first + n_loc) dstl[v - first] = jj;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        uint32_t* o = ord + sg * n_loc;
+        uint64_t seen = 0;
+        int pos = 0;
+        for (int r = 0; r < n_loc; ++r) {  // chains start where the receiver is remote
+          const int dg = dstl[r];
+          if (dg >= first && dg < first + n_loc) continue;
+          head_dst[sg * n_loc + r] = dg;
+          int pr = r;
+          uint32_t flag = kHStart | kHHead;
+          while (true) {
+            seen |= 1ull << pr;
+            const int sgl = row[first + pr] - first;
+            if (sgl < 0 || sgl >= n_loc) {  // source remote: chain tail
+              o[pos++] = (uint32_t)pr | flag | kHEnd | kHTail;
+              break;
+            }
+            o[pos++] = (uint32_t)pr | flag;
+            flag = 0;
+            pr = sgl;
+          }
+        }
+        for (int r0 = 0; r0 < n_loc; ++r0) {  // the rest: cycles of local workers
+          if ((seen >> r0) & 1ull) continue;
+          int pr = r0;
+          uint32_t flag = kHStart;
+          do {
+            seen |= 1ull << pr;
+            const int nx = row[first + pr] - first;
+            o[pos++] = (uint32_t)pr | flag | (nx == r0 ? kHEnd : 0u);
+            flag = 0;
+            pr = nx;
+          } while (pr != r0);
+        }
+      }
+      if (blockIdx.x == 0)
+        for (int r = lane; r < n_loc; r += 32) {
+          const int sgl = row[first + r] - first;
+          a.tail_tbl[sg * n_loc + r] = (sgl < 0 || sgl >= n_loc) ? 1 : 0;
+        }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // ping-pong safety: every GPU finished its mix of epoch e-2 (last reader of this inbox parity)
+  if (threadIdx.x < a.nprocs && a.epoch >= 3) {
+    const uint32_t* done = reinterpret_cast<const uint32_t*>(mine + a.off_done);
+    if (!wait_acquire(done + threadIdx.x, a.epoch - 2)) atomicOr(&s_timeout, 1);
+  }
+  __syncthreads();
+  // push-sum weights of the chain heads go with their y (reading C-11)
+  if (blockIdx.x == 0 && !*timeout)
+    for (int i = threadIdx.x; i < a.k * n_loc; i += blockDim.x) {
+      const int sg = i / n_loc, r = i - sg * n_loc;
+      const int dg = head_dst[sg * n_loc + r];
+      const uint32_t* o = ord + sg * n_loc;
+      bool head = false;
+      for (int pp = 0; pp < n_loc; ++pp)
+        if ((o[pp] & kHIdx) == (uint32_t)r && (o[pp] & kHHead)) head = true;
+      if (!head) continue;
+      const int rp = dg / n_loc, rl = dg - rp * n_loc;
+      reinterpret_cast<float*>(a.peers[rp] + a.off_wbox)[((int64_t)par * n_loc + rl) * a.k + sg] =
+          a.psw[(int64_t)r * a.k + sg];
+    }
+
+  const int64_t ld = a.ld;
+  if (warp == kHCons / 32) {
+    // ---------------- producer: rows of each tile in walk order ------------------
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < a.n_tiles && !*timeout; t += gridDim.x) {
+        const TileDesc td = a.tiles[t];
+        const uint32_t bytes = (uint32_t)(((td.len + 3) & ~3) * sizeof(float));
+        const uint32_t* o = ord + td.seg * n_loc;
+        for (int p = 0; p < n_loc; ++p, ++it) {
+          const int st = (int)(it % kHStages);
+          ptx::mbar_wait(&empty[st], ((it / kHStages) & 1u) ^ 1u);
+          const int64_t off = (int64_t)(o[p] & kHIdx) * ld + td.c0;
+          float* buf = stage_buf + (size_t)st * 3 * kTmaTileMax;
+          ptx::mbar_arrive_expect_tx(&full[st], 3 * bytes);
+          ptx::bulk_g2s(buf, a.x + off, bytes, &full[st]);
+          ptx::bulk_g2s(buf + kTmaTileMax, a.m + off, bytes, &full[st]);
+          ptx::bulk_g2s(buf + 2 * kTmaTileMax, a.g + off, bytes, &full[st]);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- consumers: the walk, heads pushed over NVLink, tails kept ------
+    bool bad = false;
+    uint32_t it = 0;
+    for (int t = blockIdx.x; t < a.n_tiles && !*timeout; t += gridDim.x) {
+      const TileDesc td = a.tiles[t];
+      const uint32_t* o = ord + td.seg * n_loc;
+      float4 yfirst[kHVPT], yprev[kHVPT];
+      uint32_t prev_row = 0;
+      for (int p = 0; p < n_loc; ++p, ++it) {
+        const int st = (int)(it % kHStages);
+        ptx::mbar_wait(&full[st], (it / kHStages) & 1u);
+        const float* buf = stage_buf + (size_t)st * 3 * kTmaTileMax;
+        const uint32_t e = o[p];
+        const uint32_t row = e & kHIdx;
+        float* inbox = nullptr;
+        if (e & kHHead) {
+          const int dg = head_dst[td.seg * n_loc + row];
+          const int rp = dg / n_loc, rl = dg - rp * n_loc;
+          inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * n_loc + rl) * ld;
+        }
+#pragma unroll
+        for (int c = 0; c < kHVPT; ++c) {
+          const int v = c * kHCons + threadIdx.x;
+          const int valid = td.len - 4 * v;
+          if (valid > 0) {
+            const int vv = valid < 4 ? valid : 4;
+            const float4 cx = reinterpret_cast<const float4*>(buf)[v];
+            const float4 cm = reinterpret_cast<const float4*>(buf + kTmaTileMax)[v];
+            const float4 cg = reinterpret_cast<const float4*>(buf + 2 * kTmaTileMax)[v];
+            bad |= nonfinite4(cg);
+            const float4 mn = mom4(cm, cg, a.mu);
+            const float4 y = sgd4(cx, mn, a.lr);
+            const int64_t j = td.c0 + 4 * v;
+            st4_cs(a.m + (int64_t)row * ld + j, mn, vv);
+            if (e & kHStart) {
+              yfirst[c] = y;
+              if (e & kHHead) st4(inbox + j, y, vv);  // NVLink push of the chain head
+            } else {
+              st4_cs(a.x + (int64_t)prev_row * ld + j, mean4(yprev[c], y), vv);
+            }
+            if (e & kHEnd) {
+              if (e & kHTail) st4(a.x + (int64_t)row * ld + j, y, vv);  // finished by k_hyb_tail
+              else st4_cs(a.x + (int64_t)row * ld + j, mean4(y, yfirst[c]), vv);
+            }
+            yprev[c] = y;
+          }
+        }
+        prev_row = row;
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[st]);
+      }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.err + kErrDiverged, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_timeout) atomicOr(a.err + kErrTimeout, 1);
+    __threadfence_system();  // this CTA's NVLink stores before its arrival
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(mine + a.off_pcount);
+    const uint32_t prev = atomicAdd(cnt, 1u);
+    s_timeout = (prev + 1 == a.pdone_target) ? 2 : 0;  // reuse as "last CTA" marker
+  }
+  __syncthreads();
+  if (s_timeout == 2) {
+    // last CTA: weights of the workers whose source is local (snapshot: nothing wrote psw yet)
+    for (int i = threadIdx.x; i < a.k * n_loc; i += blockDim.x) {
+      const int sg = i / n_loc, r = i - sg * n_loc;
+      if (a.tail_tbl[sg * n_loc + r]) continue;
+      // the local source: the ord entry after r in its cycle (or chain)
+      const uint32_t* o = ord + sg * n_loc;
+      int pos = 0;
+      while ((o[pos] & kHIdx) != (uint32_t)r) ++pos;
+      int srcl;
+      if (o[pos] & kHEnd) {  // cycle end: closes with its start
+        int q = pos;
+        while (!(o[q] & kHStart)) --q;
+        srcl = (int)(o[q] & kHIdx);
+      } else {
+        srcl = (int)(o[pos + 1] & kHIdx);
+      }
+      reinterpret_cast<float*>(stage_buf)[i] = pair_mean1(a.psw[(int64_t)r * a.k + sg], a.psw[(int64_t)srcl * a.k + sg]);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.k * n_loc; i += blockDim.x) {
+      const int sg = i / n_loc, r = i - sg * n_loc;
+      if (!a.tail_tbl[sg * n_loc + r]) a.psw[(int64_t)r * a.k + sg] = reinterpret_cast<const float*>(stage_buf)[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int p = 0; p < a.nprocs; ++p)
+        ptx::st_release_sys(reinterpret_cast<uint32_t*>(a.peers[p] + a.off_pdone) + a.rank, a.epoch);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_hyb_tail(const HybArgs a) {
+  __shared__ uint8_t tail[kHMaxTable];
+  __shared__ int s_timeout;
+  char* mine = a.peers[a.rank];
+  const int par = (int)(a.epoch & 1u);
+  const int n_loc = a.n_loc;
+  if (threadIdx.x == 0) s_timeout = 0;
+  for (int i = threadIdx.x; i < a.k * n_loc; i += blockDim.x) tail[i] = a.tail_tbl[i];
+  __syncthreads();
+  if (threadIdx.x < a.nprocs) {  // every GPU's chain heads have landed
+    const uint32_t* pd = reinterpret_cast<const uint32_t*>(mine + a.off_pdone);
+    if (!wait_acquire(pd + threadIdx.x, a.epoch)) atomicOr(&s_timeout, 1);
+  }
+  __syncthreads();
+  if (!s_timeout) {
+    const int64_t nv = (a.d + 3) >> 2;
+    const int64_t total = nv * n_loc;
+    const float* inbox0 = reinterpret_cast<const float*>(mine + a.off_inbox) + (int64_t)par * n_loc * a.ld;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = idx / nv, v = idx - r * nv;
+      const int64_t j = 4 * v;
+      const int sg = (int)imin64(a.k - 1, (((j >> 5) + 1) * a.k - 1) / a.nq);
+      if (!tail[sg * n_loc + r]) continue;
+      const int64_t off = r * a.ld + j;
+      const float4 y = __ldcs(reinterpret_cast<const float4*>(a.x + off));
+      const float4 yi = __ldcs(reinterpret_cast<const float4*>(inbox0 + off));
+      st4_cs(a.x + off, mean4(y, yi), (int)imin64(4, a.d - j));
+    }
+    if (blockIdx.x == 0)
+      for (int i = threadIdx.x; i < a.k * n_loc; i += blockDim.x) {
+        const int sg = i / n_loc, r = i - sg * n_loc;
+        if (!tail[i]) continue;
+        const float* wbox = reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * n_loc + r) * a.k;
+        float* wp = a.psw + (int64_t)r * a.k + sg;
+        *wp = pair_mean1(*wp, __ldcg(wbox + sg));
+      }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_timeout) atomicOr(a.err + kErrTimeout, 1);
+    publish_when_last(a.peers, mine, a.off_count, a.off_done, a.rank, 0, a.nprocs, a.epoch, a.done_target,
+                      a.pieces, a.flag_stride);
+  }
+}
+
 }  // namespace
 
 const char* peer_error() { return g_peer_err.c_str(); }
@@ -714,6 +1038,37 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   p.grid_push = sms * occ_push < n_units ? sms * occ_push : n_units;
   p.grid_mix = sms * occ_mix;
   p.grid_hier = sms * occ_h;
+  // hybrid flat step when several workers share a GPU (CS_PEER_HYBRID=0 disables it)
+  {
+    const char* hy = getenv("CS_PEER_HYBRID");
+    p.use_hybrid = n_loc >= 2 && n_loc <= 64 && (int64_t)k * n_loc <= kHMaxTable && !(hy && atoi(hy) == 0);
+  }
+  if (p.use_hybrid) {
+    const size_t hs = hyb_smem_bytes(k, n_loc);
+    int occ_w = 0, occ_t = 0;
+    e = cudaFuncSetAttribute(k_hyb_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hs);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_w, k_hyb_walk, kHThreads, hs);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, k_hyb_tail, 256, 0);
+    if (e != cudaSuccess || occ_w < 1 || occ_t < 1) return perr(CS_ECUDA, "hybrid occupancy", e);
+    p.grid_hyb = sms * occ_w;
+    p.grid_tail = sms * occ_t;
+    const int T = tma_tile_len(d, p.grid_hyb);
+    std::vector<TileDesc> tiles;
+    for (int s = 0; s < k; ++s)
+      for (int64_t c = bounds[s]; c < bounds[s + 1]; c += T) {
+        TileDesc td;
+        td.c0 = c;
+        td.seg = s;
+        td.len = (int32_t)((c + T < bounds[s + 1] ? c + T : bounds[s + 1]) - c);
+        tiles.push_back(td);
+      }
+    p.n_htiles = (int)tiles.size();
+    e = cudaMalloc(&p.d_htiles, sizeof(TileDesc) * tiles.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p.d_htiles, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&p.d_tail_tbl, (size_t)k * n_loc);
+    if (e != cudaSuccess) return perr(CS_ECUDA, "hybrid tables", e);
+  }
   // pieces per step (CS_PEER_PIECES)
   {
     // default 1: measured on 2 B200s (c3), 2 and 3 pieces cost more in repeated push
@@ -757,6 +1112,8 @@ void peer_release(PeerState& p) {
   for (int q = 0; q < PeerState::kMaxPieces; ++q)
     if (p.ev_push[q]) cudaEventDestroy(p.ev_push[q]);
   if (p.ev_mix) cudaEventDestroy(p.ev_mix);
+  if (p.d_htiles) cudaFree(p.d_htiles);
+  if (p.d_tail_tbl) cudaFree(p.d_tail_tbl);
   p = PeerState();
 }
 
@@ -891,6 +1248,54 @@ int launch_push_mix(PeerState& p, const PeerKernelArgs& ka, cudaStream_t st) {
 int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEvent_t ev0,
                    cudaEvent_t ev1) {
   int rc = CS_OK;
+  if (p.use_hybrid) {
+    const bool fused = a.world <= 64;
+    if (!fused && a.given == nullptr) rc = launch_topology_for(a, a.world, CS_TAG_FLAT, st);
+    if (rc) return rc;
+    HybArgs h;
+    h.x = a.x;
+    h.m = a.m;
+    h.g = a.g;
+    h.psw = a.psw;
+    h.ld = a.ld;
+    h.d = a.d;
+    h.nq = a.nq;
+    h.k = a.k;
+    h.world = a.world;
+    h.n_loc = a.n_loc;
+    h.first = a.first;
+    h.rank = a.rank;
+    h.nprocs = a.nprocs;
+    h.seed = a.seed;
+    h.step = a.step;
+    h.given = a.given;
+    h.src_tbl = a.src;
+    h.fused = fused ? 1 : 0;
+    h.lr = a.lr;
+    h.mu = a.mu;
+    h.tiles = p.d_htiles;
+    h.n_tiles = p.n_htiles;
+    h.peers = p.d_peer_base;
+    h.off_inbox = p.off_inbox;
+    h.off_wbox = p.off_wbox;
+    h.off_done = p.off_done;
+    h.off_pdone = p.off_pdone;
+    h.off_count = p.off_count;
+    h.off_pcount = p.off_pcount;
+    h.flag_stride = p.flag_stride;
+    h.pieces = p.pieces;
+    h.epoch = ++p.epoch;
+    h.pdone_target = (p.tot_pcount[0] += (uint32_t)p.grid_hyb);
+    h.done_target = (p.tot_count[0] += (uint32_t)p.grid_tail);
+    h.tail_tbl = p.d_tail_tbl;
+    h.err = a.err;
+    if (ev0) cudaEventRecord(ev0, st);
+    k_hyb_walk<<<p.grid_hyb, kHThreads, hyb_smem_bytes(a.k, a.n_loc), st>>>(h);
+    k_hyb_tail<<<p.grid_tail, 256, 0, st>>>(h);
+    if (ev1) cudaEventRecord(ev1, st);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "hybrid launch", e);
+  }
   if (!fused_topo_ok(a.world, a.k, a.n_loc)) rc = launch_topology_for(a, a.world, CS_TAG_FLAT, st);
   if (rc) return rc;
   PeerKernelArgs ka = kernel_args(p, a, ++p.epoch, false);

@@ -68,6 +68,11 @@ struct PeerState {
   // running totals of CTAs launched against each arrival counter (kernel targets)
   uint32_t tot_count[kMaxPieces] = {}, tot_pcount[kMaxPieces] = {};
   uint32_t tot_c1 = 0, tot_c2 = 0, tot_c3 = 0;
+  // hybrid flat step (several workers per GPU): local cycle walk + NVLink chain heads
+  bool use_hybrid = false;
+  struct TileDesc* d_htiles = nullptr;
+  int n_htiles = 0, grid_hyb = 0, grid_tail = 0;
+  uint8_t* d_tail_tbl = nullptr;
 };
 
 // gs: GPUs per hierarchical group when a hierarchical step is possible (one worker

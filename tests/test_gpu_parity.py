@@ -297,13 +297,17 @@ def test_resume_via_set_step():
 
 # ---- every kernel path is bit-identical to the oracle ---------------------------------
 
-PATHS = {"reg": 1, "tma": 2, "peer": 3}
+PATHS = {"reg": 1, "tma": 2, "peer": 3, "peer_pm": 3}
 
 
-@pytest.mark.parametrize("path", ["reg", "tma", "peer"])
+@pytest.mark.parametrize("path", ["reg", "tma", "peer", "peer_pm"])
 @pytest.mark.parametrize("n,d,k,ld", [(2, 7, 1, 8), (3, 4099, 3, 4100), (8, 100_003, 4, 100_004),
                                       (16, 65_536, 8, 65_536), (5, 12_345, 5, 12_348)])
-def test_each_path_bitwise(path, n, d, k, ld):
+def test_each_path_bitwise(path, n, d, k, ld, monkeypatch):
+    # peer: the multi-GPU exchange kernels run with every receiver local (hybrid walk for
+    # several workers per GPU); peer_pm: the push/mix pair used for one worker per GPU
+    if path == "peer_pm":
+        monkeypatch.setenv("CS_PEER_HYBRID", "0")
     x, m, w, bank2 = _bind(n, d, k, 17, ld=ld, path=PATHS[path])
     x[:, d:] = 3.0
     orc = OracleRun(n, d, k, 17)
@@ -312,7 +316,8 @@ def test_each_path_bitwise(path, n, d, k, ld):
         orc.step(LR, MU)
     cs.cs_sync()
     name, _ = cs.cs_kernel_info()
-    assert name == {"reg": "k_gossip_local", "tma": "k_gossip_tma", "peer": "k_peer_push+k_peer_mix"}[path]
+    assert name == {"reg": "k_gossip_local", "tma": "k_gossip_tma", "peer": "k_hyb_walk+k_hyb_tail",
+                    "peer_pm": "k_peer_push+k_peer_mix"}[path]
     xg = x.cpu().numpy()
     assert np.array_equal(xg[:, :d], orc.x)
     assert np.array_equal(m.cpu().numpy()[:, :d], orc.m)
@@ -324,6 +329,7 @@ def test_each_path_bitwise(path, n, d, k, ld):
 def test_peer_path_pieces_bitwise(pieces, monkeypatch):
     # the step cut into pieces: push(p+1) on the caller's stream overlaps mix(p) on the aux stream
     monkeypatch.setenv("CS_PEER_PIECES", str(pieces))
+    monkeypatch.setenv("CS_PEER_HYBRID", "0")  # pieces apply to the push/mix pair
     n, d, k = 3, 70_003, 5
     x, m, w, bank2 = _bind(n, d, k, 23, path=PATHS["peer"])
     orc = OracleRun(n, d, k, 23)
@@ -336,9 +342,10 @@ def test_peer_path_pieces_bitwise(pieces, monkeypatch):
     assert np.array_equal(w.cpu().numpy(), orc.w)
 
 
-def test_peer_path_single_gpu_resnet50_pair_sampled():
-    # the multi-GPU exchange protocol (inbox push, per-unit flags, epochs) with both
-    # workers of BASELINE configs[2] co-resident: 2 x 25,557,032, k = 8, 10 steps
+def test_peer_path_single_gpu_resnet50_pair_sampled(monkeypatch):
+    # the multi-GPU exchange protocol (inbox push, flags, epochs) with both workers of
+    # BASELINE configs[2] co-resident: 2 x 25,557,032, k = 8, 10 steps
+    monkeypatch.setenv("CS_PEER_HYBRID", "0")
     n, d, k = 2, 25_557_032, 8
     x, m, w, bank2 = _bind(n, d, k, 0, path=PATHS["peer"])
     cols = synth.sample_columns(d, T.segment_bounds(d, k))
