@@ -491,7 +491,6 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
   if (!g.use_peer) {
     rc = enqueue_flat_step(params, grads, psw, lr, momentum, diag);
   } else {
-    if (diag) return fail(CS_EUNSUPPORTED, "diagnostics are not implemented on the peer-exchange path");
     if (!g.peer.imported) return fail(CS_ENOTBOUND, "multi-GPU: cs_ipc_import has not been called");
     PeerStepArgs pa = peer_args(params, grads, psw, lr, momentum);
     pa.given = g.has_override ? g.d_given : nullptr;
@@ -500,6 +499,10 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
     if (rc) return rc;
     rc = peer_flat_step(g.peer, pa, g.stream, ev[0], ev[1]);
     if (rc) return fail(rc, "%s", peer_error());
+    if (diag) {
+      rc = peer_diag(g.peer, pa, g.d_partials, local_max_grid(), g.d_diag, g.stream);
+      if (rc) return fail(rc, "%s", peer_error());
+    }
     const bool fused_topo = g.world <= 64;  // the topology is drawn inside the first kernel
     g.launches_per_step = fused_topo ? 2 : 3;
     g.hot_kernel = g.peer.use_hybrid ? "k_hyb_walk+k_hyb_tail" : "k_peer_push+k_peer_mix";
@@ -542,7 +545,6 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
   if (rc) return rc;
   const bool diag = g.diag != 0;
   if (g.nprocs > 1) {
-    if (diag) return fail(CS_EUNSUPPORTED, "diagnostics are not implemented on the peer-exchange path");
     if (g.n_loc != 1)
       return fail(CS_EUNSUPPORTED, "multi-GPU hierarchical step needs one worker per GPU (world == nprocs)");
     if (!g.peer.imported) return fail(CS_ENOTBOUND, "multi-GPU: cs_ipc_import has not been called");
@@ -552,6 +554,11 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
     if (rc) return rc;
     rc = peer_hier_step(g.peer, pa, g.stream, ev[0], ev[1]);
     if (rc) return fail(rc, "%s", peer_error());
+    if (diag) {
+      rc = peer_diag(g.peer, pa, g.d_partials, local_max_grid(), g.d_diag, g.stream);
+      if (rc) return fail(rc, "%s", peer_error());
+      g.diag_valid = true;
+    }
     g.launches_per_step = g.groups >= 2 ? 5 : 3;  // (topology,) scatter, reduce, push(, mix)
     g.hot_kernel = "k_hier_scatter+k_hier_reduce+k_peer_push+k_peer_mix";
     g.step += 1;

@@ -950,9 +950,216 @@ __global__ void __launch_bounds__(256) k_hyb_tail(const HybArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Multi-GPU diagnostics (reading B-3).  GPU q owns columns
+// [q*chunk, (q+1)*chunk).  k_diag_scatter sends every local worker's x' of each
+// chunk, and its psw row, to the chunk's owner; k_diag_reduce computes the same
+// shifted fp64 column sums as the single-GPU kernels over all n workers of its
+// chunk and publishes its partial (sum_j sum_i (z - zbar)^2, sum_j zbar) to every
+// GPU; k_diag_final adds the partials in rank order (deterministic).
+struct DiagArgs {
+  const float* x;
+  const float* psw;
+  char* const* peers;
+  int64_t ld, d, nq, chunk;
+  int k, world, n_loc, first, rank, nprocs;
+  uint32_t epoch;  // diagnostics epoch (>= 1)
+  uint32_t c1_target, c2_target;
+  size_t off_dx, off_dw, off_dpart, off_dd1, off_dd2, off_dc1, off_dc2;
+  double* partials;  // [gridDim.x][2] scratch of k_diag_reduce
+  double* out;       // [2] {CD, mean checksum}
+  int* err;
+};
+
+__global__ void __launch_bounds__(256) k_diag_scatter(const DiagArgs a) {
+  char* mine = a.peers[a.rank];
+  __shared__ int s_timeout;
+  if (threadIdx.x == 0) s_timeout = 0;
+  __syncthreads();
+  // the owners finished reducing the previous diagnostics (their dx is free again)
+  if (threadIdx.x < a.nprocs && a.epoch >= 2) {
+    const uint32_t* dd2 = reinterpret_cast<const uint32_t*>(mine + a.off_dd2);
+    if (!wait_acquire(dd2 + threadIdx.x, a.epoch - 1)) atomicOr(&s_timeout, 1);
+  }
+  __syncthreads();
+  if (!s_timeout) {
+    const int64_t cv = a.chunk / 4;
+    const int64_t total = (int64_t)a.nprocs * a.n_loc * cv;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+      const int q = (int)(idx / ((int64_t)a.n_loc * cv));
+      const int64_t rem = idx - (int64_t)q * a.n_loc * cv;
+      const int r = (int)(rem / cv);
+      const int64_t v = rem - (int64_t)r * cv;
+      const int64_t j = q * a.chunk + 4 * v;
+      const int valid = (int)imin64(4, a.d - j);
+      if (valid <= 0) continue;
+      float* dst = reinterpret_cast<float*>(a.peers[q] + a.off_dx) + (int64_t)(a.first + r) * a.chunk + 4 * v;
+      st4(dst, ld4_valid(a.x + (int64_t)r * a.ld + j, valid), valid);
+    }
+    if (blockIdx.x == 0)
+      for (int i = threadIdx.x; i < a.nprocs * a.n_loc * a.k; i += blockDim.x) {
+        const int q = i / (a.n_loc * a.k), rem = i - q * a.n_loc * a.k;
+        const int r = rem / a.k, s = rem - r * a.k;
+        reinterpret_cast<float*>(a.peers[q] + a.off_dw)[(int64_t)(a.first + r) * a.k + s] = a.psw[(int64_t)r * a.k + s];
+      }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_timeout) atomicOr(a.err + kErrTimeout, 1);
+    __threadfence_system();
+    publish_when_last(a.peers, mine, a.off_dc1, a.off_dd1, a.rank, 0, a.nprocs, a.epoch, a.c1_target);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_diag_reduce(const DiagArgs a) {
+  extern __shared__ double wsum[];  // [k]: 1 / sum_i w_{i,s}
+  __shared__ int s_timeout;
+  __shared__ double red[2][8];
+  char* mine = a.peers[a.rank];
+  if (threadIdx.x == 0) s_timeout = 0;
+  __syncthreads();
+  if (threadIdx.x < a.nprocs) {  // every GPU's columns of this chunk have arrived
+    const uint32_t* dd1 = reinterpret_cast<const uint32_t*>(mine + a.off_dd1);
+    if (!wait_acquire(dd1 + threadIdx.x, a.epoch)) atomicOr(&s_timeout, 1);
+  }
+  __syncthreads();
+  const float* dx = reinterpret_cast<const float*>(mine + a.off_dx);
+  const float* dw = reinterpret_cast<const float*>(mine + a.off_dw);
+  for (int s = threadIdx.x; s < a.k; s += blockDim.x) {
+    double sum = 0.0;
+    for (int i = 0; i < a.world; ++i) sum += (double)__ldcg(dw + (int64_t)i * a.k + s);
+    wsum[s] = 1.0 / sum;
+  }
+  __syncthreads();
+  double dacc = 0.0, zacc = 0.0;
+  if (!s_timeout) {
+    const int64_t c0 = (int64_t)a.rank * a.chunk;
+    const int64_t cols = imin64(a.chunk, a.d - c0);
+    for (int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; jj < cols;
+         jj += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t j = c0 + jj;
+      const int s = (int)imin64(a.k - 1, (((j >> 5) + 1) * a.k - 1) / a.nq);
+      double c = 0.0, s1 = 0.0, s2 = 0.0, xs = 0.0;
+      for (int i = 0; i < a.world; ++i) {
+        const double xv = (double)__ldcg(dx + (int64_t)i * a.chunk + jj);
+        const double z = xv / (double)__ldcg(dw + (int64_t)i * a.k + s);
+        if (i == 0) c = z;
+        const double dz = z - c;
+        s1 += dz;
+        s2 += dz * dz;
+        xs += xv;
+      }
+      const double zbar = xs * wsum[s];
+      const double dm = zbar - c;
+      dacc += s2 - 2.0 * dm * s1 + (double)a.world * dm * dm;
+      zacc += zbar;
+    }
+  }
+  // fixed-order block reduction -> per-block partial; the last CTA adds them in order
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    dacc += __shfl_xor_sync(0xffffffffu, dacc, off);
+    zacc += __shfl_xor_sync(0xffffffffu, zacc, off);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { red[0][warp] = dacc; red[1][warp] = zacc; }
+  __syncthreads();
+  __shared__ int s_last;
+  if (threadIdx.x == 0) {
+    double da = 0.0, za = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { da += red[0][w]; za += red[1][w]; }
+    a.partials[2 * blockIdx.x] = da;
+    a.partials[2 * blockIdx.x + 1] = za;
+    __threadfence();
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(mine + a.off_dc2);
+    s_last = (atomicAdd(cnt, 1u) + 1 == a.c2_target);
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    double da = 0.0, za = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) {
+      da += __ldcg(a.partials + 2 * b);
+      za += __ldcg(a.partials + 2 * b + 1);
+    }
+    for (int q = 0; q < a.nprocs; ++q) {
+      double* dp = reinterpret_cast<double*>(a.peers[q] + a.off_dpart) + 2 * a.rank;
+      dp[0] = da;
+      dp[1] = za;
+    }
+    if (s_timeout) atomicOr(a.err + kErrTimeout, 1);
+    __threadfence_system();
+    for (int q = 0; q < a.nprocs; ++q)
+      ptx::st_release_sys(reinterpret_cast<uint32_t*>(a.peers[q] + a.off_dd2) + a.rank, a.epoch);
+  }
+}
+
+__global__ void k_diag_final(const DiagArgs a) {
+  char* mine = a.peers[a.rank];
+  if (threadIdx.x != 0) return;
+  for (int q = 0; q < a.nprocs; ++q)
+    if (!wait_acquire(reinterpret_cast<const uint32_t*>(mine + a.off_dd2) + q, a.epoch)) {
+      atomicOr(a.err + kErrTimeout, 1);
+      return;
+    }
+  double da = 0.0, za = 0.0;
+  const double* dp = reinterpret_cast<const double*>(mine + a.off_dpart);
+  for (int q = 0; q < a.nprocs; ++q) {
+    da += __ldcg(dp + 2 * q);
+    za += __ldcg(dp + 2 * q + 1);
+  }
+  a.out[0] = sqrt(fmax(da, 0.0) / (double)a.world);
+  a.out[1] = za;
+}
+
 }  // namespace
 
 const char* peer_error() { return g_peer_err.c_str(); }
+
+int peer_diag(PeerState& p, const PeerStepArgs& a, double* partials, int partials_cap, double* out,
+              cudaStream_t st) {
+  DiagArgs da;
+  da.x = a.x;
+  da.psw = a.psw;
+  da.peers = p.d_peer_base;
+  da.ld = a.ld;
+  da.d = a.d;
+  da.nq = a.nq;
+  da.chunk = p.diag_chunk;
+  da.k = a.k;
+  da.world = a.world;
+  da.n_loc = a.n_loc;
+  da.first = a.first;
+  da.rank = a.rank;
+  da.nprocs = a.nprocs;
+  da.epoch = ++p.diag_epoch;
+  da.off_dx = p.off_dx;
+  da.off_dw = p.off_dw;
+  da.off_dpart = p.off_dpart;
+  da.off_dd1 = p.off_dd1;
+  da.off_dd2 = p.off_dd2;
+  da.off_dc1 = p.off_dc1;
+  da.off_dc2 = p.off_dc2;
+  da.partials = partials;
+  da.out = out;
+  da.err = a.err;
+  const int64_t sv = (int64_t)a.nprocs * a.n_loc * (p.diag_chunk / 4);
+  int gs = (int)((sv + 255) / 256);
+  if (gs > p.grid_mix) gs = p.grid_mix;
+  if (gs < 1) gs = 1;
+  int gr = (int)((p.diag_chunk + 255) / 256);
+  if (gr > p.grid_mix) gr = p.grid_mix;
+  if (gr > partials_cap) gr = partials_cap;
+  if (gr < 1) gr = 1;
+  da.c1_target = (p.tot_dc1 += (uint32_t)gs);
+  da.c2_target = (p.tot_dc2 += (uint32_t)gr);
+  k_diag_scatter<<<gs, 256, 0, st>>>(da);
+  k_diag_reduce<<<gr, 256, sizeof(double) * a.k, st>>>(da);
+  k_diag_final<<<1, 32, 0, st>>>(da);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "diagnostics launch", e);
+}
 
 int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs, int rank, int gs) {
   p = PeerState();
@@ -994,6 +1201,14 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
     p.off_wsync = align_up(p.off_msync + sizeof(float) * (size_t)ld, 256);
     off = align_up(p.off_wsync + sizeof(float) * (size_t)k, 256);
   }
+  // diagnostics: a column chunk per GPU, all workers' x' and psw for it, partials
+  p.diag_chunk = ((d + nprocs - 1) / nprocs + 3) / 4 * 4;
+  p.off_dx = off;
+  off = align_up(off + sizeof(float) * (size_t)(n_loc * nprocs) * p.diag_chunk, 256);
+  p.off_dw = off;
+  off = align_up(off + sizeof(float) * (size_t)(n_loc * nprocs) * k, 256);
+  p.off_dpart = off;
+  off = align_up(off + sizeof(double) * 2 * (size_t)nprocs, 256);
   auto flags = [&](size_t& o) {
     o = off;
     off = align_up(off + sizeof(uint32_t) * (size_t)nprocs, 256);
@@ -1006,13 +1221,17 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   flags(p.off_d1);
   flags(p.off_d2);
   flags(p.off_d3);
+  flags(p.off_dd1);
+  flags(p.off_dd2);
   p.off_count = off;                           // [kMaxPieces] counters, 64 B apart
   p.off_pcount = off + 64 * PeerState::kMaxPieces;
   off += 2 * 64 * PeerState::kMaxPieces;
   p.off_c1 = off;
   p.off_c2 = off + 64;
   p.off_c3 = off + 128;
-  p.bytes = align_up(off + 192, 4096);
+  p.off_dc1 = off + 192;
+  p.off_dc2 = off + 256;
+  p.bytes = align_up(off + 320, 4096);
   cudaError_t e = cudaMalloc(&p.base, p.bytes);
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region cudaMalloc", e);
   e = cudaMemset(p.base, 0, p.bytes);  // inbox padding is read by 16-byte-rounded bulk copies

@@ -68,6 +68,12 @@ struct PeerState {
   // running totals of CTAs launched against each arrival counter (kernel targets)
   uint32_t tot_count[kMaxPieces] = {}, tot_pcount[kMaxPieces] = {};
   uint32_t tot_c1 = 0, tot_c2 = 0, tot_c3 = 0;
+  // multi-GPU diagnostics: every GPU owns a column chunk of diag_chunk columns and
+  // receives all workers' x' (off_dx, [world][diag_chunk]) and psw (off_dw, [world][k])
+  // for it; per-GPU partials (off_dpart, [nprocs][2] fp64) are combined in rank order
+  int64_t diag_chunk = 0;
+  size_t off_dx = 0, off_dw = 0, off_dpart = 0, off_dd1 = 0, off_dd2 = 0, off_dc1 = 0, off_dc2 = 0;
+  uint32_t tot_dc1 = 0, tot_dc2 = 0, diag_epoch = 0;
   // hybrid flat step (several workers per GPU): local cycle walk + NVLink chain heads
   bool use_hybrid = false;
   struct TileDesc* d_htiles = nullptr;
@@ -86,6 +92,9 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
                    cudaEvent_t ev1);
 int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEvent_t ev0,
                    cudaEvent_t ev1);
+// diagnostics of the current state (after a step), all GPUs; out: device double[2]
+int peer_diag(PeerState& p, const PeerStepArgs& a, double* partials, int partials_cap, double* out,
+              cudaStream_t st);
 const char* peer_error();
 
 }  // namespace cs

@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--rng-seed", type=int, default=0)
     ap.add_argument("--compare-all", action="store_true", help="compare every column (small d)")
     ap.add_argument("--hier-groups", type=int, default=0, help="hierarchical step with this many groups")
+    ap.add_argument("--diag", action="store_true", help="check the multi-GPU diagnostics too")
     a = ap.parse_args()
     rank, ws, lr_ = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(lr_)
@@ -66,11 +67,21 @@ def main():
     step_fn = cs.cs_hier_step if a.hier_groups else cs.cs_gossip_step
     idx = torch.from_numpy(cols).to(dev)
     ok = True
+    if a.diag:
+        cs.cs_set_diag(True)
+        from oracle.diagnostics import consensus
     for t in range(a.num_steps):
         o = (t + first) % B
         step_fn(x, bank[o:o + n_loc], w, lr, mu)
         orc.step(lr, mu)
         cs.cs_sync()
+        if a.diag:
+            cd, msum = cs.cs_get_diag()
+            cd0, ms0 = consensus(orc.x, orc.w, orc.seg)
+            if not (abs(cd - cd0) <= 1e-9 * abs(cd0) and abs(msum - ms0) <= 1e-9 * max(1.0, abs(ms0)) + 1e-9 * d):
+                print(f"rank {rank} step {t}: diagnostics {cd, msum} vs oracle {cd0, ms0}", flush=True)
+                ok = False
+                break
         xs = x.index_select(1, idx).cpu().numpy()
         ms = m.index_select(1, idx).cpu().numpy()
         rows = slice(first, first + n_loc)

@@ -48,6 +48,17 @@ def test_two_gpu_resnet50_sampled():
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("n_loc,groups", [(3, 0), (1, 0), (1, 2)])
+def test_two_gpu_diagnostics(n_loc, groups):
+    # consensus distance / mean checksum across GPUs vs the oracle (<= 1e-9 relative)
+    args = ["--workers-per-gpu", n_loc, "--vector-len", 100_003, "--segments", 5, "--num-steps", 3,
+            "--compare-all", "--diag"]
+    if groups:
+        args += ["--hier-groups", groups]
+    _run(2, *args)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("pieces", [3, 8])
 def test_two_gpu_pieces_bitwise(pieces):
     # push(p+1) / mix(p) overlap across the caller's and the aux stream, across GPUs

@@ -360,10 +360,19 @@ def test_peer_path_single_gpu_resnet50_pair_sampled(monkeypatch):
     assert np.array_equal(w.cpu().numpy(), orc.w)
 
 
-def test_peer_path_rejects_diagnostics():
-    x, m, w, bank2 = _bind(4, 1024, 2, 1, path=PATHS["peer"])
+@pytest.mark.parametrize("hybrid", ["1", "0"])
+def test_peer_path_diagnostics_match_oracle(hybrid, monkeypatch):
+    # the multi-GPU diagnostics pass (column chunks per GPU, rank-ordered partials)
+    monkeypatch.setenv("CS_PEER_HYBRID", hybrid)
+    n, d, k = 4, 50_003, 3
+    x, m, w, bank2 = _bind(n, d, k, 1, path=PATHS["peer"])
+    orc = OracleRun(n, d, k, 1)
     cs.cs_set_diag(True)
-    with pytest.raises(cs.CSError) as e:
-        cs.cs_gossip_step(x, grads_view(bank2, 4, 0), w, LR, MU)
-    assert e.value.code == -12
+    for t in range(3):
+        cs.cs_gossip_step(x, grads_view(bank2, n, t), w, LR, MU)
+        orc.step(LR, MU)
+        cd, ms = cs.cs_get_diag()
+        cd0, ms0 = consensus(orc.x, orc.w, orc.seg)
+        assert abs(cd - cd0) <= 1e-9 * abs(cd0), (t, cd, cd0)
+        assert abs(ms - ms0) <= 1e-9 * max(1.0, abs(ms0)) + 1e-9 * d, (t, ms, ms0)
     cs.cs_set_diag(False)
