@@ -182,8 +182,16 @@ int cs_gossip_step_host(float* params, const float* grads_host, float* psw, floa
  *   h2  leaders apply a3 with gbar, then a4/a5 among the G leaders with the
  *       leader topology (tag HIER); G == 1 skips the exchange (x = y)
  *   h3  every member's params and psw become its leader's (bitwise)
- * `grads` is read only.  Momentum is defined at leaders only: members' momentum
- * rows are left unspecified.  Errors as cs_gossip_step. */
+ * `grads` is read only.  Momentum is defined at leaders only.
+ * One GPU: members' momentum rows are left untouched.
+ * Several GPUs (one worker per GPU, world == nprocs): the group's gradient is
+ * reduce-scattered over NVLink and summed in ascending member order (so the result
+ * is the same bits as on one GPU), every member holds an exact replica of its
+ * leader's params, momentum and psw and exchanges with the member of the same index
+ * in the source group.  The first hierarchical step after cs_bind / cs_set_step
+ * copies each leader's state to its members; callers must not modify a member's
+ * state between hierarchical steps.  Other layouts: CS_EUNSUPPORTED.
+ * Errors as cs_gossip_step. */
 int cs_hier_step(float* params, float* grads, float* psw, float lr, float momentum);
 
 /* ---- state, diagnostics, test hooks ------------------------------------------ */
@@ -198,8 +206,11 @@ int cs_set_diag(int enable);
 /* Diagnostics of the most recent step that had them enabled:
  *   cd_out    = sqrt((1/n) sum_i sum_j (z_ij - zbar_j)^2),  z = x / psw
  *   mean_out  = sum_j zbar_j,   zbar_j = sum_i x_ij / sum_i psw_{i,s(j)}
- * Synchronises the stream.  Errors: CS_EINVAL if no diagnosed step yet,
- * CS_EDIVERGED. */
+ * over ALL world workers.  One GPU: fused into the step kernel.  Several GPUs: a
+ * pass after the step sends every worker's x' of a column chunk to the chunk's
+ * owner GPU and combines the per-GPU partials in rank order (every process gets
+ * the same value).  fp64, deterministic.  Synchronises the stream.
+ * Errors: CS_EINVAL if no diagnosed step yet, CS_EDIVERGED, CS_ETIMEOUT. */
 int cs_get_diag(double* cd_out, double* mean_out);
 
 /* Wait for all enqueued work; reports deferred device errors. */
