@@ -85,6 +85,16 @@ def test_four_gpu_hierarchical_bitwise(groups, d, k):
 
 
 @pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
+@pytest.mark.parametrize("n_loc,groups", [(2, 0), (1, 2)])
+def test_four_gpu_diagnostics(n_loc, groups):
+    args = ["--workers-per-gpu", n_loc, "--vector-len", 200_001, "--segments", 7, "--num-steps", 3,
+            "--compare-all", "--diag"]
+    if groups:
+        args += ["--hier-groups", groups]
+    _run(4, *args)
+
+
+@pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
 @pytest.mark.parametrize("n_loc,d,k", [(1, 25_557_032, 8), (8, 1_000_000, 16)])
 def test_four_gpu_parity(n_loc, d, k):
     _run(4, "--workers-per-gpu", n_loc, "--vector-len", d, "--segments", k, "--num-steps", 6)
