@@ -217,6 +217,7 @@ def main():
     ap.add_argument("--cpu-cols", type=int, default=1_000_000)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-interval", action="store_true", help="skip the communication-interval sub-measurement")
     ap.add_argument("--path", default="auto", choices=["auto", "reg", "tma", "peer"],
                     help="library kernel path (cs_set_path); peer with 1 GPU = single-GPU emulation")
     args = ap.parse_args()
@@ -384,9 +385,47 @@ def main():
                "api": "cs_gossip_step_host" if host_api else "H2D copy + cs_gossip_step + psw D2H"}
         del host_bank
 
+    hpeak, hpeak_src = hbm_peak()
+
+    # ---- communication-interval mode (Table 1: I = 42) ------------------
+    # one interval = I cs_accumulate micro-steps + one gossip round with the mean gradient;
+    # the accumulate kernel is timed alone on the bound stream (12 B/param mid-interval)
+    interval = None
+    if not args.no_interval:
+        I = 42
+        acc = torch.empty(n_loc, d, device=dev)
+        for u in range(I):  # warm-up interval
+            cs.cs_accumulate(acc, grads(t + u), u, I)
+        step_fn(x, acc, w, lr, mu)
+        t += 1
+        barrier()
+        torch.cuda.synchronize()
+        ia, ib, ic = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        ia.record(stream)
+        for u in range(I):
+            cs.cs_accumulate(acc, grads(t + u), u, I)
+        ib.record(stream)
+        step_fn(x, acc, w, lr, mu)
+        t += 1
+        ic.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        acc_ms, int_ms = ia.elapsed_time(ib), ia.elapsed_time(ic)
+        st = torch.tensor([acc_ms, int_ms], dtype=torch.float64, device=dev)
+        if world_size > 1:
+            dist.all_reduce(st, op=dist.ReduceOp.MAX)
+        acc_ms, int_ms = st.tolist()
+        acc_bytes = (8.0 + 12.0 * (I - 1)) * n_loc * d   # count 0 reads g only
+        acc_ach = acc_bytes / (acc_ms * 1e-3) / 1e9
+        interval = {"I": I, "ms_per_interval": int_ms, "accumulate_ms": acc_ms,
+                    "accumulate_roofline": {"bound": "hbm", "achieved": acc_ach, "peak": hpeak, "unit": "GB/s",
+                                            "frac": acc_ach / hpeak, "kernel": "k_accumulate",
+                                            "bytes_formula": "(8 + 12 (I-1)) B x n_loc x d per interval"},
+                    "gpu_launches": I + launches_per_step}
+        del acc
+
     # ---- roofline of the hot kernel --------------------------------------------------
     avg_kern_s = kern_ms_max / max(1, kern_launches) * 1e-3
-    hpeak, hpeak_src = hbm_peak()
     hbm_per_launch = hbm_b / args.steps
     hbm_ach = hbm_per_launch / avg_kern_s / 1e9
     roof_hbm = {"bound": "hbm", "achieved": hbm_ach, "peak": hpeak, "unit": "GB/s", "frac": hbm_ach / hpeak,
@@ -427,7 +466,7 @@ def main():
                          "l2": f"inputs larger than L2 ({20.0 * n_loc * d / 1e9:.2f} GB moved per step per GPU)"},
               "step_us": ms_step * 1e3,
               "traffic_GBps": 20.0 * world * d / (ms_step * 1e-3) / 1e9,
-              "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+              "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "interval": interval,
               "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary()})
     if world_size > 1:
         dist.barrier()

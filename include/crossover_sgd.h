@@ -196,6 +196,22 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
 
 /* ---- state, diagnostics, test hooks ------------------------------------------ */
 
+/* Communication-interval mode (section 4: "increase the communication
+ * interval and accumulate the loss during this interval"; Table 1 "Communication
+ * Interval 42"; SPEC accumulate_and_flush).  Micro-step `count`
+ * (0 <= count < interval) of an interval of `interval` micro-steps, over the
+ * bound [n_loc, ld] rows (columns [0, d); padding columns are never written):
+ *   count == 0             acc = 0 + grads            (acc is not read)
+ *   0 < count              acc = fl(acc + grads)
+ *   count == interval - 1  then acc = fl(acc / interval)   (IEEE division)
+ * After the last micro-step acc holds the interval's mean gradient and is passed
+ * to cs_gossip_step / cs_hier_step as `grads`: one gossip round per interval.
+ * The caller owns both buffers (device, 16-byte aligned, row stride ld) and the
+ * count.  Local to each process: no exchange.  Enqueued on the bound stream.
+ * Errors: CS_ENOTBOUND, CS_EINVAL (NULL, count outside [0, interval), interval
+ * outside [1, 2^24)), CS_ELAYOUT (alignment), CS_ECUDA. */
+int cs_accumulate(float* acc, const float* grads, int count, int interval);
+
 /* Set / read the step counter t (resume = restore buffers + cs_set_step). */
 int cs_set_step(int64_t step);
 int cs_get_step(int64_t* step_out);

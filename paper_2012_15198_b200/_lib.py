@@ -53,6 +53,7 @@ _SIGS = {
     "cs_gossip_step": (_c_int, [_vp, _vp, _vp, _c_f, _c_f]),
     "cs_gossip_step_host": (_c_int, [_vp, _vp, _vp, _c_f, _c_f, _vp]),
     "cs_hier_step": (_c_int, [_vp, _vp, _vp, _c_f, _c_f]),
+    "cs_accumulate": (_c_int, [_vp, _vp, _c_int, _c_int]),
     "cs_set_step": (_c_int, [_c_i64]),
     "cs_get_step": (_c_int, [_vp]),
     "cs_set_diag": (_c_int, [_c_int]),
@@ -187,6 +188,12 @@ def cs_gossip_step_host(params, grads_host, psw, lr: float, momentum: float) -> 
 
 def cs_hier_step(params, grads, psw, lr: float, momentum: float) -> None:
     _check(lib.cs_hier_step(_ptr(params), _ptr(grads), _ptr(psw), lr, momentum), "cs_hier_step")
+
+
+def cs_accumulate(acc, grads, count: int, interval: int) -> None:
+    """Micro-step `count` of a communication interval (Table 1):
+    acc = 0 + g at count 0, acc += g after, acc /= interval at count interval-1."""
+    _check(lib.cs_accumulate(_ptr(acc), _ptr(grads), count, interval), "cs_accumulate")
 
 
 def cs_set_step(step: int) -> None:

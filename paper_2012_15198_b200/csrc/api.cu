@@ -584,6 +584,19 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
   return CS_OK;
 }
 
+int cs_accumulate(float* acc, const float* grads, int count, int interval) {
+  int rc = check_bound();
+  if (rc) return rc;
+  if (!acc || !grads) return fail(CS_EINVAL, "NULL acc/grads");
+  if (interval < 1 || interval >= (1 << 24))
+    return fail(CS_EINVAL, "interval %d outside [1, 2^24)", interval);
+  if (count < 0 || count >= interval)
+    return fail(CS_EINVAL, "count %d outside [0, interval=%d)", count, interval);
+  if (!aligned16(acc) || !aligned16(grads)) return fail(CS_ELAYOUT, "acc and grads must be 16-byte aligned");
+  CS_CUDA(launch_accumulate(acc, grads, g.n_loc, g.d, g.ld, count, interval, g.stream));
+  return CS_OK;
+}
+
 int cs_set_step(int64_t step) {
   if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
   if (step < 0 || step >= (int64_t(1) << 32)) return fail(CS_EINVAL, "step outside [0, 2^32)");

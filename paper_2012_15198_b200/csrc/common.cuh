@@ -97,6 +97,8 @@ int tma_tile_len(int64_t d, int grid);
 cudaError_t launch_gossip_tma(const LocalArgs& a, bool diag, int grid, cudaStream_t st);
 cudaError_t launch_synth(float* out, int64_t rows, int64_t d, int64_t ld, uint64_t seed,
                          int tag, int64_t row0, float scale, cudaStream_t st);
+cudaError_t launch_accumulate(float* acc, const float* g, int64_t rows, int64_t d, int64_t ld,
+                              int count, int interval, cudaStream_t st);
 
 }  // namespace cs
 
