@@ -98,3 +98,35 @@ def sample_columns(d: int, bounds, stride: int = 1024, seed: int = 0) -> np.ndar
     rng = np.random.default_rng(seed)
     cols.update(int(c) for c in rng.integers(0, d, size=min(d, 256)))
     return np.array(sorted(cols), dtype=np.int64)
+
+
+def resnet50_layers():
+    """ResNet-50's parameter tensors in definition order (the
+    paper's model and its "blocks and FC layer" segments).  Shapes follow the
+    architecture (He et al. 2016; torchvision layout): stem conv 7x7/64 + BN, four
+    stages of [3, 4, 6, 3] bottlenecks (1x1, 3x3, 1x1 convs, expansion 4, a 1x1
+    projection + BN in each stage's first block), FC 2048 -> 1000.  BN running
+    statistics are buffers, not parameters.
+
+    Returns (sizes, block): element count of each of the 161 tensors and its block
+    id (0 = stem, 1..16 = bottleneck blocks, 17 = FC).  Structure only, no values."""
+    sizes, block = [], []
+
+    def conv_bn(cin, cout, kk, b):
+        sizes.extend([cout * cin * kk * kk, cout, cout])  # conv weight, BN weight, BN bias
+        block.extend([b, b, b])
+
+    conv_bn(3, 64, 7, 0)
+    cin, b = 64, 0
+    for stage, (blocks, width) in enumerate(zip([3, 4, 6, 3], [64, 128, 256, 512])):
+        for i in range(blocks):
+            b += 1
+            conv_bn(cin, width, 1, b)
+            conv_bn(width, width, 3, b)
+            conv_bn(width, width * 4, 1, b)
+            if i == 0:
+                conv_bn(cin, width * 4, 1, b)  # projection shortcut
+            cin = width * 4
+    sizes.extend([1000 * 2048, 1000])
+    block.extend([b + 1, b + 1])
+    return sizes, block
