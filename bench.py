@@ -47,7 +47,10 @@ WORKLOADS = {
     "c4": (1, 25_557_032, 16, "hierarchical: 1 worker/GPU, groups of 4 GPUs (or all GPUs if fewer), "
                               "ResNet-50-sized 25,557,032 fp32, k=16 (BASELINE configs[3])"),
     "c5": (8, 25_557_032, 8, "8 workers/GPU x ResNet-50-sized 25,557,032 fp32 (BASELINE configs[4])"),
+    "c6": (16, 25_557_032, 18, "LARS (SURVEY 8(f) #2): 16 workers x ResNet-50's 161 tensors, segments = stem + "
+                               "16 blocks + FC (k=18, Table 1), eta 0.0025, wd 5e-5, lr 9"),
 }
+LARS = {"c6": (0.0025, 5e-5, 1e-9, 9.0)}   # eta, weight decay, eps, lr (Table 1)
 
 
 def hbm_peak():
@@ -125,17 +128,30 @@ class ClockSampler:
 class OracleSample:
     """The oracle as it stands, on all n workers x the first `cols` columns of the workload."""
 
-    def __init__(self, n: int, d: int, k: int, seed: int, cols: int):
+    def __init__(self, n: int, d: int, k: int, seed: int, cols: int, lars=None):
         import synth
         from oracle import topology as T
         from oracle.gossip import gossip_step
         self.synth, self.T, self.gossip_step = synth, T, gossip_step
         self.n, self.d, self.k, self.seed = n, d, k, seed
-        c = np.arange(min(cols, d))
+        self.lars = lars
+        if lars is None:
+            c = np.arange(min(cols, d))
+            bounds = T.segment_bounds(d, k)
+        else:
+            # LARS needs whole layers: the first ResNet-50 layers that fit in `cols` (>= 1)
+            from oracle.lars import lars_gossip_step, plan_bounds
+            self.lars_step = lars_gossip_step
+            sizes, block = synth.resnet50_layers()
+            lb = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+            j = max(1, int(np.searchsorted(lb, min(cols, d), side="right")) - 1)
+            self.lb = lb[:j + 1]
+            c = np.arange(int(self.lb[-1]))
+            bounds = plan_bounds(lb, block)
         self.cols = len(c)
         self.x = synth.init_params(seed, range(n), d, c)
         self.bank = synth.grad_bank(seed, n, d, c)
-        self.seg = T.segment_of_columns(T.segment_bounds(d, k), c)
+        self.seg = T.segment_of_columns(bounds, c)
         self.m = np.zeros_like(self.x)
         self.w = np.ones((n, k), np.float32)
         self.t = 0
@@ -143,9 +159,14 @@ class OracleSample:
     def step(self) -> float:
         t0 = time.perf_counter()
         src = self.T.topology(self.seed, self.t, self.n, self.k)
-        self.x, self.m, self.w = self.gossip_step(self.x, self.m, self.synth.grads_at(self.bank, self.n, self.t),
-                                                  self.w, src, self.seg, self.synth.DEFAULT_LR,
-                                                  self.synth.DEFAULT_MOMENTUM)
+        g = self.synth.grads_at(self.bank, self.n, self.t)
+        if self.lars is not None:
+            eta, wd, eps, lr = self.lars
+            self.x, self.m, self.w, _ = self.lars_step(self.x, self.m, g, self.w, src, self.seg, self.lb, lr,
+                                                       self.synth.DEFAULT_MOMENTUM, eta, wd, eps)
+        else:
+            self.x, self.m, self.w = self.gossip_step(self.x, self.m, g, self.w, src, self.seg,
+                                                      self.synth.DEFAULT_LR, self.synth.DEFAULT_MOMENTUM)
         self.t += 1
         return time.perf_counter() - t0
 
@@ -153,13 +174,15 @@ class OracleSample:
         return {"value": 4.0 * self.n * self.cols / per_step / 1e9, "unit": UNIT, "cores": 1,
                 "host_cores": len(os.sched_getaffinity(0)), "kind": "oracle",
                 "sample": f"{self.n} workers x first {self.cols} of {self.d} columns, k={self.k}, {steps} steps, "
+                          + ("LARS on whole layers, " if self.lars is not None else "")
+                          + 
                           f"{per_step:.3f} s/step (NumPy elementwise, single-threaded)",
                 "steps": steps, "s_per_step": per_step}
 
 
-def cpu_oracle_sample(n: int, d: int, k: int, seed: int, budget_s: float, cols: int):
+def cpu_oracle_sample(n: int, d: int, k: int, seed: int, budget_s: float, cols: int, lars=None):
     """Time the oracle for ~budget_s (at least one step) on a column sample."""
-    o = OracleSample(n, d, k, seed, cols)
+    o = OracleSample(n, d, k, seed, cols, lars)
     steps, el = 0, 0.0
     while steps == 0 or (el < budget_s and steps < 1000):
         el += o.step()
@@ -181,11 +204,13 @@ def run_reference(args, rank, world_size):
     k = args.k or k
     n = n_loc * world_size
     total = args.steps + args.warmup
-    probe = OracleSample(n, d, k, 0, min(args.cpu_cols, 100_000, d))
+    lars = LARS.get(args.config)
+    probe = OracleSample(n, d, k, 0, min(args.cpu_cols, 100_000, d), lars)
     probe.step()
     per_col = probe.step() / probe.cols
     cols = int(max(4096, min(args.cpu_cols, d, 60.0 / max(1, total) / per_col)))
-    o = OracleSample(n, d, k, 0, cols)
+    o = OracleSample(n, d, k, 0, cols, lars)
+    cols = o.cols
     for _ in range(args.warmup):
         o.step()
     res = [o.record(dt, 1) for dt in (o.step() for _ in range(max(1, args.steps)))]
@@ -255,6 +280,9 @@ def main():
         raise SystemExit(f"config {args.config} needs >= 2 workers in total")
     seed = 0
     lr, mu = float(synth.DEFAULT_LR), float(synth.DEFAULT_MOMENTUM)
+    lars = LARS.get(args.config)
+    if lars is not None:
+        lr = lars[3]
     first = rank * n_loc
     B = world + 1
 
@@ -270,6 +298,12 @@ def main():
         w = torch.ones(n_loc, k, device=dev)
         bank = torch.empty(B + n_loc, d, device=dev)
     cs.cs_bind(m, d, d, rank, world_size, stream)
+    if lars is not None:
+        sizes, block = synth.resnet50_layers()
+        if d != sum(sizes):
+            raise SystemExit("c6 needs the ResNet-50 vector (no --d)")
+        cs.cs_set_layers(np.concatenate([[0], np.cumsum(sizes)]), block)
+        cs.cs_set_lars(*lars[:3])
     cs.cs_synth_fill(x, n_loc, d, d, seed, synth.TAG_INIT, first, 1.0)
     cs.cs_synth_fill(bank, B, d, d, seed, synth.TAG_GRAD, 0, float(synth.GRAD_SCALE))
     stream.synchronize()
@@ -432,7 +466,8 @@ def main():
                 "traffic": ncu_traffic(f"{args.config}" + ("" if args.path == "auto" else f":{args.path}")
                                        + ("" if world_size == 1 else f"@{world_size}")),
                 "peak_source": hpeak_src, "kernel": hot_kernel,
-                "algorithmic_bytes_per_launch": hbm_per_launch, "bytes_formula": "20 B x n_loc x d",
+                "algorithmic_bytes_per_launch": hbm_per_launch, "bytes_formula": ("28 B x n_loc x d (LARS norms 8 B + step 20 B)" if lars else
+                                                                   "20 B x n_loc x d"),
                 "avg_kernel_us": avg_kern_s * 1e6, "launches_timed": kern_launches}
     if world_size == 1:
         roofline = roof_hbm
@@ -454,7 +489,7 @@ def main():
 
     cpu = None
     if rank == 0 and world_size == 1 and not args.no_cpu:
-        cpu = cpu_oracle_sample(n_loc * world_size, d, k, seed, args.cpu_seconds, args.cpu_cols)
+        cpu = cpu_oracle_sample(n_loc * world_size, d, k, seed, args.cpu_seconds, args.cpu_cols, lars)
 
     if rank == 0:
         emit({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": args.steps,

@@ -50,6 +50,7 @@ extern "C" {
 #define CS_MAX_WORLD       1024   /* device Alg. 2 keeps a 1024-bit availability mask     */
 #define CS_MAX_SEGMENTS    4096
 #define CS_QUANTUM           32   /* segment bounds are multiples of 32 elements (C-2)    */
+#define CS_MAX_LAYERS     65536   /* layer-table entries (cs_set_layers)                  */
 #define CS_IPC_HANDLE_BYTES  64   /* sizeof(cudaIpcMemHandle_t)                           */
 
 #define CS_TAG_FLAT 0             /* Philox domain tag of the flat topology               */
@@ -212,6 +213,44 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
  * outside [1, 2^24)), CS_ELAYOUT (alignment), CS_ECUDA. */
 int cs_accumulate(float* acc, const float* grads, int count, int interval);
 
+/* Layer-aligned segment plan helper (host only; SPEC.md:40-47 build_segment_plan,
+ * Table 1 "Segmenting blocks and FC layer").  Partitions n_layers
+ * consecutive layers of element counts layer_sizes[] into k contiguous non-empty
+ * segments minimising the largest segment; among those, each segment left to right
+ * takes as many layers as possible (reading C-19).  Writes seg_of_layer_out[n_layers].
+ * Errors: CS_EINVAL (NULL, n_layers outside [1, CS_MAX_LAYERS], a size < 1),
+ * CS_EINVAL_SEGMENTS (k outside [1, n_layers]). */
+int cs_segment_plan(const int64_t* layer_sizes, int n_layers, int k, int32_t* seg_of_layer_out);
+
+/* Layer table of the bound vector (host arrays, copied): layer l is columns
+ * [layer_bounds[l], layer_bounds[l+1]), layer_bounds[0] = 0, layer_bounds[n_layers] = d,
+ * strictly increasing, every interior bound a multiple of 4 elements (16-byte rows for
+ * bulk copies).  seg_of_layer (may be NULL) assigns the layers to the k segments of
+ * cs_init: non-decreasing from 0 to k-1 in steps of 0 or 1; the segment bounds become
+ * the layer bounds where it steps (the paper's "blocks and FC layer" plan).  NULL keeps
+ * the equal split of reading C-2; the layers then only serve LARS.  layer_bounds NULL
+ * or n_layers 0 clears the table.  Lives until the next cs_bind.
+ * Runs on the single-GPU bulk-TMA path (world <= 64, k*world <= 2048); the
+ * hierarchical step refuses a layer table.
+ * Errors: CS_ENOTBOUND, CS_EINVAL, CS_ELAYOUT (bounds), CS_EINVAL_SEGMENTS,
+ * CS_EUNSUPPORTED (multi-GPU or the register path), CS_ECUDA. */
+int cs_set_layers(const int64_t* layer_bounds, int n_layers, const int32_t* seg_of_layer);
+
+/* LARS in the flat step ("adapts the learning rate of each layer by the
+ * ratio of the weight norm to the gradient norm"; Table 1: eta 0.0025, weight decay
+ * 5e-5).  eta > 0 enables, eta == 0 disables.  With it enabled,
+ * every flat step computes, for each worker i and layer l, from this step's x and g:
+ *   scale = eta*|x_il| / ((|g_il| + wd*|x_il|) + eps)   (fp64; 1 if a norm is 0)
+ *   lrs   = fp32(lr * scale)
+ * and applies  m = mu*m + (g + wd*x),  y = x - lrs*m  before the exchange (C-18).
+ * Needs a layer table at step time (CS_EINVAL otherwise).  Three launches per
+ * step: k_lars_norms, k_lars_scale, k_gossip_tma.  Errors: CS_ENOTINIT, CS_EINVAL. */
+int cs_set_lars(float eta, float weight_decay, float eps);
+
+/* Rates lrs [n_loc][n_layers] (host, row-major) of the most recent LARS step.
+ * Synchronises the stream.  Errors: CS_EINVAL (no LARS step since cs_set_layers). */
+int cs_get_lars_rates(float* rates_out);
+
 /* Set / read the step counter t (resume = restore buffers + cs_set_step). */
 int cs_set_step(int64_t step);
 int cs_get_step(int64_t* step_out);
@@ -250,12 +289,14 @@ int cs_synth_fill(float* out, int64_t rows, int64_t d, int64_t ld, uint64_t seed
 
 /* Bytes per step the hot kernel moves, for roofline accounting:
  * out[0] = algorithmic HBM bytes, out[1] = NVLink bytes into this GPU at step t
- * (exact, from the topology), for flat (hier = 0) or hierarchical (hier = 1). */
+ * (exact, from the topology), for flat (hier = 0) or hierarchical (hier = 1).
+ * Flat: 20 B per parameter per local worker, 28 B with LARS (the norm pass re-reads
+ * x and g). */
 int cs_step_bytes(int64_t step, int hier, double* out);
 
 /* Kernel timing for roofline accounting: with cs_set_timing(1) every later step
- * records a CUDA event pair on the bound stream around its hot kernel
- * (k_gossip_local / k_hier_local / k_gossip_peer).  cs_set_timing(1) also
+ * records a CUDA event pair on the bound stream around its hot kernel(s)
+ * (the names cs_kernel_info returns; with LARS the pair brackets all three launches).  cs_set_timing(1) also
  * clears earlier records.  cs_get_timing synchronises and returns the summed
  * event-measured duration (ms) and the number of timed launches. */
 int cs_set_timing(int enable);

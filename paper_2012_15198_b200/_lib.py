@@ -54,6 +54,10 @@ _SIGS = {
     "cs_gossip_step_host": (_c_int, [_vp, _vp, _vp, _c_f, _c_f, _vp]),
     "cs_hier_step": (_c_int, [_vp, _vp, _vp, _c_f, _c_f]),
     "cs_accumulate": (_c_int, [_vp, _vp, _c_int, _c_int]),
+    "cs_segment_plan": (_c_int, [_vp, _c_int, _c_int, _vp]),
+    "cs_set_layers": (_c_int, [_vp, _c_int, _vp]),
+    "cs_set_lars": (_c_int, [_c_f, _c_f, _c_f]),
+    "cs_get_lars_rates": (_c_int, [_vp]),
     "cs_set_step": (_c_int, [_c_i64]),
     "cs_get_step": (_c_int, [_vp]),
     "cs_set_diag": (_c_int, [_c_int]),
@@ -194,6 +198,36 @@ def cs_accumulate(acc, grads, count: int, interval: int) -> None:
     """Micro-step `count` of a communication interval (Table 1):
     acc = 0 + g at count 0, acc += g after, acc /= interval at count interval-1."""
     _check(lib.cs_accumulate(_ptr(acc), _ptr(grads), count, interval), "cs_accumulate")
+
+
+def cs_segment_plan(layer_sizes, k: int) -> np.ndarray:
+    """Layer-aligned segment plan (SPEC build_segment_plan, Table 1): seg_of_layer."""
+    sz = np.ascontiguousarray(layer_sizes, dtype=np.int64)
+    out = np.zeros(len(sz), dtype=np.int32)
+    _check(lib.cs_segment_plan(sz.ctypes.data, len(sz), k, out.ctypes.data), "cs_segment_plan")
+    return out
+
+
+def cs_set_layers(layer_bounds, seg_of_layer=None) -> None:
+    """Layer table [n_layers + 1] of the bound vector, optionally the segment of each layer."""
+    if layer_bounds is None:
+        _check(lib.cs_set_layers(None, 0, None), "cs_set_layers")
+        return
+    lb = np.ascontiguousarray(layer_bounds, dtype=np.int64)
+    sl = None if seg_of_layer is None else np.ascontiguousarray(seg_of_layer, dtype=np.int32)
+    _check(lib.cs_set_layers(lb.ctypes.data, len(lb) - 1, None if sl is None else sl.ctypes.data),
+           "cs_set_layers")
+
+
+def cs_set_lars(eta: float, weight_decay: float = 0.0, eps: float = 0.0) -> None:
+    """LARS in the flat step (Table 1); eta == 0 disables."""
+    _check(lib.cs_set_lars(eta, weight_decay, eps), "cs_set_lars")
+
+
+def cs_get_lars_rates(n_loc: int, n_layers: int) -> np.ndarray:
+    out = np.zeros((n_loc, n_layers), dtype=np.float32)
+    _check(lib.cs_get_lars_rates(out.ctypes.data), "cs_get_lars_rates")
+    return out
 
 
 def cs_set_step(step: int) -> None:

@@ -7,6 +7,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+#include <cmath>
 #include <string>
 #include <vector>
 
@@ -85,6 +87,17 @@ struct Ctx {
 
   PeerState peer;             // multi-GPU exchange region (nprocs > 1)
 
+  // layer table (cs_set_layers) and LARS (cs_set_lars); the layer table is per cs_bind
+  std::vector<int64_t> layer_bounds;  // [n_layers + 1]; empty: no table
+  std::vector<int64_t> plan;          // segment bounds in use [k + 1]
+  int n_layers = 0;
+  int32_t* d_tile_first = nullptr;    // [n_layers + 1] tile range of each layer
+  float* d_lrs = nullptr;             // [n_loc][n_layers] rates of the last LARS step
+  double* d_lars_part = nullptr;      // [n_tiles][n_loc][2]
+  bool lars = false;
+  float lars_eta = 0.f, lars_wd = 0.f, lars_eps = 0.f;
+  bool lars_valid = false;
+
   // hot-kernel timing (cs_set_timing): event pairs recorded around each launch
   bool timing = false;
   std::vector<cudaEvent_t> events;
@@ -118,6 +131,9 @@ void free_device() {
   auto f = [](void* p) { if (p) cudaFree(p); };
   f(g.d_bounds); f(g.d_src); f(g.d_dst); f(g.d_ord); f(g.d_given); f(g.d_rw);
   f(g.d_inv_wsum); f(g.d_err); f(g.d_partials); f(g.d_diag); f(g.d_stage); f(g.d_counter); f(g.d_tiles);
+  f(g.d_tile_first); f(g.d_lrs); f(g.d_lars_part);
+  g.d_tile_first = nullptr; g.d_lrs = nullptr; g.d_lars_part = nullptr;
+  g.layer_bounds.clear(); g.plan.clear(); g.n_layers = 0; g.lars_valid = false;
   g.d_bounds = nullptr; g.d_src = nullptr; g.d_dst = nullptr; g.d_ord = nullptr;
   g.d_given = nullptr; g.d_rw = nullptr; g.d_inv_wsum = nullptr; g.d_err = nullptr;
   g.d_partials = nullptr; g.d_diag = nullptr; g.d_stage = nullptr; g.d_counter = nullptr;
@@ -138,6 +154,45 @@ std::vector<int64_t> host_bounds(int64_t d, int k) {
 }
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// Bulk-TMA tiles: every (segment, layer) intersection in column order, cut into pieces
+// of at most T columns, so each tile lies in one segment and one layer and the tiles of
+// a layer are a contiguous range.  Without a layer table the whole vector is layer 0.
+int build_tma_tiles() {
+  const std::vector<int64_t>& b = g.plan;
+  std::vector<int64_t> lb = g.layer_bounds.empty() ? std::vector<int64_t>{0, g.d} : g.layer_bounds;
+  const int L = (int)lb.size() - 1;
+  const int T = tma_tile_len(g.d, g.tma_grid_plain);
+  std::vector<TileDesc> tiles;
+  std::vector<int32_t> first(L + 1, 0);
+  int l = 0;
+  for (int s = 0; s < g.k; ++s) {
+    int64_t c = b[s];
+    while (c < b[s + 1]) {
+      while (lb[l + 1] <= c) first[++l] = (int32_t)tiles.size();
+      const int64_t end = std::min(std::min(b[s + 1], lb[l + 1]), c + T);
+      TileDesc td;
+      td.c0 = c;
+      td.seg = s;
+      td.len = (int32_t)(end - c);
+      td.layer = l;
+      td.pad_ = 0;
+      tiles.push_back(td);
+      c = end;
+    }
+  }
+  while (l < L) first[++l] = (int32_t)tiles.size();
+  if (g.d_tiles) cudaFree(g.d_tiles);
+  if (g.d_tile_first) cudaFree(g.d_tile_first);
+  g.d_tiles = nullptr;
+  g.d_tile_first = nullptr;
+  g.n_tiles = (int)tiles.size();
+  CS_CUDA(cudaMalloc(&g.d_tiles, sizeof(TileDesc) * tiles.size()));
+  CS_CUDA(cudaMemcpy(g.d_tiles, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice));
+  CS_CUDA(cudaMalloc(&g.d_tile_first, sizeof(int32_t) * first.size()));
+  CS_CUDA(cudaMemcpy(g.d_tile_first, first.data(), sizeof(int32_t) * first.size(), cudaMemcpyHostToDevice));
+  return CS_OK;
+}
 
 int check_bound() {
   if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
@@ -217,6 +272,9 @@ LocalArgs local_args(float* params, const float* grads, float* psw, int n, int g
   a.err = g.d_err;
   a.tiles = g.d_tiles;
   a.n_tiles = g.n_tiles;
+  a.lrs = nullptr;
+  a.n_layers = 0;
+  a.wd = 0.f;
   return a;
 }
 
@@ -271,16 +329,29 @@ int enqueue_flat_step(float* params, const float* grads, float* psw, float lr, f
   const int n = g.world;
   const bool fused = fused_topology_ok(n, g.k);
   LocalArgs a = local_args(params, grads, psw, n, 1, CS_TAG_FLAT, lr, mu);
+  if (g.lars && g.n_layers == 0) return fail(CS_EINVAL, "LARS needs a layer table (cs_set_layers)");
+  if (g.lars && !(fused && g.use_tma))
+    return fail(CS_EUNSUPPORTED, "LARS runs on the bulk-TMA path (world <= 64, k*world <= 2048)");
   if (fused && g.use_tma) {
     a.given = g.has_override ? g.d_given : nullptr;
     cudaEvent_t ev[2];
     int rc = next_event_pair(ev);
     if (rc) return rc;
     if (ev[0]) CS_CUDA(cudaEventRecord(ev[0], g.stream));
+    if (g.lars) {
+      // per-(worker, layer) rates from this step's x and g, then the LARS step kernel
+      CS_CUDA(launch_lars_rates(params, grads, g.ld, g.d_tiles, g.n_tiles, g.n_loc, g.d_tile_first,
+                                g.n_layers, g.d_lars_part, lr, g.lars_eta, g.lars_wd, g.lars_eps,
+                                g.d_lrs, g.stream));
+      a.lrs = g.d_lrs;
+      a.n_layers = g.n_layers;
+      a.wd = g.lars_wd;
+    }
     CS_CUDA(launch_gossip_tma(a, diag, diag ? g.tma_grid_diag : g.tma_grid_plain, g.stream));
     if (ev[1]) CS_CUDA(cudaEventRecord(ev[1], g.stream));
-    g.launches_per_step = 1;
-    g.hot_kernel = "k_gossip_tma";
+    g.launches_per_step = g.lars ? 3 : 1;
+    g.hot_kernel = g.lars ? "k_lars_norms+k_lars_scale+k_gossip_tma" : "k_gossip_tma";
+    if (g.lars) g.lars_valid = true;
     return CS_OK;
   }
   if (fused) {
@@ -399,6 +470,7 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
   CS_CUDA(cudaGetDevice(&g.device));
   const size_t kn = (size_t)g.k * g.world;
   std::vector<int64_t> b = host_bounds(d, g.k);
+  g.plan = b;
   CS_CUDA(cudaMalloc(&g.d_bounds, sizeof(int64_t) * b.size()));
   CS_CUDA(cudaMemcpy(g.d_bounds, b.data(), sizeof(int64_t) * b.size(), cudaMemcpyHostToDevice));
   CS_CUDA(cudaMalloc(&g.d_src, sizeof(int32_t) * kn));
@@ -421,19 +493,8 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
     g.tma_grid_plain = tma_grid(g.world, g.k, false);
     g.tma_grid_diag = tma_grid(g.world, g.k, true);
     CS_CUDA(cudaGetLastError());
-    const int T = tma_tile_len(d, g.tma_grid_plain);
-    std::vector<TileDesc> tiles;
-    for (int s = 0; s < g.k; ++s)
-      for (int64_t c = b[s]; c < b[s + 1]; c += T) {
-        TileDesc td;
-        td.c0 = c;
-        td.seg = s;
-        td.len = (int32_t)((c + T < b[s + 1] ? c + T : b[s + 1]) - c);
-        tiles.push_back(td);
-      }
-    g.n_tiles = (int)tiles.size();
-    CS_CUDA(cudaMalloc(&g.d_tiles, sizeof(TileDesc) * tiles.size()));
-    CS_CUDA(cudaMemcpy(g.d_tiles, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice));
+    int rc = build_tma_tiles();
+    if (rc) return rc;
   }
   if (g.use_peer) {
     // hierarchical steps over the peer path: one worker per GPU, groups of world/groups GPUs
@@ -492,6 +553,7 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
     rc = enqueue_flat_step(params, grads, psw, lr, momentum, diag);
   } else {
     if (!g.peer.imported) return fail(CS_ENOTBOUND, "multi-GPU: cs_ipc_import has not been called");
+    if (g.lars) return fail(CS_EUNSUPPORTED, "LARS runs on the single-GPU bulk-TMA path");
     PeerStepArgs pa = peer_args(params, grads, psw, lr, momentum);
     pa.given = g.has_override ? g.d_given : nullptr;
     cudaEvent_t ev[2];
@@ -541,6 +603,8 @@ int cs_gossip_step_host(float* params, const float* grads_host, float* psw, floa
 int cs_hier_step(float* params, float* grads, float* psw, float lr, float momentum) {
   int rc = check_bound();
   if (rc) return rc;
+  if (g.lars || g.n_layers > 0)
+    return fail(CS_EUNSUPPORTED, "LARS / layer tables are not implemented for the hierarchical step");
   rc = check_step_args(params, grads, psw);
   if (rc) return rc;
   const bool diag = g.diag != 0;
@@ -582,6 +646,126 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
   g.hot_kernel = "k_hier_local";
   g.step += 1;
   return CS_OK;
+}
+
+int cs_segment_plan(const int64_t* layer_sizes, int n_layers, int k, int32_t* seg_of_layer_out) {
+  if (!layer_sizes || !seg_of_layer_out) return fail(CS_EINVAL, "NULL layer_sizes/seg_of_layer_out");
+  if (n_layers < 1 || n_layers > CS_MAX_LAYERS)
+    return fail(CS_EINVAL, "n_layers %d outside [1, %d]", n_layers, CS_MAX_LAYERS);
+  if (k < 1 || k > n_layers) return fail(CS_EINVAL_SEGMENTS, "k %d outside [1, n_layers=%d]", k, n_layers);
+  std::vector<int64_t> pre(n_layers + 1, 0);
+  int64_t mx = 0;
+  for (int i = 0; i < n_layers; ++i) {
+    if (layer_sizes[i] < 1) return fail(CS_EINVAL, "layer %d has size %lld", i, (long long)layer_sizes[i]);
+    pre[i + 1] = pre[i] + layer_sizes[i];
+    mx = std::max(mx, layer_sizes[i]);
+  }
+  // can layers [i, n) be cut into at most `pieces` contiguous runs of <= cap?
+  auto feasible = [&](int i, int pieces, int64_t cap) {
+    int used = (i < n_layers) ? 1 : 0;
+    int64_t cur = 0;
+    for (int j = i; j < n_layers; ++j) {
+      if (cur + layer_sizes[j] > cap) { ++used; cur = layer_sizes[j]; }
+      else cur += layer_sizes[j];
+    }
+    return used <= pieces;
+  };
+  // smallest cap (a contiguous sum) admitting k pieces: binary search on integers
+  int64_t lo = mx, hi = pre[n_layers];
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (feasible(0, k, mid)) hi = mid; else lo = mid + 1;
+  }
+  const int64_t cap = lo;
+  // each segment, left to right, takes as many layers as the cap and the rest allow
+  int start = 0;
+  for (int s = 0; s < k; ++s) {
+    const int left = k - s - 1;
+    int end = n_layers;
+    if (left > 0) {
+      int e1 = start + 1;  // largest end with sum(start, e1) <= cap
+      while (e1 + 1 <= n_layers - left && pre[e1 + 1] - pre[start] <= cap) ++e1;
+      end = e1;
+      while (end > start + 1 && !feasible(end, left, cap)) --end;
+    }
+    for (int i = start; i < end; ++i) seg_of_layer_out[i] = s;
+    start = end;
+  }
+  return CS_OK;
+}
+
+int cs_set_layers(const int64_t* layer_bounds, int n_layers, const int32_t* seg_of_layer) {
+  int rc = check_bound();
+  if (rc) return rc;
+  if (!layer_bounds || n_layers == 0) {  // clear: back to the equal split, no layers
+    g.layer_bounds.clear();
+    g.n_layers = 0;
+    g.plan = host_bounds(g.d, g.k);
+    return g.use_tma ? build_tma_tiles() : CS_OK;
+  }
+  if (n_layers < 1 || n_layers > CS_MAX_LAYERS)
+    return fail(CS_EINVAL, "n_layers %d outside [1, %d]", n_layers, CS_MAX_LAYERS);
+  if (g.use_peer || !g.use_tma)
+    return fail(CS_EUNSUPPORTED, "layer tables run on the single-GPU bulk-TMA path");
+  if (layer_bounds[0] != 0 || layer_bounds[n_layers] != g.d)
+    return fail(CS_ELAYOUT, "layer bounds must run from 0 to d = %lld", (long long)g.d);
+  for (int i = 0; i < n_layers; ++i) {
+    if (layer_bounds[i + 1] <= layer_bounds[i])
+      return fail(CS_ELAYOUT, "layer %d is empty or the bounds decrease", i);
+    if (layer_bounds[i] % 4 != 0)
+      return fail(CS_ELAYOUT, "layer bound %lld is not a multiple of 4 elements", (long long)layer_bounds[i]);
+  }
+  std::vector<int64_t> plan;
+  if (seg_of_layer) {
+    if (seg_of_layer[0] != 0 || seg_of_layer[n_layers - 1] != g.k - 1)
+      return fail(CS_EINVAL_SEGMENTS, "seg_of_layer must run from 0 to k-1 = %d", g.k - 1);
+    plan.push_back(0);
+    for (int i = 1; i < n_layers; ++i) {
+      const int step = seg_of_layer[i] - seg_of_layer[i - 1];
+      if (step != 0 && step != 1)
+        return fail(CS_EINVAL_SEGMENTS, "seg_of_layer must be contiguous (layer %d)", i);
+      if (step == 1) plan.push_back(layer_bounds[i]);
+    }
+    plan.push_back(g.d);
+  } else {
+    plan = host_bounds(g.d, g.k);
+  }
+  g.layer_bounds.assign(layer_bounds, layer_bounds + n_layers + 1);
+  g.n_layers = n_layers;
+  g.plan = plan;
+  rc = build_tma_tiles();
+  if (rc) return rc;
+  if (g.d_lrs) cudaFree(g.d_lrs);
+  if (g.d_lars_part) cudaFree(g.d_lars_part);
+  g.d_lrs = nullptr;
+  g.d_lars_part = nullptr;
+  CS_CUDA(cudaMalloc(&g.d_lrs, sizeof(float) * (size_t)g.n_loc * n_layers));
+  CS_CUDA(cudaMalloc(&g.d_lars_part, sizeof(double) * 2 * (size_t)g.n_tiles * g.n_loc));
+  g.lars_valid = false;
+  return CS_OK;
+}
+
+int cs_set_lars(float eta, float weight_decay, float eps) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (!(eta >= 0.f) || !(weight_decay >= 0.f) || !(eps >= 0.f) || !std::isfinite(eta) ||
+      !std::isfinite(weight_decay) || !std::isfinite(eps))
+    return fail(CS_EINVAL, "LARS eta, weight_decay, eps must be finite and >= 0");
+  g.lars = eta > 0.f;
+  g.lars_eta = eta;
+  g.lars_wd = weight_decay;
+  g.lars_eps = eps;
+  return CS_OK;
+}
+
+int cs_get_lars_rates(float* rates_out) {
+  int rc = check_bound();
+  if (rc) return rc;
+  if (!rates_out) return fail(CS_EINVAL, "NULL rates_out");
+  if (!g.lars_valid || !g.d_lrs) return fail(CS_EINVAL, "no LARS step since the layer table was set");
+  CS_CUDA(cudaStreamSynchronize(g.stream));
+  CS_CUDA(cudaMemcpy(rates_out, g.d_lrs, sizeof(float) * (size_t)g.n_loc * g.n_layers,
+                     cudaMemcpyDeviceToHost));
+  return poll_device_errors();
 }
 
 int cs_accumulate(float* acc, const float* grads, int count, int interval) {
@@ -691,7 +875,7 @@ int cs_step_bytes(int64_t step, int hier, double* out) {
   const double d = (double)g.d;
   std::vector<int64_t> b = host_bounds(g.d, g.k);
   if (!hier) {
-    out[0] = 20.0 * g.n_loc * d;  // read x, m, g; write x', m'
+    out[0] = (g.lars ? 28.0 : 20.0) * g.n_loc * d;  // read x, m, g; write x', m' (+ LARS norms: x, g)
     std::vector<int32_t> src((size_t)g.k * g.world);
     int rc = cs_topology(step, src.data());
     if (rc) return rc;

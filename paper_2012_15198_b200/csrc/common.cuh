@@ -68,13 +68,20 @@ struct LocalArgs {
   // bulk-TMA kernel: segment-aligned column tiles
   const TileDesc* tiles;
   int n_tiles;
+  // LARS (k_gossip_tma<., true>): per-(row, layer) rates of this step and the weight decay
+  const float* lrs;    // [rows][n_layers]
+  int n_layers;
+  float wd;
 };
 
-// A column tile [c0, c0 + len) inside segment seg (len <= kTmaTileMax, c0 % 32 == 0).
+// A column tile [c0, c0 + len) inside segment seg and layer `layer` (len <= kTmaTileMax,
+// c0 % 4 == 0; c0 % 32 == 0 under the equal split without a layer table).
 struct TileDesc {
   int64_t c0;
   int32_t seg;
   int32_t len;
+  int32_t layer;
+  int32_t pad_;
 };
 
 constexpr int kTmaTileMax = 2048;   // elements per row-tile (8 KB per array)
@@ -97,6 +104,12 @@ int tma_tile_len(int64_t d, int grid);
 cudaError_t launch_gossip_tma(const LocalArgs& a, bool diag, int grid, cudaStream_t st);
 cudaError_t launch_synth(float* out, int64_t rows, int64_t d, int64_t ld, uint64_t seed,
                          int tag, int64_t row0, float scale, cudaStream_t st);
+// LARS (lars.cu): per-(tile, row) fp64 partial sums of x^2, g^2, then per-(row, layer)
+// rates lrs = fp32(lr * scale).  tile_first: [n_layers + 1] tile ranges of the layers.
+cudaError_t launch_lars_rates(const float* x, const float* g, int64_t ld, const TileDesc* tiles,
+                              int n_tiles, int rows, const int32_t* tile_first, int n_layers,
+                              double* part, float lr, float eta, float wd, float eps, float* lrs,
+                              cudaStream_t st);
 cudaError_t launch_accumulate(float* acc, const float* g, int64_t rows, int64_t d, int64_t ld,
                               int count, int interval, cudaStream_t st);
 

@@ -53,6 +53,12 @@ __device__ __forceinline__ float4 momentum_update(float4 m, float4 g, float mu) 
                      __fadd_rn(__fmul_rn(mu, m.z), g.z), __fadd_rn(__fmul_rn(mu, m.w), g.w));
 }
 
+// LARS's weight-decayed gradient g + wd*x (reading C-18)
+__device__ __forceinline__ float4 decay4(float4 g, float4 x, float wd) {
+  return make_float4(__fadd_rn(g.x, __fmul_rn(wd, x.x)), __fadd_rn(g.y, __fmul_rn(wd, x.y)),
+                     __fadd_rn(g.z, __fmul_rn(wd, x.z)), __fadd_rn(g.w, __fmul_rn(wd, x.w)));
+}
+
 __device__ __forceinline__ float4 sgd_apply(float4 x, float4 m, float lr) {
   return make_float4(__fsub_rn(x.x, __fmul_rn(lr, m.x)), __fsub_rn(x.y, __fmul_rn(lr, m.y)),
                      __fsub_rn(x.z, __fmul_rn(lr, m.z)), __fsub_rn(x.w, __fmul_rn(lr, m.w)));
@@ -505,19 +511,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 __host__ __device__ inline size_t tma_smem_bytes(int n, int k, bool diag) {
-  return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t) +
+  return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t) + kStages * sizeof(float) +
          fused_smem_bytes(n, k, kTmaThreads / 32, diag);
 }
 
 }  // namespace
 
-template <bool DIAG>
+// LARS (reading C-18): the producer stages the row's per-layer rate
+// lrs[row][tile.layer] with each ring slot (st.shared before the release-arrive), and
+// the update becomes m' = mu*m + (g + wd*x), y = x - rate*m'.
+template <bool DIAG, bool LARS>
 __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage_buf = reinterpret_cast<float*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-  SmemTopo t = carve(reinterpret_cast<unsigned char*>(empty + kStages), a.n, a.k, DIAG);
+  float* srate = reinterpret_cast<float*>(empty + kStages);  // [kStages]
+  SmemTopo t = carve(reinterpret_cast<unsigned char*>(srate + kStages), a.n, a.k, DIAG);
 
   const int n = a.n;
   const int64_t ld = a.ld;
@@ -545,6 +555,7 @@ __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
           mbar_wait(&empty[st], ((it / kStages) & 1u) ^ 1u);
           const int64_t off = (int64_t)(ord[p] & kOrdIdx) * ld + td.c0;
           float* buf = stage_buf + (size_t)st * 3 * kTmaTileMax;
+          if (LARS) srate[st] = a.lrs[(int64_t)(ord[p] & kOrdIdx) * a.n_layers + td.layer];
           mbar_arrive_expect_tx(&full[st], 3 * bytes);
           bulk_g2s(buf, a.x + off, bytes, &full[st]);
           bulk_g2s(buf + kTmaTileMax, a.m + off, bytes, &full[st]);
@@ -576,6 +587,7 @@ __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
         const float* buf = stage_buf + (size_t)st * 3 * kTmaTileMax;
         const uint32_t e = ord[p];
         const uint32_t row = e & kOrdIdx;
+        const float rate = LARS ? srate[st] : lr;
 #pragma unroll
         for (int c = 0; c < kVPT; ++c) {
           const int v = c * kTmaConsumers + threadIdx.x;       // float4 index in the tile
@@ -586,8 +598,8 @@ __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
             const float4 cm = reinterpret_cast<const float4*>(buf + kTmaTileMax)[v];
             const float4 cg = reinterpret_cast<const float4*>(buf + 2 * kTmaTileMax)[v];
             bad |= nonfinite4(cg);
-            const float4 mn = momentum_update(cm, cg, mu);
-            const float4 y = sgd_apply(cx, mn, lr);
+            const float4 mn = momentum_update(cm, LARS ? decay4(cg, cx, a.wd) : cg, mu);
+            const float4 y = sgd_apply(cx, mn, rate);
             const int64_t j = td.c0 + 4 * v;
             st_stream(a.m + (int64_t)row * ld + j, mn, vv);
             if (e & kOrdStart) {
@@ -626,8 +638,10 @@ __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
 
 int tma_grid(int n, int k, bool diag) {
   const size_t smem = tma_smem_bytes(n, k, diag);
-  auto kern = diag ? k_gossip_tma<true> : k_gossip_tma<false>;
+  auto kern = diag ? k_gossip_tma<true, false> : k_gossip_tma<false, false>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(diag ? k_gossip_tma<true, true> : k_gossip_tma<false, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTmaThreads, smem);
   if (occ < 1) occ = 1;
@@ -652,8 +666,11 @@ int tma_tile_len(int64_t d, int grid) {
 
 cudaError_t launch_gossip_tma(const LocalArgs& a, bool diag, int grid, cudaStream_t st) {
   const size_t smem = tma_smem_bytes(a.n, a.k, diag);
-  if (diag) k_gossip_tma<true><<<grid, kTmaThreads, smem, st>>>(a);
-  else k_gossip_tma<false><<<grid, kTmaThreads, smem, st>>>(a);
+  const bool lars = a.lrs != nullptr;
+  if (diag && lars) k_gossip_tma<true, true><<<grid, kTmaThreads, smem, st>>>(a);
+  else if (diag) k_gossip_tma<true, false><<<grid, kTmaThreads, smem, st>>>(a);
+  else if (lars) k_gossip_tma<false, true><<<grid, kTmaThreads, smem, st>>>(a);
+  else k_gossip_tma<false, false><<<grid, kTmaThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
 

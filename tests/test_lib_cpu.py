@@ -113,3 +113,21 @@ def test_segment_bounds_errors():
     with pytest.raises(cs.CSError) as e:
         cs.cs_segment_bounds(64, 3)
     assert e.value.code == -3
+
+
+def test_host_segment_plan_matches_oracle():
+    # C++ cs_segment_plan (binary search + greedy) vs oracle/lars.segment_plan (bit-exact)
+    from oracle.lars import segment_plan
+    import synth
+    rng = np.random.default_rng(7)
+    for _ in range(200):
+        L = int(rng.integers(1, 30))
+        sizes = [int(v) for v in rng.integers(1, 50, size=L) * 4]
+        for k in sorted({1, L, int(rng.integers(1, L + 1))}):
+            assert cs.cs_segment_plan(sizes, k).tolist() == segment_plan(sizes, k), (sizes, k)
+    sizes, _ = synth.resnet50_layers()
+    for k in (2, 8, 18, 161):
+        assert cs.cs_segment_plan(sizes, k).tolist() == segment_plan(sizes, k), k
+    for bad_k in (0, 162):
+        with pytest.raises(cs.CSError):
+            cs.cs_segment_plan(sizes, bad_k)
