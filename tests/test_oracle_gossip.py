@@ -100,9 +100,9 @@ def test_p8_k1_exponential_equals_sgp_pushsum(n):
     w = np.ones((n, 1), F32)
     vals, wts = [x[i].copy() for i in range(n)], [w[i].copy() for i in range(n)]
     seg = np.zeros(d, int)
+    from oracle.sgp import exponential_topology
     for t in range(7):
-        off = 1 << (t % (n.bit_length() - 1))
-        src = np.array([[(i - off) % n for i in range(n)]], np.int32)
+        src = exponential_topology(t, n, 1)
         x, m, w = gossip_step(x, m, np.zeros_like(x), w, src, seg, 0.0, 0.96)
         vals, wts = _pushsum_round(vals, wts, t)
         assert np.array_equal(x, np.stack(vals))
