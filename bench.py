@@ -243,6 +243,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-interval", action="store_true", help="skip the communication-interval sub-measurement")
+    ap.add_argument("--scheme", default="crossover", choices=["crossover", "sgp", "allreduce"],
+                    help="SURVEY 8(f) #3 baselines on the same machinery: sgp = SGP's directed exponential "
+                         "graph, model-wise (k=1 unless --k); allreduce = AllReduce-SGD (hierarchical, 1 group)")
     ap.add_argument("--path", default="auto", choices=["auto", "reg", "tma", "peer"],
                     help="library kernel path (cs_set_path); peer with 1 GPU = single-GPU emulation")
     args = ap.parse_args()
@@ -286,9 +289,13 @@ def main():
     first = rank * n_loc
     B = world + 1
 
-    hier = args.config == "c4"
-    groups = max(1, world // 4) if hier else world
+    hier = args.config == "c4" or args.scheme == "allreduce"
+    groups = 1 if args.scheme == "allreduce" else (max(1, world // 4) if hier else world)
+    if args.scheme == "sgp" and not args.k:
+        k = 1
     cs.cs_init(world, groups, k, seed)
+    if args.scheme == "sgp":
+        cs.cs_set_topology_kind(cs.TOPO_EXPONENTIAL)
     step_fn = cs.cs_hier_step if hier else cs.cs_gossip_step
     cs.cs_set_path({"auto": 0, "reg": 1, "tma": 2, "peer": 3}[args.path])
     stream = torch.cuda.Stream(dev)
@@ -497,7 +504,7 @@ def main():
               "vs_baseline": None, "dtype": "f32", "data": "synthetic",
               "config": {"workload": f"{args.config}: {desc}", "world": world, "workers_per_gpu": n_loc,
                          "d": d, "k": k, "seed": seed, "lr": lr, "momentum": mu,
-                         "parallelism": f"workers partitioned over {world_size} GPU(s)",
+                         "parallelism": f"workers partitioned over {world_size} GPU(s)", "scheme": args.scheme,
                          "l2": f"inputs larger than L2 ({20.0 * n_loc * d / 1e9:.2f} GB moved per step per GPU)"},
               "step_us": ms_step * 1e3,
               "traffic_GBps": 20.0 * world * d / (ms_step * 1e-3) / 1e9,

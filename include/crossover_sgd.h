@@ -56,6 +56,10 @@ extern "C" {
 #define CS_TAG_FLAT 0             /* Philox domain tag of the flat topology               */
 #define CS_TAG_HIER 1             /* Philox domain tag of the leader topology (C-13)      */
 
+/* Topology kinds (cs_set_topology_kind). */
+#define CS_TOPO_CROSSOVER   0   /* Alg. 2 load-balanced random topology per segment (default) */
+#define CS_TOPO_EXPONENTIAL 1   /* SGP's directed exponential graph, the baseline */
+
 /* ---- context -------------------------------------------------------------- */
 
 /* Create the process-wide context.
@@ -250,6 +254,20 @@ int cs_set_lars(float eta, float weight_decay, float eps);
 /* Rates lrs [n_loc][n_layers] (host, row-major) of the most recent LARS step.
  * Synchronises the stream.  Errors: CS_EINVAL (no LARS step since cs_set_layers). */
 int cs_get_lars_rates(float* rates_out);
+
+/* Topology of the flat step (the SGP baseline on the same machinery).
+ * CS_TOPO_CROSSOVER: Alg. 2, a fresh load-balanced random derangement per segment
+ * (PAPER.md:165-191).  CS_TOPO_EXPONENTIAL: SGP's directed exponential graph
+ * ("model-wise communication and directed exponential network topology";
+ * SPEC.md:136-144): at step t worker i receives from (i - 2^(t mod log2 world)) mod world,
+ * the same peer for every segment (use k = 1 for SGP's model-wise exchange).  The
+ * update, merge and push-sum weights are unchanged: halving and pushing to one peer is
+ * the merge of Alg. 1 l.17.  Applies to cs_gossip_step, cs_gossip_step_host and
+ * cs_topology on every path; the hierarchical step keeps Alg. 2 for its leaders.
+ * AllReduce-SGD, the other baseline, is cs_hier_step with groups = 1.
+ * Errors: CS_ENOTINIT, CS_EINVAL (unknown kind), CS_EUNSUPPORTED (exponential with a
+ * world that is not a power of two), CS_ECUDA. */
+int cs_set_topology_kind(int kind);
 
 /* Set / read the step counter t (resume = restore buffers + cs_set_step). */
 int cs_set_step(int64_t step);

@@ -54,6 +54,7 @@ _SIGS = {
     "cs_gossip_step_host": (_c_int, [_vp, _vp, _vp, _c_f, _c_f, _vp]),
     "cs_hier_step": (_c_int, [_vp, _vp, _vp, _c_f, _c_f]),
     "cs_accumulate": (_c_int, [_vp, _vp, _c_int, _c_int]),
+    "cs_set_topology_kind": (_c_int, [_c_int]),
     "cs_segment_plan": (_c_int, [_vp, _c_int, _c_int, _vp]),
     "cs_set_layers": (_c_int, [_vp, _c_int, _vp]),
     "cs_set_lars": (_c_int, [_c_f, _c_f, _c_f]),
@@ -228,6 +229,14 @@ def cs_get_lars_rates(n_loc: int, n_layers: int) -> np.ndarray:
     out = np.zeros((n_loc, n_layers), dtype=np.float32)
     _check(lib.cs_get_lars_rates(out.ctypes.data), "cs_get_lars_rates")
     return out
+
+
+TOPO_CROSSOVER, TOPO_EXPONENTIAL = 0, 1
+
+
+def cs_set_topology_kind(kind: int) -> None:
+    """TOPO_CROSSOVER (Alg. 2, default) or TOPO_EXPONENTIAL (SGP's graph)."""
+    _check(lib.cs_set_topology_kind(kind), "cs_set_topology_kind")
 
 
 def cs_set_step(step: int) -> None:

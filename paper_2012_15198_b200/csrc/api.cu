@@ -98,6 +98,11 @@ struct Ctx {
   float lars_eta = 0.f, lars_wd = 0.f, lars_eps = 0.f;
   bool lars_valid = false;
 
+  // topology kind (cs_set_topology_kind): SGP's exponential graph as [H][k][world] tables
+  int topo_kind = CS_TOPO_CROSSOVER;
+  int32_t* d_exp = nullptr;
+  int exp_h = 0;
+
   // hot-kernel timing (cs_set_timing): event pairs recorded around each launch
   bool timing = false;
   std::vector<cudaEvent_t> events;
@@ -131,7 +136,8 @@ void free_device() {
   auto f = [](void* p) { if (p) cudaFree(p); };
   f(g.d_bounds); f(g.d_src); f(g.d_dst); f(g.d_ord); f(g.d_given); f(g.d_rw);
   f(g.d_inv_wsum); f(g.d_err); f(g.d_partials); f(g.d_diag); f(g.d_stage); f(g.d_counter); f(g.d_tiles);
-  f(g.d_tile_first); f(g.d_lrs); f(g.d_lars_part);
+  f(g.d_tile_first); f(g.d_lrs); f(g.d_lars_part); f(g.d_exp);
+  g.d_exp = nullptr;
   g.d_tile_first = nullptr; g.d_lrs = nullptr; g.d_lars_part = nullptr;
   g.layer_bounds.clear(); g.plan.clear(); g.n_layers = 0; g.lars_valid = false;
   g.d_bounds = nullptr; g.d_src = nullptr; g.d_dst = nullptr; g.d_ord = nullptr;
@@ -154,6 +160,42 @@ std::vector<int64_t> host_bounds(int64_t d, int k) {
 }
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// SGP's directed exponential graph: worker i sends to
+// (i + 2^(t mod log2 n)) mod n, so it receives from (i - 2^(t mod log2 n)) mod n, in
+// every segment.  n is a power of two.
+int log2_exact(int n) {
+  int h = 0;
+  while ((1 << h) < n) ++h;
+  return h;
+}
+
+void exponential_rows(int64_t step, int n, int k, int32_t* src) {
+  const int off = 1 << (int)(step % log2_exact(n));
+  for (int s = 0; s < k; ++s)
+    for (int i = 0; i < n; ++i) src[(int64_t)s * n + i] = (i - off + n) % n;
+}
+
+// The flat step's injected topology: the test override, else the exponential table
+// row of this step, else nullptr (Alg. 2 drawn on the device).
+const int32_t* flat_given() {
+  if (g.has_override) return g.d_given;
+  if (g.topo_kind == CS_TOPO_EXPONENTIAL && g.d_exp)
+    return g.d_exp + (g.step % g.exp_h) * (int64_t)g.k * g.world;
+  return nullptr;
+}
+
+int upload_exponential() {
+  if (g.d_exp) cudaFree(g.d_exp);
+  g.d_exp = nullptr;
+  g.exp_h = log2_exact(g.world);
+  const size_t kn = (size_t)g.k * g.world;
+  std::vector<int32_t> tab(kn * g.exp_h);
+  for (int h = 0; h < g.exp_h; ++h) exponential_rows(h, g.world, g.k, tab.data() + h * kn);
+  CS_CUDA(cudaMalloc(&g.d_exp, sizeof(int32_t) * tab.size()));
+  CS_CUDA(cudaMemcpy(g.d_exp, tab.data(), sizeof(int32_t) * tab.size(), cudaMemcpyHostToDevice));
+  return CS_OK;
+}
 
 // Bulk-TMA tiles: every (segment, layer) intersection in column order, cut into pieces
 // of at most T columns, so each tile lies in one segment and one layer and the tiles of
@@ -333,7 +375,7 @@ int enqueue_flat_step(float* params, const float* grads, float* psw, float lr, f
   if (g.lars && !(fused && g.use_tma))
     return fail(CS_EUNSUPPORTED, "LARS runs on the bulk-TMA path (world <= 64, k*world <= 2048)");
   if (fused && g.use_tma) {
-    a.given = g.has_override ? g.d_given : nullptr;
+    a.given = flat_given();
     cudaEvent_t ev[2];
     int rc = next_event_pair(ev);
     if (rc) return rc;
@@ -355,10 +397,10 @@ int enqueue_flat_step(float* params, const float* grads, float* psw, float lr, f
     return CS_OK;
   }
   if (fused) {
-    a.given = g.has_override ? g.d_given : nullptr;
+    a.given = flat_given();
   } else {
     TopoArgs t = topo_args(n, CS_TAG_FLAT, psw, 1);
-    if (g.has_override) t.given = g.d_given;
+    t.given = flat_given();
     CS_CUDA(launch_topology(t, g.stream));
   }
   cudaEvent_t ev[2];
@@ -423,6 +465,10 @@ static int topology_common(int64_t step, int n, int tag, int32_t* src_out) {
   if (!src_out) return fail(CS_EINVAL, "NULL src_out");
   if (step < 0 || step >= (int64_t(1) << 32))
     return fail(CS_EINVAL, "step %lld outside [0, 2^32)", (long long)step);
+  if (tag == CS_TAG_FLAT && g.topo_kind == CS_TOPO_EXPONENTIAL) {
+    exponential_rows(step, n, g.k, src_out);
+    return CS_OK;
+  }
   for (int s = 0; s < g.k; ++s) {
     if (host_alg2(g.seed, (uint32_t)step, (uint32_t)s, n, tag, src_out + (int64_t)s * n) < 0)
       return fail(CS_ETOPOLOGY, "Alg.2 restart limit (10,000) exceeded");
@@ -506,8 +552,23 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
       if (rc) return fail(rc, "%s", peer_error());
     }
   }
+  if (g.topo_kind == CS_TOPO_EXPONENTIAL) {
+    int rc = upload_exponential();
+    if (rc) return rc;
+  }
   g.bound = true;
   g.diag_valid = false;
+  return CS_OK;
+}
+
+int cs_set_topology_kind(int kind) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (kind != CS_TOPO_CROSSOVER && kind != CS_TOPO_EXPONENTIAL)
+    return fail(CS_EINVAL, "unknown topology kind %d", kind);
+  if (kind == CS_TOPO_EXPONENTIAL && (g.world & (g.world - 1)) != 0)
+    return fail(CS_EUNSUPPORTED, "the exponential graph needs a power-of-two world (have %d)", g.world);
+  g.topo_kind = kind;
+  if (g.bound && kind == CS_TOPO_EXPONENTIAL) return upload_exponential();
   return CS_OK;
 }
 
@@ -555,7 +616,7 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
     if (!g.peer.imported) return fail(CS_ENOTBOUND, "multi-GPU: cs_ipc_import has not been called");
     if (g.lars) return fail(CS_EUNSUPPORTED, "LARS runs on the single-GPU bulk-TMA path");
     PeerStepArgs pa = peer_args(params, grads, psw, lr, momentum);
-    pa.given = g.has_override ? g.d_given : nullptr;
+    pa.given = flat_given();
     cudaEvent_t ev[2];
     rc = next_event_pair(ev);
     if (rc) return rc;

@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--compare-all", action="store_true", help="compare every column (small d)")
     ap.add_argument("--hier-groups", type=int, default=0, help="hierarchical step with this many groups")
     ap.add_argument("--diag", action="store_true", help="check the multi-GPU diagnostics too")
+    ap.add_argument("--exponential", action="store_true", help="SGP's exponential graph (cs_set_topology_kind)")
     a = ap.parse_args()
     rank, ws, lr_ = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(lr_)
@@ -47,6 +48,9 @@ def main():
     lr, mu = float(synth.DEFAULT_LR), float(synth.DEFAULT_MOMENTUM)
     groups = a.hier_groups or world
     cs.cs_init(world, groups, k, seed)
+    if a.exponential:
+        cs.cs_set_topology_kind(cs.TOPO_EXPONENTIAL)
+        from oracle.sgp import exponential_topology
     stream = torch.cuda.current_stream(dev)
     ld = (d + 3) // 4 * 4
     x = torch.zeros(n_loc, ld, device=dev)
@@ -73,7 +77,7 @@ def main():
     for t in range(a.num_steps):
         o = (t + first) % B
         step_fn(x, bank[o:o + n_loc], w, lr, mu)
-        orc.step(lr, mu)
+        orc.step(lr, mu, src=exponential_topology(t, world, k) if a.exponential else None)
         cs.cs_sync()
         if a.diag:
             cd, msum = cs.cs_get_diag()

@@ -59,6 +59,14 @@ def test_two_gpu_diagnostics(n_loc, groups):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("n_loc,k", [(1, 1), (4, 1), (2, 3)])
+def test_two_gpu_exponential_bitwise(n_loc, k):
+    # SGP's directed exponential graph across GPUs (push/mix for 1 worker/GPU, hybrid otherwise)
+    _run(2, "--workers-per-gpu", n_loc, "--vector-len", 100_003, "--segments", k, "--num-steps", 5,
+         "--compare-all", "--exponential")
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("pieces", [3, 8])
 def test_two_gpu_pieces_bitwise(pieces):
     # push(p+1) / mix(p) overlap across the caller's and the aux stream, across GPUs

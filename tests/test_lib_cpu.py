@@ -131,3 +131,20 @@ def test_host_segment_plan_matches_oracle():
     for bad_k in (0, 162):
         with pytest.raises(cs.CSError):
             cs.cs_segment_plan(sizes, bad_k)
+
+
+def test_host_exponential_topology_matches_oracle():
+    from oracle.sgp import exponential_topology
+    for n, k in [(2, 1), (8, 3), (64, 1), (1024, 2)]:
+        cs.cs_init(n, n, k, 5)
+        cs.cs_set_topology_kind(cs.TOPO_EXPONENTIAL)
+        for t in [0, 1, 2, 9, 2**32 - 1]:
+            assert np.array_equal(cs.cs_topology(t, n, k), exponential_topology(t, n, k))
+        cs.cs_set_topology_kind(cs.TOPO_CROSSOVER)
+        assert np.array_equal(cs.cs_topology(3, n, k), T.topology(5, 3, n, k))
+    cs.cs_init(12, 12, 1, 0)
+    with pytest.raises(cs.CSError) as e:
+        cs.cs_set_topology_kind(cs.TOPO_EXPONENTIAL)
+    assert e.value.code == -12
+    with pytest.raises(cs.CSError):
+        cs.cs_set_topology_kind(7)
