@@ -9,6 +9,8 @@ for N in 1 2 4 8; do
   for scheme in crossover sgp allreduce; do
     for c in c3 c2; do
       [ "$N" = 1 ] && [ "$c" = c3 ] && continue
+      # the multi-GPU hierarchical step (AllReduce-SGD = 1 group) takes one worker per GPU
+      [ "$N" != 1 ] && [ "$c" = c2 ] && [ "$scheme" = allreduce ] && continue
       log=gpurun_out/scheme_n${N}_${c}_${scheme}.log
       if [ "$N" = 1 ]; then
         CUDA_VISIBLE_DEVICES=$DEVS timeout 300 python bench.py --steps 50 --warmup 5 --config $c \
