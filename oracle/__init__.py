@@ -19,6 +19,7 @@ Plain, slow, obviously-correct NumPy/pure-Python restatements of the paper:
   interval.py      communication-interval accumulator (Table 1).
   lars.py          LARS per-layer rates + layer-aligned segment plan (Table 1; §8(f) #2).
   sgp.py           SGP directed exponential graph, the comparison baseline (§8(f) #3).
+  wire.py          bf16 wire format for received segments (§8(f) #4; reading C-20).
 
 Every function is pinned by `-m "not gpu"` tests against values fixed by the
 paper or mathematics (tests/test_oracle_*.py).  Parity unpinned:

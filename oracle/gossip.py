@@ -40,22 +40,26 @@ def local_update(x: np.ndarray, m: np.ndarray, g: np.ndarray, lr, mu):
     return m_new, y
 
 
-def mix(y: np.ndarray, w: np.ndarray, src: np.ndarray, seg_of_col: np.ndarray):
+def mix(y: np.ndarray, w: np.ndarray, src: np.ndarray, seg_of_col: np.ndarray, wire=None):
     """a4+a5 over a snapshot: x'[i, j] = (y[i, j] + y[src[seg(j), i], j]) * 0.5;
-    w'[i, s] = (w[i, s] + w[src[s, i], s]) * 0.5."""
+    w'[i, s] = (w[i, s] + w[src[s, i], s]) * 0.5.
+    wire="bf16": the received y is rounded to bf16 first (oracle/wire.py, reading C-20)."""
     k = src.shape[0]
     x_new = np.empty_like(y)
     w_new = np.empty_like(w)
     for s in range(k):
         cols = np.nonzero(seg_of_col == s)[0]
         received = y[src[s]][:, cols]              # row i holds y_{src_s(i)}
+        if wire == "bf16":
+            from .wire import bf16_round
+            received = bf16_round(received)
         x_new[:, cols] = ((y[:, cols] + received).astype(F32) * HALF).astype(F32)
         w_new[:, s] = ((w[:, s] + w[src[s], s]).astype(F32) * HALF).astype(F32)
     return x_new, w_new
 
 
-def gossip_step(x, m, g, w, src, seg_of_col, lr, mu):
+def gossip_step(x, m, g, w, src, seg_of_col, lr, mu, wire=None):
     """One flat step (a3 -> a4 -> a5).  Returns (x', m', w')."""
     m_new, y = local_update(x, m, g, lr, mu)
-    x_new, w_new = mix(y, w, src, seg_of_col)
+    x_new, w_new = mix(y, w, src, seg_of_col, wire)
     return x_new, m_new, w_new
