@@ -243,6 +243,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-interval", action="store_true", help="skip the communication-interval sub-measurement")
+    ap.add_argument("--wire", default="fp32", choices=["fp32", "bf16"],
+                    help="SURVEY 8(f) #4: bf16 wire format for received segments (reading C-20)")
     ap.add_argument("--scheme", default="crossover", choices=["crossover", "sgp", "allreduce"],
                     help="SURVEY 8(f) #3 baselines on the same machinery: sgp = SGP's directed exponential "
                          "graph, model-wise (k=1 unless --k); allreduce = AllReduce-SGD (hierarchical, 1 group)")
@@ -296,6 +298,8 @@ def main():
     cs.cs_init(world, groups, k, seed)
     if args.scheme == "sgp":
         cs.cs_set_topology_kind(cs.TOPO_EXPONENTIAL)
+    if args.wire == "bf16":
+        cs.cs_set_wire(cs.WIRE_BF16)
     step_fn = cs.cs_hier_step if hier else cs.cs_gossip_step
     cs.cs_set_path({"auto": 0, "reg": 1, "tma": 2, "peer": 3}[args.path])
     stream = torch.cuda.Stream(dev)
@@ -505,6 +509,7 @@ def main():
               "config": {"workload": f"{args.config}: {desc}", "world": world, "workers_per_gpu": n_loc,
                          "d": d, "k": k, "seed": seed, "lr": lr, "momentum": mu,
                          "parallelism": f"workers partitioned over {world_size} GPU(s)", "scheme": args.scheme,
+                         "wire": args.wire,
                          "l2": f"inputs larger than L2 ({20.0 * n_loc * d / 1e9:.2f} GB moved per step per GPU)"},
               "step_us": ms_step * 1e3,
               "traffic_GBps": 20.0 * world * d / (ms_step * 1e-3) / 1e9,

@@ -60,6 +60,10 @@ extern "C" {
 #define CS_TOPO_CROSSOVER   0   /* Alg. 2 load-balanced random topology per segment (default) */
 #define CS_TOPO_EXPONENTIAL 1   /* SGP's directed exponential graph, the baseline */
 
+/* Wire formats of exchanged segments (cs_set_wire). */
+#define CS_WIRE_FP32 0   /* received segments in fp32 (default; the fp32 step of the paper)   */
+#define CS_WIRE_BF16 1   /* received segments rounded to bf16; master state stays fp32 (C-20) */
+
 /* ---- context -------------------------------------------------------------- */
 
 /* Create the process-wide context.
@@ -268,6 +272,18 @@ int cs_get_lars_rates(float* rates_out);
  * Errors: CS_ENOTINIT, CS_EINVAL (unknown kind), CS_EUNSUPPORTED (exponential with a
  * world that is not a power of two), CS_ECUDA. */
 int cs_set_topology_kind(int kind);
+
+/* Wire format of the exchanged segments (mixed
+ * precision).  CS_WIRE_BF16: every segment a worker receives is the sender's y rounded
+ * to the nearest bf16 (ties to even) and widened back exactly; the worker's own y, the
+ * momentum, params and push-sum weights stay fp32 (reading C-20):
+ *   x'_i = fl(fl(y_i + bf16(y_src(i))) * 0.5)
+ * It applies to every received segment, on the same GPU or not, so results do not
+ * depend on the placement of workers; across GPUs the inbox holds bf16, halving the
+ * NVLink bytes (cs_step_bytes counts 2 B per remote element).  Flat step only (the
+ * hierarchical step refuses it).  Takes effect at the next step.
+ * Errors: CS_ENOTINIT, CS_EINVAL (unknown format). */
+int cs_set_wire(int format);
 
 /* Set / read the step counter t (resume = restore buffers + cs_set_step). */
 int cs_set_step(int64_t step);

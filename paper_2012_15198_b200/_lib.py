@@ -55,6 +55,7 @@ _SIGS = {
     "cs_hier_step": (_c_int, [_vp, _vp, _vp, _c_f, _c_f]),
     "cs_accumulate": (_c_int, [_vp, _vp, _c_int, _c_int]),
     "cs_set_topology_kind": (_c_int, [_c_int]),
+    "cs_set_wire": (_c_int, [_c_int]),
     "cs_segment_plan": (_c_int, [_vp, _c_int, _c_int, _vp]),
     "cs_set_layers": (_c_int, [_vp, _c_int, _vp]),
     "cs_set_lars": (_c_int, [_c_f, _c_f, _c_f]),
@@ -232,6 +233,12 @@ def cs_get_lars_rates(n_loc: int, n_layers: int) -> np.ndarray:
 
 
 TOPO_CROSSOVER, TOPO_EXPONENTIAL = 0, 1
+WIRE_FP32, WIRE_BF16 = 0, 1
+
+
+def cs_set_wire(fmt: int) -> None:
+    """WIRE_FP32 (default) or WIRE_BF16: received segments rounded to bf16 (reading C-20)."""
+    _check(lib.cs_set_wire(fmt), "cs_set_wire")
 
 
 def cs_set_topology_kind(kind: int) -> None:

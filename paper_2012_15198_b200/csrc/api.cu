@@ -100,6 +100,7 @@ struct Ctx {
 
   // topology kind (cs_set_topology_kind): SGP's exponential graph as [H][k][world] tables
   int topo_kind = CS_TOPO_CROSSOVER;
+  int wire = CS_WIRE_FP32;   // cs_set_wire
   int32_t* d_exp = nullptr;
   int exp_h = 0;
 
@@ -317,6 +318,7 @@ LocalArgs local_args(float* params, const float* grads, float* psw, int n, int g
   a.lrs = nullptr;
   a.n_layers = 0;
   a.wd = 0.f;
+  a.wire = g.wire == CS_WIRE_BF16 ? 1 : 0;
   return a;
 }
 
@@ -346,6 +348,7 @@ PeerStepArgs peer_args(float* params, const float* grads, float* psw, float lr, 
   pa.groups = g.groups;
   pa.gs = 0;
   pa.inv_gs = 1.0f / (float)(g.world / g.groups);
+  pa.wire = g.wire == CS_WIRE_BF16 ? 1 : 0;
   return pa;
 }
 
@@ -561,6 +564,13 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
   return CS_OK;
 }
 
+int cs_set_wire(int format) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (format != CS_WIRE_FP32 && format != CS_WIRE_BF16) return fail(CS_EINVAL, "unknown wire format %d", format);
+  g.wire = format;
+  return CS_OK;
+}
+
 int cs_set_topology_kind(int kind) {
   if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
   if (kind != CS_TOPO_CROSSOVER && kind != CS_TOPO_EXPONENTIAL)
@@ -666,6 +676,8 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
   if (rc) return rc;
   if (g.lars || g.n_layers > 0)
     return fail(CS_EUNSUPPORTED, "LARS / layer tables are not implemented for the hierarchical step");
+  if (g.wire != CS_WIRE_FP32)
+    return fail(CS_EUNSUPPORTED, "the bf16 wire format is implemented for the flat step only");
   rc = check_step_args(params, grads, psw);
   if (rc) return rc;
   const bool diag = g.diag != 0;
@@ -943,7 +955,8 @@ int cs_step_bytes(int64_t step, int hier, double* out) {
     double nvl = 0.0;
     for (int s = 0; s < g.k; ++s)
       for (int i = g.first; i < g.first + g.n_loc; ++i)
-        if (src[(size_t)s * g.world + i] / g.n_loc != g.rank) nvl += 4.0 * (double)(b[s + 1] - b[s]);
+        if (src[(size_t)s * g.world + i] / g.n_loc != g.rank)
+          nvl += (g.wire == CS_WIRE_BF16 ? 2.0 : 4.0) * (double)(b[s + 1] - b[s]);
     out[1] = nvl;
   } else if (g.nprocs == 1) {
     const int gs = g.world / g.groups;

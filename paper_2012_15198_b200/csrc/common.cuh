@@ -1,5 +1,6 @@
 // Internal declarations shared by the library's translation units.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -72,7 +73,24 @@ struct LocalArgs {
   const float* lrs;    // [rows][n_layers]
   int n_layers;
   float wd;
+  int wire;            // CS_WIRE_BF16: the received y is rounded to bf16 (reading C-20)
 };
+
+// bf16 wire format (reading C-20): round to the nearest bf16 (ties to even), widen back.
+__device__ __forceinline__ float bf16r(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+__device__ __forceinline__ float4 bf16r4(float4 v) {
+  return make_float4(bf16r(v.x), bf16r(v.y), bf16r(v.z), bf16r(v.w));
+}
+// 4 values packed as 4 bf16 (8 bytes) and back
+__device__ __forceinline__ uint2 pack_bf16x4(float4 v) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+  return make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+}
+__device__ __forceinline__ float4 unpack_bf16x4(uint2 u) {
+  // a bf16 is the top half of the fp32 with the same value: widening is exact
+  return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u),
+                     __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xFFFF0000u));
+}
 
 // A column tile [c0, c0 + len) inside segment seg and layer `layer` (len <= kTmaTileMax,
 // c0 % 4 == 0; c0 % 32 == 0 under the equal split without a layer table).

@@ -354,12 +354,12 @@ __global__ void __launch_bounds__(kThreads) k_gossip_local(const LocalArgs a) {
           if (e & kOrdStart) {
             yfirst = y;
           } else {
-            const float4 xo = pair_mean(yprev, y);
+            const float4 xo = pair_mean(yprev, a.wire ? bf16r4(y) : y);
             st_stream(a.x + prev_off, xo, valid);
             if (DIAG) { cd.add(xo, rw[prev_row], first_diag, 1.0); first_diag = false; }
           }
           if (e & kOrdEnd) {
-            const float4 xo = pair_mean(y, yfirst);
+            const float4 xo = pair_mean(y, a.wire ? bf16r4(yfirst) : yfirst);
             st_stream(a.x + off, xo, valid);
             if (DIAG) { cd.add(xo, rw[row], first_diag, 1.0); first_diag = false; }
           }
@@ -605,12 +605,12 @@ __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
             if (e & kOrdStart) {
               yfirst[c] = y;
             } else {
-              const float4 xo = pair_mean(yprev[c], y);
+              const float4 xo = pair_mean(yprev[c], a.wire ? bf16r4(y) : y);
               st_stream(a.x + (int64_t)prev_row * ld + j, xo, vv);
               if (DIAG) cd[c].add(xo, rw[prev_row], first_diag, 1.0);
             }
             if (e & kOrdEnd) {
-              const float4 xo = pair_mean(y, yfirst[c]);
+              const float4 xo = pair_mean(y, a.wire ? bf16r4(yfirst[c]) : yfirst[c]);
               st_stream(a.x + (int64_t)row * ld + j, xo, vv);
               if (DIAG) cd[c].add(xo, rw[row], first_diag && (e & kOrdStart), 1.0);
             }

@@ -367,7 +367,8 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
             st4_cs(s.x + rowoff + j, y, vv);
           } else {
             st4(s.x + rowoff + j, y, vv);
-            yt[v] = y;
+            if (s.wire) reinterpret_cast<uint2*>(yt)[v] = pack_bf16x4(y);  // bf16 wire (C-20)
+            else yt[v] = y;
           }
         }
       }
@@ -416,8 +417,15 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
         ptx::mbar_wait(&y_full[sy], (uint32_t)((i / kSlotsY) & 1));
         int rp, rl;
         receiver_of(a, M, U.seg, U.r, rp, rl);
-        float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
-        ptx::bulk_s2g(inbox + U.c0, ringY + (size_t)sy * kPeerTile, (uint32_t)(((U.len + 3) & ~3) * 4));
+        if (s.wire) {  // half the bytes: a bf16 row, rounded up to whole 16-byte units
+          const int64_t ldw = (s.ld + 7) & ~7;
+          uint16_t* inbox = reinterpret_cast<uint16_t*>(a.peers[rp] + a.off_inbox) +
+                            ((int64_t)par * s.n_loc + rl) * ldw;
+          ptx::bulk_s2g(inbox + U.c0, ringY + (size_t)sy * kPeerTile, (uint32_t)(((U.len + 7) & ~7) * 2));
+        } else {
+          float* inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * s.n_loc + rl) * s.ld;
+          ptx::bulk_s2g(inbox + U.c0, ringY + (size_t)sy * kPeerTile, (uint32_t)(((U.len + 3) & ~3) * 4));
+        }
         ptx::bulk_commit();
         ptx::bulk_wait_read<1>();  // groups of units < i have read their tiles
         if (i >= 1) ptx::mbar_arrive(&y_empty[(i - 1) % kSlotsY]);
@@ -456,6 +464,8 @@ __global__ void __launch_bounds__(kMixThreads) k_peer_mix(const PeerKernelArgs a
     const int64_t nv = (a.col_hi - a.col_lo + 3) >> 2;
     const int64_t total = nv * s.n_loc;
     const float* inbox0 = reinterpret_cast<const float*>(mine + a.off_inbox) + (int64_t)par * s.n_loc * s.ld;
+    const int64_t ldw = (s.ld + 7) & ~7;
+    const uint16_t* inbox0w = reinterpret_cast<const uint16_t*>(mine + a.off_inbox) + (int64_t)par * s.n_loc * ldw;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     constexpr int U = 4;  // float4 pairs in flight per thread
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < total; base += U * stride) {
@@ -472,7 +482,11 @@ __global__ void __launch_bounds__(kMixThreads) k_peer_mix(const PeerKernelArgs a
           valid[h] = (int)imin64(4, a.col_hi - j);
           off[h] = r * s.ld + j;
           yo[h] = __ldcs(reinterpret_cast<const float4*>(s.x + off[h]));
-          yi[h] = __ldcs(reinterpret_cast<const float4*>(inbox0 + off[h]));
+          if (s.wire)
+            yi[h] = unpack_bf16x4(__ldcs(reinterpret_cast<const uint2*>(
+                reinterpret_cast<const uint16_t*>(inbox0w) + r * ldw + j)));
+          else
+            yi[h] = __ldcs(reinterpret_cast<const float4*>(inbox0 + off[h]));
         }
       }
 #pragma unroll
@@ -674,6 +688,7 @@ struct HybArgs {
   uint32_t epoch, pdone_target, done_target;
   uint8_t* tail_tbl;        // [k][n_loc]: 1 = the worker's segment source is remote
   int* err;
+  int wire;                 // bf16 wire format (reading C-20)
 };
 
 __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
@@ -823,10 +838,13 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
         const uint32_t e = o[p];
         const uint32_t row = e & kHIdx;
         float* inbox = nullptr;
+        uint16_t* inboxw = nullptr;
         if (e & kHHead) {
           const int dg = head_dst[td.seg * n_loc + row];
           const int rp = dg / n_loc, rl = dg - rp * n_loc;
           inbox = reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * n_loc + rl) * ld;
+          inboxw = reinterpret_cast<uint16_t*>(a.peers[rp] + a.off_inbox) +
+                   ((int64_t)par * n_loc + rl) * ((ld + 7) & ~7);
         }
 #pragma unroll
         for (int c = 0; c < kHVPT; ++c) {
@@ -844,13 +862,16 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
             st4_cs(a.m + (int64_t)row * ld + j, mn, vv);
             if (e & kHStart) {
               yfirst[c] = y;
-              if (e & kHHead) st4(inbox + j, y, vv);  // NVLink push of the chain head
+              if (e & kHHead) {  // NVLink push of the chain head
+                if (a.wire) *reinterpret_cast<uint2*>(inboxw + j) = pack_bf16x4(y);
+                else st4(inbox + j, y, vv);
+              }
             } else {
-              st4_cs(a.x + (int64_t)prev_row * ld + j, mean4(yprev[c], y), vv);
+              st4_cs(a.x + (int64_t)prev_row * ld + j, mean4(yprev[c], a.wire ? bf16r4(y) : y), vv);
             }
             if (e & kHEnd) {
               if (e & kHTail) st4(a.x + (int64_t)row * ld + j, y, vv);  // finished by k_hyb_tail
-              else st4_cs(a.x + (int64_t)row * ld + j, mean4(y, yfirst[c]), vv);
+              else st4_cs(a.x + (int64_t)row * ld + j, mean4(y, a.wire ? bf16r4(yfirst[c]) : yfirst[c]), vv);
             }
             yprev[c] = y;
           }
@@ -921,7 +942,10 @@ __global__ void __launch_bounds__(256) k_hyb_tail(const HybArgs a) {
   if (!s_timeout) {
     const int64_t nv = (a.d + 3) >> 2;
     const int64_t total = nv * n_loc;
-    const float* inbox0 = reinterpret_cast<const float*>(mine + a.off_inbox) + (int64_t)par * n_loc * a.ld;
+    const float* inbox0 = a.wire
+        ? reinterpret_cast<const float*>(reinterpret_cast<const uint16_t*>(mine + a.off_inbox) +
+                                         (int64_t)par * n_loc * ((a.ld + 7) & ~7))
+        : reinterpret_cast<const float*>(mine + a.off_inbox) + (int64_t)par * n_loc * a.ld;
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
       const int64_t r = idx / nv, v = idx - r * nv;
@@ -930,7 +954,9 @@ __global__ void __launch_bounds__(256) k_hyb_tail(const HybArgs a) {
       if (!tail[sg * n_loc + r]) continue;
       const int64_t off = r * a.ld + j;
       const float4 y = __ldcs(reinterpret_cast<const float4*>(a.x + off));
-      const float4 yi = __ldcs(reinterpret_cast<const float4*>(inbox0 + off));
+      const float4 yi = a.wire ? unpack_bf16x4(__ldcs(reinterpret_cast<const uint2*>(
+                                     reinterpret_cast<const uint16_t*>(inbox0) + r * ((a.ld + 7) & ~7) + j)))
+                               : __ldcs(reinterpret_cast<const float4*>(inbox0 + off));
       st4_cs(a.x + off, mean4(y, yi), (int)imin64(4, a.d - j));
     }
     if (blockIdx.x == 0)
@@ -1488,6 +1514,7 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     h.seed = a.seed;
     h.step = a.step;
     h.given = a.given;
+    h.wire = a.wire;
     h.src_tbl = a.src;
     h.fused = fused ? 1 : 0;
     h.lr = a.lr;

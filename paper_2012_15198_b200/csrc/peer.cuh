@@ -27,6 +27,8 @@ struct PeerStepArgs {
   int groups;     // G; the topology is over the G groups
   int gs;         // GPUs (= workers) per group; 0 for the flat step
   float inv_gs;   // fp32(1/|G|)
+  // bf16 wire format (reading C-20): inbox rows hold bf16 with stride (ld + 7) & ~7
+  int wire;
 };
 
 struct PeerState {

@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--hier-groups", type=int, default=0, help="hierarchical step with this many groups")
     ap.add_argument("--diag", action="store_true", help="check the multi-GPU diagnostics too")
     ap.add_argument("--exponential", action="store_true", help="SGP's exponential graph (cs_set_topology_kind)")
+    ap.add_argument("--wire-bf16", action="store_true", help="bf16 wire format (cs_set_wire)")
     a = ap.parse_args()
     rank, ws, lr_ = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(lr_)
@@ -48,6 +49,8 @@ def main():
     lr, mu = float(synth.DEFAULT_LR), float(synth.DEFAULT_MOMENTUM)
     groups = a.hier_groups or world
     cs.cs_init(world, groups, k, seed)
+    if a.wire_bf16:
+        cs.cs_set_wire(cs.WIRE_BF16)
     if a.exponential:
         cs.cs_set_topology_kind(cs.TOPO_EXPONENTIAL)
         from oracle.sgp import exponential_topology
@@ -77,7 +80,8 @@ def main():
     for t in range(a.num_steps):
         o = (t + first) % B
         step_fn(x, bank[o:o + n_loc], w, lr, mu)
-        orc.step(lr, mu, src=exponential_topology(t, world, k) if a.exponential else None)
+        orc.step(lr, mu, src=exponential_topology(t, world, k) if a.exponential else None,
+                 wire="bf16" if a.wire_bf16 else None)
         cs.cs_sync()
         if a.diag:
             cd, msum = cs.cs_get_diag()

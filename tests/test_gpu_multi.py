@@ -67,6 +67,16 @@ def test_two_gpu_exponential_bitwise(n_loc, k):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("n_loc,d,k", [(1, 100_003, 3), (3, 50_001, 5), (1, 25_557_032, 8)])
+def test_two_gpu_bf16_wire_bitwise(n_loc, d, k):
+    # bf16 inbox rows over NVLink (push/mix for 1 worker/GPU, hybrid heads otherwise)
+    args = ["--workers-per-gpu", n_loc, "--vector-len", d, "--segments", k, "--num-steps", 5, "--wire-bf16"]
+    if d < 1_000_000:
+        args.append("--compare-all")
+    _run(2, *args)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("pieces", [3, 8])
 def test_two_gpu_pieces_bitwise(pieces):
     # push(p+1) / mix(p) overlap across the caller's and the aux stream, across GPUs
