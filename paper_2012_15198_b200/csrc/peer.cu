@@ -33,11 +33,12 @@
 // Hierarchical step (§3.3), one worker per GPU, groups of gs
 // consecutive GPUs:
 //   k_hier_scatter  each member sends chunk c of its gradient to member c's gbox
-//                   (reduce-scatter, NVLink);
-//   k_hier_reduce   member c sums the chunk over the members in ascending order
-//                   and scales by fp32(1/|G|) (reading C-12 — the oracle's exact
-//                   order, so the result is bit-identical), then all-gathers the
-//                   mean chunk into every member's gbar;
+//                   (reduce-scatter, NVLink, destinations rotated);
+//   k_hier_reduce   member c sums the chunk over the members in ascending order and
+//                   scales by fp32(1/|G|) (reading C-12 — the oracle's exact order,
+//                   so the result is bit-identical), then all-gathers the mean chunk
+//                   into every member's gbar; with one group the vector is cut into
+//                   pieces and the update of piece q overlaps h1 of piece q+1;
 //   k_peer_push/mix with g = gbar over the leader topology (tag HIER): every
 //                   member exchanges with the member of the same index in the
 //                   source group.  All members hold the leader's state bit for bit
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
     }
     // ... and make sure every GPU finished its mix of epoch e-2 (the last reader of the
     // inbox parity this step writes) before anything is pushed
-    if (threadIdx.x < s.nprocs && e >= 3) {
+    if (threadIdx.x < s.nprocs && e >= 3 && !a.final_only) {  // final_only writes no inbox
       const uint32_t* done = reinterpret_cast<const uint32_t*>(mine + a.off_done);
       if (!wait_acquire(done + threadIdx.x, e - 2)) atomicOr(&s_timeout, 1);
     }
@@ -517,7 +518,9 @@ __global__ void __launch_bounds__(kMixThreads) k_peer_mix(const PeerKernelArgs a
 struct HierArgs {
   const float* g;            // this GPU's worker gradient [d]
   char* const* peers;
-  int64_t d, chunk;          // chunk: columns per member (multiple of 4)
+  int64_t d, chunk;          // chunk: columns per member in this piece (multiple of 4)
+  int64_t col_lo, col_hi;    // this piece's columns
+  int64_t gstride;           // gbox slot stride (elements)
   int rank, gs;
   float inv_gs;
   uint32_t epoch;
@@ -526,19 +529,33 @@ struct HierArgs {
   int* err;
 };
 
+// h1 over the columns [col_lo, col_hi) of one piece, split into gs member chunks of
+// `chunk` columns (multiple of 4).  gbox slots are full rows (stride gstride), indexed by
+// absolute column, so pieces need no layout of their own.
+//   k_hier_scatter  member m sends chunk c of its gradient to member c's gbox slot m
+//                   (reduce-scatter over NVLink).  Destinations rotate every 32 float4
+//                   (512 contiguous bytes per warp), starting at this member's offset:
+//                   the group's GPUs spread their stores over every peer at once instead
+//                   of all writing member 0's chunk first (incast on one GPU's links).
+//                   The own chunk stays in g.
+//   k_hier_reduce   member c: gbar = fl(sum over members, ascending) * fp32(1/|G|) of its
+//                   chunk (reading C-12), all-gathered into every member's gbar.
 __global__ void __launch_bounds__(kHierThreads) k_hier_scatter(const HierArgs h) {
   const int grp = h.rank / h.gs, member = h.rank - grp * h.gs, gbase = grp * h.gs;
   const int64_t cv = h.chunk / 4;
-  const int64_t total = cv * h.gs;
+  const int64_t nblk = (cv + 31) / 32;
+  const int64_t total = nblk * 32 * h.gs;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(idx / cv);
-    const int64_t v = idx - c * cv;
-    const int64_t j = c * h.chunk + 4 * v;
-    const int valid = (int)imin64(4, h.d - j);
+    const int64_t b = idx >> 5;
+    const int c = (int)((b + member) % h.gs);
+    const int64_t v = (b / h.gs) * 32 + (idx & 31);
+    if (c == member || v >= cv) continue;
+    const int64_t j = h.col_lo + c * h.chunk + 4 * v;
+    const int valid = (int)imin64(4, imin64(h.col_hi, h.col_lo + (c + 1) * h.chunk) - j);
     if (valid <= 0) continue;
-    float* gbox = reinterpret_cast<float*>(h.peers[gbase + c] + h.off_gbox) + (int64_t)member * h.chunk;
-    st4(gbox + 4 * v, ld4_valid(h.g + j, valid), valid);
+    float* slot = reinterpret_cast<float*>(h.peers[gbase + c] + h.off_gbox) + (int64_t)member * h.gstride;
+    st4(slot + j, ld4_valid(h.g + j, valid), valid);
   }
   __syncthreads();
   if (threadIdx.x == 0)
@@ -551,26 +568,29 @@ __global__ void __launch_bounds__(kHierThreads) k_hier_reduce(const HierArgs h) 
   __shared__ int s_timeout;
   if (threadIdx.x == 0) s_timeout = 0;
   __syncthreads();
-  if (threadIdx.x < h.gs) {  // every member's chunk has arrived
+  if (threadIdx.x < h.gs && threadIdx.x != member) {  // the other members' chunks have arrived
     const uint32_t* d1 = reinterpret_cast<const uint32_t*>(mine + h.off_d1);
     if (!wait_acquire(d1 + gbase + threadIdx.x, h.epoch)) atomicOr(&s_timeout, 1);
   }
   __syncthreads();
   if (!s_timeout) {
     const float* gbox = reinterpret_cast<const float*>(mine + h.off_gbox);
-    const int64_t c0 = member * h.chunk;
-    const int64_t cv = h.chunk / 4;
+    const int64_t c0 = h.col_lo + member * h.chunk;
+    const int64_t c1 = imin64(h.col_hi, c0 + h.chunk);
+    const int64_t cv = (c1 - c0 + 3) / 4;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < cv; v += (int64_t)gridDim.x * blockDim.x) {
       const int64_t j = c0 + 4 * v;
-      const int valid = (int)imin64(4, h.d - j);
-      if (valid <= 0) continue;
+      const int valid = (int)imin64(4, c1 - j);
       // reading C-12: gbar = fl(...fl(g_0 + g_1)... + g_{gs-1}) * fp32(1/|G|), ascending members
-      float4 acc = __ldcg(reinterpret_cast<const float4*>(gbox + 4 * v));
+      float4 acc = member == 0 ? ld4_valid(h.g + j, valid) : __ldcg(reinterpret_cast<const float4*>(gbox + j));
       for (int mm = 1; mm < h.gs; ++mm)
-        acc = add4(acc, __ldcg(reinterpret_cast<const float4*>(gbox + (int64_t)mm * h.chunk + 4 * v)));
+        acc = add4(acc, mm == member ? ld4_valid(h.g + j, valid)
+                                     : __ldcg(reinterpret_cast<const float4*>(gbox + (int64_t)mm * h.gstride + j)));
       const float4 mean = scale4(acc, h.inv_gs);
-      for (int mm = 0; mm < h.gs; ++mm)
+      for (int q = 0; q < h.gs; ++q) {  // rotated start: spread the all-gather over every peer
+        const int mm = (q + member + (int)(v >> 5)) % h.gs;
         st4(reinterpret_cast<float*>(h.peers[gbase + mm] + h.off_gbar) + j, mean, valid);
+      }
     }
   }
   __syncthreads();
@@ -1220,8 +1240,8 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   size_t off = align_up(p.off_wbox + sizeof(float) * 2 * (size_t)n_loc * k, 256);
   if (gs > 0) {
     p.off_gbox = off;
-    p.off_gbar = align_up(p.off_gbox + sizeof(float) * (size_t)gs * p.chunk, 256);
-    off = align_up(p.off_gbar + sizeof(float) * (size_t)(ld > gs * p.chunk ? ld : gs * p.chunk), 256);
+    p.off_gbar = align_up(p.off_gbox + sizeof(float) * (size_t)gs * ld, 256);  // gbox [gs][ld]
+    off = align_up(p.off_gbar + sizeof(float) * (size_t)ld, 256);
     p.off_xsync = off;
     p.off_msync = align_up(p.off_xsync + sizeof(float) * (size_t)ld, 256);
     p.off_wsync = align_up(p.off_msync + sizeof(float) * (size_t)ld, 256);
@@ -1244,20 +1264,23 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   off += PeerState::kMaxPieces * p.flag_stride;
   p.off_pdone = off;
   off += PeerState::kMaxPieces * p.flag_stride;
-  flags(p.off_d1);
-  flags(p.off_d2);
+  p.off_d1 = off;  // [kMaxPieces] x [nprocs] each, like done / pdone
+  off += PeerState::kMaxPieces * p.flag_stride;
+  p.off_d2 = off;
+  off += PeerState::kMaxPieces * p.flag_stride;
   flags(p.off_d3);
   flags(p.off_dd1);
   flags(p.off_dd2);
   p.off_count = off;                           // [kMaxPieces] counters, 64 B apart
   p.off_pcount = off + 64 * PeerState::kMaxPieces;
   off += 2 * 64 * PeerState::kMaxPieces;
-  p.off_c1 = off;
-  p.off_c2 = off + 64;
-  p.off_c3 = off + 128;
-  p.off_dc1 = off + 192;
-  p.off_dc2 = off + 256;
-  p.bytes = align_up(off + 320, 4096);
+  p.off_c1 = off;                              // [kMaxPieces] counters, 64 B apart
+  p.off_c2 = off + 64 * PeerState::kMaxPieces;
+  off += 2 * 64 * PeerState::kMaxPieces;
+  p.off_c3 = off;
+  p.off_dc1 = off + 64;
+  p.off_dc2 = off + 128;
+  p.bytes = align_up(off + 192, 4096);
   cudaError_t e = cudaMalloc(&p.base, p.bytes);
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region cudaMalloc", e);
   e = cudaMemset(p.base, 0, p.bytes);  // inbox padding is read by 16-byte-rounded bulk copies
@@ -1325,6 +1348,16 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
     if (P > PeerState::kMaxPieces) P = PeerState::kMaxPieces;
     if (P > p.n_tiles) P = p.n_tiles;
     p.pieces = P;
+    // hierarchical step with one group: update of piece q overlaps h1 of piece q+1.
+    // Default 1: at 4 GPUs (c3 vector) P = 1, 2, 4, 8 measured 399, 409, 445, 558 us; the
+    // update kernel takes the SMs the NVLink stores of the next piece need
+    int HP = 1;
+    const char* henv = getenv("CS_HIER_PIECES");
+    if (henv) HP = atoi(henv);
+    if (HP < 1) HP = 1;
+    if (HP > PeerState::kMaxPieces) HP = PeerState::kMaxPieces;
+    if (HP > p.n_tiles) HP = p.n_tiles;
+    p.hier_pieces = HP;
     p.piece_tile.resize(P + 1);
     for (int q = 0; q <= P; ++q) p.piece_tile[q] = (int)((int64_t)q * p.n_tiles / P);
     int lo = 0, hi = 0;
@@ -1341,7 +1374,12 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   return CS_OK;
 }
 
+namespace {
+void phase_report();
+}  // namespace
+
 void peer_release(PeerState& p) {
+  phase_report();
   if (p.imported) {
     for (int r = 0; r < p.nprocs; ++r)
       if (r != p.rank && p.peer_base[r]) cudaIpcCloseMemHandle(p.peer_base[r]);
@@ -1552,6 +1590,47 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   return rc;
 }
 
+// Debug knob CS_PHASE_TIMING=1: events between the hierarchical kernels; the per-phase
+// averages are printed to stderr when the peer state is released.
+namespace {
+struct PhaseTimes {
+  std::vector<cudaEvent_t> ev;  // 4 per step: start, after scatter, after reduce, after update
+  bool on = false, checked = false;
+};
+PhaseTimes g_phase;
+
+void phase_record(int i, cudaStream_t st) {
+  if (!g_phase.checked) {
+    const char* v = getenv("CS_PHASE_TIMING");
+    g_phase.on = v && v[0] == '1';
+    g_phase.checked = true;
+  }
+  if (!g_phase.on) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  g_phase.ev.push_back(e);
+  (void)i;
+}
+
+void phase_report() {
+  if (!g_phase.on || g_phase.ev.size() < 4) return;
+  cudaDeviceSynchronize();
+  double t[3] = {0, 0, 0};
+  const size_t steps = g_phase.ev.size() / 4;
+  for (size_t s = 0; s < steps; ++s)
+    for (int k = 0; k < 3; ++k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, g_phase.ev[4 * s + k], g_phase.ev[4 * s + k + 1]);
+      t[k] += ms;
+    }
+  fprintf(stderr, "[cs phase] steps=%zu scatter %.1f us  reduce+allgather %.1f us  update %.1f us\n", steps,
+          1e3 * t[0] / steps, 1e3 * t[1] / steps, 1e3 * t[2] / steps);
+  for (cudaEvent_t e : g_phase.ev) cudaEventDestroy(e);
+  g_phase.ev.clear();
+}
+}  // namespace
+
 int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEvent_t ev0,
                    cudaEvent_t ev1) {
   if (p.gs <= 0 || a.n_loc != 1) return perr(CS_EUNSUPPORTED, "multi-GPU hierarchical step needs one worker per GPU", cudaSuccess);
@@ -1599,17 +1678,62 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     k_hier_sync<<<p.grid_hier, kHierThreads, 0, st>>>(sa);
   }
   p.need_sync = false;
-  const int64_t scatter_v = p.chunk / 4 * p.gs;
-  int gsc = (int)((scatter_v + kHierThreads - 1) / kHierThreads);
-  if (gsc > p.grid_hier) gsc = p.grid_hier;
-  if (gsc < 1) gsc = 1;
-  h.c1_target = (p.tot_c1 += (uint32_t)gsc);
-  h.c2_target = (p.tot_c2 += (uint32_t)p.grid_hier);
-  k_hier_scatter<<<gsc, kHierThreads, 0, st>>>(h);
-  k_hier_reduce<<<p.grid_hier, kHierThreads, 0, st>>>(h);
+  // One group (no leader exchange): the vector is cut into P column pieces; h1 of piece
+  // q+1 (NVLink-bound) runs on the caller's stream while the update of piece q (HBM-bound,
+  // k_peer_push in final_only mode, waiting on piece q's d2 flags) runs on the aux stream.
+  const int P = exchange ? 1 : p.hier_pieces;
+  h.gstride = a.ld;
+  int rc = CS_OK;
+  for (int q = 0; q < P; ++q) {
+    const int t_lo = (int)((int64_t)q * p.n_tiles / P), t_hi = (int)((int64_t)(q + 1) * p.n_tiles / P);
+    h.col_lo = tile_col(p, t_lo);
+    h.col_hi = tile_col(p, t_hi);
+    h.chunk = ((h.col_hi - h.col_lo + p.gs - 1) / p.gs + 3) / 4 * 4;
+    h.off_d1 = p.off_d1 + q * p.flag_stride;
+    h.off_d2 = p.off_d2 + q * p.flag_stride;
+    h.off_c1 = p.off_c1 + 64 * q;
+    h.off_c2 = p.off_c2 + 64 * q;
+    h.c1_target = (p.tot_c1[q] += (uint32_t)p.grid_hier);
+    h.c2_target = (p.tot_c2[q] += (uint32_t)p.grid_hier);
+    phase_record(0, st);
+    k_hier_scatter<<<p.grid_hier, kHierThreads, 0, st>>>(h);
+    phase_record(1, st);
+    k_hier_reduce<<<p.grid_hier, kHierThreads, 0, st>>>(h);
+    phase_record(2, st);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return perr(CS_ECUDA, "hierarchical launch", e);
+    if (exchange) {
+      rc = launch_push_mix(p, ka, st);
+      phase_record(3, st);
+      continue;
+    }
+    PeerKernelArgs kq = ka;
+    kq.tile_lo = t_lo;
+    kq.tile_hi = t_hi;
+    kq.col_lo = h.col_lo;
+    kq.col_hi = h.col_hi;
+    kq.off_d2 = h.off_d2;
+    kq.off_done = p.off_done;
+    kq.off_count = p.off_count + 64 * q;
+    kq.pieces = q == P - 1 ? p.pieces : 0;  // the last update advances every flat piece's done flag
+    const int grid = p.grid_push < (t_hi - t_lo) ? p.grid_push : (t_hi - t_lo > 0 ? t_hi - t_lo : 1);
+    kq.done_target = (p.tot_count[q] += (uint32_t)grid);
+    const size_t smem = push_smem_bytes(ka.s.k, ka.s.n_loc);
+    if (P == 1) {
+      k_peer_push<<<grid, kPushThreads, smem, st>>>(kq);
+    } else {
+      cudaEventRecord(p.ev_push[q], st);
+      cudaStreamWaitEvent(p.aux, p.ev_push[q], 0);
+      k_peer_push<<<grid, kPushThreads, smem, p.aux>>>(kq);
+    }
+    phase_record(3, P == 1 ? st : p.aux);
+  }
+  if (!exchange && P > 1) {
+    cudaEventRecord(p.ev_mix, p.aux);
+    cudaStreamWaitEvent(st, p.ev_mix, 0);
+  }
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return perr(CS_ECUDA, "hierarchical launch", e);
-  int rc = launch_push_mix(p, ka, st);
+  if (e != cudaSuccess) return perr(CS_ECUDA, "hierarchical update launch", e);
   if (ev1) cudaEventRecord(ev1, st);
   return rc;
 }

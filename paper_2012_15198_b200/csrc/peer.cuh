@@ -69,7 +69,8 @@ struct PeerState {
   cudaEvent_t ev_mix = nullptr;
   // running totals of CTAs launched against each arrival counter (kernel targets)
   uint32_t tot_count[kMaxPieces] = {}, tot_pcount[kMaxPieces] = {};
-  uint32_t tot_c1 = 0, tot_c2 = 0, tot_c3 = 0;
+  uint32_t tot_c1[kMaxPieces] = {}, tot_c2[kMaxPieces] = {}, tot_c3 = 0;
+  int hier_pieces = 1;
   // multi-GPU diagnostics: every GPU owns a column chunk of diag_chunk columns and
   // receives all workers' x' (off_dx, [world][diag_chunk]) and psw (off_dw, [world][k])
   // for it; per-GPU partials (off_dpart, [nprocs][2] fp64) are combined in rank order
