@@ -522,7 +522,6 @@ struct HierArgs {
   int64_t d, chunk;          // chunk: columns per member in this piece (multiple of 4)
   int64_t col_lo, col_hi;    // this piece's columns
   int64_t gstride;           // gbox slot stride (elements)
-  int ce;                    // copy-engine transfers: k_hier_reduce writes the local gbar only
   int rank, gs;
   float inv_gs;
   uint32_t epoch;
@@ -589,10 +588,6 @@ __global__ void __launch_bounds__(kHierThreads) k_hier_reduce(const HierArgs h) 
         acc = add4(acc, mm == member ? ld4_valid(h.g + j, valid)
                                      : __ldcg(reinterpret_cast<const float4*>(gbox + (int64_t)mm * h.gstride + j)));
       const float4 mean = scale4(acc, h.inv_gs);
-      if (h.ce) {  // the copy engines all-gather it afterwards
-        st4(reinterpret_cast<float*>(mine + h.off_gbar) + j, mean, valid);
-        continue;
-      }
       for (int q = 0; q < h.gs; ++q) {  // rotated start: spread the all-gather over every peer
         const int mm = (q + member + (int)(v >> 5)) % h.gs;
         st4(reinterpret_cast<float*>(h.peers[gbase + mm] + h.off_gbar) + j, mean, valid);
@@ -602,16 +597,7 @@ __global__ void __launch_bounds__(kHierThreads) k_hier_reduce(const HierArgs h) 
   __syncthreads();
   if (threadIdx.x == 0) {
     if (s_timeout) atomicOr(h.err + kErrTimeout, 1);
-    if (!h.ce) publish_when_last(h.peers, mine, h.off_c2, h.off_d2, h.rank, gbase, h.gs, h.epoch, h.c2_target);
-  }
-}
-
-// Copy-engine mode: after the stream's peer copies have completed, release this rank's
-// flag (epoch) in every group member's flag array.
-__global__ void k_signal(char* const* peers, size_t flag_off, int rank, int first, int count, uint32_t epoch) {
-  if ((int)threadIdx.x < count) {
-    __threadfence_system();
-    ptx::st_release_sys(reinterpret_cast<uint32_t*>(peers[first + threadIdx.x] + flag_off) + rank, epoch);
+    publish_when_last(h.peers, mine, h.off_c2, h.off_d2, h.rank, gbase, h.gs, h.epoch, h.c2_target);
   }
 }
 
@@ -1711,34 +1697,9 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     h.c1_target = (p.tot_c1[q] += (uint32_t)p.grid_hier);
     h.c2_target = (p.tot_c2[q] += (uint32_t)p.grid_hier);
     phase_record(0, st);
-    static const int ce = getenv("CS_HIER_CE") ? atoi(getenv("CS_HIER_CE")) : 0;
-    h.ce = ce;
-    const int grp = a.rank / p.gs, member = a.rank - grp * p.gs, gbase = grp * p.gs;
-    if (ce) {
-      // reduce-scatter by the copy engines: chunk c of g -> member c's gbox slot `member`
-      for (int r = 1; r < p.gs; ++r) {
-        const int c = (member + r) % p.gs;
-        const int64_t c0 = h.col_lo + c * h.chunk, c1 = std::min(h.col_hi, c0 + h.chunk);
-        if (c1 > c0)
-          cudaMemcpyAsync(reinterpret_cast<float*>(p.peer_base[gbase + c] + p.off_gbox) + (int64_t)member * h.gstride + c0,
-                          a.g + c0, sizeof(float) * (size_t)(c1 - c0), cudaMemcpyDeviceToDevice, st);
-      }
-      k_signal<<<1, 32, 0, st>>>(p.d_peer_base, h.off_d1, a.rank, gbase, p.gs, epoch);
-    } else {
-      k_hier_scatter<<<p.grid_hier, kHierThreads, 0, st>>>(h);
-    }
+    k_hier_scatter<<<p.grid_hier, kHierThreads, 0, st>>>(h);
     phase_record(1, st);
     k_hier_reduce<<<p.grid_hier, kHierThreads, 0, st>>>(h);
-    if (ce) {  // all-gather of this member's mean chunk by the copy engines
-      const int64_t c0 = h.col_lo + member * h.chunk, c1 = std::min(h.col_hi, c0 + h.chunk);
-      for (int r = 1; r < p.gs && c1 > c0; ++r) {
-        const int c = (member + r) % p.gs;
-        cudaMemcpyAsync(reinterpret_cast<float*>(p.peer_base[gbase + c] + p.off_gbar) + c0,
-                        reinterpret_cast<const float*>(p.base + p.off_gbar) + c0, sizeof(float) * (size_t)(c1 - c0),
-                        cudaMemcpyDeviceToDevice, st);
-      }
-      k_signal<<<1, 32, 0, st>>>(p.d_peer_base, h.off_d2, a.rank, gbase, p.gs, epoch);
-    }
     phase_record(2, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return perr(CS_ECUDA, "hierarchical launch", e);
