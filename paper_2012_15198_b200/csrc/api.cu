@@ -349,6 +349,9 @@ PeerStepArgs peer_args(float* params, const float* grads, float* psw, float lr, 
   pa.gs = 0;
   pa.inv_gs = 1.0f / (float)(g.world / g.groups);
   pa.wire = g.wire == CS_WIRE_BF16 ? 1 : 0;
+  pa.lrs = nullptr;
+  pa.n_layers = 0;
+  pa.wd = 0.f;
   return pa;
 }
 
@@ -624,12 +627,25 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
     rc = enqueue_flat_step(params, grads, psw, lr, momentum, diag);
   } else {
     if (!g.peer.imported) return fail(CS_ENOTBOUND, "multi-GPU: cs_ipc_import has not been called");
-    if (g.lars) return fail(CS_EUNSUPPORTED, "LARS runs on the single-GPU bulk-TMA path");
+    if (g.lars && g.n_layers == 0) return fail(CS_EINVAL, "LARS needs a layer table (cs_set_layers)");
+    if (g.n_layers > 0 && g.wire != CS_WIRE_FP32)
+      return fail(CS_EUNSUPPORTED, "bf16 wire with a layer table is not implemented on the multi-GPU path");
     PeerStepArgs pa = peer_args(params, grads, psw, lr, momentum);
     pa.given = flat_given();
     cudaEvent_t ev[2];
     rc = next_event_pair(ev);
     if (rc) return rc;
+    if (g.lars) {  // per-(worker, layer) rates from this step's x and g, over the peer tiles
+      if (ev[0]) CS_CUDA(cudaEventRecord(ev[0], g.stream));  // the timed pair covers the rates
+      ev[0] = nullptr;
+      CS_CUDA(launch_lars_rates(params, grads, g.ld, peer_tiles(g.peer), peer_tile_count(g.peer), g.n_loc,
+                                g.d_tile_first, g.n_layers, g.d_lars_part, lr, g.lars_eta, g.lars_wd,
+                                g.lars_eps, g.d_lrs, g.stream));
+      pa.lrs = g.d_lrs;
+      pa.n_layers = g.n_layers;
+      pa.wd = g.lars_wd;
+      g.lars_valid = true;
+    }
     rc = peer_flat_step(g.peer, pa, g.stream, ev[0], ev[1]);
     if (rc) return fail(rc, "%s", peer_error());
     if (diag) {
@@ -637,8 +653,10 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
       if (rc) return fail(rc, "%s", peer_error());
     }
     const bool fused_topo = g.world <= 64;  // the topology is drawn inside the first kernel
-    g.launches_per_step = fused_topo ? 2 : 3;
-    g.hot_kernel = g.peer.use_hybrid ? "k_hyb_walk+k_hyb_tail" : "k_peer_push+k_peer_mix";
+    g.launches_per_step = (fused_topo ? 2 : 3) + (g.lars ? 2 : 0);
+    g.hot_kernel = g.peer.use_hybrid ? "k_hyb_walk+k_hyb_tail"
+                   : g.lars          ? "k_lars_norms+k_lars_scale+k_peer_push+k_peer_mix"
+                                     : "k_peer_push+k_peer_mix";
   }
   if (rc) return rc;
   if (diag) g.diag_valid = true;
@@ -774,12 +792,17 @@ int cs_set_layers(const int64_t* layer_bounds, int n_layers, const int32_t* seg_
     g.layer_bounds.clear();
     g.n_layers = 0;
     g.plan = host_bounds(g.d, g.k);
+    if (g.use_peer) {
+      std::vector<int32_t> first;
+      rc = peer_set_layers(g.peer, g.plan, g.layer_bounds, first);
+      return rc ? fail(rc, "%s", peer_error()) : CS_OK;
+    }
     return g.use_tma ? build_tma_tiles() : CS_OK;
   }
   if (n_layers < 1 || n_layers > CS_MAX_LAYERS)
     return fail(CS_EINVAL, "n_layers %d outside [1, %d]", n_layers, CS_MAX_LAYERS);
-  if (g.use_peer || !g.use_tma)
-    return fail(CS_EUNSUPPORTED, "layer tables run on the single-GPU bulk-TMA path");
+  if (g.use_peer ? (g.n_loc != 1 || g.peer.use_hybrid) : !g.use_tma)
+    return fail(CS_EUNSUPPORTED, "layer tables run on the single-GPU bulk-TMA path and the one-worker-per-GPU push/mix path");
   if (layer_bounds[0] != 0 || layer_bounds[n_layers] != g.d)
     return fail(CS_ELAYOUT, "layer bounds must run from 0 to d = %lld", (long long)g.d);
   for (int i = 0; i < n_layers; ++i) {
@@ -806,14 +829,28 @@ int cs_set_layers(const int64_t* layer_bounds, int n_layers, const int32_t* seg_
   g.layer_bounds.assign(layer_bounds, layer_bounds + n_layers + 1);
   g.n_layers = n_layers;
   g.plan = plan;
-  rc = build_tma_tiles();
-  if (rc) return rc;
+  int tiles_for_norms = 0;
+  if (g.use_peer) {  // every process sets the same table (collective by convention)
+    CS_CUDA(cudaStreamSynchronize(g.stream));
+    std::vector<int32_t> first;
+    rc = peer_set_layers(g.peer, g.plan, g.layer_bounds, first);
+    if (rc) return fail(rc, "%s", peer_error());
+    if (g.d_tile_first) cudaFree(g.d_tile_first);
+    g.d_tile_first = nullptr;
+    CS_CUDA(cudaMalloc(&g.d_tile_first, sizeof(int32_t) * first.size()));
+    CS_CUDA(cudaMemcpy(g.d_tile_first, first.data(), sizeof(int32_t) * first.size(), cudaMemcpyHostToDevice));
+    tiles_for_norms = peer_tile_count(g.peer);
+  } else {
+    rc = build_tma_tiles();
+    if (rc) return rc;
+    tiles_for_norms = g.n_tiles;
+  }
   if (g.d_lrs) cudaFree(g.d_lrs);
   if (g.d_lars_part) cudaFree(g.d_lars_part);
   g.d_lrs = nullptr;
   g.d_lars_part = nullptr;
   CS_CUDA(cudaMalloc(&g.d_lrs, sizeof(float) * (size_t)g.n_loc * n_layers));
-  CS_CUDA(cudaMalloc(&g.d_lars_part, sizeof(double) * 2 * (size_t)g.n_tiles * g.n_loc));
+  CS_CUDA(cudaMalloc(&g.d_lars_part, sizeof(double) * 2 * (size_t)tiles_for_norms * g.n_loc));
   g.lars_valid = false;
   return CS_OK;
 }

@@ -132,6 +132,7 @@ struct PeerKernelArgs {
   char* const* peers;       // [nprocs] region bases
   const int64_t* bounds;    // [k+1] segment bounds
   const int32_t* seg_t0;    // [k+1] first tile of each segment (seg_t0[k] = n_tiles)
+  const TileDesc* tiles;    // explicit tile table (layer table set) or nullptr
   int n_tiles;
   int tile_lo, tile_hi;     // this launch's piece of the step: tiles [tile_lo, tile_hi)
   int pieces;               // pieces per step and the stride of their flag arrays
@@ -145,6 +146,10 @@ struct PeerKernelArgs {
   size_t off_inbox, off_wbox, off_done, off_count, off_pdone, off_pcount, off_d2;
 };
 
+__device__ __forceinline__ float4 decay4(float4 g, float4 x, float wd) {  // g + wd*x (C-18)
+  return make_float4(__fadd_rn(g.x, __fmul_rn(wd, x.x)), __fadd_rn(g.y, __fmul_rn(wd, x.y)),
+                     __fadd_rn(g.z, __fmul_rn(wd, x.z)), __fadd_rn(g.w, __fmul_rn(wd, x.w)));
+}
 __device__ __forceinline__ float4 mom4(float4 m, float4 g, float mu) {
   return make_float4(__fadd_rn(__fmul_rn(mu, m.x), g.x), __fadd_rn(__fmul_rn(mu, m.y), g.y),
                      __fadd_rn(__fmul_rn(mu, m.z), g.z), __fadd_rn(__fmul_rn(mu, m.w), g.w));
@@ -207,7 +212,7 @@ struct Meta {
 };
 
 struct Unit {
-  int tile, r, seg, len;
+  int tile, r, seg, len, layer;
   int64_t c0;
   bool first_tile;
 };
@@ -218,11 +223,19 @@ __device__ __forceinline__ Unit unit_at(const PeerKernelArgs& a, const Meta& M, 
   x.r = u - x.tile * a.s.n_loc;
   while (M.t0[cursor + 1] <= x.tile) ++cursor;
   x.seg = cursor;
+  x.first_tile = x.tile == M.t0[cursor];
+  if (a.tiles != nullptr) {  // layer table: explicit tiles
+    const TileDesc td = a.tiles[x.tile];
+    x.c0 = td.c0;
+    x.len = td.len;
+    x.layer = td.layer;
+    return x;
+  }
   const int64_t c0 = M.bnd[cursor] + (int64_t)(x.tile - M.t0[cursor]) * kPeerTile;
   const int64_t c1 = c0 + kPeerTile < M.bnd[cursor + 1] ? c0 + kPeerTile : M.bnd[cursor + 1];
   x.c0 = c0;
   x.len = (int)(c1 - c0);
-  x.first_tile = x.tile == M.t0[cursor];
+  x.layer = 0;
   return x;
 }
 
@@ -361,8 +374,9 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
           const float4 cm = reinterpret_cast<const float4*>(bx + kPeerTile)[v];
           const float4 cg = reinterpret_cast<const float4*>(bx + 2 * kPeerTile)[v];
           bad |= nonfinite4(cg);
-          const float4 mn = mom4(cm, cg, s.mu);
-          const float4 y = sgd4(cx, mn, s.lr);
+          // LARS (C-18): m' = mu*m + (g + wd*x), y = x - lrs[r][layer]*m'
+          const float4 mn = mom4(cm, s.lrs ? decay4(cg, cx, s.wd) : cg, s.mu);
+          const float4 y = sgd4(cx, mn, s.lrs ? __ldg(s.lrs + (int64_t)U.r * s.n_layers + U.layer) : s.lr);
           const int64_t j = U.c0 + 4 * (int64_t)v;
           st4_cs(s.m + rowoff + j, mn, vv);
           if (a.final_only) {
@@ -1009,6 +1023,7 @@ struct DiagArgs {
   const float* psw;
   char* const* peers;
   int64_t ld, d, nq, chunk;
+  const int64_t* bounds;  // [k+1] segment bounds (the plan in use)
   int k, world, n_loc, first, rank, nprocs;
   uint32_t epoch;  // diagnostics epoch (>= 1)
   uint32_t c1_target, c2_target;
@@ -1086,7 +1101,11 @@ __global__ void __launch_bounds__(256) k_diag_reduce(const DiagArgs a) {
     for (int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; jj < cols;
          jj += (int64_t)gridDim.x * blockDim.x) {
       const int64_t j = c0 + jj;
-      const int s = (int)imin64(a.k - 1, (((j >> 5) + 1) * a.k - 1) / a.nq);
+      int s = 0;  // segment of column j: the last bound <= j (binary search over the plan)
+      for (int lo = 0, hi = a.k - 1; lo <= hi;) {
+        const int mid = (lo + hi) >> 1;
+        if (a.bounds[mid] <= j) { s = mid; lo = mid + 1; } else { hi = mid - 1; }
+      }
       double c = 0.0, s1 = 0.0, s2 = 0.0, xs = 0.0;
       for (int i = 0; i < a.world; ++i) {
         const double xv = (double)__ldcg(dx + (int64_t)i * a.chunk + jj);
@@ -1173,6 +1192,7 @@ int peer_diag(PeerState& p, const PeerStepArgs& a, double* partials, int partial
   da.ld = a.ld;
   da.d = a.d;
   da.nq = a.nq;
+  da.bounds = p.d_bounds;
   da.chunk = p.diag_chunk;
   da.k = a.k;
   da.world = a.world;
@@ -1304,6 +1324,7 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_h, k_hier_reduce, kHierThreads, 0);
   if (e != cudaSuccess || occ_push < 1 || occ_mix < 1 || occ_h < 1) return perr(CS_ECUDA, "occupancy", e);
   const int n_units = p.n_tiles * n_loc;
+  p.grid_push_max = sms * occ_push;
   p.grid_push = sms * occ_push < n_units ? sms * occ_push : n_units;
   p.grid_mix = sms * occ_mix;
   p.grid_hier = sms * occ_h;
@@ -1387,6 +1408,7 @@ void peer_release(PeerState& p) {
   }
   if (p.base) cudaFree(p.base);
   if (p.d_peer_base) cudaFree(p.d_peer_base);
+  if (p.d_ptiles) cudaFree(p.d_ptiles);
   if (p.d_bounds) cudaFree(p.d_bounds);
   if (p.d_seg_t0) cudaFree(p.d_seg_t0);
   if (p.aux) {
@@ -1443,6 +1465,7 @@ PeerKernelArgs kernel_args(const PeerState& p, const PeerStepArgs& a, uint32_t e
   ka.peers = p.d_peer_base;
   ka.bounds = p.d_bounds;
   ka.seg_t0 = p.d_seg_t0;
+  ka.tiles = p.d_ptiles;
   ka.n_tiles = p.n_tiles;
   ka.epoch = epoch;
   ka.final_only = final_only ? 1 : 0;
@@ -1479,8 +1502,82 @@ int launch_topology_for(const PeerStepArgs& a, int n, int tag, cudaStream_t st) 
   return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "topology launch", e);
 }
 
+}  // namespace
+
+int peer_set_layers(PeerState& p, const std::vector<int64_t>& plan, const std::vector<int64_t>& layer_bounds,
+                    std::vector<int32_t>& tile_first) {
+  const int k = p.k;
+  if ((int)plan.size() != k + 1) return perr(CS_EINVAL, "segment plan size", cudaSuccess);
+  std::vector<int64_t> lb = layer_bounds.empty() ? std::vector<int64_t>{0, p.d} : layer_bounds;
+  const int L = (int)lb.size() - 1;
+  std::vector<TileDesc> tiles;
+  std::vector<int32_t> seg_t0(k + 1, 0);
+  tile_first.assign(L + 1, 0);
+  int l = 0;
+  for (int s = 0; s < k; ++s) {
+    seg_t0[s] = (int32_t)tiles.size();
+    int64_t c = plan[s];
+    while (c < plan[s + 1]) {
+      while (lb[l + 1] <= c) tile_first[++l] = (int32_t)tiles.size();
+      const int64_t end = std::min(std::min(plan[s + 1], lb[l + 1]), c + (int64_t)kPeerTile);
+      TileDesc td;
+      td.c0 = c;
+      td.seg = s;
+      td.len = (int32_t)(end - c);
+      td.layer = l;
+      td.pad_ = 0;
+      tiles.push_back(td);
+      c = end;
+    }
+  }
+  seg_t0[k] = (int32_t)tiles.size();
+  while (l < L) tile_first[++l] = (int32_t)tiles.size();
+  cudaError_t e = cudaSuccess;
+  if (p.d_ptiles) cudaFree(p.d_ptiles);
+  p.d_ptiles = nullptr;
+  p.h_tile_c0.clear();
+  if (layer_bounds.empty()) {
+    // back to the closed-form equal split (tiles of kPeerTile)
+    int n = 0;
+    for (int s = 0; s < k; ++s) {
+      seg_t0[s] = n;
+      n += (int)((plan[s + 1] - plan[s] + kPeerTile - 1) / kPeerTile);
+    }
+    seg_t0[k] = n;
+  } else {
+    e = cudaMalloc(&p.d_ptiles, sizeof(TileDesc) * tiles.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p.d_ptiles, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice);
+    p.h_tile_c0.resize(tiles.size() + 1);
+    for (size_t t = 0; t < tiles.size(); ++t) p.h_tile_c0[t] = tiles[t].c0;
+    p.h_tile_c0[tiles.size()] = p.d;
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p.d_bounds, plan.data(), sizeof(int64_t) * (k + 1), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(p.d_seg_t0, seg_t0.data(), sizeof(int32_t) * (k + 1), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return perr(CS_ECUDA, "peer layer tiles", e);
+  p.h_bounds = plan;
+  p.h_seg_t0 = seg_t0;
+  p.n_tiles = seg_t0[k];
+  const int units = p.n_tiles * p.n_loc;
+  p.grid_push = p.grid_push_max < units ? p.grid_push_max : units;
+  // pieces follow the new tile count
+  if (p.pieces > p.n_tiles) p.pieces = p.n_tiles;
+  p.piece_tile.resize(p.pieces + 1);
+  for (int q = 0; q <= p.pieces; ++q) p.piece_tile[q] = (int)((int64_t)q * p.n_tiles / p.pieces);
+  if (p.hier_pieces > p.n_tiles) p.hier_pieces = p.n_tiles;
+  return CS_OK;
+}
+
+const TileDesc* peer_tiles(const PeerState& p) { return p.d_ptiles; }
+int peer_tile_count(const PeerState& p) { return p.n_tiles; }
+
+namespace {
+
 int64_t tile_col(const PeerState& p, int t) {
   if (t >= p.n_tiles) return p.d;
+  if (!p.h_tile_c0.empty()) return p.h_tile_c0[t];
   int sg = 0;
   while (p.h_seg_t0[sg + 1] <= t) ++sg;
   return p.h_bounds[sg] + (int64_t)(t - p.h_seg_t0[sg]) * kPeerTile;

@@ -29,6 +29,10 @@ struct PeerStepArgs {
   float inv_gs;   // fp32(1/|G|)
   // bf16 wire format (reading C-20): inbox rows hold bf16 with stride (ld + 7) & ~7
   int wire;
+  // LARS (reading C-18): per-(local worker, layer) rates of this step, weight decay
+  const float* lrs;
+  int n_layers;
+  float wd;
 };
 
 struct PeerState {
@@ -79,6 +83,11 @@ struct PeerState {
   uint32_t tot_dc1 = 0, tot_dc2 = 0, diag_epoch = 0;
   // hybrid flat step (several workers per GPU): local cycle walk + NVLink chain heads
   bool use_hybrid = false;
+  // layer table (cs_set_layers, one worker per GPU): explicit tiles split at segment and
+  // layer bounds; nullptr = the closed-form equal split of kPeerTile tiles
+  struct TileDesc* d_ptiles = nullptr;
+  std::vector<int64_t> h_tile_c0;     // [n_tiles + 1] first column of each tile (d at the end)
+  int grid_push_max = 0;
   struct TileDesc* d_htiles = nullptr;
   int n_htiles = 0, grid_hyb = 0, grid_tail = 0;
   uint8_t* d_tail_tbl = nullptr;
@@ -93,6 +102,13 @@ int peer_import(PeerState& p, const char* all_handles);
 int peer_import_self(PeerState& p);  // nprocs == 1: the only peer is this GPU
 int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEvent_t ev0,
                    cudaEvent_t ev1);
+// Layer table on the push/mix path: tiles split at the plan's segment bounds and the layer
+// bounds.  Returns the tile range of each layer in tile_first [n_layers + 1].  Empty
+// layer_bounds restores the equal split.
+int peer_set_layers(PeerState& p, const std::vector<int64_t>& plan, const std::vector<int64_t>& layer_bounds,
+                    std::vector<int32_t>& tile_first);
+const struct TileDesc* peer_tiles(const PeerState& p);
+int peer_tile_count(const PeerState& p);
 int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEvent_t ev0,
                    cudaEvent_t ev1);
 // diagnostics of the current state (after a step), all GPUs; out: device double[2]

@@ -38,6 +38,9 @@ def main():
     ap.add_argument("--diag", action="store_true", help="check the multi-GPU diagnostics too")
     ap.add_argument("--exponential", action="store_true", help="SGP's exponential graph (cs_set_topology_kind)")
     ap.add_argument("--wire-bf16", action="store_true", help="bf16 wire format (cs_set_wire)")
+    ap.add_argument("--layers", type=int, default=0, help="random layer table with this many layers")
+    ap.add_argument("--layer-plan", action="store_true", help="segments from the layer plan (cs_segment_plan)")
+    ap.add_argument("--lars", action="store_true", help="LARS (Table 1 constants, lr 9)")
     a = ap.parse_args()
     rank, ws, lr_ = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(lr_)
@@ -71,6 +74,20 @@ def main():
 
     cols = np.arange(d) if a.compare_all else synth.sample_columns(d, T.segment_bounds(d, k))
     orc = OracleRun(world, d, k, seed, cols=cols, groups=a.hier_groups or None)
+    lb = None
+    if a.layers:
+        from oracle.lars import lars_gossip_step, plan_bounds, segment_plan
+        rng = np.random.default_rng(a.layers)
+        cuts = np.unique(rng.integers(1, d // 4, size=a.layers - 1) * 4)
+        lb = np.concatenate([[0], cuts, [d]]).astype(np.int64)
+        sizes = np.diff(lb).tolist()
+        plan = segment_plan(sizes, k) if a.layer_plan else None
+        cs.cs_set_layers(lb, plan)
+        orc.seg = T.segment_of_columns(plan_bounds(lb, plan) if plan else T.segment_bounds(d, k), cols)
+    if a.lars:
+        ETA, WD, EPS = 0.0025, 5e-5, 1e-9
+        cs.cs_set_lars(ETA, WD, EPS)
+        lr = 9.0
     step_fn = cs.cs_hier_step if a.hier_groups else cs.cs_gossip_step
     idx = torch.from_numpy(cols).to(dev)
     ok = True
@@ -80,8 +97,20 @@ def main():
     for t in range(a.num_steps):
         o = (t + first) % B
         step_fn(x, bank[o:o + n_loc], w, lr, mu)
-        orc.step(lr, mu, src=exponential_topology(t, world, k) if a.exponential else None,
-                 wire="bf16" if a.wire_bf16 else None)
+        if a.lars:  # full rows (--compare-all): LARS needs whole layers
+            g_all = synth.grads_at(orc.bank, world, orc.t)
+            orc.x, orc.m, orc.w, lrs = lars_gossip_step(orc.x, orc.m, g_all, orc.w, T.topology(seed, orc.t, world, k),
+                                                        orc.seg, lb, lr, mu, ETA, WD, EPS)
+            orc.t += 1
+            got = cs.cs_get_lars_rates(n_loc, len(lb) - 1)
+            want = lrs[first:first + n_loc]
+            if not np.all(np.abs(got.astype(np.float64) - want) <= np.spacing(np.abs(want))):
+                print(f"rank {rank} step {t}: LARS rates differ by more than 1 ulp", flush=True)
+                ok = False
+                break
+        else:
+            orc.step(lr, mu, src=exponential_topology(t, world, k) if a.exponential else None,
+                     wire="bf16" if a.wire_bf16 else None)
         cs.cs_sync()
         if a.diag:
             cd, msum = cs.cs_get_diag()
@@ -99,8 +128,12 @@ def main():
         if a.hier_groups and first % gs != 0:
             lead = (first // gs) * gs
             m_ok = np.array_equal(ms, orc.m[lead:lead + 1])  # the replica equals its leader's
-        if not (np.array_equal(xs, orc.x[rows]) and m_ok
-                and np.array_equal(w.cpu().numpy(), orc.w[rows])):
+        if a.lars:  # norms in another fp64 order: rates within 1 ulp, params within 1e-6
+            xs_ok = np.all(np.abs(xs - orc.x[rows]) <= 1e-6 * np.abs(orc.x[rows]).max(axis=1, keepdims=True))
+            m_ok = np.all(np.abs(ms - orc.m[rows]) <= 1e-5 * np.abs(orc.m[rows]).max(axis=1, keepdims=True))
+        else:
+            xs_ok = np.array_equal(xs, orc.x[rows])
+        if not (xs_ok and m_ok and np.array_equal(w.cpu().numpy(), orc.w[rows])):
             bad = np.argwhere(xs != orc.x[rows])
             print(f"rank {rank} step {t}: mismatch at {bad[:5].tolist()} of {bad.shape[0]}", flush=True)
             ok = False

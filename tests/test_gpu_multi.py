@@ -77,6 +77,17 @@ def test_two_gpu_bf16_wire_bitwise(n_loc, d, k):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("layers,plan,lars,diag", [(9, True, False, True), (25, True, True, False),
+                                                   (12, False, True, True)])
+def test_two_gpu_layers_and_lars(layers, plan, lars, diag):
+    # layer table on the push/mix path: layer-plan segments bitwise; LARS within 1 ulp / 1e-6
+    args = ["--workers-per-gpu", 1, "--vector-len", 200_000, "--segments", 6, "--num-steps", 5, "--compare-all",
+            "--layers", layers]
+    args += (["--layer-plan"] if plan else []) + (["--lars"] if lars else []) + (["--diag"] if diag else [])
+    _run(2, *args)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("pieces", [3, 8])
 def test_two_gpu_pieces_bitwise(pieces):
     # push(p+1) / mix(p) overlap across the caller's and the aux stream, across GPUs
