@@ -137,3 +137,28 @@ def lars_gossip_step(x, m, g, w, src, seg_of_col, layer_bounds, lr, mu, eta, wei
     m_new, y = lars_update(x, m, g, lrs, layer_of_col, mu, weight_decay)
     x_new, w_new = mix(y, w, src, seg_of_col)
     return x_new, m_new, w_new, lrs
+
+
+def lars_hier_step(x, m, g, w, groups, seed, step, k, seg_of_col, layer_bounds, lr, mu, eta, weight_decay, eps):
+    """Hierarchical step with LARS (LARS needs the gradient norm synchronised,
+    so the leader applies it to the group-reduced gradient).  h1 group mean; the leaders'
+    rates come from their x and the group mean gbar (C-18); h2 leader gossip; h3 members
+    take the leader's x and w.  Full rows only.  Returns (x', m', w', lrs_of_leaders)."""
+    from .hierarchical import group_mean
+    from .topology import TAG_HIER, topology
+    n = x.shape[0]
+    gs = n // groups
+    leaders = [G * gs for G in range(groups)]
+    gbar = group_mean(g, groups)
+    lrs = layer_lr(x[leaders], gbar, layer_bounds, lr, eta, weight_decay, eps)
+    d = x.shape[1]
+    layer_of_col = np.searchsorted(np.asarray(layer_bounds), np.arange(d), side="right") - 1
+    mL, yL = lars_update(x[leaders], m[leaders], gbar, lrs, layer_of_col, mu, weight_decay)
+    m_new = m.copy()
+    m_new[leaders] = mL
+    wL = w[leaders]
+    if groups >= 2:
+        xL, wL = mix(yL, wL, topology(seed, step, groups, k, TAG_HIER), seg_of_col)
+    else:
+        xL = yL
+    return np.repeat(xL, gs, axis=0), m_new, np.repeat(wL, gs, axis=0), lrs

@@ -120,3 +120,39 @@ def test_layer_rates_are_per_worker_and_per_layer():
     expect = a.copy()
     expect[1, 1] = a[1, 1] * F32(2)
     assert np.array_equal(b, expect)
+
+
+def test_lars_hier_groups_equal_world_is_flat_lars():
+    # G = n: each group is one worker, the group mean is its own gradient and the leader
+    # topology (tag HIER) is used: equal to the flat LARS step with that topology
+    from oracle.lars import lars_hier_step
+    rng = np.random.default_rng(9)
+    n, d, k = 4, 48, 2
+    lb = [0, 16, 48]
+    x = rng.standard_normal((n, d)).astype(F32)
+    g = rng.standard_normal((n, d)).astype(F32)
+    m = rng.standard_normal((n, d)).astype(F32)
+    w = np.ones((n, k), F32)
+    seg = T.segment_of_columns(T.segment_bounds(d, k), np.arange(d))
+    a = lars_hier_step(x, m, g, w, n, 3, 5, k, seg, lb, 0.5, 0.9, 0.01, 1e-3, 1e-9)
+    src = T.topology(3, 5, n, k, T.TAG_HIER)
+    b = lars_gossip_step(x, m, g, w, src, seg, lb, 0.5, 0.9, 0.01, 1e-3, 1e-9)
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
+
+
+def test_lars_hier_one_group_uses_the_synchronised_norm():
+    # G = 1: every worker ends with the same x, updated with the rate of the MEAN gradient's
+    # norm, not any single worker's; with identical gradients it equals flat LARS
+    from oracle.lars import lars_hier_step
+    rng = np.random.default_rng(10)
+    n, d = 4, 32
+    lb = [0, 32]
+    x = np.repeat(rng.standard_normal((1, d)).astype(F32), n, axis=0)
+    g1 = rng.standard_normal((1, d)).astype(F32)
+    g = np.repeat(g1, n, axis=0) * F32(2)   # identical gradients, exact mean
+    z = np.zeros_like(x)
+    xh, _, _, lrs = lars_hier_step(x, z, g, np.ones((n, 1), F32), 1, 0, 0, 1, np.zeros(d, np.int64), lb,
+                                   1.0, 0.0, 0.01, 0.0, 0.0)
+    assert lrs.shape == (1, 1) and np.all(xh == xh[0])
+    assert lrs[0, 0] == layer_lr(x[:1], g[:1], lb, 1.0, 0.01, 0.0, 0.0)[0, 0]
