@@ -200,6 +200,9 @@ int cs_gossip_step_host(float* params, const float* grads_host, float* psw, floa
  * in the source group.  The first hierarchical step after cs_bind / cs_set_step
  * copies each leader's state to its members; callers must not modify a member's
  * state between hierarchical steps.  Other layouts: CS_EUNSUPPORTED.
+ * With LARS (cs_set_lars, multi-GPU only) the leader's rates come from its x and the
+ * group-reduced gradient gbar, so the gradient norm is the synchronised one
+ * (PAPER.md:197); every member computes the same rates from its replica.
  * Errors as cs_gossip_step. */
 int cs_hier_step(float* params, float* grads, float* psw, float lr, float momentum);
 

@@ -352,6 +352,11 @@ PeerStepArgs peer_args(float* params, const float* grads, float* psw, float lr, 
   pa.lrs = nullptr;
   pa.n_layers = 0;
   pa.wd = 0.f;
+  pa.lrs_out = nullptr;
+  pa.eta = 0.f;
+  pa.eps = 0.f;
+  pa.tile_first = nullptr;
+  pa.lars_part = nullptr;
   return pa;
 }
 
@@ -692,8 +697,9 @@ int cs_gossip_step_host(float* params, const float* grads_host, float* psw, floa
 int cs_hier_step(float* params, float* grads, float* psw, float lr, float momentum) {
   int rc = check_bound();
   if (rc) return rc;
-  if (g.lars || g.n_layers > 0)
-    return fail(CS_EUNSUPPORTED, "LARS / layer tables are not implemented for the hierarchical step");
+  if ((g.lars || g.n_layers > 0) && g.nprocs == 1)
+    return fail(CS_EUNSUPPORTED, "LARS / layer tables in the hierarchical step need the multi-GPU path");
+  if (g.lars && g.n_layers == 0) return fail(CS_EINVAL, "LARS needs a layer table (cs_set_layers)");
   if (g.wire != CS_WIRE_FP32)
     return fail(CS_EUNSUPPORTED, "the bf16 wire format is implemented for the flat step only");
   rc = check_step_args(params, grads, psw);
@@ -704,6 +710,16 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
       return fail(CS_EUNSUPPORTED, "multi-GPU hierarchical step needs one worker per GPU (world == nprocs)");
     if (!g.peer.imported) return fail(CS_ENOTBOUND, "multi-GPU: cs_ipc_import has not been called");
     PeerStepArgs pa = peer_args(params, grads, psw, lr, momentum);
+    if (g.lars) {  // rates from the leader replica's x and the group mean
+      pa.lrs_out = g.d_lrs;
+      pa.n_layers = g.n_layers;
+      pa.wd = g.lars_wd;
+      pa.eta = g.lars_eta;
+      pa.eps = g.lars_eps;
+      pa.tile_first = g.d_tile_first;
+      pa.lars_part = g.d_lars_part;
+      g.lars_valid = true;
+    }
     cudaEvent_t ev[2];
     rc = next_event_pair(ev);
     if (rc) return rc;
@@ -714,8 +730,9 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
       if (rc) return fail(rc, "%s", peer_error());
       g.diag_valid = true;
     }
-    g.launches_per_step = g.groups >= 2 ? 5 : 3;  // (topology,) scatter, reduce, push(, mix)
-    g.hot_kernel = "k_hier_scatter+k_hier_reduce+k_peer_push+k_peer_mix";
+    g.launches_per_step = (g.groups >= 2 ? 5 : 3) + (g.lars ? 2 : 0);  // (topology,) scatter, reduce, push(, mix)
+    g.hot_kernel = g.lars ? "k_hier_scatter+k_hier_reduce+k_lars_norms+k_lars_scale+k_peer_push+k_peer_mix"
+                          : "k_hier_scatter+k_hier_reduce+k_peer_push+k_peer_mix";
     g.step += 1;
     return CS_OK;
   }

@@ -124,10 +124,18 @@ cudaError_t launch_synth(float* out, int64_t rows, int64_t d, int64_t ld, uint64
                          int tag, int64_t row0, float scale, cudaStream_t st);
 // LARS (lars.cu): per-(tile, row) fp64 partial sums of x^2, g^2, then per-(row, layer)
 // rates lrs = fp32(lr * scale).  tile_first: [n_layers + 1] tile ranges of the layers.
+// Optional wait before the norms (hierarchical: the group mean is complete when every
+// member's flag flags[first .. first+count) reaches epoch).
+struct LarsWait {
+  const uint32_t* flags = nullptr;
+  int first = 0, count = 0;
+  uint32_t epoch = 0;
+  int* err = nullptr;
+};
 cudaError_t launch_lars_rates(const float* x, const float* g, int64_t ld, const TileDesc* tiles,
                               int n_tiles, int rows, const int32_t* tile_first, int n_layers,
                               double* part, float lr, float eta, float wd, float eps, float* lrs,
-                              cudaStream_t st);
+                              cudaStream_t st, LarsWait w = LarsWait());
 cudaError_t launch_accumulate(float* acc, const float* g, int64_t rows, int64_t d, int64_t ld,
                               int count, int interval, cudaStream_t st);
 

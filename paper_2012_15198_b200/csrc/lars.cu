@@ -13,6 +13,7 @@
 // The tiles are the step kernel's layer-split tiles, so a layer's tiles are the
 // contiguous range [tile_first[l], tile_first[l+1]).
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace cs {
 namespace {
@@ -47,8 +48,31 @@ __device__ __forceinline__ double2 block_sum2(double a, double b, double2* red) 
 
 __global__ void __launch_bounds__(kNormThreads)
     k_lars_norms(const float* __restrict__ x, const float* __restrict__ g, int64_t ld,
-                 const TileDesc* __restrict__ tiles, int n_tiles, int rows, double2* __restrict__ part) {
+                 const TileDesc* __restrict__ tiles, int n_tiles, int rows, double2* __restrict__ part,
+                 LarsWait w) {
   __shared__ double2 red[kNormThreads / 32];
+  if (w.flags != nullptr) {
+    // hierarchical: g is the group mean, complete once every member's all-gather arrived
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    if ((int)threadIdx.x < w.count) {
+      const uint32_t* f = w.flags + w.first + threadIdx.x;
+      uint64_t t0 = 0;
+      while ((int32_t)(ptx::ld_relaxed_sys(f) - w.epoch) < 0) {
+        const uint64_t now = ptx::globaltimer();
+        if (t0 == 0) t0 = now;
+        if (now - t0 > 20000000000ull) { s_bad = 1; break; }
+        __nanosleep(64);
+      }
+      ptx::fence_acq_rel_sys();
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (threadIdx.x == 0) atomicOr(w.err + kErrTimeout, 1);
+      return;
+    }
+  }
   const int64_t pairs = (int64_t)n_tiles * rows;
   for (int64_t p = blockIdx.x; p < pairs; p += gridDim.x) {
     const int u = (int)(p / rows), r = (int)(p % rows);
@@ -102,14 +126,14 @@ __global__ void __launch_bounds__(kNormThreads)
 cudaError_t launch_lars_rates(const float* x, const float* g, int64_t ld, const TileDesc* tiles,
                               int n_tiles, int rows, const int32_t* tile_first, int n_layers,
                               double* part, float lr, float eta, float wd, float eps, float* lrs,
-                              cudaStream_t st) {
+                              cudaStream_t st, LarsWait w) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t pairs = (int64_t)n_tiles * rows;
   const int grid = (int)(pairs < (int64_t)sms * 8 ? pairs : (int64_t)sms * 8);
   k_lars_norms<<<grid > 0 ? grid : 1, kNormThreads, 0, st>>>(x, g, ld, tiles, n_tiles, rows,
-                                                             reinterpret_cast<double2*>(part));
+                                                             reinterpret_cast<double2*>(part), w);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_lars_scale<<<n_layers, kNormThreads, 0, st>>>(reinterpret_cast<const double2*>(part), rows,

@@ -1757,6 +1757,10 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   PeerStepArgs b = a;
   b.g = reinterpret_cast<const float*>(p.base + p.off_gbar);  // the group mean
   b.gs = p.gs;
+  if (a.lrs_out) {  // LARS with the group-reduced gradient: b.lrs is filled after h1 below
+    b.lrs = a.lrs_out;
+    if (p.hier_pieces != 1 && !exchange) return perr(CS_EUNSUPPORTED, "hierarchical LARS needs CS_HIER_PIECES=1", cudaSuccess);
+  }
   PeerKernelArgs ka = kernel_args(p, b, epoch, !exchange);
   if (ev0) cudaEventRecord(ev0, st);
   if (p.need_sync && p.gs > 1) {  // members become exact replicas of their leader
@@ -1798,6 +1802,17 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     phase_record(1, st);
     k_hier_reduce<<<p.grid_hier, kHierThreads, 0, st>>>(h);
     phase_record(2, st);
+    if (a.lrs_out) {  // rates from the leader replica's x and the group mean, once gbar is whole
+      LarsWait w;
+      w.flags = reinterpret_cast<const uint32_t*>(p.base + p.off_d2);
+      w.first = (a.rank / p.gs) * p.gs;
+      w.count = p.gs;
+      w.epoch = epoch;
+      w.err = a.err;
+      cudaError_t le = launch_lars_rates(a.x, b.g, a.ld, p.d_ptiles, p.n_tiles, 1, a.tile_first, a.n_layers,
+                                         a.lars_part, a.lr, a.eta, a.wd, a.eps, a.lrs_out, st, w);
+      if (le != cudaSuccess) return perr(CS_ECUDA, "hierarchical LARS rates", le);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return perr(CS_ECUDA, "hierarchical launch", e);
     if (exchange) {

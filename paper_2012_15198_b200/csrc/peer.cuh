@@ -33,6 +33,12 @@ struct PeerStepArgs {
   const float* lrs;
   int n_layers;
   float wd;
+  // hierarchical LARS: the rates are computed inside peer_hier_step from x and the group
+  // mean into lrs_out
+  float* lrs_out;
+  float eta, eps;
+  const int32_t* tile_first;
+  double* lars_part;
 };
 
 struct PeerState {

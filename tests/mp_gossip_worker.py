@@ -99,15 +99,23 @@ def main():
         step_fn(x, bank[o:o + n_loc], w, lr, mu)
         if a.lars:  # full rows (--compare-all): LARS needs whole layers
             g_all = synth.grads_at(orc.bank, world, orc.t)
-            orc.x, orc.m, orc.w, lrs = lars_gossip_step(orc.x, orc.m, g_all, orc.w, T.topology(seed, orc.t, world, k),
-                                                        orc.seg, lb, lr, mu, ETA, WD, EPS)
+            if a.hier_groups:  # LARS on the group-reduced gradient
+                from oracle.lars import lars_hier_step
+                orc.x, orc.m, orc.w, lrs = lars_hier_step(orc.x, orc.m, g_all, orc.w, a.hier_groups, seed, orc.t, k,
+                                                          orc.seg, lb, lr, mu, ETA, WD, EPS)
+                grp = first // (world // a.hier_groups)
+                want = lrs[grp:grp + 1]
+            else:
+                orc.x, orc.m, orc.w, lrs = lars_gossip_step(orc.x, orc.m, g_all, orc.w,
+                                                            T.topology(seed, orc.t, world, k), orc.seg, lb, lr, mu,
+                                                            ETA, WD, EPS)
+                want = lrs[first:first + n_loc]
             orc.t += 1
             got = cs.cs_get_lars_rates(n_loc, len(lb) - 1)
-            want = lrs[first:first + n_loc]
             if not np.all(np.abs(got.astype(np.float64) - want) <= np.spacing(np.abs(want))):
                 print(f"rank {rank} step {t}: LARS rates differ by more than 1 ulp", flush=True)
                 ok = False
-                break
+                failed = True  # keep stepping in lockstep with the other ranks
         else:
             orc.step(lr, mu, src=exponential_topology(t, world, k) if a.exponential else None,
                      wire="bf16" if a.wire_bf16 else None)
@@ -118,7 +126,7 @@ def main():
             if not (abs(cd - cd0) <= 1e-9 * abs(cd0) and abs(msum - ms0) <= 1e-9 * max(1.0, abs(ms0)) + 1e-9 * d):
                 print(f"rank {rank} step {t}: diagnostics {cd, msum} vs oracle {cd0, ms0}", flush=True)
                 ok = False
-                break
+                failed = True  # keep stepping in lockstep with the other ranks
         xs = x.index_select(1, idx).cpu().numpy()
         ms = m.index_select(1, idx).cpu().numpy()
         rows = slice(first, first + n_loc)
@@ -130,14 +138,16 @@ def main():
             m_ok = np.array_equal(ms, orc.m[lead:lead + 1])  # the replica equals its leader's
         if a.lars:  # norms in another fp64 order: rates within 1 ulp, params within 1e-6
             xs_ok = np.all(np.abs(xs - orc.x[rows]) <= 1e-6 * np.abs(orc.x[rows]).max(axis=1, keepdims=True))
-            m_ok = np.all(np.abs(ms - orc.m[rows]) <= 1e-5 * np.abs(orc.m[rows]).max(axis=1, keepdims=True))
+            # hierarchical members hold their leader's momentum (reading B-4)
+            mref = orc.m[lead:lead + 1] if (a.hier_groups and first % gs != 0) else orc.m[rows]
+            m_ok = np.all(np.abs(ms - mref) <= 1e-5 * np.abs(mref).max(axis=1, keepdims=True))
         else:
             xs_ok = np.array_equal(xs, orc.x[rows])
         if not (xs_ok and m_ok and np.array_equal(w.cpu().numpy(), orc.w[rows])):
             bad = np.argwhere(xs != orc.x[rows])
             print(f"rank {rank} step {t}: mismatch at {bad[:5].tolist()} of {bad.shape[0]}", flush=True)
             ok = False
-            break
+            failed = True  # keep stepping in lockstep with the other ranks
     okt = torch.tensor([1 if ok else 0], device=dev)
     dist.all_reduce(okt, op=dist.ReduceOp.MIN)
     if rank == 0:

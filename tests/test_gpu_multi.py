@@ -88,6 +88,22 @@ def test_two_gpu_layers_and_lars(layers, plan, lars, diag):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("groups,plan", [(1, True), (2, False)])
+def test_two_gpu_hierarchical_lars(groups, plan):
+    # LARS on the group-reduced gradient: one group (AllReduce-SGD + LARS) and
+    # two groups of one (leader gossip), with a layer table
+    args = ["--workers-per-gpu", 1, "--vector-len", 120_000, "--segments", 4, "--num-steps", 4, "--compare-all",
+            "--layers", 10, "--lars", "--hier-groups", groups] + (["--layer-plan"] if plan else [])
+    _run(2, *args)
+
+
+@pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
+def test_four_gpu_hierarchical_lars():
+    _run(4, "--workers-per-gpu", 1, "--vector-len", 200_000, "--segments", 6, "--num-steps", 4, "--compare-all",
+         "--layers", 14, "--lars", "--hier-groups", 2, "--layer-plan")
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("pieces", [3, 8])
 def test_two_gpu_pieces_bitwise(pieces):
     # push(p+1) / mix(p) overlap across the caller's and the aux stream, across GPUs
