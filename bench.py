@@ -234,9 +234,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None, choices=sorted(WORKLOADS))
-    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--segments", dest="k", type=int, default=None, help="segment count k (default: the config's)")
     ap.add_argument("--workers-per-gpu", type=int, default=None)
-    ap.add_argument("--d", type=int, default=None)
+    ap.add_argument("--vector-len", dest="d", type=int, default=None, help="parameters per worker (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--cpu-cols", type=int, default=1_000_000)
