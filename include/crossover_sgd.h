@@ -292,6 +292,16 @@ int cs_set_topology_kind(int kind);
  * Errors: CS_ENOTINIT, CS_EINVAL (unknown format). */
 int cs_set_wire(int format);
 
+/* Completes deferred work of earlier steps, enqueued on the bound stream (no host sync).
+ * On the multi-GPU push/mix schedule (one worker per GPU) the merge a5 of step t runs
+ * inside step t+1's push kernel, tile by tile, before that step's update; this removes
+ * a full pass and a cross-GPU wait per step.  Between the two, params hold step t's y
+ * and psw its pre-merge weights.  cs_flush, cs_sync, diagnostics, cs_set_step, cs_bind,
+ * cs_finalize, LARS and the hierarchical step complete a pending merge first.  Pass the
+ * same params/psw buffers to consecutive steps (other buffers flush first).
+ * CS_PEER_FUSE=0 in the environment disables the deferral.  Errors: CS_ENOTBOUND, CS_ECUDA. */
+int cs_flush(void);
+
 /* Set / read the step counter t (resume = restore buffers + cs_set_step). */
 int cs_set_step(int64_t step);
 int cs_get_step(int64_t* step_out);

@@ -56,6 +56,7 @@ _SIGS = {
     "cs_accumulate": (_c_int, [_vp, _vp, _c_int, _c_int]),
     "cs_set_topology_kind": (_c_int, [_c_int]),
     "cs_set_wire": (_c_int, [_c_int]),
+    "cs_flush": (_c_int, []),
     "cs_segment_plan": (_c_int, [_vp, _c_int, _c_int, _vp]),
     "cs_set_layers": (_c_int, [_vp, _c_int, _vp]),
     "cs_set_lars": (_c_int, [_c_f, _c_f, _c_f]),
@@ -244,6 +245,11 @@ def cs_set_wire(fmt: int) -> None:
 def cs_set_topology_kind(kind: int) -> None:
     """TOPO_CROSSOVER (Alg. 2, default) or TOPO_EXPONENTIAL (SGP's graph)."""
     _check(lib.cs_set_topology_kind(kind), "cs_set_topology_kind")
+
+
+def cs_flush() -> None:
+    """Complete deferred work (the multi-GPU deferred merge) on the bound stream."""
+    _check(lib.cs_flush(), "cs_flush")
 
 
 def cs_set_step(step: int) -> None:

@@ -133,6 +133,13 @@ int next_event_pair(cudaEvent_t* ev) {
   return CS_OK;
 }
 
+// Completes a deferred merge of the multi-GPU push/mix schedule (see cs_flush).
+int flush_pending() {
+  if (!g.bound || !g.use_peer) return CS_OK;
+  const int rc = peer_flush(g.peer, g.stream);
+  return rc ? fail(rc, "%s", peer_error()) : CS_OK;
+}
+
 void free_device() {
   auto f = [](void* p) { if (p) cudaFree(p); };
   f(g.d_bounds); f(g.d_src); f(g.d_dst); f(g.d_ord); f(g.d_given); f(g.d_rw);
@@ -453,6 +460,7 @@ int cs_init(int world, int groups, int k_segments, uint64_t seed) {
 
 void cs_finalize(void) {
   if (g.bound) {
+    flush_pending();
     cudaStreamSynchronize(g.stream);
     free_device();
   }
@@ -511,6 +519,7 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
   if ((d + kQuantum - 1) / kQuantum < g.k)
     return fail(CS_EINVAL_SEGMENTS, "k %d > ceil(d/32) = %lld", g.k, (long long)((d + 31) / 32));
   if (g.bound) {
+    flush_pending();
     cudaStreamSynchronize(g.stream);
     free_device();
     g.bound = false;
@@ -574,6 +583,7 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
 
 int cs_set_wire(int format) {
   if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (int rc = flush_pending()) return rc;  // a pending merge reads the inbox in the current format
   if (format != CS_WIRE_FP32 && format != CS_WIRE_BF16) return fail(CS_EINVAL, "unknown wire format %d", format);
   g.wire = format;
   return CS_OK;
@@ -642,6 +652,7 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
     if (rc) return rc;
     if (g.lars) {  // per-(worker, layer) rates from this step's x and g, over the peer tiles
       if (ev[0]) CS_CUDA(cudaEventRecord(ev[0], g.stream));  // the timed pair covers the rates
+      if ((rc = flush_pending()) != CS_OK) return rc;        // the norms need the merged x
       ev[0] = nullptr;
       CS_CUDA(launch_lars_rates(params, grads, g.ld, peer_tiles(g.peer), peer_tile_count(g.peer), g.n_loc,
                                 g.d_tile_first, g.n_layers, g.d_lars_part, lr, g.lars_eta, g.lars_wd,
@@ -654,14 +665,17 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
     rc = peer_flat_step(g.peer, pa, g.stream, ev[0], ev[1]);
     if (rc) return fail(rc, "%s", peer_error());
     if (diag) {
+      if ((rc = flush_pending()) != CS_OK) return rc;  // diagnostics of the merged x'
       rc = peer_diag(g.peer, pa, g.d_partials, local_max_grid(), g.d_diag, g.stream);
       if (rc) return fail(rc, "%s", peer_error());
     }
     const bool fused_topo = g.world <= 64;  // the topology is drawn inside the first kernel
-    g.launches_per_step = (fused_topo ? 2 : 3) + (g.lars ? 2 : 0);
-    g.hot_kernel = g.peer.use_hybrid ? "k_hyb_walk+k_hyb_tail"
-                   : g.lars          ? "k_lars_norms+k_lars_scale+k_peer_push+k_peer_mix"
-                                     : "k_peer_push+k_peer_mix";
+    // deferred merge: one push launch per step (its merge runs in the next push / cs_flush)
+    g.launches_per_step = (g.peer.last_fused ? 1 : 2) + (fused_topo ? 0 : 1) + (g.lars ? 2 : 0);
+    g.hot_kernel = g.peer.use_hybrid  ? "k_hyb_walk+k_hyb_tail"
+                   : g.lars           ? "k_lars_norms+k_lars_scale+k_peer_push+k_peer_mix"
+                   : g.peer.last_fused ? "k_peer_push(fused merge)"
+                                       : "k_peer_push+k_peer_mix";
   }
   if (rc) return rc;
   if (diag) g.diag_valid = true;
@@ -709,6 +723,7 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
     if (g.n_loc != 1)
       return fail(CS_EUNSUPPORTED, "multi-GPU hierarchical step needs one worker per GPU (world == nprocs)");
     if (!g.peer.imported) return fail(CS_ENOTBOUND, "multi-GPU: cs_ipc_import has not been called");
+    if ((rc = flush_pending()) != CS_OK) return rc;
     PeerStepArgs pa = peer_args(params, grads, psw, lr, momentum);
     if (g.lars) {  // rates from the leader replica's x and the group mean
       pa.lrs_out = g.d_lrs;
@@ -805,6 +820,7 @@ int cs_segment_plan(const int64_t* layer_sizes, int n_layers, int k, int32_t* se
 int cs_set_layers(const int64_t* layer_bounds, int n_layers, const int32_t* seg_of_layer) {
   int rc = check_bound();
   if (rc) return rc;
+  if ((rc = flush_pending()) != CS_OK) return rc;  // the tiles change
   if (!layer_bounds || n_layers == 0) {  // clear: back to the equal split, no layers
     g.layer_bounds.clear();
     g.n_layers = 0;
@@ -908,9 +924,17 @@ int cs_accumulate(float* acc, const float* grads, int count, int interval) {
   return CS_OK;
 }
 
+int cs_flush(void) {
+  int rc = check_bound();
+  if (rc) return rc;
+  return flush_pending();
+}
+
 int cs_set_step(int64_t step) {
   if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
   if (step < 0 || step >= (int64_t(1) << 32)) return fail(CS_EINVAL, "step outside [0, 2^32)");
+  int rc = flush_pending();
+  if (rc) return rc;
   g.step = step;
   g.peer.need_sync = true;  // resumed state: re-replicate leaders to members on the next hier step
   return CS_OK;
@@ -947,6 +971,7 @@ int cs_get_diag(double* cd_out, double* mean_out) {
 int cs_sync(void) {
   int rc = check_bound();
   if (rc) return rc;
+  if ((rc = flush_pending()) != CS_OK) return rc;
   CS_CUDA(cudaStreamSynchronize(g.stream));
   CS_CUDA(cudaGetLastError());
   return poll_device_errors();

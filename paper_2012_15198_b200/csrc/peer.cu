@@ -142,6 +142,8 @@ struct PeerKernelArgs {
   uint32_t done_target;     // arrival targets (see publish_when_last)
   uint32_t pdone_target;
   int final_only;           // hierarchical with one group: x = y, no exchange
+  int fuse_mix;             // x holds y of epoch-1 and the inbox its received half: apply that
+                            // step's merge x = (y + inbox)/2 (and psw) before this update
   int fused_topo;           // draw the topology in the push prologue (<= 64 ranks)
   size_t off_inbox, off_wbox, off_done, off_count, off_pdone, off_pcount, off_d2;
 };
@@ -260,6 +262,9 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
   extern __shared__ __align__(128) float smem_f[];
   float* ringA = smem_f;                                     // [kStagesA][3][kPeerTile]
   float* ringY = ringA + (size_t)kStagesA * 3 * kPeerTile;   // [kSlotsY][kPeerTile]
+  // fused merge: the ring holds x, m, g and the previous step's inbox tile, 2 stages deep
+  // (the same 9-tile region; 2 x 4 = 8 tiles)
+  const int NS = a.fuse_mix ? 2 : kStagesA, NA = a.fuse_mix ? 4 : 3;
   __shared__ uint64_t a_full[kStagesA], a_empty[kStagesA], y_full[kSlotsY], y_empty[kSlotsY];
   __shared__ int s_timeout;
   const PeerStepArgs& s = a.s;
@@ -306,6 +311,10 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
       const uint32_t* d2 = reinterpret_cast<const uint32_t*>(mine + a.off_d2);
       const int gbase = (s.rank / s.gs) * s.gs;
       if (!wait_acquire(d2 + gbase + lane, e)) atomicOr(&s_timeout, 1);
+    }
+    if (a.fuse_mix && lane < s.nprocs) {  // every GPU's pushes of epoch e-1 have landed here
+      const uint32_t* pd = reinterpret_cast<const uint32_t*>(mine + a.off_pdone);
+      if (!wait_acquire(pd + lane, e - 1)) atomicOr(&s_timeout, 1);
     }
     __syncwarp();
   } else {
@@ -358,10 +367,10 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
     int cur = 0;
     for (int i = 0; i < n_my && !*timeout; ++i) {
       const Unit U = unit_at(a, M, u_lo + blockIdx.x + i * G, cur);
-      const int st = i % kStagesA, sy = i % kSlotsY;
-      ptx::mbar_wait(&a_full[st], (uint32_t)((i / kStagesA) & 1));
+      const int st = i % NS, sy = i % kSlotsY;
+      ptx::mbar_wait(&a_full[st], (uint32_t)((i / NS) & 1));
       if (!a.final_only) ptx::mbar_wait(&y_empty[sy], (uint32_t)(((i / kSlotsY) & 1) ^ 1));
-      const float* bx = ringA + (size_t)st * 3 * kPeerTile;
+      const float* bx = ringA + (size_t)st * NA * kPeerTile;
       float4* yt = reinterpret_cast<float4*>(ringY + (size_t)sy * kPeerTile);
       const int64_t rowoff = (int64_t)U.r * s.ld;
 #pragma unroll
@@ -370,9 +379,11 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
         const int valid = U.len - 4 * v;
         if (valid > 0) {
           const int vv = valid < 4 ? valid : 4;
-          const float4 cx = reinterpret_cast<const float4*>(bx)[v];
+          float4 cx = reinterpret_cast<const float4*>(bx)[v];
           const float4 cm = reinterpret_cast<const float4*>(bx + kPeerTile)[v];
           const float4 cg = reinterpret_cast<const float4*>(bx + 2 * kPeerTile)[v];
+          if (a.fuse_mix)  // the previous step's a5: x = (y + received y) / 2 (Alg.1 l.17)
+            cx = mean4(cx, reinterpret_cast<const float4*>(bx + 3 * kPeerTile)[v]);
           bad |= nonfinite4(cg);
           // LARS (C-18): m' = mu*m + (g + wd*x), y = x - lrs[r][layer]*m'
           const float4 mn = mom4(cm, s.lrs ? decay4(cg, cx, s.wd) : cg, s.mu);
@@ -393,7 +404,11 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
           int rp, rl;
           receiver_of(a, M, U.seg, U.r, rp, rl);
           float* wbox = reinterpret_cast<float*>(a.peers[rp] + a.off_wbox) + ((int64_t)par * s.n_loc + rl) * s.k;
-          wbox[U.seg] = s.psw[(int64_t)U.r * s.k + U.seg];
+          const float wv = s.psw[(int64_t)U.r * s.k + U.seg];
+          // fused merge: the weight this worker holds after the previous step's merge
+          wbox[U.seg] = a.fuse_mix ? pair_mean1(wv, __ldcg(reinterpret_cast<const float*>(mine + a.off_wbox) +
+                                                           ((int64_t)(par ^ 1) * s.n_loc + U.r) * s.k + U.seg))
+                                   : wv;
         }
         ptx::fence_proxy_async_shared();  // y tile -> the TMA engine's reads
       }
@@ -411,15 +426,19 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
       int cur = 0;
       for (int i = 0; i < n_my && !*timeout; ++i) {
         const Unit U = unit_at(a, M, u_lo + blockIdx.x + i * G, cur);
-        const int st = i % kStagesA;
-        ptx::mbar_wait(&a_empty[st], (uint32_t)(((i / kStagesA) & 1) ^ 1));
+        const int st = i % NS;
+        ptx::mbar_wait(&a_empty[st], (uint32_t)(((i / NS) & 1) ^ 1));
         const uint32_t bytes = (uint32_t)(((U.len + 3) & ~3) * 4);
         const int64_t off = (int64_t)U.r * s.ld + U.c0;
-        float* buf = ringA + (size_t)st * 3 * kPeerTile;
-        ptx::mbar_arrive_expect_tx(&a_full[st], 3 * bytes);
+        float* buf = ringA + (size_t)st * NA * kPeerTile;
+        ptx::mbar_arrive_expect_tx(&a_full[st], NA * bytes);
         ptx::bulk_g2s(buf, s.x + off, bytes, &a_full[st]);
         ptx::bulk_g2s(buf + kPeerTile, s.m + off, bytes, &a_full[st]);
         ptx::bulk_g2s(buf + 2 * kPeerTile, s.g + off, bytes, &a_full[st]);
+        if (a.fuse_mix)  // the previous step's received tile (inbox parity of epoch e-1)
+          ptx::bulk_g2s(buf + 3 * kPeerTile,
+                        reinterpret_cast<const float*>(mine + a.off_inbox) + (int64_t)(par ^ 1) * s.n_loc * s.ld + off,
+                        bytes, &a_full[st]);
       }
     }
     __syncwarp();
@@ -453,6 +472,33 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
     __syncwarp();
   }
   __syncthreads();
+  if (a.fuse_mix) {
+    // the last CTA: every CTA has read psw and the previous inbox.  Store the previous step's
+    // merged weights, then publish this step's pushes (pdone = e) and the consumption of the
+    // previous inbox (done = e - 1, the flag the senders' ping-pong wait reads)
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+      if (s_timeout) atomicOr(s.err + kErrTimeout, 1);
+      __threadfence();
+      const uint32_t prev = atomicAdd(reinterpret_cast<uint32_t*>(mine + a.off_pcount), 1u);
+      s_last = prev + 1 == a.pdone_target;
+    }
+    __syncthreads();
+    if (s_last) {
+      const float* wprev = reinterpret_cast<const float*>(mine + a.off_wbox) + (int64_t)(par ^ 1) * s.n_loc * s.k;
+      for (int i = threadIdx.x; i < s.n_loc * s.k; i += blockDim.x)
+        s.psw[i] = pair_mean1(s.psw[i], __ldcg(wprev + i));
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int q = 0; q < s.nprocs; ++q) {
+          ptx::st_release_sys(reinterpret_cast<uint32_t*>(a.peers[q] + a.off_pdone) + s.rank, e);
+          ptx::st_release_sys(reinterpret_cast<uint32_t*>(a.peers[q] + a.off_done) + s.rank, e - 1);
+        }
+      }
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     if (s_timeout) atomicOr(s.err + kErrTimeout, 1);
     if (a.final_only)  // nothing to exchange: this step is complete, for every piece
@@ -1380,6 +1426,8 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
     if (HP > PeerState::kMaxPieces) HP = PeerState::kMaxPieces;
     if (HP > p.n_tiles) HP = p.n_tiles;
     p.hier_pieces = HP;
+    const char* fz = getenv("CS_PEER_FUSE");
+    p.fuse = !(fz && fz[0] == '0');
     p.piece_tile.resize(P + 1);
     for (int q = 0; q <= P; ++q) p.piece_tile[q] = (int)((int64_t)q * p.n_tiles / P);
     int lo = 0, hi = 0;
@@ -1469,6 +1517,7 @@ PeerKernelArgs kernel_args(const PeerState& p, const PeerStepArgs& a, uint32_t e
   ka.n_tiles = p.n_tiles;
   ka.epoch = epoch;
   ka.final_only = final_only ? 1 : 0;
+  ka.fuse_mix = 0;
   ka.fused_topo = fused_topo_ok(a.gs > 0 ? a.groups : a.world, a.k, a.n_loc) ? 1 : 0;
   ka.off_inbox = p.off_inbox;
   ka.off_wbox = p.off_wbox;
@@ -1630,6 +1679,7 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
                    cudaEvent_t ev1) {
   int rc = CS_OK;
   if (p.use_hybrid) {
+    p.last_fused = false;
     const bool fused = a.world <= 64;
     if (!fused && a.given == nullptr) rc = launch_topology_for(a, a.world, CS_TAG_FLAT, st);
     if (rc) return rc;
@@ -1678,14 +1728,53 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "hybrid launch", e);
   }
+  // deferred merge: this step's push applies the previous step's merge tile by tile, and
+  // its own merge waits for the next push (or peer_flush); the separate mix pass and its
+  // cross-GPU wait disappear from the step
+  const bool fuse = p.fuse && p.pieces == 1 && !a.wire && a.lrs == nullptr;
+  p.last_fused = fuse;
+  if (ev0) cudaEventRecord(ev0, st);
+  if (!fuse || (p.pending && (p.pending_args.x != a.x || p.pending_args.psw != a.psw))) {
+    rc = peer_flush(p, st);
+    if (rc) return rc;
+  }
   if (!fused_topo_ok(a.world, a.k, a.n_loc)) rc = launch_topology_for(a, a.world, CS_TAG_FLAT, st);
   if (rc) return rc;
   PeerKernelArgs ka = kernel_args(p, a, ++p.epoch, false);
   ka.s.gs = 0;
-  if (ev0) cudaEventRecord(ev0, st);
-  rc = launch_push_mix(p, ka, st);
+  if (fuse) {
+    ka.fuse_mix = p.pending != 0 ? 1 : 0;
+    ka.tile_lo = 0;
+    ka.tile_hi = p.n_tiles;
+    ka.col_lo = 0;
+    ka.col_hi = p.d;
+    const int units = p.n_tiles * a.n_loc;
+    const int grid = p.grid_push < units ? p.grid_push : (units > 0 ? units : 1);
+    ka.pdone_target = (p.tot_pcount[0] += (uint32_t)grid);
+    k_peer_push<<<grid, kPushThreads, push_smem_bytes(a.k, a.n_loc), st>>>(ka);
+    p.pending = ka.epoch;
+    p.pending_args = ka.s;
+    rc = cudaGetLastError() == cudaSuccess ? CS_OK : perr(CS_ECUDA, "fused push launch", cudaGetLastError());
+  } else {
+    rc = launch_push_mix(p, ka, st);
+  }
   if (ev1) cudaEventRecord(ev1, st);
   return rc;
+}
+
+int peer_flush(PeerState& p, cudaStream_t st) {
+  if (!p.pending) return CS_OK;
+  PeerKernelArgs ka = kernel_args(p, p.pending_args, p.pending, false);
+  ka.s.gs = 0;
+  ka.tile_lo = 0;
+  ka.tile_hi = p.n_tiles;
+  ka.col_lo = 0;
+  ka.col_hi = p.d;
+  ka.done_target = (p.tot_count[0] += (uint32_t)p.grid_mix);
+  k_peer_mix<<<p.grid_mix, kMixThreads, 0, st>>>(ka);
+  p.pending = 0;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "deferred merge launch", e);
 }
 
 // Debug knob CS_PHASE_TIMING=1: events between the hierarchical kernels; the per-phase

@@ -89,6 +89,12 @@ struct PeerState {
   uint32_t tot_dc1 = 0, tot_dc2 = 0, diag_epoch = 0;
   // hybrid flat step (several workers per GPU): local cycle walk + NVLink chain heads
   bool use_hybrid = false;
+  // deferred merge (CS_PEER_FUSE, default on; push/mix schedule): the merge of step `pending`
+  // runs inside the next step's push kernel, or in peer_flush
+  bool fuse = false;
+  uint32_t pending = 0;
+  bool last_fused = false;   // the last flat step ran as one fused push launch
+  PeerStepArgs pending_args{};
   // layer table (cs_set_layers, one worker per GPU): explicit tiles split at segment and
   // layer bounds; nullptr = the closed-form equal split of kPeerTile tiles
   struct TileDesc* d_ptiles = nullptr;
@@ -115,6 +121,8 @@ int peer_set_layers(PeerState& p, const std::vector<int64_t>& plan, const std::v
                     std::vector<int32_t>& tile_first);
 const struct TileDesc* peer_tiles(const PeerState& p);
 int peer_tile_count(const PeerState& p);
+// Completes a deferred merge (no-op if none is pending).
+int peer_flush(PeerState& p, cudaStream_t st);
 int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEvent_t ev0,
                    cudaEvent_t ev1);
 // diagnostics of the current state (after a step), all GPUs; out: device double[2]

@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--layers", type=int, default=0, help="random layer table with this many layers")
     ap.add_argument("--layer-plan", action="store_true", help="segments from the layer plan (cs_segment_plan)")
     ap.add_argument("--lars", action="store_true", help="LARS (Table 1 constants, lr 9)")
+    ap.add_argument("--sync-at-end", action="store_true",
+                    help="no cs_sync between steps (deferred merges run inside the next push); compare at the end")
     a = ap.parse_args()
     rank, ws, lr_ = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(lr_)
@@ -119,6 +121,8 @@ def main():
         else:
             orc.step(lr, mu, src=exponential_topology(t, world, k) if a.exponential else None,
                      wire="bf16" if a.wire_bf16 else None)
+        if a.sync_at_end and t < a.num_steps - 1:
+            continue
         cs.cs_sync()
         if a.diag:
             cd, msum = cs.cs_get_diag()

@@ -104,6 +104,18 @@ def test_four_gpu_hierarchical_lars():
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("n_loc,d,k,extra", [(1, 100_003, 3, []), (1, 25_557_032, 8, []), (3, 60_001, 4, []),
+                                             (1, 50_001, 2, ["--exponential"])])
+def test_two_gpu_deferred_merge_bitwise(n_loc, d, k, extra):
+    # no cs_sync between steps: each step's merge runs inside the next step's push kernel
+    # (push/mix schedule; n_loc > 1 with the hybrid walk off), flushed by the final cs_sync
+    args = ["--workers-per-gpu", n_loc, "--vector-len", d, "--segments", k, "--num-steps", 7, "--sync-at-end"]
+    if d < 1_000_000:
+        args.append("--compare-all")
+    _run(2, *args, *extra, env={"CS_PEER_HYBRID": "0"})
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("pieces", [3, 8])
 def test_two_gpu_pieces_bitwise(pieces):
     # push(p+1) / mix(p) overlap across the caller's and the aux stream, across GPUs
