@@ -672,7 +672,7 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
     const bool fused_topo = g.world <= 64;  // the topology is drawn inside the first kernel
     // deferred merge: one push launch per step (its merge runs in the next push / cs_flush)
     g.launches_per_step = (g.peer.last_fused ? 1 : 2) + (fused_topo ? 0 : 1) + (g.lars ? 2 : 0);
-    g.hot_kernel = g.peer.use_hybrid  ? "k_hyb_walk+k_hyb_tail"
+    g.hot_kernel = g.peer.use_hybrid  ? (g.peer.last_fused ? "k_hyb_walk(fused tail merge)" : "k_hyb_walk+k_hyb_tail")
                    : g.lars           ? "k_lars_norms+k_lars_scale+k_peer_push+k_peer_mix"
                    : g.peer.last_fused ? "k_peer_push(fused merge)"
                                        : "k_peer_push+k_peer_mix";

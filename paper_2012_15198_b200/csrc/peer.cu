@@ -745,7 +745,7 @@ constexpr int kHMaxTable = 2048;  // k * n_loc
 
 size_t hyb_smem_bytes(int k, int n_loc) {
   return kHStages * kHStageBytes + sizeof(uint32_t) * 2 * (size_t)k * n_loc +
-         sizeof(uint32_t) * 192 * (kHThreads / 32);
+         sizeof(uint32_t) * 192 * (kHThreads / 32) + sizeof(float) * (size_t)k * n_loc + (size_t)k * n_loc;
 }
 
 struct HybArgs {
@@ -770,6 +770,10 @@ struct HybArgs {
   uint8_t* tail_tbl;        // [k][n_loc]: 1 = the worker's segment source is remote
   int* err;
   int wire;                 // bf16 wire format (reading C-20)
+  // deferred merge: the previous step's chain tails (tail_prev, its [k][n_loc] table) are
+  // merged with the previous inbox inside this walk, and this step's tails wait for the next
+  int fuse;
+  const uint8_t* tail_prev;
 };
 
 __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
@@ -778,6 +782,10 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
   uint32_t* ord = reinterpret_cast<uint32_t*>(smem_raw + kHStages * kHStageBytes);  // [k][n_loc]
   int32_t* head_dst = reinterpret_cast<int32_t*>(ord + a.k * a.n_loc);             // [k][n_loc]
   uint32_t* scratch = reinterpret_cast<uint32_t*>(head_dst + a.k * a.n_loc);         // [warps][192]
+  float* cur_w = reinterpret_cast<float*>(scratch + 192 * (kHThreads / 32));         // [k][n_loc]
+  uint8_t* tprev = reinterpret_cast<uint8_t*>(cur_w + a.k * a.n_loc);               // [k][n_loc]
+  // deferred merge: 3 stages of x, m, g and the previous inbox tile (the same 12-tile region)
+  const int NS = a.fuse ? 3 : kHStages, NA = a.fuse ? 4 : 3;
   __shared__ uint64_t full[kHStages], empty[kHStages];
   __shared__ int s_timeout;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -866,6 +874,23 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
     if (!wait_acquire(done + threadIdx.x, a.epoch - 2)) atomicOr(&s_timeout, 1);
   }
   __syncthreads();
+  // the weights each worker holds now: after the previous step's deferred tail merges
+  if (a.fuse && threadIdx.x < a.nprocs) {  // every GPU's pushes of epoch e-1 have landed here
+    const uint32_t* pd = reinterpret_cast<const uint32_t*>(mine + a.off_pdone);
+    if (!wait_acquire(pd + threadIdx.x, a.epoch - 1)) atomicOr(&s_timeout, 1);
+  }
+  __syncthreads();
+  ptx::fence_proxy_async_global();  // the acquired inbox tiles -> the producer's bulk copies
+  for (int i = threadIdx.x; i < a.k * n_loc; i += blockDim.x) {
+    const int sg = i / n_loc, r = i - sg * n_loc;
+    const uint8_t tp = a.fuse ? a.tail_prev[i] : 0;
+    const float w = a.psw[(int64_t)r * a.k + sg];
+    tprev[i] = tp;
+    cur_w[i] = tp ? pair_mean1(w, __ldcg(reinterpret_cast<const float*>(mine + a.off_wbox) +
+                                         ((int64_t)(par ^ 1) * n_loc + r) * a.k + sg))
+                  : w;
+  }
+  __syncthreads();
   // push-sum weights of the chain heads go with their y (reading C-11)
   if (blockIdx.x == 0 && !*timeout)
     for (int i = threadIdx.x; i < a.k * n_loc; i += blockDim.x) {
@@ -877,8 +902,7 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
         if ((o[pp] & kHIdx) == (uint32_t)r && (o[pp] & kHHead)) head = true;
       if (!head) continue;
       const int rp = dg / n_loc, rl = dg - rp * n_loc;
-      reinterpret_cast<float*>(a.peers[rp] + a.off_wbox)[((int64_t)par * n_loc + rl) * a.k + sg] =
-          a.psw[(int64_t)r * a.k + sg];
+      reinterpret_cast<float*>(a.peers[rp] + a.off_wbox)[((int64_t)par * n_loc + rl) * a.k + sg] = cur_w[i];
     }
 
   const int64_t ld = a.ld;
@@ -891,14 +915,20 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
         const uint32_t bytes = (uint32_t)(((td.len + 3) & ~3) * sizeof(float));
         const uint32_t* o = ord + td.seg * n_loc;
         for (int p = 0; p < n_loc; ++p, ++it) {
-          const int st = (int)(it % kHStages);
-          ptx::mbar_wait(&empty[st], ((it / kHStages) & 1u) ^ 1u);
-          const int64_t off = (int64_t)(o[p] & kHIdx) * ld + td.c0;
-          float* buf = stage_buf + (size_t)st * 3 * kTmaTileMax;
-          ptx::mbar_arrive_expect_tx(&full[st], 3 * bytes);
+          const int st = (int)(it % NS);
+          ptx::mbar_wait(&empty[st], ((it / NS) & 1u) ^ 1u);
+          const uint32_t row = o[p] & kHIdx;
+          const int64_t off = (int64_t)row * ld + td.c0;
+          float* buf = stage_buf + (size_t)st * NA * kTmaTileMax;
+          const bool merge = tprev[td.seg * n_loc + row];
+          ptx::mbar_arrive_expect_tx(&full[st], (merge ? 4 : 3) * bytes);
           ptx::bulk_g2s(buf, a.x + off, bytes, &full[st]);
           ptx::bulk_g2s(buf + kTmaTileMax, a.m + off, bytes, &full[st]);
           ptx::bulk_g2s(buf + 2 * kTmaTileMax, a.g + off, bytes, &full[st]);
+          if (merge)  // the previous step's received y of this tail row
+            ptx::bulk_g2s(buf + 3 * kTmaTileMax,
+                          reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)(par ^ 1) * n_loc) * ld + off,
+                          bytes, &full[st]);
         }
       }
     }
@@ -913,11 +943,12 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
       float4 yfirst[kHVPT], yprev[kHVPT];
       uint32_t prev_row = 0;
       for (int p = 0; p < n_loc; ++p, ++it) {
-        const int st = (int)(it % kHStages);
-        ptx::mbar_wait(&full[st], (it / kHStages) & 1u);
-        const float* buf = stage_buf + (size_t)st * 3 * kTmaTileMax;
+        const int st = (int)(it % NS);
+        ptx::mbar_wait(&full[st], (it / NS) & 1u);
+        const float* buf = stage_buf + (size_t)st * NA * kTmaTileMax;
         const uint32_t e = o[p];
         const uint32_t row = e & kHIdx;
+        const bool merge = tprev[td.seg * n_loc + row];
         float* inbox = nullptr;
         uint16_t* inboxw = nullptr;
         if (e & kHHead) {
@@ -933,9 +964,11 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
           const int valid = td.len - 4 * v;
           if (valid > 0) {
             const int vv = valid < 4 ? valid : 4;
-            const float4 cx = reinterpret_cast<const float4*>(buf)[v];
+            float4 cx = reinterpret_cast<const float4*>(buf)[v];
             const float4 cm = reinterpret_cast<const float4*>(buf + kTmaTileMax)[v];
             const float4 cg = reinterpret_cast<const float4*>(buf + 2 * kTmaTileMax)[v];
+            if (merge)  // the previous step's a5 for this chain tail (Alg.1 l.17)
+              cx = mean4(cx, reinterpret_cast<const float4*>(buf + 3 * kTmaTileMax)[v]);
             bad |= nonfinite4(cg);
             const float4 mn = mom4(cm, cg, a.mu);
             const float4 y = sgd4(cx, mn, a.lr);
@@ -990,18 +1023,22 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
       } else {
         srcl = (int)(o[pos + 1] & kHIdx);
       }
-      reinterpret_cast<float*>(stage_buf)[i] = pair_mean1(a.psw[(int64_t)r * a.k + sg], a.psw[(int64_t)srcl * a.k + sg]);
+      reinterpret_cast<float*>(stage_buf)[i] = pair_mean1(cur_w[i], cur_w[sg * n_loc + srcl]);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < a.k * n_loc; i += blockDim.x) {
       const int sg = i / n_loc, r = i - sg * n_loc;
-      if (!a.tail_tbl[sg * n_loc + r]) a.psw[(int64_t)r * a.k + sg] = reinterpret_cast<const float*>(stage_buf)[i];
+      // tails of this step keep their current weight; their merge comes with the next step
+      a.psw[(int64_t)r * a.k + sg] = a.tail_tbl[sg * n_loc + r] ? cur_w[i] : reinterpret_cast<const float*>(stage_buf)[i];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence_system();
-      for (int p = 0; p < a.nprocs; ++p)
+      for (int p = 0; p < a.nprocs; ++p) {
         ptx::st_release_sys(reinterpret_cast<uint32_t*>(a.peers[p] + a.off_pdone) + a.rank, a.epoch);
+        if (a.fuse)  // the previous inbox is consumed
+          ptx::st_release_sys(reinterpret_cast<uint32_t*>(a.peers[p] + a.off_done) + a.rank, a.epoch - 1);
+      }
     }
   }
 }
@@ -1402,7 +1439,7 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
     e = cudaMalloc(&p.d_htiles, sizeof(TileDesc) * tiles.size());
     if (e == cudaSuccess)
       e = cudaMemcpy(p.d_htiles, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&p.d_tail_tbl, (size_t)k * n_loc);
+    if (e == cudaSuccess) e = cudaMalloc(&p.d_tail_tbl, 2 * (size_t)k * n_loc);  // by step parity
     if (e != cudaSuccess) return perr(CS_ECUDA, "hybrid tables", e);
   }
   // pieces per step (CS_PEER_PIECES)
@@ -1675,55 +1712,83 @@ int launch_push_mix(PeerState& p, const PeerKernelArgs& ka, cudaStream_t st) {
 
 }  // namespace
 
+namespace {
+HybArgs hyb_args(const PeerState& p, const PeerStepArgs& a, uint32_t epoch) {
+  HybArgs h;
+  h.x = a.x;
+  h.m = a.m;
+  h.g = a.g;
+  h.psw = a.psw;
+  h.ld = a.ld;
+  h.d = a.d;
+  h.nq = a.nq;
+  h.k = a.k;
+  h.world = a.world;
+  h.n_loc = a.n_loc;
+  h.first = a.first;
+  h.rank = a.rank;
+  h.nprocs = a.nprocs;
+  h.seed = a.seed;
+  h.step = a.step;
+  h.given = a.given;
+  h.wire = a.wire;
+  h.src_tbl = a.src;
+  h.fused = a.world <= 64 ? 1 : 0;
+  h.lr = a.lr;
+  h.mu = a.mu;
+  h.tiles = p.d_htiles;
+  h.n_tiles = p.n_htiles;
+  h.peers = p.d_peer_base;
+  h.off_inbox = p.off_inbox;
+  h.off_wbox = p.off_wbox;
+  h.off_done = p.off_done;
+  h.off_pdone = p.off_pdone;
+  h.off_count = p.off_count;
+  h.off_pcount = p.off_pcount;
+  h.flag_stride = p.flag_stride;
+  h.pieces = p.pieces;
+  h.epoch = epoch;
+  h.pdone_target = 0;
+  h.done_target = 0;
+  h.tail_tbl = nullptr;
+  h.err = a.err;
+  h.fuse = 0;
+  h.tail_prev = nullptr;
+  return h;
+}
+}  // namespace
+
 int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEvent_t ev0,
                    cudaEvent_t ev1) {
   int rc = CS_OK;
   if (p.use_hybrid) {
-    p.last_fused = false;
+    // deferred merge: this step's chain tails are merged inside the next walk (or
+    // peer_flush); the previous step's tails are merged here before their update
+    const bool fuse = p.fuse && !a.wire;
+    p.last_fused = fuse;
+    if (ev0) cudaEventRecord(ev0, st);
+    if (!fuse || (p.pending && (p.pending_args.x != a.x || p.pending_args.psw != a.psw))) {
+      rc = peer_flush(p, st);
+      if (rc) return rc;
+    }
     const bool fused = a.world <= 64;
     if (!fused && a.given == nullptr) rc = launch_topology_for(a, a.world, CS_TAG_FLAT, st);
     if (rc) return rc;
-    HybArgs h;
-    h.x = a.x;
-    h.m = a.m;
-    h.g = a.g;
-    h.psw = a.psw;
-    h.ld = a.ld;
-    h.d = a.d;
-    h.nq = a.nq;
-    h.k = a.k;
-    h.world = a.world;
-    h.n_loc = a.n_loc;
-    h.first = a.first;
-    h.rank = a.rank;
-    h.nprocs = a.nprocs;
-    h.seed = a.seed;
-    h.step = a.step;
-    h.given = a.given;
-    h.wire = a.wire;
-    h.src_tbl = a.src;
-    h.fused = fused ? 1 : 0;
-    h.lr = a.lr;
-    h.mu = a.mu;
-    h.tiles = p.d_htiles;
-    h.n_tiles = p.n_htiles;
-    h.peers = p.d_peer_base;
-    h.off_inbox = p.off_inbox;
-    h.off_wbox = p.off_wbox;
-    h.off_done = p.off_done;
-    h.off_pdone = p.off_pdone;
-    h.off_count = p.off_count;
-    h.off_pcount = p.off_pcount;
-    h.flag_stride = p.flag_stride;
-    h.pieces = p.pieces;
-    h.epoch = ++p.epoch;
+    HybArgs h = hyb_args(p, a, ++p.epoch);
+    const size_t tbl = (size_t)a.k * a.n_loc;
+    h.tail_tbl = p.d_tail_tbl + (h.epoch & 1u) * tbl;
     h.pdone_target = (p.tot_pcount[0] += (uint32_t)p.grid_hyb);
-    h.done_target = (p.tot_count[0] += (uint32_t)p.grid_tail);
-    h.tail_tbl = p.d_tail_tbl;
-    h.err = a.err;
-    if (ev0) cudaEventRecord(ev0, st);
-    k_hyb_walk<<<p.grid_hyb, kHThreads, hyb_smem_bytes(a.k, a.n_loc), st>>>(h);
-    k_hyb_tail<<<p.grid_tail, 256, 0, st>>>(h);
+    if (fuse) {
+      h.fuse = p.pending ? 1 : 0;
+      h.tail_prev = p.d_tail_tbl + ((h.epoch - 1) & 1u) * tbl;
+      k_hyb_walk<<<p.grid_hyb, kHThreads, hyb_smem_bytes(a.k, a.n_loc), st>>>(h);
+      p.pending = h.epoch;
+      p.pending_args = a;
+    } else {
+      h.done_target = (p.tot_count[0] += (uint32_t)p.grid_tail);
+      k_hyb_walk<<<p.grid_hyb, kHThreads, hyb_smem_bytes(a.k, a.n_loc), st>>>(h);
+      k_hyb_tail<<<p.grid_tail, 256, 0, st>>>(h);
+    }
     if (ev1) cudaEventRecord(ev1, st);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "hybrid launch", e);
@@ -1764,6 +1829,15 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
 
 int peer_flush(PeerState& p, cudaStream_t st) {
   if (!p.pending) return CS_OK;
+  if (p.use_hybrid) {  // the pending step's chain tails: x = (y + inbox)/2, psw likewise
+    HybArgs h = hyb_args(p, p.pending_args, p.pending);
+    h.tail_tbl = p.d_tail_tbl + (p.pending & 1u) * (size_t)p.pending_args.k * p.pending_args.n_loc;
+    h.done_target = (p.tot_count[0] += (uint32_t)p.grid_tail);
+    k_hyb_tail<<<p.grid_tail, 256, 0, st>>>(h);
+    p.pending = 0;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "deferred tail merge launch", e);
+  }
   PeerKernelArgs ka = kernel_args(p, p.pending_args, p.pending, false);
   ka.s.gs = 0;
   ka.tile_lo = 0;

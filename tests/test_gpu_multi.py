@@ -116,6 +116,14 @@ def test_two_gpu_deferred_merge_bitwise(n_loc, d, k, extra):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("n_loc,d,k,extra", [(4, 100_003, 5, []), (8, 400_000, 16, []), (4, 50_001, 2, ["--exponential"])])
+def test_two_gpu_hybrid_deferred_tail_merge_bitwise(n_loc, d, k, extra):
+    # several workers per GPU (hybrid walk): each step's chain tails merge inside the next walk
+    _run(2, "--workers-per-gpu", n_loc, "--vector-len", d, "--segments", k, "--num-steps", 7, "--sync-at-end",
+         "--compare-all", *extra)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("pieces", [3, 8])
 def test_two_gpu_pieces_bitwise(pieces):
     # push(p+1) / mix(p) overlap across the caller's and the aux stream, across GPUs
