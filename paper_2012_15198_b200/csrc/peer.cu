@@ -383,7 +383,8 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
           const float4 cm = reinterpret_cast<const float4*>(bx + kPeerTile)[v];
           const float4 cg = reinterpret_cast<const float4*>(bx + 2 * kPeerTile)[v];
           if (a.fuse_mix)  // the previous step's a5: x = (y + received y) / 2 (Alg.1 l.17)
-            cx = mean4(cx, reinterpret_cast<const float4*>(bx + 3 * kPeerTile)[v]);
+            cx = mean4(cx, s.wire ? unpack_bf16x4(reinterpret_cast<const uint2*>(bx + 3 * kPeerTile)[v])
+                                  : reinterpret_cast<const float4*>(bx + 3 * kPeerTile)[v]);
           bad |= nonfinite4(cg);
           // LARS (C-18): m' = mu*m + (g + wd*x), y = x - lrs[r][layer]*m'
           const float4 mn = mom4(cm, s.lrs ? decay4(cg, cx, s.wd) : cg, s.mu);
@@ -431,14 +432,21 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
         const uint32_t bytes = (uint32_t)(((U.len + 3) & ~3) * 4);
         const int64_t off = (int64_t)U.r * s.ld + U.c0;
         float* buf = ringA + (size_t)st * NA * kPeerTile;
-        ptx::mbar_arrive_expect_tx(&a_full[st], NA * bytes);
+        ptx::mbar_arrive_expect_tx(&a_full[st], 3 * bytes + (a.fuse_mix ? (s.wire ? (uint32_t)(((U.len + 7) & ~7) * 2) : bytes) : 0u));
         ptx::bulk_g2s(buf, s.x + off, bytes, &a_full[st]);
         ptx::bulk_g2s(buf + kPeerTile, s.m + off, bytes, &a_full[st]);
         ptx::bulk_g2s(buf + 2 * kPeerTile, s.g + off, bytes, &a_full[st]);
-        if (a.fuse_mix)  // the previous step's received tile (inbox parity of epoch e-1)
-          ptx::bulk_g2s(buf + 3 * kPeerTile,
-                        reinterpret_cast<const float*>(mine + a.off_inbox) + (int64_t)(par ^ 1) * s.n_loc * s.ld + off,
-                        bytes, &a_full[st]);
+        if (a.fuse_mix) {  // the previous step's received tile (inbox parity of epoch e-1)
+          if (s.wire)  // bf16 rows, stride (ld + 7) & ~7, 16-byte units
+            ptx::bulk_g2s(buf + 3 * kPeerTile,
+                          reinterpret_cast<const uint16_t*>(mine + a.off_inbox) +
+                              ((int64_t)(par ^ 1) * s.n_loc + U.r) * ((s.ld + 7) & ~7) + U.c0,
+                          (uint32_t)(((U.len + 7) & ~7) * 2), &a_full[st]);
+          else
+            ptx::bulk_g2s(buf + 3 * kPeerTile,
+                          reinterpret_cast<const float*>(mine + a.off_inbox) + (int64_t)(par ^ 1) * s.n_loc * s.ld + off,
+                          bytes, &a_full[st]);
+        }
       }
     }
     __syncwarp();
@@ -921,11 +929,17 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
           const int64_t off = (int64_t)row * ld + td.c0;
           float* buf = stage_buf + (size_t)st * NA * kTmaTileMax;
           const bool merge = tprev[td.seg * n_loc + row];
-          ptx::mbar_arrive_expect_tx(&full[st], (merge ? 4 : 3) * bytes);
+          const uint32_t ibytes = a.wire ? (uint32_t)(((td.len + 7) & ~7) * 2) : bytes;
+          ptx::mbar_arrive_expect_tx(&full[st], 3 * bytes + (merge ? ibytes : 0u));
           ptx::bulk_g2s(buf, a.x + off, bytes, &full[st]);
           ptx::bulk_g2s(buf + kTmaTileMax, a.m + off, bytes, &full[st]);
           ptx::bulk_g2s(buf + 2 * kTmaTileMax, a.g + off, bytes, &full[st]);
-          if (merge)  // the previous step's received y of this tail row
+          if (merge && a.wire)  // the previous step's received y of this tail row (bf16 rows)
+            ptx::bulk_g2s(buf + 3 * kTmaTileMax,
+                          reinterpret_cast<const uint16_t*>(mine + a.off_inbox) +
+                              ((int64_t)(par ^ 1) * n_loc + row) * ((ld + 7) & ~7) + td.c0,
+                          ibytes, &full[st]);
+          else if (merge)
             ptx::bulk_g2s(buf + 3 * kTmaTileMax,
                           reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)(par ^ 1) * n_loc) * ld + off,
                           bytes, &full[st]);
@@ -968,7 +982,8 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
             const float4 cm = reinterpret_cast<const float4*>(buf + kTmaTileMax)[v];
             const float4 cg = reinterpret_cast<const float4*>(buf + 2 * kTmaTileMax)[v];
             if (merge)  // the previous step's a5 for this chain tail (Alg.1 l.17)
-              cx = mean4(cx, reinterpret_cast<const float4*>(buf + 3 * kTmaTileMax)[v]);
+              cx = mean4(cx, a.wire ? unpack_bf16x4(reinterpret_cast<const uint2*>(buf + 3 * kTmaTileMax)[v])
+                                    : reinterpret_cast<const float4*>(buf + 3 * kTmaTileMax)[v]);
             bad |= nonfinite4(cg);
             const float4 mn = mom4(cm, cg, a.mu);
             const float4 y = sgd4(cx, mn, a.lr);
@@ -1764,7 +1779,7 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   if (p.use_hybrid) {
     // deferred merge: this step's chain tails are merged inside the next walk (or
     // peer_flush); the previous step's tails are merged here before their update
-    const bool fuse = p.fuse && !a.wire;
+    const bool fuse = p.fuse;
     p.last_fused = fuse;
     if (ev0) cudaEventRecord(ev0, st);
     if (!fuse || (p.pending && (p.pending_args.x != a.x || p.pending_args.psw != a.psw))) {
@@ -1796,7 +1811,7 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   // deferred merge: this step's push applies the previous step's merge tile by tile, and
   // its own merge waits for the next push (or peer_flush); the separate mix pass and its
   // cross-GPU wait disappear from the step
-  const bool fuse = p.fuse && p.pieces == 1 && !a.wire && a.lrs == nullptr;
+  const bool fuse = p.fuse && p.pieces == 1 && a.lrs == nullptr;
   p.last_fused = fuse;
   if (ev0) cudaEventRecord(ev0, st);
   if (!fuse || (p.pending && (p.pending_args.x != a.x || p.pending_args.psw != a.psw))) {

@@ -105,7 +105,7 @@ def test_four_gpu_hierarchical_lars():
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("n_loc,d,k,extra", [(1, 100_003, 3, []), (1, 25_557_032, 8, []), (3, 60_001, 4, []),
-                                             (1, 50_001, 2, ["--exponential"])])
+                                             (1, 50_001, 2, ["--exponential"]), (1, 100_003, 5, ["--wire-bf16"])])
 def test_two_gpu_deferred_merge_bitwise(n_loc, d, k, extra):
     # no cs_sync between steps: each step's merge runs inside the next step's push kernel
     # (push/mix schedule; n_loc > 1 with the hybrid walk off), flushed by the final cs_sync
@@ -116,7 +116,8 @@ def test_two_gpu_deferred_merge_bitwise(n_loc, d, k, extra):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("n_loc,d,k,extra", [(4, 100_003, 5, []), (8, 400_000, 16, []), (4, 50_001, 2, ["--exponential"])])
+@pytest.mark.parametrize("n_loc,d,k,extra", [(4, 100_003, 5, []), (8, 400_000, 16, []), (4, 50_001, 2, ["--exponential"]),
+                                             (3, 70_001, 6, ["--wire-bf16"])])
 def test_two_gpu_hybrid_deferred_tail_merge_bitwise(n_loc, d, k, extra):
     # several workers per GPU (hybrid walk): each step's chain tails merge inside the next walk
     _run(2, "--workers-per-gpu", n_loc, "--vector-len", d, "--segments", k, "--num-steps", 7, "--sync-at-end",
