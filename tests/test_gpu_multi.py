@@ -33,7 +33,8 @@ def _run(nproc, *args, timeout=600, env=None):
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("n_loc,d,k,steps,full", [(1, 4099, 3, 6, True), (3, 50_001, 5, 5, True),
-                                                  (8, 200_000, 32, 4, True), (1, 1_000_003, 8, 8, True)])
+                                                  (8, 200_000, 32, 4, True), (1, 1_000_003, 8, 8, True),
+                                                  (40, 30_001, 8, 4, True)])  # world 80 > 64: k_topology tables
 def test_two_gpu_parity(n_loc, d, k, steps, full):
     args = ["--workers-per-gpu", n_loc, "--vector-len", d, "--segments", k, "--num-steps", steps]
     if full:
