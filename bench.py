@@ -412,6 +412,7 @@ def main():
                 for _ in range(esteps):
                     stage.copy_(hgrads(t), non_blocking=True)
                     step_fn(x, stage, w, lr, mu)
+                    cs.cs_flush()  # the step's result is read: complete a deferred merge first
                     wout.copy_(w, non_blocking=True)
                     stream.synchronize()
                     t += 1
@@ -428,7 +429,7 @@ def main():
         e2e = {"value": 4.0 * world * d / (ems / esteps * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": esteps,
                "ms_per_step": ems / esteps, "wall_s": wall,
-               "api": "cs_gossip_step_host" if host_api else "H2D copy + cs_gossip_step + psw D2H"}
+               "api": "cs_gossip_step_host" if host_api else "H2D copy + cs_gossip_step + cs_flush + psw D2H"}
         del host_bank
 
     hpeak, hpeak_src = hbm_peak()
