@@ -243,6 +243,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-interval", action="store_true", help="skip the communication-interval sub-measurement")
+    ap.add_argument("--hier-groups", type=int, default=0,
+                    help="c4: number of groups (default: groups of 4 GPUs, or one group if fewer)")
     ap.add_argument("--wire", default="fp32", choices=["fp32", "bf16"],
                     help="SURVEY 8(f) #4: bf16 wire format for received segments (reading C-20)")
     ap.add_argument("--scheme", default="crossover", choices=["crossover", "sgp", "allreduce"],
@@ -293,6 +295,8 @@ def main():
 
     hier = args.config == "c4" or args.scheme == "allreduce"
     groups = 1 if args.scheme == "allreduce" else (max(1, world // 4) if hier else world)
+    if hier and args.hier_groups:
+        groups = args.hier_groups
     if args.scheme == "sgp" and not args.k:
         k = 1
     cs.cs_init(world, groups, k, seed)

@@ -723,7 +723,6 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
     if (g.n_loc != 1)
       return fail(CS_EUNSUPPORTED, "multi-GPU hierarchical step needs one worker per GPU (world == nprocs)");
     if (!g.peer.imported) return fail(CS_ENOTBOUND, "multi-GPU: cs_ipc_import has not been called");
-    if ((rc = flush_pending()) != CS_OK) return rc;
     PeerStepArgs pa = peer_args(params, grads, psw, lr, momentum);
     if (g.lars) {  // rates from the leader replica's x and the group mean
       pa.lrs_out = g.d_lrs;
@@ -741,11 +740,13 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
     rc = peer_hier_step(g.peer, pa, g.stream, ev[0], ev[1]);
     if (rc) return fail(rc, "%s", peer_error());
     if (diag) {
+      if ((rc = flush_pending()) != CS_OK) return rc;  // diagnostics of the merged x'
       rc = peer_diag(g.peer, pa, g.d_partials, local_max_grid(), g.d_diag, g.stream);
       if (rc) return fail(rc, "%s", peer_error());
       g.diag_valid = true;
     }
-    g.launches_per_step = (g.groups >= 2 ? 5 : 3) + (g.lars ? 2 : 0);  // (topology,) scatter, reduce, push(, mix)
+    // (topology,) scatter, reduce, push (, mix unless the leader exchange's merge is deferred)
+    g.launches_per_step = (g.groups >= 2 ? (g.peer.last_fused ? 4 : 5) : 3) + (g.lars ? 2 : 0);
     g.hot_kernel = g.lars ? "k_hier_scatter+k_hier_reduce+k_lars_norms+k_lars_scale+k_peer_push+k_peer_mix"
                           : "k_hier_scatter+k_hier_reduce+k_peer_push+k_peer_mix";
     g.step += 1;

@@ -126,6 +126,20 @@ def test_two_gpu_hybrid_deferred_tail_merge_bitwise(n_loc, d, k, extra):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+def test_two_gpu_hier_deferred_exchange_merge_bitwise():
+    # groups >= 2: the leader exchange's merge runs inside the next hierarchical push
+    # (opt-in schedule, CS_HIER_FUSE=1)
+    _run(2, "--workers-per-gpu", 1, "--vector-len", 150_001, "--segments", 5, "--num-steps", 6,
+         "--hier-groups", 2, "--compare-all", "--sync-at-end", env={"CS_HIER_FUSE": "1"})
+
+
+@pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
+def test_four_gpu_hier_deferred_exchange_merge_bitwise():
+    _run(4, "--workers-per-gpu", 1, "--vector-len", 150_001, "--segments", 7, "--num-steps", 6,
+         "--hier-groups", 2, "--compare-all", "--sync-at-end", env={"CS_HIER_FUSE": "1"})
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("pieces", [3, 8])
 def test_two_gpu_pieces_bitwise(pieces):
     # push(p+1) / mix(p) overlap across the caller's and the aux stream, across GPUs
