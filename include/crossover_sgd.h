@@ -174,8 +174,12 @@ int cs_ipc_import(const char* all_handles /* nprocs * CS_IPC_HANDLE_BYTES */);
  *   psw     fp32 device [n_loc][k] push-sum weights, updated in place (start at 1).
  *   lr, momentum  fp32 scalars.
  * Every output reads only the pre-step snapshot.  Multi-GPU: every
- * process must call with the same t.  Errors: CS_ENOTBOUND, CS_ELAYOUT, CS_EINVAL,
- * CS_ECUDA, CS_ETOPOLOGY, CS_EDIVERGED (from an earlier step). */
+ * process must call with the same t, and a5 of this step may be deferred into the
+ * next step's kernel: call cs_flush or cs_sync before reading params / psw (see
+ * cs_flush).  Also: cs_set_topology_kind (SGP graph), cs_set_wire (bf16 wire),
+ * cs_set_lars + cs_set_layers (LARS).  Errors: CS_ENOTBOUND, CS_ELAYOUT, CS_EINVAL,
+ * CS_ECUDA, CS_ETOPOLOGY, CS_EDIVERGED (from an earlier step), CS_ETIMEOUT,
+ * CS_EUNSUPPORTED (a combination listed as such at the setters). */
 int cs_gossip_step(float* params, const float* grads, float* psw, float lr, float momentum);
 
 /* End-to-end variant of cs_gossip_step for host-resident gradients: copies
