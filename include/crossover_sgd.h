@@ -246,11 +246,11 @@ int cs_segment_plan(const int64_t* layer_sizes, int n_layers, int k, int32_t* se
  * the equal split of reading C-2; the layers then only serve LARS.  layer_bounds NULL
  * or n_layers 0 clears the table.  Lives until the next cs_bind.
  * Runs on the single-GPU bulk-TMA path (world <= 64, k*world <= 2048) and on the
- * multi-GPU push/mix path with one worker per GPU (every process must pass the same
- * table; synchronises the bound stream).  The hierarchical step refuses a layer table,
- * and the multi-GPU path refuses it together with the bf16 wire.
+ * multi-GPU paths, push/mix and hybrid walk (every process must pass the same table;
+ * synchronises the bound stream).  The single-GPU hierarchical step refuses a layer
+ * table, and the multi-GPU paths refuse it together with the bf16 wire.
  * Errors: CS_ENOTBOUND, CS_EINVAL, CS_ELAYOUT (bounds), CS_EINVAL_SEGMENTS,
- * CS_EUNSUPPORTED (several workers per GPU across GPUs, or the register path), CS_ECUDA. */
+ * CS_EUNSUPPORTED (the register path), CS_ECUDA. */
 int cs_set_layers(const int64_t* layer_bounds, int n_layers, const int32_t* seg_of_layer);
 
 /* LARS in the flat step ("adapts the learning rate of each layer by the
@@ -261,8 +261,9 @@ int cs_set_layers(const int64_t* layer_bounds, int n_layers, const int32_t* seg_
  *   lrs   = fp32(lr * scale)
  * and applies  m = mu*m + (g + wd*x),  y = x - lrs*m  before the exchange (C-18).
  * Needs a layer table at step time (CS_EINVAL otherwise).  Two extra launches per
- * step before the update: k_lars_norms, k_lars_scale (then k_gossip_tma on one GPU, or
- * k_peer_push + k_peer_mix with one worker per GPU across GPUs).
+ * step before the update: k_lars_norms, k_lars_scale (then k_gossip_tma on one GPU,
+ * k_peer_push + k_peer_mix or k_hyb_walk + k_hyb_tail across GPUs; the deferred merge is
+ * off with LARS because the norms need the merged parameters).
  * Errors: CS_ENOTINIT, CS_EINVAL. */
 int cs_set_lars(float eta, float weight_decay, float eps);
 

@@ -835,8 +835,8 @@ int cs_set_layers(const int64_t* layer_bounds, int n_layers, const int32_t* seg_
   }
   if (n_layers < 1 || n_layers > CS_MAX_LAYERS)
     return fail(CS_EINVAL, "n_layers %d outside [1, %d]", n_layers, CS_MAX_LAYERS);
-  if (g.use_peer ? (g.n_loc != 1 || g.peer.use_hybrid) : !g.use_tma)
-    return fail(CS_EUNSUPPORTED, "layer tables run on the single-GPU bulk-TMA path and the one-worker-per-GPU push/mix path");
+  if (g.use_peer ? false : !g.use_tma)
+    return fail(CS_EUNSUPPORTED, "layer tables run on the single-GPU bulk-TMA path and the multi-GPU paths");
   if (layer_bounds[0] != 0 || layer_bounds[n_layers] != g.d)
     return fail(CS_ELAYOUT, "layer bounds must run from 0 to d = %lld", (long long)g.d);
   for (int i = 0; i < n_layers; ++i) {

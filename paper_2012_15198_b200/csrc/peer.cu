@@ -753,7 +753,8 @@ constexpr int kHMaxTable = 2048;  // k * n_loc
 
 size_t hyb_smem_bytes(int k, int n_loc) {
   return kHStages * kHStageBytes + sizeof(uint32_t) * 2 * (size_t)k * n_loc +
-         sizeof(uint32_t) * 192 * (kHThreads / 32) + sizeof(float) * (size_t)k * n_loc + (size_t)k * n_loc;
+         sizeof(uint32_t) * 192 * (kHThreads / 32) + sizeof(float) * (size_t)k * n_loc + (size_t)k * n_loc +
+         16 + sizeof(float) * kHStages;  // + per-slot LARS rates (4-byte aligned)
 }
 
 struct HybArgs {
@@ -782,6 +783,11 @@ struct HybArgs {
   // merged with the previous inbox inside this walk, and this step's tails wait for the next
   int fuse;
   const uint8_t* tail_prev;
+  // LARS (reading C-18): per-(local worker, layer) rates staged per ring slot; weight decay
+  const float* lrs;
+  int n_layers;
+  float wd;
+  const int64_t* bounds;    // [k+1] the segment plan (layer plans move the bounds)
 };
 
 __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
@@ -792,6 +798,7 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
   uint32_t* scratch = reinterpret_cast<uint32_t*>(head_dst + a.k * a.n_loc);         // [warps][192]
   float* cur_w = reinterpret_cast<float*>(scratch + 192 * (kHThreads / 32));         // [k][n_loc]
   uint8_t* tprev = reinterpret_cast<uint8_t*>(cur_w + a.k * a.n_loc);               // [k][n_loc]
+  float* srate = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(tprev + a.k * a.n_loc) + 15) & ~uintptr_t(15));
   // deferred merge: 3 stages of x, m, g and the previous inbox tile (the same 12-tile region)
   const int NS = a.fuse ? 3 : kHStages, NA = a.fuse ? 4 : 3;
   __shared__ uint64_t full[kHStages], empty[kHStages];
@@ -930,6 +937,7 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
           float* buf = stage_buf + (size_t)st * NA * kTmaTileMax;
           const bool merge = tprev[td.seg * n_loc + row];
           const uint32_t ibytes = a.wire ? (uint32_t)(((td.len + 7) & ~7) * 2) : bytes;
+          if (a.lrs) srate[st] = a.lrs[(int64_t)row * a.n_layers + td.layer];  // before the release-arrive
           ptx::mbar_arrive_expect_tx(&full[st], 3 * bytes + (merge ? ibytes : 0u));
           ptx::bulk_g2s(buf, a.x + off, bytes, &full[st]);
           ptx::bulk_g2s(buf + kTmaTileMax, a.m + off, bytes, &full[st]);
@@ -985,8 +993,9 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
               cx = mean4(cx, a.wire ? unpack_bf16x4(reinterpret_cast<const uint2*>(buf + 3 * kTmaTileMax)[v])
                                     : reinterpret_cast<const float4*>(buf + 3 * kTmaTileMax)[v]);
             bad |= nonfinite4(cg);
-            const float4 mn = mom4(cm, cg, a.mu);
-            const float4 y = sgd4(cx, mn, a.lr);
+            // LARS (C-18): m' = mu*m + (g + wd*x), y = x - lrs[row][layer]*m'
+            const float4 mn = mom4(cm, a.lrs ? decay4(cg, cx, a.wd) : cg, a.mu);
+            const float4 y = sgd4(cx, mn, a.lrs ? srate[st] : a.lr);
             const int64_t j = td.c0 + 4 * v;
             st4_cs(a.m + (int64_t)row * ld + j, mn, vv);
             if (e & kHStart) {
@@ -1083,7 +1092,11 @@ __global__ void __launch_bounds__(256) k_hyb_tail(const HybArgs a) {
          idx += (int64_t)gridDim.x * blockDim.x) {
       const int64_t r = idx / nv, v = idx - r * nv;
       const int64_t j = 4 * v;
-      const int sg = (int)imin64(a.k - 1, (((j >> 5) + 1) * a.k - 1) / a.nq);
+      int sg = 0;  // segment of column j: the last plan bound <= j
+      for (int lo = 0, hi = a.k - 1; lo <= hi;) {
+        const int mid = (lo + hi) >> 1;
+        if (a.bounds[mid] <= j) { sg = mid; lo = mid + 1; } else { hi = mid - 1; }
+      }
       if (!tail[sg * n_loc + r]) continue;
       const int64_t off = r * a.ld + j;
       const float4 y = __ldcs(reinterpret_cast<const float4*>(a.x + off));
@@ -1448,6 +1461,8 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
         td.c0 = c;
         td.seg = s;
         td.len = (int32_t)((c + T < bounds[s + 1] ? c + T : bounds[s + 1]) - c);
+        td.layer = 0;
+        td.pad_ = 0;
         tiles.push_back(td);
       }
     p.n_htiles = (int)tiles.size();
@@ -1661,6 +1676,37 @@ int peer_set_layers(PeerState& p, const std::vector<int64_t>& plan, const std::v
   p.h_bounds = plan;
   p.h_seg_t0 = seg_t0;
   p.n_tiles = seg_t0[k];
+  if (p.use_hybrid) {
+    // the hybrid walk's own tiles (TMA-sized), split the same way; LARS norms use them
+    const int T = tma_tile_len(p.d, p.grid_hyb);
+    std::vector<TileDesc> ht;
+    std::vector<int32_t> hfirst(L + 1, 0);
+    int hl = 0;
+    for (int s2 = 0; s2 < k; ++s2) {
+      int64_t c = plan[s2];
+      while (c < plan[s2 + 1]) {
+        while (lb[hl + 1] <= c) hfirst[++hl] = (int32_t)ht.size();
+        const int64_t end = std::min(std::min(plan[s2 + 1], lb[hl + 1]), c + (int64_t)T);
+        TileDesc td;
+        td.c0 = c;
+        td.seg = s2;
+        td.len = (int32_t)(end - c);
+        td.layer = hl;
+        td.pad_ = 0;
+        ht.push_back(td);
+        c = end;
+      }
+    }
+    while (hl < L) hfirst[++hl] = (int32_t)ht.size();
+    if (p.d_htiles) cudaFree(p.d_htiles);
+    p.d_htiles = nullptr;
+    cudaError_t e2 = cudaMalloc(&p.d_htiles, sizeof(TileDesc) * ht.size());
+    if (e2 == cudaSuccess)
+      e2 = cudaMemcpy(p.d_htiles, ht.data(), sizeof(TileDesc) * ht.size(), cudaMemcpyHostToDevice);
+    if (e2 != cudaSuccess) return perr(CS_ECUDA, "hybrid layer tiles", e2);
+    p.n_htiles = (int)ht.size();
+    tile_first = hfirst;
+  }
   const int units = p.n_tiles * p.n_loc;
   p.grid_push = p.grid_push_max < units ? p.grid_push_max : units;
   // pieces follow the new tile count
@@ -1671,8 +1717,9 @@ int peer_set_layers(PeerState& p, const std::vector<int64_t>& plan, const std::v
   return CS_OK;
 }
 
-const TileDesc* peer_tiles(const PeerState& p) { return p.d_ptiles; }
-int peer_tile_count(const PeerState& p) { return p.n_tiles; }
+// The tiles of the kernel that runs the flat step (LARS norms are computed over them).
+const TileDesc* peer_tiles(const PeerState& p) { return p.use_hybrid ? p.d_htiles : p.d_ptiles; }
+int peer_tile_count(const PeerState& p) { return p.use_hybrid ? p.n_htiles : p.n_tiles; }
 
 namespace {
 
@@ -1769,6 +1816,10 @@ HybArgs hyb_args(const PeerState& p, const PeerStepArgs& a, uint32_t epoch) {
   h.err = a.err;
   h.fuse = 0;
   h.tail_prev = nullptr;
+  h.lrs = a.lrs;
+  h.n_layers = a.n_layers;
+  h.wd = a.wd;
+  h.bounds = p.d_bounds;
   return h;
 }
 }  // namespace
@@ -1779,7 +1830,7 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   if (p.use_hybrid) {
     // deferred merge: this step's chain tails are merged inside the next walk (or
     // peer_flush); the previous step's tails are merged here before their update
-    const bool fuse = p.fuse;
+    const bool fuse = p.fuse && a.lrs == nullptr;  // LARS norms need the merged x
     p.last_fused = fuse;
     if (ev0) cudaEventRecord(ev0, st);
     if (!fuse || (p.pending && (p.pending_args.x != a.x || p.pending_args.psw != a.psw))) {

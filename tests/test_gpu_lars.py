@@ -102,6 +102,38 @@ def test_lars_matches_oracle(n, L, k, plan, diag):
         assert np.array_equal(x.cpu().numpy()[:, :d], X)
 
 
+@pytest.mark.parametrize("hybrid,plan", [(1, True), (0, True), (1, False)])
+def test_lars_and_layer_plan_on_the_peer_kernels(hybrid, plan, monkeypatch):
+    # the multi-GPU kernels in single-GPU emulation: hybrid walk (several workers per GPU)
+    # or push/mix, with a layer table (and plan) and LARS; 10 steps, no sync in between
+    monkeypatch.setenv("CS_PEER_HYBRID", str(hybrid))
+    n, L, k, seed = 6, 30, 5, 4
+    sizes, lb = _layers(200 + L, L)
+    d = int(lb[-1])
+    ld = (d + 3) // 4 * 4
+    cs.cs_init(n, n, k, seed)
+    cs.cs_set_path(3)
+    x, m, w, bank2 = device_state(cs, n, d, k, seed, ld=ld)
+    cs.cs_bind(m, d, ld, 0, 1, torch.cuda.current_stream())
+    sol = segment_plan(sizes, k) if plan else None
+    cs.cs_set_layers(lb, sol)
+    cs.cs_set_lars(ETA, WD, EPS)
+    seg = T.segment_of_columns(plan_bounds(lb, sol) if plan else T.segment_bounds(d, k), np.arange(d))
+    X = synth.init_params(seed, range(n), d)
+    M, W = np.zeros_like(X), np.ones((n, k), F32)
+    bank = synth.grad_bank(seed, n, d)
+    for t in range(10):
+        cs.cs_gossip_step(x, grads_view(bank2, n, t), w, 9.0, MU)
+        X, M, W, lrs = lars_gossip_step(X, M, synth.grads_at(bank, n, t), W, T.topology(seed, t, n, k), seg,
+                                        lb, 9.0, MU, ETA, WD, EPS)
+    assert _ulp_close(cs.cs_get_lars_rates(n, L), lrs)
+    cs.cs_sync()
+    assert np.all(np.abs(x.cpu().numpy()[:, :d] - X) <= 1e-6 * np.abs(X).max(axis=1, keepdims=True))
+    assert np.array_equal(w.cpu().numpy(), W)
+    cs.cs_set_lars(0.0)
+    cs.cs_set_path(0)
+
+
 def test_lars_resnet50_blocks_plan():
     # the paper's setting: ResNet-50's 161 tensors, segments = stem + 16 blocks + FC (k = 18)
     sizes, block = synth.resnet50_layers()

@@ -89,6 +89,16 @@ def test_two_gpu_layers_and_lars(layers, plan, lars, diag):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("n_loc,plan,diag", [(3, True, True), (4, False, False)])
+def test_two_gpu_hybrid_layers_and_lars(n_loc, plan, diag):
+    # several workers per GPU (hybrid walk) with a layer table and LARS
+    args = ["--workers-per-gpu", n_loc, "--vector-len", 180_000, "--segments", 5, "--num-steps", 5,
+            "--compare-all", "--layers", 16, "--lars"]
+    args += (["--layer-plan"] if plan else []) + (["--diag"] if diag else [])
+    _run(2, *args)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("groups,plan", [(1, True), (2, False)])
 def test_two_gpu_hierarchical_lars(groups, plan):
     # LARS on the group-reduced gradient: one group (AllReduce-SGD + LARS) and
