@@ -128,7 +128,8 @@ def test_two_gpu_deferred_merge_bitwise(n_loc, d, k, extra):
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("n_loc,d,k,extra", [(4, 100_003, 5, []), (8, 400_000, 16, []), (4, 50_001, 2, ["--exponential"]),
-                                             (3, 70_001, 6, ["--wire-bf16"])])
+                                             (3, 70_001, 6, ["--wire-bf16"]),
+                                             (40, 30_001, 8, [])])  # world 80: k_topology tables every step
 def test_two_gpu_hybrid_deferred_tail_merge_bitwise(n_loc, d, k, extra):
     # several workers per GPU (hybrid walk): each step's chain tails merge inside the next walk
     _run(2, "--workers-per-gpu", n_loc, "--vector-len", d, "--segments", k, "--num-steps", 7, "--sync-at-end",
