@@ -418,7 +418,21 @@ __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
       const float4 cm = ld_stream(a.m + lead_off);
       float4 gsum = ld_stream(a.g + lead_off);
       bad |= nonfinite4(gsum);
-      for (int r = 1; r < gs; ++r) {
+      // the members' rows are loaded 8 at a time (independent loads in flight), then added
+      // in ascending member order (reading C-12), so the sum is the same bits
+      int r = 1;
+      for (; r + 8 <= gs; r += 8) {
+        float4 gb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) gb[u] = ld_stream(a.g + lead_off + (int64_t)(r + u) * ld);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          bad |= nonfinite4(gb[u]);
+          gsum = make_float4(__fadd_rn(gsum.x, gb[u].x), __fadd_rn(gsum.y, gb[u].y),
+                             __fadd_rn(gsum.z, gb[u].z), __fadd_rn(gsum.w, gb[u].w));
+        }
+      }
+      for (; r < gs; ++r) {
         const float4 gr = ld_stream(a.g + lead_off + (int64_t)r * ld);
         bad |= nonfinite4(gr);
         gsum = make_float4(__fadd_rn(gsum.x, gr.x), __fadd_rn(gsum.y, gr.y),
