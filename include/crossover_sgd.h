@@ -204,9 +204,10 @@ int cs_gossip_step_host(float* params, const float* grads_host, float* psw, floa
  * in the source group.  The first hierarchical step after cs_bind / cs_set_step
  * copies each leader's state to its members; callers must not modify a member's
  * state between hierarchical steps.  Other layouts: CS_EUNSUPPORTED.
- * With LARS (cs_set_lars, multi-GPU only) the leader's rates come from its x and the
- * group-reduced gradient gbar, so the gradient norm is the synchronised one
- * (PAPER.md:197); every member computes the same rates from its replica.
+ * With LARS (cs_set_lars) the leader's rates come from its x and the group-reduced
+ * gradient gbar, so the gradient norm is the synchronised one; on
+ * several GPUs every member computes the same rates from its replica.  On one GPU
+ * cs_get_lars_rates' first `groups` rows are the groups' rates.
  * Errors as cs_gossip_step. */
 int cs_hier_step(float* params, float* grads, float* psw, float lr, float momentum);
 
@@ -247,8 +248,8 @@ int cs_segment_plan(const int64_t* layer_sizes, int n_layers, int k, int32_t* se
  * or n_layers 0 clears the table.  Lives until the next cs_bind.
  * Runs on the single-GPU bulk-TMA path (world <= 64, k*world <= 2048) and on the
  * multi-GPU paths, push/mix and hybrid walk (every process must pass the same table;
- * synchronises the bound stream).  The single-GPU hierarchical step refuses a layer
- * table, and the multi-GPU paths refuse it together with the bf16 wire.
+ * synchronises the bound stream), for the flat and the hierarchical step.  The
+ * multi-GPU paths refuse it together with the bf16 wire.
  * Errors: CS_ENOTBOUND, CS_EINVAL, CS_ELAYOUT (bounds), CS_EINVAL_SEGMENTS,
  * CS_EUNSUPPORTED (the register path), CS_ECUDA. */
 int cs_set_layers(const int64_t* layer_bounds, int n_layers, const int32_t* seg_of_layer);

@@ -93,6 +93,7 @@ struct Ctx {
   int n_layers = 0;
   int32_t* d_tile_first = nullptr;    // [n_layers + 1] tile range of each layer
   float* d_lrs = nullptr;             // [n_loc][n_layers] rates of the last LARS step
+  int64_t* d_layer_bounds = nullptr;  // [n_layers + 1] (single-GPU hierarchical kernel)
   double* d_lars_part = nullptr;      // [n_tiles][n_loc][2]
   bool lars = false;
   float lars_eta = 0.f, lars_wd = 0.f, lars_eps = 0.f;
@@ -144,8 +145,9 @@ void free_device() {
   auto f = [](void* p) { if (p) cudaFree(p); };
   f(g.d_bounds); f(g.d_src); f(g.d_dst); f(g.d_ord); f(g.d_given); f(g.d_rw);
   f(g.d_inv_wsum); f(g.d_err); f(g.d_partials); f(g.d_diag); f(g.d_stage); f(g.d_counter); f(g.d_tiles);
-  f(g.d_tile_first); f(g.d_lrs); f(g.d_lars_part); f(g.d_exp);
+  f(g.d_tile_first); f(g.d_lrs); f(g.d_lars_part); f(g.d_exp); f(g.d_layer_bounds);
   g.d_exp = nullptr;
+  g.d_layer_bounds = nullptr;
   g.d_tile_first = nullptr; g.d_lrs = nullptr; g.d_lars_part = nullptr;
   g.layer_bounds.clear(); g.plan.clear(); g.n_layers = 0; g.lars_valid = false;
   g.d_bounds = nullptr; g.d_src = nullptr; g.d_dst = nullptr; g.d_ord = nullptr;
@@ -326,6 +328,8 @@ LocalArgs local_args(float* params, const float* grads, float* psw, int n, int g
   a.n_layers = 0;
   a.wd = 0.f;
   a.wire = g.wire == CS_WIRE_BF16 ? 1 : 0;
+  a.seg_bounds = nullptr;
+  a.layer_bounds = nullptr;
   return a;
 }
 
@@ -711,8 +715,8 @@ int cs_gossip_step_host(float* params, const float* grads_host, float* psw, floa
 int cs_hier_step(float* params, float* grads, float* psw, float lr, float momentum) {
   int rc = check_bound();
   if (rc) return rc;
-  if ((g.lars || g.n_layers > 0) && g.nprocs == 1)
-    return fail(CS_EUNSUPPORTED, "LARS / layer tables in the hierarchical step need the multi-GPU path");
+  if ((g.lars || g.n_layers > 0) && g.nprocs == 1 && (g.use_peer || !g.use_tma))
+    return fail(CS_EUNSUPPORTED, "LARS / layer tables in the single-GPU hierarchical step need the bulk-TMA tiles");
   if (g.lars && g.n_layers == 0) return fail(CS_EINVAL, "LARS needs a layer table (cs_set_layers)");
   if (g.wire != CS_WIRE_FP32)
     return fail(CS_EUNSUPPORTED, "the bf16 wire format is implemented for the flat step only");
@@ -755,6 +759,11 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
   const int L = g.groups, gs = g.world / g.groups;
   const bool fused = fused_topology_ok(L, g.k);
   LocalArgs a = local_args(params, grads, psw, L, gs, CS_TAG_HIER, lr, momentum);
+  if (g.n_layers > 0) {  // layer plan (C-19) and layer lookups for LARS
+    a.seg_bounds = g.d_bounds;
+    a.layer_bounds = g.d_layer_bounds;
+    a.n_layers = g.n_layers;
+  }
   if (!fused) {
     TopoArgs t = topo_args(L, CS_TAG_HIER, psw, gs);
     CS_CUDA(launch_topology(t, g.stream));
@@ -763,11 +772,19 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
   rc = next_event_pair(ev);
   if (rc) return rc;
   if (ev[0]) CS_CUDA(cudaEventRecord(ev[0], g.stream));
+  if (g.lars) {  // rates per (group, layer) from the leader's x and the group mean
+    CS_CUDA(launch_lars_rates_hier(params, grads, g.ld, g.d_tiles, g.n_tiles, L, gs, a.inv_group, g.d_tile_first,
+                                   g.n_layers, g.d_lars_part, lr, g.lars_eta, g.lars_wd, g.lars_eps, g.d_lrs,
+                                   g.stream));
+    a.lrs = g.d_lrs;
+    a.wd = g.lars_wd;
+    g.lars_valid = true;
+  }
   CS_CUDA(launch_hier_local(a, diag, fused, g.stream, nullptr));
   if (ev[1]) CS_CUDA(cudaEventRecord(ev[1], g.stream));
   if (diag) g.diag_valid = true;
-  g.launches_per_step = fused ? 1 : 2;
-  g.hot_kernel = "k_hier_local";
+  g.launches_per_step = (fused ? 1 : 2) + (g.lars ? 2 : 0);
+  g.hot_kernel = g.lars ? "k_lars_norms_hier+k_lars_scale+k_hier_local" : "k_hier_local";
   g.step += 1;
   return CS_OK;
 }
@@ -826,6 +843,7 @@ int cs_set_layers(const int64_t* layer_bounds, int n_layers, const int32_t* seg_
     g.layer_bounds.clear();
     g.n_layers = 0;
     g.plan = host_bounds(g.d, g.k);
+    CS_CUDA(cudaMemcpy(g.d_bounds, g.plan.data(), sizeof(int64_t) * g.plan.size(), cudaMemcpyHostToDevice));
     if (g.use_peer) {
       std::vector<int32_t> first;
       rc = peer_set_layers(g.peer, g.plan, g.layer_bounds, first);
@@ -885,6 +903,12 @@ int cs_set_layers(const int64_t* layer_bounds, int n_layers, const int32_t* seg_
   g.d_lars_part = nullptr;
   CS_CUDA(cudaMalloc(&g.d_lrs, sizeof(float) * (size_t)g.n_loc * n_layers));
   CS_CUDA(cudaMalloc(&g.d_lars_part, sizeof(double) * 2 * (size_t)tiles_for_norms * g.n_loc));
+  // the plan and the layer bounds on the device (the single-GPU hierarchical kernel looks them up)
+  if (g.d_layer_bounds) cudaFree(g.d_layer_bounds);
+  g.d_layer_bounds = nullptr;
+  CS_CUDA(cudaMalloc(&g.d_layer_bounds, sizeof(int64_t) * (size_t)(n_layers + 1)));
+  CS_CUDA(cudaMemcpy(g.d_layer_bounds, layer_bounds, sizeof(int64_t) * (size_t)(n_layers + 1), cudaMemcpyHostToDevice));
+  CS_CUDA(cudaMemcpy(g.d_bounds, g.plan.data(), sizeof(int64_t) * g.plan.size(), cudaMemcpyHostToDevice));
   g.lars_valid = false;
   return CS_OK;
 }

@@ -74,6 +74,9 @@ struct LocalArgs {
   int n_layers;
   float wd;
   int wire;            // CS_WIRE_BF16: the received y is rounded to bf16 (reading C-20)
+  // k_hier_local with a layer table: the segment plan and the layer bounds (device), or nullptr
+  const int64_t* seg_bounds;    // [k+1]
+  const int64_t* layer_bounds;  // [n_layers+1]
 };
 
 // bf16 wire format (reading C-20): round to the nearest bf16 (ties to even), widen back.
@@ -136,6 +139,12 @@ cudaError_t launch_lars_rates(const float* x, const float* g, int64_t ld, const 
                               int n_tiles, int rows, const int32_t* tile_first, int n_layers,
                               double* part, float lr, float eta, float wd, float eps, float* lrs,
                               cudaStream_t st, LarsWait w = LarsWait());
+// Hierarchical LARS on one GPU: rates per (group, layer) from the leader's x and the group
+// mean gbar, formed exactly as k_hier_local forms it (ascending sum, then * inv).
+cudaError_t launch_lars_rates_hier(const float* x, const float* g, int64_t ld, const TileDesc* tiles,
+                                   int n_tiles, int groups, int gs, float inv, const int32_t* tile_first,
+                                   int n_layers, double* part, float lr, float eta, float wd, float eps,
+                                   float* lrs, cudaStream_t st);
 cudaError_t launch_accumulate(float* acc, const float* g, int64_t rows, int64_t d, int64_t ld,
                               int count, int interval, cudaStream_t st);
 

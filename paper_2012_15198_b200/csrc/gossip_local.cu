@@ -59,6 +59,16 @@ __device__ __forceinline__ float4 decay4(float4 g, float4 x, float wd) {
                      __fadd_rn(g.z, __fmul_rn(wd, x.z)), __fadd_rn(g.w, __fmul_rn(wd, x.w)));
 }
 
+// index of the last bound <= j among bounds[0 .. count) (bounds ascending, bounds[0] = 0)
+__device__ __forceinline__ int last_bound_le(const int64_t* bounds, int count, int64_t j) {
+  int s = 0;
+  for (int lo = 0, hi = count - 1; lo <= hi;) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(bounds + mid) <= j) { s = mid; lo = mid + 1; } else { hi = mid - 1; }
+  }
+  return s;
+}
+
 __device__ __forceinline__ float4 sgd_apply(float4 x, float4 m, float lr) {
   return make_float4(__fsub_rn(x.x, __fmul_rn(lr, m.x)), __fsub_rn(x.y, __fmul_rn(lr, m.y)),
                      __fsub_rn(x.z, __fmul_rn(lr, m.z)), __fsub_rn(x.w, __fmul_rn(lr, m.w)));
@@ -401,7 +411,9 @@ __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
     const int64_t j = v << 2;
     const int valid = (int)imin64(4, d - j);
     const int64_t q = j >> 5;
-    const int s = (int)imin64(a.k - 1, ((q + 1) * a.k - 1) / a.nq);
+    int s = (int)imin64(a.k - 1, ((q + 1) * a.k - 1) / a.nq);
+    if (a.seg_bounds) s = last_bound_le(a.seg_bounds, a.k, j);  // layer plan (C-19)
+    const int layer = a.lrs ? last_bound_le(a.layer_bounds, a.n_layers, j) : 0;
     const uint32_t* ord = ord_all + (int64_t)s * L;
     const double* rw = DIAG ? rw_all + (int64_t)s * L : nullptr;
     float4 yfirst = make_float4(0.f, 0.f, 0.f, 0.f), yprev = yfirst;
@@ -440,8 +452,9 @@ __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
       }
       const float4 gbar = make_float4(__fmul_rn(gsum.x, inv), __fmul_rn(gsum.y, inv),
                                       __fmul_rn(gsum.z, inv), __fmul_rn(gsum.w, inv));
-      const float4 mn = momentum_update(cm, gbar, mu);
-      const float4 y = sgd_apply(cx, mn, lr);
+      // LARS on the group-reduced gradient (C-18): m' = mu*m + (gbar + wd*x)
+      const float4 mn = momentum_update(cm, a.lrs ? decay4(gbar, cx, a.wd) : gbar, mu);
+      const float4 y = sgd_apply(cx, mn, a.lrs ? __ldg(a.lrs + (int64_t)G * a.n_layers + layer) : lr);
       st_stream(a.m + lead_off, mn, valid);
       if (L == 1) {
         for (int r = 0; r < gs; ++r) st_stream(a.x + lead_off + (int64_t)r * ld, y, valid);

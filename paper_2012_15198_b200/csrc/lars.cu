@@ -121,7 +121,59 @@ __global__ void __launch_bounds__(kNormThreads)
   }
 }
 
+// Hierarchical (one GPU): pair p = (tile u, group G); sums of the leader's x^2 and of
+// gbar^2 with gbar = fl(sum_{r ascending} g[G*gs + r]) * inv, as k_hier_local forms it.
+__global__ void __launch_bounds__(kNormThreads)
+    k_lars_norms_hier(const float* __restrict__ x, const float* __restrict__ g, int64_t ld,
+                      const TileDesc* __restrict__ tiles, int n_tiles, int groups, int gs, float inv,
+                      double2* __restrict__ part) {
+  __shared__ double2 red[kNormThreads / 32];
+  const int64_t pairs = (int64_t)n_tiles * groups;
+  for (int64_t p = blockIdx.x; p < pairs; p += gridDim.x) {
+    const int u = (int)(p / groups), G = (int)(p % groups);
+    const TileDesc td = tiles[u];
+    const float* xr = x + (int64_t)G * gs * ld + td.c0;
+    const float* gr = g + (int64_t)G * gs * ld + td.c0;
+    double sx = 0.0, sg = 0.0;
+    for (int v = threadIdx.x; 4 * v < td.len; v += kNormThreads) {
+      const float4 a = __ldcs(reinterpret_cast<const float4*>(xr) + v);
+      float4 b = __ldcs(reinterpret_cast<const float4*>(gr) + v);
+      for (int r = 1; r < gs; ++r) {
+        const float4 c = __ldcs(reinterpret_cast<const float4*>(gr + (int64_t)r * ld) + v);
+        b = make_float4(__fadd_rn(b.x, c.x), __fadd_rn(b.y, c.y), __fadd_rn(b.z, c.z), __fadd_rn(b.w, c.w));
+      }
+      b = make_float4(__fmul_rn(b.x, inv), __fmul_rn(b.y, inv), __fmul_rn(b.z, inv), __fmul_rn(b.w, inv));
+      const int valid = td.len - 4 * v;
+      sx = __dadd_rn(sx, sq(a.x));
+      sg = __dadd_rn(sg, sq(b.x));
+      if (valid > 1) { sx = __dadd_rn(sx, sq(a.y)); sg = __dadd_rn(sg, sq(b.y)); }
+      if (valid > 2) { sx = __dadd_rn(sx, sq(a.z)); sg = __dadd_rn(sg, sq(b.z)); }
+      if (valid > 3) { sx = __dadd_rn(sx, sq(a.w)); sg = __dadd_rn(sg, sq(b.w)); }
+    }
+    const double2 s = block_sum2(sx, sg, red);
+    if (threadIdx.x == 0) part[p] = s;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_lars_rates_hier(const float* x, const float* g, int64_t ld, const TileDesc* tiles,
+                                   int n_tiles, int groups, int gs, float inv, const int32_t* tile_first,
+                                   int n_layers, double* part, float lr, float eta, float wd, float eps,
+                                   float* lrs, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t pairs = (int64_t)n_tiles * groups;
+  const int grid = (int)(pairs < (int64_t)sms * 8 ? pairs : (int64_t)sms * 8);
+  k_lars_norms_hier<<<grid > 0 ? grid : 1, kNormThreads, 0, st>>>(x, g, ld, tiles, n_tiles, groups, gs, inv,
+                                                                  reinterpret_cast<double2*>(part));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_lars_scale<<<n_layers, kNormThreads, 0, st>>>(reinterpret_cast<const double2*>(part), groups, tile_first,
+                                                  n_layers, lr, eta, wd, eps, lrs);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_lars_rates(const float* x, const float* g, int64_t ld, const TileDesc* tiles,
                               int n_tiles, int rows, const int32_t* tile_first, int n_layers,

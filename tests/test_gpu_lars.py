@@ -134,6 +134,48 @@ def test_lars_and_layer_plan_on_the_peer_kernels(hybrid, plan, monkeypatch):
     cs.cs_set_path(0)
 
 
+@pytest.mark.parametrize("groups,lars", [(2, False), (4, False), (2, True), (1, True)])
+def test_hierarchical_one_gpu_layers_and_lars(groups, lars):
+    # single-GPU hierarchical kernel with a layer plan (bitwise) and LARS on the group mean
+    # (rates within 1 ulp, parameters within 1e-6)
+    from oracle.hierarchical import hier_step
+    from oracle.lars import lars_hier_step
+    n, L, k, seed = 8, 20, 4, 6
+    sizes, lb = _layers(300 + L, L)
+    d = int(lb[-1])
+    ld = (d + 3) // 4 * 4
+    cs.cs_init(n, groups, k, seed)
+    x, m, w, bank2 = device_state(cs, n, d, k, seed, ld=ld)
+    cs.cs_bind(m, d, ld, 0, 1, torch.cuda.current_stream())
+    sol = segment_plan(sizes, k)
+    cs.cs_set_layers(lb, sol)
+    if lars:
+        cs.cs_set_lars(ETA, WD, EPS)
+    seg = T.segment_of_columns(plan_bounds(lb, sol), np.arange(d))
+    X = synth.init_params(seed, range(n), d)
+    M, W = np.zeros_like(X), np.ones((n, k), F32)
+    bank = synth.grad_bank(seed, n, d)
+    lr = 9.0 if lars else LR
+    for t in range(6):
+        cs.cs_hier_step(x, grads_view(bank2, n, t), w, lr, MU)
+        if lars:
+            X, M, W, lrs = lars_hier_step(X, M, synth.grads_at(bank, n, t), W, groups, seed, t, k, seg, lb, lr, MU,
+                                          ETA, WD, EPS)
+            assert _ulp_close(cs.cs_get_lars_rates(n, L)[:groups], lrs), t
+        else:
+            X, M, W, _ = hier_step(X, M, synth.grads_at(bank, n, t), W, groups, seed, t, k, seg, lr, MU)
+    cs.cs_sync()
+    xg = x.cpu().numpy()[:, :d]
+    leaders = list(range(0, n, n // groups))
+    if lars:
+        assert np.all(np.abs(xg - X) <= 1e-6 * np.abs(X).max(axis=1, keepdims=True))
+    else:
+        assert np.array_equal(xg, X)
+        assert np.array_equal(m.cpu().numpy()[leaders, :d], M[leaders])
+    assert np.array_equal(w.cpu().numpy(), W)
+    cs.cs_set_lars(0.0)
+
+
 def test_lars_resnet50_blocks_plan():
     # the paper's setting: ResNet-50's 161 tensors, segments = stem + 16 blocks + FC (k = 18)
     sizes, block = synth.resnet50_layers()
@@ -179,11 +221,12 @@ def test_layer_table_errors():
     cs.cs_set_layers([0, 512, 1024], [0, 1])
     cs.cs_gossip_step(x, g, w, LR, MU)
     cs.cs_init(n, 2, k, 0)
+    cs.cs_set_path(1)                              # the register path has no layer tiles
     cs.cs_bind(m, d, d, 0, 1, torch.cuda.current_stream())
-    cs.cs_set_layers([0, 512, 1024], [0, 1])
-    with pytest.raises(cs.CSError) as e:           # hierarchical step refuses layer tables / LARS
-        cs.cs_hier_step(x, g, w, LR, MU)
+    with pytest.raises(cs.CSError) as e:
+        cs.cs_set_layers([0, 512, 1024], [0, 1])
     assert e.value.code == -12
+    cs.cs_set_path(0)
     with pytest.raises(cs.CSError):
         cs.cs_set_lars(-1.0)
     cs.cs_set_lars(0.0)
