@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kThreads) k_gossip_local(const LocalArgs a) {
 //   h2  leader: m <- mu*m + gbar, y <- x - lr*m; then the cycle walk over the
 //       leader topology mixes leaders' y (tag HIER); one leader: x' = y
 //   h3  x' written to every member row of the group (bitwise identical)
-template <bool DIAG, bool FUSED>
+template <bool DIAG, bool FUSED, bool LAYERS>
 __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int L = a.n, gs = a.group_size;
@@ -412,8 +412,8 @@ __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
     const int valid = (int)imin64(4, d - j);
     const int64_t q = j >> 5;
     int s = (int)imin64(a.k - 1, ((q + 1) * a.k - 1) / a.nq);
-    if (a.seg_bounds) s = last_bound_le(a.seg_bounds, a.k, j);  // layer plan (C-19)
-    const int layer = a.lrs ? last_bound_le(a.layer_bounds, a.n_layers, j) : 0;
+    if (LAYERS && a.seg_bounds) s = last_bound_le(a.seg_bounds, a.k, j);  // layer plan (C-19)
+    const int layer = (LAYERS && a.lrs) ? last_bound_le(a.layer_bounds, a.n_layers, j) : 0;
     const uint32_t* ord = ord_all + (int64_t)s * L;
     const double* rw = DIAG ? rw_all + (int64_t)s * L : nullptr;
     float4 yfirst = make_float4(0.f, 0.f, 0.f, 0.f), yprev = yfirst;
@@ -453,8 +453,9 @@ __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
       const float4 gbar = make_float4(__fmul_rn(gsum.x, inv), __fmul_rn(gsum.y, inv),
                                       __fmul_rn(gsum.z, inv), __fmul_rn(gsum.w, inv));
       // LARS on the group-reduced gradient (C-18): m' = mu*m + (gbar + wd*x)
-      const float4 mn = momentum_update(cm, a.lrs ? decay4(gbar, cx, a.wd) : gbar, mu);
-      const float4 y = sgd_apply(cx, mn, a.lrs ? __ldg(a.lrs + (int64_t)G * a.n_layers + layer) : lr);
+      const bool lars = LAYERS && a.lrs;
+      const float4 mn = momentum_update(cm, lars ? decay4(gbar, cx, a.wd) : gbar, mu);
+      const float4 y = sgd_apply(cx, mn, lars ? __ldg(a.lrs + (int64_t)G * a.n_layers + layer) : lr);
       st_stream(a.m + lead_off, mn, valid);
       if (L == 1) {
         for (int r = 0; r < gs; ++r) st_stream(a.x + lead_off + (int64_t)r * ld, y, valid);
@@ -798,13 +799,22 @@ cudaError_t launch_gossip_local(const LocalArgs& a, bool diag, bool fused, cudaS
 
 cudaError_t launch_hier_local(const LocalArgs& a, bool diag, bool fused, cudaStream_t st,
                               int* grid_out) {
+  const bool layers = a.seg_bounds != nullptr || a.lrs != nullptr;  // layer-plan / LARS variant
   const size_t smem = fused ? fused_smem_bytes(a.n, a.k, kThreads / 32, diag) : 0;
   if (fused) {
-    if (diag) return launch_persistent(k_hier_local<true, true>, a, smem, st, grid_out);
-    return launch_persistent(k_hier_local<false, true>, a, smem, st, grid_out);
+    if (layers) {
+      if (diag) return launch_persistent(k_hier_local<true, true, true>, a, smem, st, grid_out);
+      return launch_persistent(k_hier_local<false, true, true>, a, smem, st, grid_out);
+    }
+    if (diag) return launch_persistent(k_hier_local<true, true, false>, a, smem, st, grid_out);
+    return launch_persistent(k_hier_local<false, true, false>, a, smem, st, grid_out);
   }
-  if (diag) return launch_persistent(k_hier_local<true, false>, a, 0, st, grid_out);
-  return launch_persistent(k_hier_local<false, false>, a, 0, st, grid_out);
+  if (layers) {
+    if (diag) return launch_persistent(k_hier_local<true, false, true>, a, 0, st, grid_out);
+    return launch_persistent(k_hier_local<false, false, true>, a, 0, st, grid_out);
+  }
+  if (diag) return launch_persistent(k_hier_local<true, false, false>, a, 0, st, grid_out);
+  return launch_persistent(k_hier_local<false, false, false>, a, 0, st, grid_out);
 }
 
 cudaError_t launch_synth(float* out, int64_t rows, int64_t d, int64_t ld, uint64_t seed, int tag,
