@@ -1,0 +1,38 @@
+"""The bench.py reference arm's JSON contract (CPU only): `--impl reference` times the
+oracle on the host and prints one JSON line with the keys the driver reads; ranks other
+than 0 exit 0 without output."""
+import json
+import os
+import subprocess
+import sys
+
+from conftest import ROOT
+
+
+def _run(extra_env=None):
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "2", "--warmup", "1",
+           "--config", "c1", "--cpu-cols", "4096"]
+    env = {**os.environ, **(extra_env or {})}
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+
+
+def test_reference_arm_json_line():
+    p = _run()
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = [ln for ln in p.stdout.splitlines() if ln.startswith("{")][-1]
+    j = json.loads(line)
+    assert j["impl"] == "reference"
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert key in j, key
+    assert j["steps"] == 2 and j["warmup"] == 1 and j["higher_is_better"] is True and j["value"] > 0
+    assert j["cpu_baseline"]["kind"] == "oracle" and j["cpu_baseline"]["cores"] >= 1
+    assert j["cpu_baseline"]["value"] == j["value"] and "sample" in j["cpu_baseline"]
+    assert j["e2e"] == {"value": j["value"], "unit": j["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert j["config"]["workload"].startswith("c1")
+
+
+def test_reference_arm_other_ranks_are_silent():
+    p = _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
+    assert p.returncode == 0
+    assert not [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
