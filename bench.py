@@ -483,7 +483,9 @@ def main():
                 "traffic": ncu_traffic(f"{args.config}" + ("" if args.path == "auto" else f":{args.path}")
                                        + ("" if world_size == 1 else f"@{world_size}")),
                 "peak_source": hpeak_src, "kernel": hot_kernel,
-                "algorithmic_bytes_per_launch": hbm_per_launch, "bytes_formula": ("28 B x n_loc x d (LARS norms 8 B + step 20 B)" if lars else
+                "algorithmic_bytes_per_launch": hbm_per_launch, "bytes_formula": ("24 B x n_loc x d (LARS g-norm 4 B, x norms carried from the previous step, + step 20 B)"
+                                                                   if lars and world_size == 1 else
+                                                                   "28 B x n_loc x d (LARS norms 8 B + step 20 B)" if lars else
                                                                    "20 B x n_loc x d"),
                 "avg_kernel_us": avg_kern_s * 1e6, "launches_timed": kern_launches}
     if world_size == 1:

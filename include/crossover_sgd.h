@@ -347,8 +347,8 @@ int cs_synth_fill(float* out, int64_t rows, int64_t d, int64_t ld, uint64_t seed
 /* Bytes per step the hot kernel moves, for roofline accounting:
  * out[0] = algorithmic HBM bytes, out[1] = NVLink bytes into this GPU at step t
  * (exact, from the topology), for flat (hier = 0) or hierarchical (hier = 1).
- * Flat: 20 B per parameter per local worker, 28 B with LARS (the norm pass re-reads
- * x and g). */
+ * Flat: 20 B per parameter per local worker; with LARS 28 B (the norm pass reads x and
+ * g), or 24 B on one GPU once the previous LARS step carried the x norms. */
 int cs_step_bytes(int64_t step, int hier, double* out);
 
 /* Kernel timing for roofline accounting: with cs_set_timing(1) every later step

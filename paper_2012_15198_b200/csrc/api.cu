@@ -98,6 +98,9 @@ struct Ctx {
   bool lars = false;
   float lars_eta = 0.f, lars_wd = 0.f, lars_eps = 0.f;
   bool lars_valid = false;
+  // LARS carry: the .x halves of d_lars_part hold sum x'^2 of the last TMA LARS step on xnorm_x
+  bool xnorm_valid = false;
+  const float* xnorm_x = nullptr;
 
   // topology kind (cs_set_topology_kind): SGP's exponential graph as [H][k][world] tables
   int topo_kind = CS_TOPO_CROSSOVER;
@@ -330,6 +333,7 @@ LocalArgs local_args(float* params, const float* grads, float* psw, int n, int g
   a.wire = g.wire == CS_WIRE_BF16 ? 1 : 0;
   a.seg_bounds = nullptr;
   a.layer_bounds = nullptr;
+  a.xnorm_out = nullptr;
   return a;
 }
 
@@ -403,13 +407,21 @@ int enqueue_flat_step(float* params, const float* grads, float* psw, float lr, f
     if (rc) return rc;
     if (ev[0]) CS_CUDA(cudaEventRecord(ev[0], g.stream));
     if (g.lars) {
-      // per-(worker, layer) rates from this step's x and g, then the LARS step kernel
+      // per-(worker, layer) rates from this step's x and g, then the LARS step kernel.  The
+      // x sums come from the previous LARS step's kernel when nothing else touched params
+      // (the norm pass then reads only g: 24 instead of 28 B/param)
+      const bool carry = g.xnorm_valid && g.xnorm_x == params;
       CS_CUDA(launch_lars_rates(params, grads, g.ld, g.d_tiles, g.n_tiles, g.n_loc, g.d_tile_first,
                                 g.n_layers, g.d_lars_part, lr, g.lars_eta, g.lars_wd, g.lars_eps,
-                                g.d_lrs, g.stream));
+                                g.d_lrs, g.stream, LarsWait(), carry));
       a.lrs = g.d_lrs;
       a.n_layers = g.n_layers;
       a.wd = g.lars_wd;
+      a.xnorm_out = g.d_lars_part;
+      g.xnorm_valid = true;
+      g.xnorm_x = params;
+    } else {
+      g.xnorm_valid = false;
     }
     CS_CUDA(launch_gossip_tma(a, diag, diag ? g.tma_grid_diag : g.tma_grid_plain, g.stream));
     if (ev[1]) CS_CUDA(cudaEventRecord(ev[1], g.stream));
@@ -531,6 +543,7 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
   g.d = d;
   g.ld = ld;
   g.nq = (d + kQuantum - 1) / kQuantum;
+  g.xnorm_valid = false;
   g.rank = proc_rank;
   g.nprocs = nprocs;
   g.n_loc = g.world / nprocs;
@@ -715,6 +728,7 @@ int cs_gossip_step_host(float* params, const float* grads_host, float* psw, floa
 int cs_hier_step(float* params, float* grads, float* psw, float lr, float momentum) {
   int rc = check_bound();
   if (rc) return rc;
+  g.xnorm_valid = false;
   if ((g.lars || g.n_layers > 0) && g.nprocs == 1 && (g.use_peer || !g.use_tma))
     return fail(CS_EUNSUPPORTED, "LARS / layer tables in the single-GPU hierarchical step need the bulk-TMA tiles");
   if (g.lars && g.n_layers == 0) return fail(CS_EINVAL, "LARS needs a layer table (cs_set_layers)");
@@ -839,6 +853,7 @@ int cs_set_layers(const int64_t* layer_bounds, int n_layers, const int32_t* seg_
   int rc = check_bound();
   if (rc) return rc;
   if ((rc = flush_pending()) != CS_OK) return rc;  // the tiles change
+  g.xnorm_valid = false;
   if (!layer_bounds || n_layers == 0) {  // clear: back to the equal split, no layers
     g.layer_bounds.clear();
     g.n_layers = 0;
@@ -960,6 +975,7 @@ int cs_set_step(int64_t step) {
   if (step < 0 || step >= (int64_t(1) << 32)) return fail(CS_EINVAL, "step outside [0, 2^32)");
   int rc = flush_pending();
   if (rc) return rc;
+  g.xnorm_valid = false;  // resumed parameters: the next LARS step recomputes the x norms
   g.step = step;
   g.peer.need_sync = true;  // resumed state: re-replicate leaders to members on the next hier step
   return CS_OK;
@@ -1052,7 +1068,9 @@ int cs_step_bytes(int64_t step, int hier, double* out) {
   const double d = (double)g.d;
   std::vector<int64_t> b = host_bounds(g.d, g.k);
   if (!hier) {
-    out[0] = (g.lars ? 28.0 : 20.0) * g.n_loc * d;  // read x, m, g; write x', m' (+ LARS norms: x, g)
+    // read x, m, g; write x', m'; + LARS norms: x and g (28), or g alone when the previous
+    // single-GPU LARS step carried the x norms (24)
+    out[0] = (g.lars ? ((g.xnorm_valid && !g.use_peer) ? 24.0 : 28.0) : 20.0) * g.n_loc * d;
     std::vector<int32_t> src((size_t)g.k * g.world);
     int rc = cs_topology(step, src.data());
     if (rc) return rc;

@@ -77,6 +77,9 @@ struct LocalArgs {
   // k_hier_local with a layer table: the segment plan and the layer bounds (device), or nullptr
   const int64_t* seg_bounds;    // [k+1]
   const int64_t* layer_bounds;  // [n_layers+1]
+  // LARS on k_gossip_tma: the step writes sum_j x'^2 per (tile, row) into the .x halves of
+  // this double2 [n_tiles][rows] buffer, so the next step's norm pass reads only g
+  double* xnorm_out;
 };
 
 // bf16 wire format (reading C-20): round to the nearest bf16 (ties to even), widen back.
@@ -138,7 +141,7 @@ struct LarsWait {
 cudaError_t launch_lars_rates(const float* x, const float* g, int64_t ld, const TileDesc* tiles,
                               int n_tiles, int rows, const int32_t* tile_first, int n_layers,
                               double* part, float lr, float eta, float wd, float eps, float* lrs,
-                              cudaStream_t st, LarsWait w = LarsWait());
+                              cudaStream_t st, LarsWait w = LarsWait(), bool x_from_carry = false);
 // Hierarchical LARS on one GPU: rates per (group, layer) from the leader's x and the group
 // mean gbar, formed exactly as k_hier_local forms it (ascending sum, then * inv).
 cudaError_t launch_lars_rates_hier(const float* x, const float* g, int64_t ld, const TileDesc* tiles,

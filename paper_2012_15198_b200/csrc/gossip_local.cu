@@ -69,6 +69,20 @@ __device__ __forceinline__ int last_bound_le(const int64_t* bounds, int count, i
   return s;
 }
 
+// LARS carry helpers: fp64 sum of squares of the first `valid` lanes, fixed-order warp sum
+__device__ __forceinline__ double sumsq4(double acc, float4 v, int valid) {
+  acc = __dadd_rn(acc, __dmul_rn((double)v.x, (double)v.x));
+  if (valid > 1) acc = __dadd_rn(acc, __dmul_rn((double)v.y, (double)v.y));
+  if (valid > 2) acc = __dadd_rn(acc, __dmul_rn((double)v.z, (double)v.z));
+  if (valid > 3) acc = __dadd_rn(acc, __dmul_rn((double)v.w, (double)v.w));
+  return acc;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 __device__ __forceinline__ float4 sgd_apply(float4 x, float4 m, float lr) {
   return make_float4(__fsub_rn(x.x, __fmul_rn(lr, m.x)), __fsub_rn(x.y, __fmul_rn(lr, m.y)),
                      __fsub_rn(x.z, __fmul_rn(lr, m.z)), __fsub_rn(x.w, __fmul_rn(lr, m.w)));
@@ -540,6 +554,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 __host__ __device__ inline size_t tma_smem_bytes(int n, int k, bool diag) {
   return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t) + kStages * sizeof(float) +
+         sizeof(double) * (kTmaConsumers / 32) * (size_t)n +  // LARS: per-warp x'^2 sums per row
          fused_smem_bytes(n, k, kTmaThreads / 32, diag);
 }
 
@@ -555,7 +570,8 @@ __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
   float* srate = reinterpret_cast<float*>(empty + kStages);  // [kStages]
-  SmemTopo t = carve(reinterpret_cast<unsigned char*>(srate + kStages), a.n, a.k, DIAG);
+  double* wpart = reinterpret_cast<double*>(srate + kStages);  // [n][8] (LARS carry)
+  SmemTopo t = carve(reinterpret_cast<unsigned char*>(wpart + (kTmaConsumers / 32) * a.n), a.n, a.k, DIAG);
 
   const int n = a.n;
   const int64_t ld = a.ld;
@@ -616,6 +632,7 @@ __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
         const uint32_t e = ord[p];
         const uint32_t row = e & kOrdIdx;
         const float rate = LARS ? srate[st] : lr;
+        double qa = 0.0, qb = 0.0;  // LARS carry: this thread's sum of x'^2 for prev_row / row
 #pragma unroll
         for (int c = 0; c < kVPT; ++c) {
           const int v = c * kTmaConsumers + threadIdx.x;       // float4 index in the tile
@@ -636,19 +653,41 @@ __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
               const float4 xo = pair_mean(yprev[c], a.wire ? bf16r4(y) : y);
               st_stream(a.x + (int64_t)prev_row * ld + j, xo, vv);
               if (DIAG) cd[c].add(xo, rw[prev_row], first_diag, 1.0);
+              if (LARS) qa = sumsq4(qa, xo, vv);
             }
             if (e & kOrdEnd) {
               const float4 xo = pair_mean(y, a.wire ? bf16r4(yfirst[c]) : yfirst[c]);
               st_stream(a.x + (int64_t)row * ld + j, xo, vv);
               if (DIAG) cd[c].add(xo, rw[row], first_diag && (e & kOrdStart), 1.0);
+              if (LARS) qb = sumsq4(qb, xo, vv);
             }
             yprev[c] = y;
           }
         }
         if (DIAG && ((e & kOrdStart) == 0 || (e & kOrdEnd))) first_diag = false;
+        if (LARS && a.xnorm_out) {  // per-warp sums (fixed shuffle order) of each row's x'^2
+          if (!(e & kOrdStart)) {
+            const double s = warp_sum(qa);
+            if (lane == 0) wpart[prev_row * (kTmaConsumers / 32) + warp] = s;
+          }
+          if (e & kOrdEnd) {
+            const double s = warp_sum(qb);
+            if (lane == 0) wpart[row * (kTmaConsumers / 32) + warp] = s;
+          }
+        }
         prev_row = row;
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
+      }
+      if (LARS && a.xnorm_out) {  // the tile's x'^2 per row, warps in order -> .x of part[u][row]
+        asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
+        if (warp == 0)
+          for (int r = lane; r < n; r += 32) {
+            double s = 0.0;
+            for (int w = 0; w < kTmaConsumers / 32; ++w) s = __dadd_rn(s, wpart[r * (kTmaConsumers / 32) + w]);
+            a.xnorm_out[2 * ((int64_t)u * n + r)] = s;
+          }
+        asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers) : "memory");
       }
       if (DIAG) {
 #pragma unroll

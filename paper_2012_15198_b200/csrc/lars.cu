@@ -46,6 +46,9 @@ __device__ __forceinline__ double2 block_sum2(double a, double b, double2* red) 
   return r;  // valid in thread 0
 }
 
+// DOX = false: the x sums were carried from the previous step (k_gossip_tma wrote the .x
+// halves); only g is read and only the .y halves are written.
+template <bool DOX>
 __global__ void __launch_bounds__(kNormThreads)
     k_lars_norms(const float* __restrict__ x, const float* __restrict__ g, int64_t ld,
                  const TileDesc* __restrict__ tiles, int n_tiles, int rows, double2* __restrict__ part,
@@ -81,7 +84,7 @@ __global__ void __launch_bounds__(kNormThreads)
     const float* gr = g + (int64_t)r * ld + td.c0;
     double sx = 0.0, sg = 0.0;
     for (int v = threadIdx.x; 4 * v < td.len; v += kNormThreads) {
-      const float4 a = __ldcs(reinterpret_cast<const float4*>(xr) + v);
+      const float4 a = DOX ? __ldcs(reinterpret_cast<const float4*>(xr) + v) : make_float4(0.f, 0.f, 0.f, 0.f);
       const float4 b = __ldcs(reinterpret_cast<const float4*>(gr) + v);
       const int valid = td.len - 4 * v;  // the layer's ragged end (len % 4 != 0 only at d)
       sx = __dadd_rn(sx, sq(a.x));
@@ -91,7 +94,10 @@ __global__ void __launch_bounds__(kNormThreads)
       if (valid > 3) { sx = __dadd_rn(sx, sq(a.w)); sg = __dadd_rn(sg, sq(b.w)); }
     }
     const double2 s = block_sum2(sx, sg, red);
-    if (threadIdx.x == 0) part[p] = s;
+    if (threadIdx.x == 0) {
+      if (DOX) part[p] = s;
+      else reinterpret_cast<double*>(part)[2 * p + 1] = s.y;  // keep the carried .x
+    }
   }
 }
 
@@ -178,14 +184,18 @@ cudaError_t launch_lars_rates_hier(const float* x, const float* g, int64_t ld, c
 cudaError_t launch_lars_rates(const float* x, const float* g, int64_t ld, const TileDesc* tiles,
                               int n_tiles, int rows, const int32_t* tile_first, int n_layers,
                               double* part, float lr, float eta, float wd, float eps, float* lrs,
-                              cudaStream_t st, LarsWait w) {
+                              cudaStream_t st, LarsWait w, bool x_from_carry) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t pairs = (int64_t)n_tiles * rows;
   const int grid = (int)(pairs < (int64_t)sms * 8 ? pairs : (int64_t)sms * 8);
-  k_lars_norms<<<grid > 0 ? grid : 1, kNormThreads, 0, st>>>(x, g, ld, tiles, n_tiles, rows,
-                                                             reinterpret_cast<double2*>(part), w);
+  if (x_from_carry)
+    k_lars_norms<false><<<grid > 0 ? grid : 1, kNormThreads, 0, st>>>(x, g, ld, tiles, n_tiles, rows,
+                                                                      reinterpret_cast<double2*>(part), w);
+  else
+    k_lars_norms<true><<<grid > 0 ? grid : 1, kNormThreads, 0, st>>>(x, g, ld, tiles, n_tiles, rows,
+                                                                     reinterpret_cast<double2*>(part), w);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_lars_scale<<<n_layers, kNormThreads, 0, st>>>(reinterpret_cast<const double2*>(part), rows,
