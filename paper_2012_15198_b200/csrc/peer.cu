@@ -20,10 +20,18 @@
 //                w = (w + wbox) * 0.5 (a5, Alg.1 l.17); the last CTA publishes
 //                done[rank] = epoch.
 //
+// Deferred merge (default, CS_PEER_FUSE): the mix of step e is not launched.  Step
+// e+1's push applies it tile by tile: its load warp waits for push_done(e) from every
+// GPU and bulk-loads the inbox tile next to x, m, g, and its compute warps form
+// x = (y + inbox)/2 before the update.  Its last CTA stores the merged weights and
+// publishes push_done(e+1) and done(e).  k_peer_mix runs only in peer_flush (cs_flush,
+// cs_sync, diagnostics, LARS, reconfiguration).  The hybrid walk for several workers
+// per GPU (k_hyb_walk, below) defers its chain-tail merge the same way.
+//
 // The inbox and wbox ping-pong on the epoch parity; a push at epoch e first waits
-// until every GPU finished its mix of epoch e-2, the last reader of that parity.
-// Epochs are monotone, so no flag is ever reset.  Every wait is bounded (~20 s of
-// %globaltimer) and reports CS_ETIMEOUT instead of hanging the GPU.
+// until every GPU finished consuming epoch e-2's inbox (done >= e-2), the last reader
+// of that parity.  Epochs are monotone, so no flag is ever reset.  Every wait is
+// bounded (~20 s of %globaltimer) and reports CS_ETIMEOUT instead of hanging the GPU.
 //
 // The bulk-TMA push was chosen by measurement: on 2 B200s it moves
 // the NVLink segment traffic at ~595 GB/s per direction against ~555 GB/s for
@@ -37,8 +45,9 @@
 //   k_hier_reduce   member c sums the chunk over the members in ascending order and
 //                   scales by fp32(1/|G|) (reading C-12 — the oracle's exact order,
 //                   so the result is bit-identical), then all-gathers the mean chunk
-//                   into every member's gbar; with one group the vector is cut into
-//                   pieces and the update of piece q overlaps h1 of piece q+1;
+//                   into every member's gbar (optionally, CS_HIER_PIECES, the vector is
+//                   cut into column pieces whose update overlaps the next piece's h1;
+//                   measured slower, off by default);
 //   k_peer_push/mix with g = gbar over the leader topology (tag HIER): every
 //                   member exchanges with the member of the same index in the
 //                   source group.  All members hold the leader's state bit for bit
