@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--layers", type=int, default=0, help="random layer table with this many layers")
     ap.add_argument("--layer-plan", action="store_true", help="segments from the layer plan (cs_segment_plan)")
     ap.add_argument("--lars", action="store_true", help="LARS (Table 1 constants, lr 9)")
+    ap.add_argument("--inject-nan", action="store_true",
+                    help="rank 0 puts a NaN in its gradient at step 1: every process must see CS_EDIVERGED")
     ap.add_argument("--sync-at-end", action="store_true",
                     help="no cs_sync between steps (deferred merges run inside the next push); compare at the end")
     a = ap.parse_args()
@@ -91,6 +93,25 @@ def main():
         cs.cs_set_lars(ETA, WD, EPS)
         lr = 9.0
     step_fn = cs.cs_hier_step if a.hier_groups else cs.cs_gossip_step
+    if a.inject_nan:  # the flag must surface as CS_EDIVERGED (-10) on the rank that saw it
+        g0 = bank[:n_loc].clone()
+        if rank == 0:
+            g0[0, d // 2] = float("nan")
+        step_fn(x, bank[:n_loc], w, lr, mu)
+        step_fn(x, g0, w, lr, mu)
+        code = 0
+        try:
+            cs.cs_sync()
+        except cs.CSError as e:
+            code = e.code
+        ok_nan = (code == -10) if rank == 0 else code in (0, -10)
+        okt = torch.tensor([1 if ok_nan else 0], device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            print(f"nan injection: rank0 code {code}: {'OK' if okt.item() else 'FAIL'}", flush=True)
+        dist.barrier()
+        dist.destroy_process_group()
+        sys.exit(0 if okt.item() else 1)
     idx = torch.from_numpy(cols).to(dev)
     ok = True
     if a.diag:

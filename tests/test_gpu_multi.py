@@ -137,6 +137,16 @@ def test_two_gpu_hybrid_deferred_tail_merge_bitwise(n_loc, d, k, extra):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("n_loc,groups", [(1, 0), (3, 0), (1, 1)])
+def test_two_gpu_nonfinite_gradient_reported(n_loc, groups):
+    # push (1/GPU), hybrid walk (3/GPU) and the hierarchical step flag a NaN gradient
+    args = ["--workers-per-gpu", n_loc, "--vector-len", 50_001, "--segments", 3, "--inject-nan"]
+    if groups:
+        args += ["--hier-groups", groups]
+    _run(2, *args)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 def test_two_gpu_hier_deferred_exchange_merge_bitwise():
     # groups >= 2: the leader exchange's merge runs inside the next hierarchical push
     # (opt-in schedule, CS_HIER_FUSE=1)
