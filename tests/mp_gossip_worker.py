@@ -43,6 +43,8 @@ def main():
     ap.add_argument("--lars", action="store_true", help="LARS (Table 1 constants, lr 9)")
     ap.add_argument("--inject-nan", action="store_true",
                     help="rank 0 puts a NaN in its gradient at step 1: every process must see CS_EDIVERGED")
+    ap.add_argument("--skip-step", action="store_true",
+                    help="rank 1 skips step 1: rank 0's merge of that step must time out (CS_ETIMEOUT), not hang")
     ap.add_argument("--sync-at-end", action="store_true",
                     help="no cs_sync between steps (deferred merges run inside the next push); compare at the end")
     a = ap.parse_args()
@@ -93,6 +95,23 @@ def main():
         cs.cs_set_lars(ETA, WD, EPS)
         lr = 9.0
     step_fn = cs.cs_hier_step if a.hier_groups else cs.cs_gossip_step
+    if a.skip_step:  # bounded cross-GPU waits: CS_ETIMEOUT (-13) after ~20 s, never a hang
+        step_fn(x, bank[:n_loc], w, lr, mu)
+        if rank == 0:
+            step_fn(x, bank[:n_loc], w, lr, mu)
+        code = 0
+        try:
+            cs.cs_sync()
+        except cs.CSError as e:
+            code = e.code
+        ok_to = (code == -13) if rank == 0 else code == 0
+        okt = torch.tensor([1 if ok_to else 0], device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            print(f"skipped step: rank0 code {code}: {'OK' if okt.item() else 'FAIL'}", flush=True)
+        dist.barrier()
+        dist.destroy_process_group()
+        sys.exit(0 if okt.item() else 1)
     if a.inject_nan:  # the flag must surface as CS_EDIVERGED (-10) on the rank that saw it
         g0 = bank[:n_loc].clone()
         if rank == 0:

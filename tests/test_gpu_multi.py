@@ -147,6 +147,12 @@ def test_two_gpu_nonfinite_gradient_reported(n_loc, groups):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+def test_two_gpu_missing_peer_times_out():
+    # a peer that never pushes: the waiting GPU gives up after the ~20 s bound with CS_ETIMEOUT
+    _run(2, "--workers-per-gpu", 1, "--vector-len", 50_001, "--segments", 3, "--skip-step")
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 def test_two_gpu_hier_deferred_exchange_merge_bitwise():
     # groups >= 2: the leader exchange's merge runs inside the next hierarchical push
     # (opt-in schedule, CS_HIER_FUSE=1)
