@@ -452,7 +452,7 @@ int enqueue_flat_step(float* params, const float* grads, float* psw, float lr, f
 
 extern "C" {
 
-int cs_version(void) { return 100; }
+int cs_version(void) { return 200; }  // 0.2.0: interval, LARS, SGP topology, bf16 wire, cs_flush
 
 const char* cs_last_error(void) { return g_err.c_str(); }
 

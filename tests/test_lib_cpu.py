@@ -148,3 +148,7 @@ def test_host_exponential_topology_matches_oracle():
     assert e.value.code == -12
     with pytest.raises(cs.CSError):
         cs.cs_set_topology_kind(7)
+
+
+def test_abi_version():
+    assert cs.cs_version() == 200  # 0.2.0
