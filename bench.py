@@ -38,6 +38,8 @@ METRIC = "gossip-step time and effective GB/s (params mixed+updated) vs HBM/NVLi
 UNIT = "GB/s"
 NVLINK_PEER_GBS = 770.0      # B200_PROFILING.md: measured peer copy per direction (nominal 900)
 HBM_FALLBACK_GBS = 6650.0    # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+HBM_NOMINAL_GBS = 8000.0     # north_star "~8 TB/s HBM" (B200_PROFILING.md: 7.7 HGX / 8 DGX)
+NVLINK_NOMINAL_GBS = 900.0   # north_star "900 GB/s/dir NVLink"
 
 WORKLOADS = {
     # name: (workers per GPU, d, k, description)
@@ -487,7 +489,8 @@ def main():
                                                                    if lars and world_size == 1 else
                                                                    "28 B x n_loc x d (LARS norms 8 B + step 20 B)" if lars else
                                                                    "20 B x n_loc x d"),
-                "avg_kernel_us": avg_kern_s * 1e6, "launches_timed": kern_launches}
+                "avg_kernel_us": avg_kern_s * 1e6, "launches_timed": kern_launches,
+                "peak_nominal": HBM_NOMINAL_GBS, "frac_nominal": hbm_ach / HBM_NOMINAL_GBS}
     if world_size == 1:
         roofline = roof_hbm
     else:
@@ -500,7 +503,8 @@ def main():
                     "kernel": hot_kernel, "algorithmic_bytes_per_launch": nvl_per_launch,
                     "bytes_formula": "4 B x remote-sourced segment elements (exact from the topology), "
                                      "most-loaded GPU; hierarchical adds the in-group reduce-scatter + all-gather",
-                    "avg_kernel_us": avg_kern_s * 1e6, "launches_timed": kern_launches}
+                    "avg_kernel_us": avg_kern_s * 1e6, "launches_timed": kern_launches,
+                    "peak_nominal": NVLINK_NOMINAL_GBS, "frac_nominal": nvl_ach / NVLINK_NOMINAL_GBS}
         t_nvl = nvl_per_launch / (NVLINK_PEER_GBS * 1e9)
         t_hbm = hbm_per_launch / (hpeak * 1e9)
         roofline = dict(roof_nvl if t_nvl >= t_hbm else roof_hbm)
