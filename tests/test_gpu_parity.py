@@ -332,6 +332,24 @@ def test_each_path_bitwise(path, n, d, k, ld, fuse, monkeypatch):
     assert np.all(xg[:, d:] == 3.0)
 
 
+@pytest.mark.parametrize("path", ["peer", "peer_pm"])
+def test_peer_paths_world_128_bitwise(path, monkeypatch):
+    # world 128 = the driver's 8-GPU weak-scaling run (16 workers per GPU): topology from
+    # the device fallback generator (n > 64), every receiver local in single-GPU emulation
+    if path == "peer_pm":
+        monkeypatch.setenv("CS_PEER_HYBRID", "0")
+    n, d, k, ld = 128, 8_195, 8, 8_196
+    x, m, w, bank2 = _bind(n, d, k, 23, ld=ld, path=PATHS[path])
+    orc = OracleRun(n, d, k, 23)
+    for t in range(3):
+        cs.cs_gossip_step(x, grads_view(bank2, n, t), w, LR, MU)
+        orc.step(LR, MU)
+    cs.cs_sync()
+    assert np.array_equal(x.cpu().numpy()[:, :d], orc.x)
+    assert np.array_equal(m.cpu().numpy()[:, :d], orc.m)
+    assert np.array_equal(w.cpu().numpy(), orc.w)
+
+
 @pytest.mark.parametrize("pieces", [2, 3, 8])
 def test_peer_path_pieces_bitwise(pieces, monkeypatch):
     # the step cut into pieces: push(p+1) on the caller's stream overlaps mix(p) on the aux stream
