@@ -170,6 +170,29 @@ def test_p11_consensus_contraction_identity(n):
         assert S1 == 0.0
 
 
+@pytest.mark.parametrize("n", [3, 8, 64])
+def test_p11_expected_contraction_ratio(n):
+    # iid worker values with variance v: E[S] = (n-1) v and, for any derangement, each
+    # x'_i = (x_i + x_src(i))/2 has E[x'_i^2] = v/2, so E[S'] = n v/2 - v and
+    # E[S'] / E[S] = (n-2) / (2(n-1)).  A wrong weight or a fixed point moves the ratio
+    # (weights (2/3, 1/3) -> (5n-9)/(9(n-1)); src(i) = i -> 1).  For n = 3 every derangement
+    # is a 3-cycle C and (I + C)/2 scales the mean-free subspace by |1 + e^{2 pi i/3}|/2 =
+    # 1/2, so there S'/S = 1/4 holds column by column, not only on average.
+    d, k = 65536, 8
+    x = synth.init_params(7 + n, range(n), d)
+    seg = _segcols(d, k)
+    xo, _, _ = gossip_step(x, np.zeros_like(x), np.zeros_like(x), np.ones((n, k), F32),
+                           T.topology(5, 2, n, k), seg, 0.0, 0.96)
+    x64, xo64 = x.astype(np.float64), xo.astype(np.float64)
+    ratio = ((xo64 - xo64.mean(0)) ** 2).sum() / ((x64 - x64.mean(0)) ** 2).sum()
+    assert abs(ratio - (n - 2) / (2 * (n - 1))) <= 0.02 * (n - 2) / (2 * (n - 1))
+    if n == 3:
+        S = ((x64 - x64.mean(0)) ** 2).sum(0)
+        S1 = ((xo64 - xo64.mean(0)) ** 2).sum(0)
+        big = S > 1e-3
+        assert np.all(np.abs(S1[big] / S[big] - 0.25) <= 1e-5)
+
+
 def test_p13_identical_workers_follow_torch_sgd():
     # consensus fixed point + equal grads: gossip is the identity, so the trajectory is SGD
     n, d, k, steps = 4, 300, 3, 25
