@@ -152,3 +152,15 @@ def test_host_exponential_topology_matches_oracle():
 
 def test_abi_version():
     assert cs.cs_version() == 200  # 0.2.0
+
+
+def test_binding_constants_match_header():
+    """Every status code and constant the binding names equals the header's #define."""
+    txt = open(os.path.join(ROOT, "include", "crossover_sgd.h")).read()
+    defs = {k: int(v) for k, v in re.findall(r"^#define\s+(CS_\w+)\s+(-?\d+)", txt, flags=re.M)}
+    for code, name in cs.STATUS.items():
+        assert defs[name] == code, name
+    assert set(cs.STATUS.values()) == {k for k in defs if k == "CS_OK" or k.startswith("CS_E")}
+    for name in ("CS_MAX_WORLD", "CS_QUANTUM", "CS_IPC_HANDLE_BYTES", "CS_TAG_FLAT", "CS_TAG_HIER",
+                 "CS_PATH_AUTO", "CS_PATH_REG", "CS_PATH_TMA", "CS_PATH_PEER"):
+        assert getattr(cs, name) == defs[name], name
