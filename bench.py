@@ -255,12 +255,14 @@ def main():
     ap.add_argument("--path", default="auto", choices=["auto", "reg", "tma", "peer"],
                     help="library kernel path (cs_set_path); peer with 1 GPU = single-GPU emulation")
     args = ap.parse_args()
+    # the timing rules need W >= 3 untimed warm-up steps; the line reports the W actually run
+    args.warmup = max(args.warmup, 3)
 
     rank = int(os.environ.get("RANK", "0"))
     world_size = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.config is None:
-        args.config = "c2" if world_size == 1 else "c2"
+        args.config = "c2"
     if args.impl == "reference":
         run_reference(args, rank, world_size)
         return

@@ -17,6 +17,7 @@ def _run(extra_env=None):
 
 
 def test_reference_arm_json_line():
+    # launched with --warmup 1: the bench raises W to the timing rules' floor of 3 and reports it
     p = _run()
     assert p.returncode == 0, p.stderr[-2000:]
     line = [ln for ln in p.stdout.splitlines() if ln.startswith("{")][-1]
@@ -25,7 +26,7 @@ def test_reference_arm_json_line():
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
                 "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
         assert key in j, key
-    assert j["steps"] == 2 and j["warmup"] == 1 and j["higher_is_better"] is True and j["value"] > 0
+    assert j["steps"] == 2 and j["warmup"] == 3 and j["higher_is_better"] is True and j["value"] > 0
     assert j["cpu_baseline"]["kind"] == "oracle" and j["cpu_baseline"]["cores"] >= 1
     assert j["cpu_baseline"]["value"] == j["value"] and "sample" in j["cpu_baseline"]
     assert j["e2e"] == {"value": j["value"], "unit": j["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
