@@ -164,3 +164,5 @@ def test_binding_constants_match_header():
     for name in ("CS_MAX_WORLD", "CS_QUANTUM", "CS_IPC_HANDLE_BYTES", "CS_TAG_FLAT", "CS_TAG_HIER",
                  "CS_PATH_AUTO", "CS_PATH_REG", "CS_PATH_TMA", "CS_PATH_PEER"):
         assert getattr(cs, name) == defs[name], name
+    for name in ("TOPO_CROSSOVER", "TOPO_EXPONENTIAL", "WIRE_FP32", "WIRE_BF16"):
+        assert getattr(cs, name) == defs["CS_" + name], name

@@ -9,6 +9,9 @@
    mixes its inbox (l.17).  Run with gloo isend/irecv between processes on the
    oracle's arithmetic, routed by the library's topology, and compared with the
    single-process oracle step (bitwise): the contract the NVLink kernel implements.
+   Also with the bf16 wire (reading C-20: the sender's y rounded by torch's own bf16
+   conversion, the weight in fp32) and with SGP's exponential graph
+   (cs_set_topology_kind, PAPER.md:103).
 """
 import os
 import socket
@@ -30,7 +33,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, ws, port, n_loc, d, k, steps, q):
+def _worker(rank, ws, port, n_loc, d, k, steps, q, wire=None, exponential=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import paper_2012_15198_b200 as cs
@@ -43,6 +46,8 @@ def _worker(rank, ws, port, n_loc, d, k, steps, q):
         world, seed = n_loc * ws, 5
         first = rank * n_loc
         cs.cs_init(world, world, k, seed)
+        if exponential:
+            cs.cs_set_topology_kind(cs.TOPO_EXPONENTIAL)
         # 1. topology agreement across processes
         topo = torch.from_numpy(np.stack([cs.cs_topology(t, world, k) for t in range(steps)]))
         allt = [torch.zeros_like(topo) for _ in range(ws)]
@@ -60,7 +65,7 @@ def _worker(rank, ws, port, n_loc, d, k, steps, q):
         for t in range(steps):
             src = cs.cs_topology(t, world, k)
             g_all = synth.grads_at(bank, world, t)
-            x_all, m_all, w_all = gossip_step(x_all, m_all, g_all, w_all, src, seg, lr, mu)
+            x_all, m_all, w_all = gossip_step(x_all, m_all, g_all, w_all, src, seg, lr, mu, wire=wire)
             m, y = local_update(x, m, g_all[first:first + n_loc], lr, mu)
             inbox = np.zeros_like(y)
             wbox = np.zeros_like(w)
@@ -70,20 +75,28 @@ def _worker(rank, ws, port, n_loc, d, k, steps, q):
                 for r in range(n_loc):                      # push (isend) my segments
                     i = first + r
                     peer = dst[i]
-                    payload = torch.from_numpy(np.concatenate([y[r, b[s]:b[s + 1]], w[r, s:s + 1]]))
+                    # the wire carries y[R_s] (bf16 via torch's own rounding when wire="bf16",
+                    # reading C-20) and the fp32 push-sum weight as a second message
+                    ys = torch.from_numpy(y[r, b[s]:b[s + 1]].copy())
+                    if wire == "bf16":
+                        ys = ys.to(torch.bfloat16)
+                    ws_ = torch.from_numpy(w[r, s:s + 1].copy())
                     if peer // n_loc == rank:
-                        inbox[peer - first, b[s]:b[s + 1]] = payload[:-1].numpy()
-                        wbox[peer - first, s] = payload[-1].item()
+                        inbox[peer - first, b[s]:b[s + 1]] = ys.float().numpy()
+                        wbox[peer - first, s] = ws_.item()
                     else:
-                        reqs.append(dist.isend(payload, peer // n_loc, tag=s * world + peer))
+                        reqs.append(dist.isend(ys, peer // n_loc, tag=s * world + peer))
+                        reqs.append(dist.isend(ws_, peer // n_loc, tag=(k + s) * world + peer))
                 for r in range(n_loc):                      # irecv what my workers receive
                     i = first + r
                     sender = int(src[s][i])
                     if sender // n_loc != rank:
-                        buf = torch.zeros(b[s + 1] - b[s] + 1)
+                        buf = torch.zeros(b[s + 1] - b[s], dtype=torch.bfloat16 if wire == "bf16" else torch.float32)
+                        wbuf = torch.zeros(1)
                         dist.recv(buf, sender // n_loc, tag=s * world + i)
-                        inbox[r, b[s]:b[s + 1]] = buf[:-1].numpy()
-                        wbox[r, s] = buf[-1].item()
+                        dist.recv(wbuf, sender // n_loc, tag=(k + s) * world + i)
+                        inbox[r, b[s]:b[s + 1]] = buf.float().numpy()
+                        wbox[r, s] = wbuf.item()
             for rq in reqs:
                 rq.wait()
             x = ((y + inbox).astype(np.float32) * np.float32(0.5)).astype(np.float32)
@@ -95,12 +108,17 @@ def _worker(rank, ws, port, n_loc, d, k, steps, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_loc,d,k", [(1, 97, 2), (3, 200, 5), (4, 64, 2)])
-def test_two_process_partitioned_exchange(n_loc, d, k):
+@pytest.mark.parametrize("n_loc,d,k,wire,exponential", [
+    (1, 97, 2, None, False), (3, 200, 5, None, False), (4, 64, 2, None, False),
+    (3, 200, 5, "bf16", False),   # bf16 wire (C-20), rounded by torch on the sender side
+    (4, 96, 3, None, True),       # SGP's exponential graph from cs_set_topology_kind
+    (2, 130, 4, "bf16", True),
+])
+def test_two_process_partitioned_exchange(n_loc, d, k, wire, exponential):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_loc, d, k, 4, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_loc, d, k, 4, q, wire, exponential)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
