@@ -14,7 +14,10 @@ h3  the leader's x', w' propagate to its members.
 
 Routed by the library's topology, computed on the oracle's arithmetic, and
 compared bitwise with the single-process `oracle.hierarchical.hier_step`: the
-contract `cs_hier_step` implements with NCCL + NVLink peer memory.
+contract `cs_hier_step` implements with NCCL + NVLink peer memory.  With LARS the
+leader's per-layer rates come from its x and the group-reduced gradient (PAPER.md:197
+"LARS needs the gradient norm synchronised", reading C-18), compared with
+`oracle.lars.lars_hier_step`.
 """
 import os
 import socket
@@ -36,7 +39,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, ws, port, n_loc, d, k, groups, steps, q):
+def _worker(rank, ws, port, n_loc, d, k, groups, steps, q, lars=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import paper_2012_15198_b200 as cs
@@ -44,6 +47,7 @@ def _worker(rank, ws, port, n_loc, d, k, groups, steps, q):
     from oracle import topology as T
     from oracle.gossip import local_update
     from oracle.hierarchical import hier_step
+    from oracle.lars import lars_hier_step, lars_update, layer_lr
 
     F32 = np.float32
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=ws)
@@ -65,11 +69,21 @@ def _worker(rank, ws, port, n_loc, d, k, groups, steps, q):
         w_all = np.ones((world, k), F32)
         x, m, w = (a[first:first + n_loc].copy() for a in (x_all, m_all, w_all))
         lr, mu = synth.DEFAULT_LR, synth.DEFAULT_MOMENTUM
+        # LARS: 3 uneven layers, Table 1-style trust ratio (eta, wd, eps); PAPER.md:197 needs the
+        # leader's rate from the group-reduced gradient (reading C-18)
+        eta, wd, eps = 0.01, 1e-3, 1e-9
+        lb = np.array([0, d // 5, d // 2 + 3, d])
+        layer_of_col = np.searchsorted(lb, np.arange(d), side="right") - 1
         topo_ok = True
         for t in range(steps):
             g_all = synth.grads_at(bank, world, t)
-            x_all, m_all, w_all, srcL_oracle = hier_step(x_all, m_all, g_all, w_all, groups, seed, t, k,
-                                                        seg, lr, mu)
+            if lars:
+                x_all, m_all, w_all, _ = lars_hier_step(x_all, m_all, g_all, w_all, groups, seed, t, k, seg,
+                                                        lb, lr, mu, eta, wd, eps)
+                srcL_oracle = T.topology(seed, t, groups, k, T.TAG_HIER) if groups >= 2 else None
+            else:
+                x_all, m_all, w_all, srcL_oracle = hier_step(x_all, m_all, g_all, w_all, groups, seed, t, k,
+                                                            seg, lr, mu)
             g = g_all[first:first + n_loc]
             srcL = cs.cs_topology_hier(t, groups, k) if groups >= 2 else None
             if srcL is not None:
@@ -94,7 +108,12 @@ def _worker(rank, ws, port, n_loc, d, k, groups, steps, q):
                         gi = buf.numpy()
                     acc = gi.astype(F32) if acc is None else (acc + gi).astype(F32)
                 gbar = (acc * F32(1.0 / gs)).astype(F32)
-                mL, y = local_update(x[L - first][None], m[L - first][None], gbar[None], lr, mu)
+                if lars:
+                    rates = layer_lr(x[L - first][None], gbar[None], lb, lr, eta, wd, eps)
+                    mL, y = lars_update(x[L - first][None], m[L - first][None], gbar[None], rates,
+                                        layer_of_col, mu, wd)
+                else:
+                    mL, y = local_update(x[L - first][None], m[L - first][None], gbar[None], lr, mu)
                 m[L - first], yL[G], wL[G] = mL[0], y[0], w[L - first].copy()
             for rq in reqs:
                 rq.wait()
@@ -157,17 +176,19 @@ def _worker(rank, ws, port, n_loc, d, k, groups, steps, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_loc,d,k,groups", [
-    (4, 96, 2, 4),    # two groups inside each process
-    (4, 200, 3, 2),   # one group per process: L = 2, forced leader swap (P12)
-    (2, 97, 2, 1),    # one group spanning both processes: allreduce-SGD, no gossip
-    (3, 160, 5, 3),   # group {2,3} spans the process boundary
+@pytest.mark.parametrize("n_loc,d,k,groups,lars", [
+    (4, 96, 2, 4, False),    # two groups inside each process
+    (4, 200, 3, 2, False),   # one group per process: L = 2, forced leader swap (P12)
+    (2, 97, 2, 1, False),    # one group spanning both processes: allreduce-SGD, no gossip
+    (3, 160, 5, 3, False),   # group {2,3} spans the process boundary
+    (3, 160, 5, 3, True),    # the same with LARS on the group-reduced gradient
+    (2, 97, 2, 1, True),     # LARS with one group spanning both processes
 ])
-def test_two_process_hierarchical(n_loc, d, k, groups):
+def test_two_process_hierarchical(n_loc, d, k, groups, lars):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_loc, d, k, groups, 3, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_loc, d, k, groups, 3, q, lars)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
