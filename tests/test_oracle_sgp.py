@@ -44,3 +44,15 @@ def test_exact_average_after_log2_n_rounds(n):
         x, _, w = gossip_step(x, z, z, w, exponential_topology(t, n, 1), seg, 0.0, 0.0)
     assert np.array_equal(x, np.broadcast_to(mean.astype(F32), x.shape))
     assert np.all(w == 1)
+
+
+@pytest.mark.parametrize("n", [2, 8, 32])
+def test_peer_offsets_cycle_through_powers_of_two(n):
+    # the send offset at round t is 2^(t mod log2 n), so rounds 0..log2 n - 1
+    # use the distinct offsets 1, 2, 4, ..., n/2 and the schedule repeats with period log2 n
+    L = n.bit_length() - 1
+    offs = [(exponential_peer(0, t, n) - 0) % n for t in range(3 * L)]
+    assert offs[:L] == [1 << j for j in range(L)]
+    assert offs == offs[:L] * 3
+    for t in range(L):
+        assert np.array_equal(exponential_topology(t, n, 2), exponential_topology(t + L, n, 2))
