@@ -252,6 +252,10 @@ def main():
     ap.add_argument("--scheme", default="crossover", choices=["crossover", "sgp", "allreduce"],
                     help="SURVEY 8(f) #3 baselines on the same machinery: sgp = SGP's directed exponential "
                          "graph, model-wise (k=1 unless --k); allreduce = AllReduce-SGD (hierarchical, 1 group)")
+    ap.add_argument("--schedule", default="instep", choices=["instep", "deferred", "split"],
+                    help="multi-GPU step schedule (cs_set_schedule): instep = merged params when the step's "
+                         "work completes (default); deferred = the merge runs inside the next step (opt-in, "
+                         "params readable only after cs_flush); split = push kernel + merge kernel")
     ap.add_argument("--path", default="auto", choices=["auto", "reg", "tma", "peer"],
                     help="library kernel path (cs_set_path); peer with 1 GPU = single-GPU emulation")
     args = ap.parse_args()
@@ -308,6 +312,8 @@ def main():
         cs.cs_set_topology_kind(cs.TOPO_EXPONENTIAL)
     if args.wire == "bf16":
         cs.cs_set_wire(cs.WIRE_BF16)
+    cs.cs_set_schedule({"instep": cs.CS_SCHED_INSTEP, "deferred": cs.CS_SCHED_DEFERRED,
+                        "split": cs.CS_SCHED_SPLIT}[args.schedule])
     step_fn = cs.cs_hier_step if hier else cs.cs_gossip_step
     cs.cs_set_path({"auto": 0, "reg": 1, "tma": 2, "peer": 3}[args.path])
     stream = torch.cuda.Stream(dev)
@@ -523,6 +529,7 @@ def main():
               "config": {"workload": f"{args.config}: {desc}", "world": world, "workers_per_gpu": n_loc,
                          "d": d, "k": k, "seed": seed, "lr": lr, "momentum": mu,
                          "parallelism": f"workers partitioned over {world_size} GPU(s)", "scheme": args.scheme,
+                         "schedule": args.schedule,
                          "wire": args.wire,
                          "l2": f"inputs larger than L2 ({20.0 * n_loc * d / 1e9:.2f} GB moved per step per GPU)"},
               "step_us": ms_step * 1e3,

@@ -146,6 +146,30 @@ int cs_set_stream(void* stream);
 #define CS_PATH_PEER 3
 int cs_set_path(int path);
 
+/* Schedule of the multi-GPU flat step (applies now and to later cs_bind calls):
+ *   CS_SCHED_INSTEP    (default) the merge a5 of a step completes inside that step's
+ *                      enqueued work: when the stream reaches the end of cs_gossip_step,
+ *                      params / psw hold x', w' ("parameter averaging is
+ *                      processed after the gradient is applied"; Alg.1 l.12-17).  One worker
+ *                      per GPU: one launch (k_push_merge: update, NVLink push and per-tile
+ *                      landed-progress flags, in-kernel merge).  Several: walk + tail merge.
+ *   CS_SCHED_DEFERRED  (opt-in) the merge of step t runs inside step t+1's kernel; params
+ *                      hold y_t in between, so cs_flush / cs_sync must precede any read.
+ *   CS_SCHED_SPLIT     a push kernel, then a separate merge kernel after a cross-GPU wait.
+ * Results are bit-identical under every schedule.  Errors: CS_ENOTINIT, CS_EINVAL. */
+#define CS_SCHED_INSTEP   0
+#define CS_SCHED_DEFERRED 1
+#define CS_SCHED_SPLIT    2
+int cs_set_schedule(int schedule);
+
+/* Test hook: from the next cs_bind (nprocs == 1), run the multi-GPU protocol for
+ * `vranks` ranks on this one GPU: rank v owns rows [v*world/vranks, (v+1)*world/vranks)
+ * of the bound buffers (which hold all `world` rows), has its own exchange region, and
+ * every kernel is one cooperative launch whose CTAs are split among the ranks, so ranks
+ * that wait on one another are co-resident.  Same kernels, flags and peer addressing as
+ * across GPUs.  vranks = 1 restores the normal binding.  Errors: CS_ENOTINIT, CS_EINVAL. */
+int cs_test_emulate_ranks(int vranks);
+
 /* Multi-GPU (nprocs > 1): export this process's peer-visible exchange region
  * (allocated by cs_bind) as a CUDA IPC handle (CS_IPC_HANDLE_BYTES bytes into
  * handle_out).  The caller all-gathers the handles (e.g. over torch.distributed)

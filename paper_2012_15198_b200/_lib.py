@@ -27,6 +27,7 @@ CS_IPC_HANDLE_BYTES = 64
 CS_TAG_FLAT = 0
 CS_TAG_HIER = 1
 CS_PATH_AUTO, CS_PATH_REG, CS_PATH_TMA, CS_PATH_PEER = 0, 1, 2, 3
+CS_SCHED_INSTEP, CS_SCHED_DEFERRED, CS_SCHED_SPLIT = 0, 1, 2
 
 STATUS = {
     0: "CS_OK", -1: "CS_EINVAL_WORLD", -2: "CS_EINVAL_GROUPS", -3: "CS_EINVAL_SEGMENTS",
@@ -48,6 +49,8 @@ _SIGS = {
     "cs_bind": (_c_int, [_vp, _c_i64, _c_i64, _c_int, _c_int, _vp]),
     "cs_set_stream": (_c_int, [_vp]),
     "cs_set_path": (_c_int, [_c_int]),
+    "cs_set_schedule": (_c_int, [_c_int]),
+    "cs_test_emulate_ranks": (_c_int, [_c_int]),
     "cs_ipc_export": (_c_int, [_vp]),
     "cs_ipc_import": (_c_int, [_vp]),
     "cs_gossip_step": (_c_int, [_vp, _vp, _vp, _c_f, _c_f]),
@@ -319,3 +322,15 @@ def cs_kernel_info() -> tuple[str, int]:
 
 def cs_set_path(path: int) -> None:
     _check(lib.cs_set_path(path), "cs_set_path")
+
+
+def cs_set_schedule(schedule: int) -> None:
+    """CS_SCHED_INSTEP (default: merged params when the step's work completes),
+    CS_SCHED_DEFERRED (opt-in: the merge runs in the next step; cs_flush before reading),
+    CS_SCHED_SPLIT (push kernel + merge kernel)."""
+    _check(lib.cs_set_schedule(schedule), "cs_set_schedule")
+
+
+def cs_test_emulate_ranks(vranks: int) -> None:
+    """Test hook: the multi-GPU protocol for `vranks` ranks on this one GPU (next cs_bind)."""
+    _check(lib.cs_test_emulate_ranks(vranks), "cs_test_emulate_ranks")

@@ -108,6 +108,11 @@ struct Ctx {
   int32_t* d_exp = nullptr;
   int exp_h = 0;
 
+  // multi-GPU schedule (cs_set_schedule) and the single-GPU emulation of V ranks
+  // (cs_test_emulate_ranks): both apply from the next cs_bind
+  int sched = CS_SCHED_INSTEP;
+  int vranks = 1;
+
   // hot-kernel timing (cs_set_timing): event pairs recorded around each launch
   bool timing = false;
   std::vector<cudaEvent_t> events;
@@ -372,6 +377,13 @@ PeerStepArgs peer_args(float* params, const float* grads, float* psw, float lr, 
   pa.eps = 0.f;
   pa.tile_first = nullptr;
   pa.lars_part = nullptr;
+  pa.g_off = 0;
+  if (g.vranks > 1) {  // emulated ranks: rank 0's view; each CTA shifts to its own rank
+    pa.n_loc = g.world / g.vranks;
+    pa.nprocs = g.vranks;
+    pa.rank = 0;
+    pa.first = 0;
+  }
   return pa;
 }
 
@@ -568,7 +580,9 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
   CS_CUDA(cudaMalloc(&g.d_partials, sizeof(double) * 2 * (size_t)local_max_grid()));
   CS_CUDA(cudaMalloc(&g.d_counter, sizeof(unsigned)));
   CS_CUDA(cudaMemset(g.d_counter, 0, sizeof(unsigned)));
-  g.use_peer = nprocs > 1 || g.path == CS_PATH_PEER;
+  if (g.vranks > 1 && (nprocs != 1 || g.world % g.vranks != 0))
+    return fail(CS_EINVAL, "emulated ranks need nprocs == 1 and vranks dividing world");
+  g.use_peer = nprocs > 1 || g.path == CS_PATH_PEER || g.vranks > 1;
   if (g.path == CS_PATH_TMA && !fused_topology_ok(g.world, g.k))
     return fail(CS_EUNSUPPORTED, "CS_PATH_TMA needs world <= 64 and k*world <= 2048");
   g.use_tma = !g.use_peer && g.path != CS_PATH_REG && fused_topology_ok(g.world, g.k);
@@ -581,10 +595,14 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
   }
   if (g.use_peer) {
     // hierarchical steps over the peer path: one worker per GPU, groups of world/groups GPUs
-    const int hier_gs = (nprocs > 1 && g.n_loc == 1) ? g.world / g.groups : 0;
-    int rc = peer_alloc(g.peer, g.n_loc, d, ld, g.k, nprocs, proc_rank, hier_gs);
+    const int ranks = g.vranks > 1 ? g.vranks : nprocs;
+    const int n_loc_rank = g.world / ranks;
+    const int hier_gs = (ranks > 1 && n_loc_rank == 1) ? g.world / g.groups : 0;
+    int rc = peer_alloc(g.peer, n_loc_rank, d, ld, g.k, ranks, g.vranks > 1 ? 0 : proc_rank, hier_gs, g.vranks);
     if (rc) return fail(rc, "%s", peer_error());
-    if (nprocs == 1) {  // single-GPU emulation: the only peer is this GPU
+    rc = peer_set_schedule(g.peer, g.sched, g.stream);
+    if (rc) return fail(rc, "%s", peer_error());
+    if (nprocs == 1) {  // single-GPU emulation: every rank's region is on this GPU
       rc = peer_import_self(g.peer);
       if (rc) return fail(rc, "%s", peer_error());
     }
@@ -621,6 +639,25 @@ int cs_set_path(int path) {
   if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
   if (path < CS_PATH_AUTO || path > CS_PATH_PEER) return fail(CS_EINVAL, "unknown path %d", path);
   g.path = path;
+  return CS_OK;
+}
+
+int cs_set_schedule(int schedule) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (schedule < CS_SCHED_INSTEP || schedule > CS_SCHED_SPLIT) return fail(CS_EINVAL, "unknown schedule %d", schedule);
+  g.sched = schedule;
+  if (g.bound && g.use_peer) {
+    const int rc = peer_set_schedule(g.peer, schedule, g.stream);
+    if (rc) return fail(rc, "%s", peer_error());
+  }
+  return CS_OK;
+}
+
+int cs_test_emulate_ranks(int vranks) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  if (vranks < 1 || vranks > g.world || g.world % vranks != 0)
+    return fail(CS_EINVAL, "vranks %d must divide world %d", vranks, g.world);
+  g.vranks = vranks;
   return CS_OK;
 }
 
@@ -687,9 +724,12 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
       if (rc) return fail(rc, "%s", peer_error());
     }
     const bool fused_topo = g.world <= 64;  // the topology is drawn inside the first kernel
-    // deferred merge: one push launch per step (its merge runs in the next push / cs_flush)
-    g.launches_per_step = (g.peer.last_fused ? 1 : 2) + (fused_topo ? 0 : 1) + (g.lars ? 2 : 0);
-    g.hot_kernel = g.peer.use_hybrid  ? (g.peer.last_fused ? "k_hyb_walk(fused tail merge)" : "k_hyb_walk+k_hyb_tail")
+    const bool merge = peer_merge_ok(g.peer, pa);
+    // in-step merge: one launch; deferred merge: one push launch per step (its merge runs in
+    // the next push / cs_flush); split: push + mix
+    g.launches_per_step = ((merge || g.peer.last_fused) ? 1 : 2) + (fused_topo ? 0 : 1) + (g.lars ? 2 : 0);
+    g.hot_kernel = merge               ? (g.lars ? "k_lars_norms+k_lars_scale+k_push_merge" : "k_push_merge")
+                   : g.peer.use_hybrid ? (g.peer.last_fused ? "k_hyb_walk(fused tail merge)" : "k_hyb_walk+k_hyb_tail")
                    : g.lars           ? "k_lars_norms+k_lars_scale+k_peer_push+k_peer_mix"
                    : g.peer.last_fused ? "k_peer_push(fused merge)"
                                        : "k_peer_push+k_peer_mix";

@@ -62,8 +62,10 @@
 #include <vector>
 
 #include "../../include/crossover_sgd.h"
+#include "arith.cuh"
 #include "common.cuh"
 #include "peer.cuh"
+#include "peer_dev.cuh"
 #include "ptx.cuh"
 #include "topo_device.cuh"
 
@@ -80,7 +82,6 @@ int perr(int code, const char* what, cudaError_t e) {
   return code;
 }
 
-constexpr int kPeerTile = 2048;                     // columns per unit: 8 KB of one worker's row
 constexpr int kCompute = 256;                       // compute warps
 constexpr int kPushThreads = kCompute + 64;         // + load warp + store warp
 constexpr int kPer = kPeerTile / 4 / kCompute;      // float4 per compute thread per array
@@ -90,7 +91,6 @@ constexpr size_t kRingBytes = kTileBytes * (3 * kStagesA + kSlotsY);
 constexpr int kMaxRecvSmem = 2048;                  // receivers table in smem when k*n_loc <= this
 constexpr int kMixThreads = 256;
 constexpr int kHierThreads = 256;
-constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -103,17 +103,8 @@ size_t push_smem_bytes(int k, int n_loc) {
 
 bool fused_topo_ok(int ntop, int k, int n_loc) { return ntop <= 64 && (int64_t)k * n_loc <= kMaxRecvSmem; }
 
-// wait until (int32)(*p - target) >= 0 polling relaxed, then acquire; false on timeout
-__device__ bool wait_acquire(const uint32_t* p, uint32_t target) {
-  uint64_t t0 = 0;
-  while ((int32_t)(ptx::ld_relaxed_sys(p) - target) < 0) {
-    const uint64_t now = ptx::globaltimer();
-    if (t0 == 0) t0 = now;
-    if (now - t0 > kSpinLimitNs) return false;
-    __nanosleep(32);
-  }
-  ptx::fence_acq_rel_sys();
-  return true;
+__device__ __forceinline__ bool wait_acquire(const uint32_t* p, uint32_t target) {
+  return ptx::wait_geq_sys(p, target);
 }
 
 // Grid-wide completion: every CTA adds 1 to the arrival counter at `count_off`;
@@ -157,29 +148,6 @@ struct PeerKernelArgs {
   size_t off_inbox, off_wbox, off_done, off_count, off_pdone, off_pcount, off_d2;
 };
 
-__device__ __forceinline__ float4 decay4(float4 g, float4 x, float wd) {  // g + wd*x (C-18)
-  return make_float4(__fadd_rn(g.x, __fmul_rn(wd, x.x)), __fadd_rn(g.y, __fmul_rn(wd, x.y)),
-                     __fadd_rn(g.z, __fmul_rn(wd, x.z)), __fadd_rn(g.w, __fmul_rn(wd, x.w)));
-}
-__device__ __forceinline__ float4 mom4(float4 m, float4 g, float mu) {
-  return make_float4(__fadd_rn(__fmul_rn(mu, m.x), g.x), __fadd_rn(__fmul_rn(mu, m.y), g.y),
-                     __fadd_rn(__fmul_rn(mu, m.z), g.z), __fadd_rn(__fmul_rn(mu, m.w), g.w));
-}
-__device__ __forceinline__ float4 sgd4(float4 x, float4 m, float lr) {
-  return make_float4(__fsub_rn(x.x, __fmul_rn(lr, m.x)), __fsub_rn(x.y, __fmul_rn(lr, m.y)),
-                     __fsub_rn(x.z, __fmul_rn(lr, m.z)), __fsub_rn(x.w, __fmul_rn(lr, m.w)));
-}
-__device__ __forceinline__ float4 mean4(float4 a, float4 b) {
-  return make_float4(__fmul_rn(__fadd_rn(a.x, b.x), 0.5f), __fmul_rn(__fadd_rn(a.y, b.y), 0.5f),
-                     __fmul_rn(__fadd_rn(a.z, b.z), 0.5f), __fmul_rn(__fadd_rn(a.w, b.w), 0.5f));
-}
-__device__ __forceinline__ float pair_mean1(float a, float b) { return __fmul_rn(__fadd_rn(a, b), 0.5f); }
-__device__ __forceinline__ float4 add4(float4 a, float4 b) {
-  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
-}
-__device__ __forceinline__ float4 scale4(float4 a, float s) {
-  return make_float4(__fmul_rn(a.x, s), __fmul_rn(a.y, s), __fmul_rn(a.z, s), __fmul_rn(a.w, s));
-}
 // streaming store (evict-first): data not read again this step
 __device__ __forceinline__ void st4_cs(float* p, float4 v, int valid) {
   if (valid == 4) {
@@ -208,12 +176,6 @@ __device__ __forceinline__ float4 ld4_valid(const float* p, int valid) {
   if (valid > 2) v.z = __ldcg(p + 2);
   return v;
 }
-__device__ __forceinline__ bool nonfinite4(float4 g) {
-  const uint32_t e = 0x7f800000u;
-  return ((__float_as_uint(g.x) & e) == e) | ((__float_as_uint(g.y) & e) == e) |
-         ((__float_as_uint(g.z) & e) == e) | ((__float_as_uint(g.w) & e) == e);
-}
-
 // Shared-memory unit metadata.
 struct Meta {
   const int64_t* bnd;   // [k+1]
@@ -248,15 +210,6 @@ __device__ __forceinline__ Unit unit_at(const PeerKernelArgs& a, const Meta& M, 
   x.len = (int)(c1 - c0);
   x.layer = 0;
   return x;
-}
-
-// Global worker that receives segment s of local worker r (send_to, Alg.1 l.6):
-// flat: dst_s(first + r); hierarchical: the member of the same index in group
-// dstL_s(my group) (replicated leader).
-__device__ __forceinline__ int receiver_worker(const PeerStepArgs& s, int seg, int r) {
-  if (s.gs == 0) return s.dst[(int64_t)seg * s.world + s.first + r];
-  const int grp = s.rank / s.gs, member = s.rank - grp * s.gs;
-  return s.dst[(int64_t)seg * s.groups + grp] * s.gs + member;
 }
 
 __device__ __forceinline__ void receiver_of(const PeerKernelArgs& a, const Meta& M, int seg, int r, int& rp,
@@ -1348,8 +1301,28 @@ int peer_diag(PeerState& p, const PeerStepArgs& a, double* partials, int partial
   return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "diagnostics launch", e);
 }
 
-int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs, int rank, int gs) {
+// Chunk table of the in-step merge kernel for the current tiles (p.h_seg_t0).
+int upload_chunks(PeerState& p) {
+  const std::vector<int32_t> c = peer_merge_chunks(p.h_seg_t0, kMergeChunk, p.grid_merge);
+  if (p.d_chunk_t0) cudaFree(p.d_chunk_t0);
+  p.d_chunk_t0 = nullptr;
+  p.n_chunks = (int)c.size() - 1;
+  if (p.n_tiles > p.mflag_cap) return CS_OK;  // no room: the in-step schedule is off (peer_merge_ok)
+  cudaError_t e = cudaSuccess;
+  if (!p.d_stats) {
+    e = cudaMalloc(&p.d_stats, sizeof(unsigned int) * 4);
+    if (e == cudaSuccess) e = cudaMemset(p.d_stats, 0, sizeof(unsigned int) * 4);
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&p.d_chunk_t0, sizeof(int32_t) * c.size());
+  if (e == cudaSuccess) e = cudaMemcpy(p.d_chunk_t0, c.data(), sizeof(int32_t) * c.size(), cudaMemcpyHostToDevice);
+  return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "merge chunk table", e);
+}
+
+int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs, int rank, int gs, int vranks) {
   p = PeerState();
+  p.vranks = vranks > 1 ? vranks : 1;
+  if (p.vranks > 1 && (nprocs != p.vranks || rank != 0))
+    return perr(CS_EINVAL, "emulated ranks: nprocs must equal vranks, rank 0", cudaSuccess);
   p.nprocs = nprocs;
   p.rank = rank;
   p.n_loc = n_loc;
@@ -1421,11 +1394,35 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   p.off_c3 = off;
   p.off_dc1 = off + 64;
   p.off_dc2 = off + 128;
-  p.bytes = align_up(off + 192, 4096);
-  cudaError_t e = cudaMalloc(&p.base, p.bytes);
+  off += 192;
+  // in-step merge schedule (k_push_merge): progress words [2][k][grid_merge]; the grid is
+  // the same on every rank (same device model), checked through the header at import
+  if (n_loc == 1 && k <= 512) {
+    const int cap = peer_merge_capacity(k);
+    p.grid_merge = cap / p.vranks;
+    if (p.grid_merge < 1) p.grid_merge = 0;
+  }
+  off = align_up(off, 256);
+  p.off_claim = off;
+  off += 256;
+  p.off_mflag = off;
+  // room for the chunks of any later layer table (its tiles split at up to CS_MAX_LAYERS bounds)
+  p.mflag_cap = p.grid_merge > 0 ? (int)((d + kPeerTile - 1) / kPeerTile) + k + CS_MAX_LAYERS + 16 : 0;
+  off = align_up(off + 16 * 2 * (size_t)p.mflag_cap, 256);
+  p.off_hdr = off;
+  off += 64;
+  p.bytes = align_up(off, 4096);
+  cudaError_t e = cudaMalloc(&p.base, p.bytes * p.vranks);
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region cudaMalloc", e);
-  e = cudaMemset(p.base, 0, p.bytes);  // inbox padding is read by 16-byte-rounded bulk copies
+  e = cudaMemset(p.base, 0, p.bytes * p.vranks);  // inbox padding is read by 16-byte-rounded bulk copies
   if (e != cudaSuccess) return perr(CS_ECUDA, "peer region memset", e);
+  {
+    // layout header: every rank must run the same grids over the same tiles
+    const int64_t hdr[6] = {0x43524f5353ll, (int64_t)p.grid_merge, (int64_t)p.n_tiles, (int64_t)k, d, (int64_t)p.bytes};
+    for (int r = 0; r < p.vranks && e == cudaSuccess; ++r)
+      e = cudaMemcpy(p.base + (size_t)r * p.bytes + p.off_hdr, hdr, sizeof(hdr), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return perr(CS_ECUDA, "peer region header", e);
+  }
   e = cudaMalloc(&p.d_bounds, sizeof(int64_t) * (k + 1));
   if (e == cudaSuccess) e = cudaMalloc(&p.d_seg_t0, sizeof(int32_t) * (k + 1));
   if (e == cudaSuccess)
@@ -1502,8 +1499,7 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
     if (HP > PeerState::kMaxPieces) HP = PeerState::kMaxPieces;
     if (HP > p.n_tiles) HP = p.n_tiles;
     p.hier_pieces = HP;
-    const char* fz = getenv("CS_PEER_FUSE");
-    p.fuse = !(fz && fz[0] == '0');
+    p.fuse = false;  // the schedule (cs_set_schedule) decides; default: merge inside the step
     p.piece_tile.resize(P + 1);
     for (int q = 0; q <= P; ++q) p.piece_tile[q] = (int)((int64_t)q * p.n_tiles / P);
     int lo = 0, hi = 0;
@@ -1516,8 +1512,9 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   }
   p.peer_base.assign(nprocs, nullptr);
   p.peer_base[rank] = p.base;
+  for (int r = 1; r < p.vranks; ++r) p.peer_base[r] = p.base + (size_t)r * p.bytes;
   p.allocated = true;
-  return CS_OK;
+  return p.grid_merge > 0 ? upload_chunks(p) : CS_OK;
 }
 
 namespace {
@@ -1526,7 +1523,7 @@ void phase_report();
 
 void peer_release(PeerState& p) {
   phase_report();
-  if (p.imported) {
+  if (p.imported && p.vranks <= 1) {  // emulated ranks' regions are one local allocation
     for (int r = 0; r < p.nprocs; ++r)
       if (r != p.rank && p.peer_base[r]) cudaIpcCloseMemHandle(p.peer_base[r]);
   }
@@ -1544,6 +1541,8 @@ void peer_release(PeerState& p) {
   if (p.ev_mix) cudaEventDestroy(p.ev_mix);
   if (p.d_htiles) cudaFree(p.d_htiles);
   if (p.d_tail_tbl) cudaFree(p.d_tail_tbl);
+  if (p.d_chunk_t0) cudaFree(p.d_chunk_t0);
+  if (p.d_stats) cudaFree(p.d_stats);
   p = PeerState();
 }
 
@@ -1559,14 +1558,24 @@ int peer_export(PeerState& p, char* handle_out) {
 
 int peer_import(PeerState& p, const char* all) {
   if (!p.allocated) return perr(CS_ENOTBOUND, "peer region not allocated", cudaSuccess);
+  int64_t mine[6];
+  cudaError_t e = cudaMemcpy(mine, p.base + p.off_hdr, sizeof(mine), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return perr(CS_ECUDA, "peer header", e);
   for (int r = 0; r < p.nprocs; ++r) {
     if (r == p.rank) continue;
     cudaIpcMemHandle_t h;
     memcpy(&h, all + (size_t)r * CS_IPC_HANDLE_BYTES, sizeof(h));
     void* ptr = nullptr;
-    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) return perr(CS_ECUDA, "cudaIpcOpenMemHandle", e);
     p.peer_base[r] = (char*)ptr;
+    // the peer's layout must be ours: same offsets, grid and tiles (same-index CTAs pair up)
+    int64_t theirs[6];
+    e = cudaMemcpy(theirs, p.peer_base[r] + p.off_hdr, sizeof(theirs), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return perr(CS_ECUDA, "peer header read", e);
+    if (memcmp(mine, theirs, sizeof(mine)) != 0)
+      return perr(CS_EINVAL, "peer exchange region layout differs between ranks (device model, d, k or grid)",
+                  cudaSuccess);
   }
   return peer_import_self(p);
 }
@@ -1685,6 +1694,10 @@ int peer_set_layers(PeerState& p, const std::vector<int64_t>& plan, const std::v
   p.h_bounds = plan;
   p.h_seg_t0 = seg_t0;
   p.n_tiles = seg_t0[k];
+  if (p.grid_merge > 0) {
+    const int rc = upload_chunks(p);
+    if (rc) return rc;
+  }
   if (p.use_hybrid) {
     // the hybrid walk's own tiles (TMA-sized), split the same way; LARS norms use them
     const int T = tma_tile_len(p.d, p.grid_hyb);
@@ -1836,6 +1849,7 @@ HybArgs hyb_args(const PeerState& p, const PeerStepArgs& a, uint32_t epoch) {
 int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEvent_t ev0,
                    cudaEvent_t ev1) {
   int rc = CS_OK;
+  if (p.use_hybrid && p.vranks > 1) return perr(CS_EUNSUPPORTED, "emulated ranks: hybrid walk not emulated", cudaSuccess);
   if (p.use_hybrid) {
     // deferred merge: this step's chain tails are merged inside the next walk (or
     // peer_flush); the previous step's tails are merged here before their update
@@ -1868,9 +1882,27 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "hybrid launch", e);
   }
-  // deferred merge: this step's push applies the previous step's merge tile by tile, and
-  // its own merge waits for the next push (or peer_flush); the separate mix pass and its
-  // cross-GPU wait disappear from the step
+  if (peer_merge_ok(p, a)) {
+    // default (one worker per GPU): the merge completes inside this step's kernel
+    p.last_fused = false;
+    if (ev0) cudaEventRecord(ev0, st);
+    rc = peer_flush(p, st);  // a merge left pending by the deferred schedule
+    if (rc) return rc;
+    if (a.world > 64) rc = launch_topology_for(a, a.world, CS_TAG_FLAT, st);
+    if (rc) return rc;
+    PeerStepArgs b = a;
+    b.gs = 0;
+    b.g_off = 0;
+    rc = peer_merge_launch(p, b, ++p.epoch, st);
+    if (rc) return perr(rc, "k_push_merge launch", cudaGetLastError());
+    if (ev1) cudaEventRecord(ev1, st);
+    return CS_OK;
+  }
+  if (p.vranks > 1) return perr(CS_EUNSUPPORTED, "emulated ranks: this schedule is not emulated", cudaSuccess);
+  // deferred merge (opt-in, kSchedDeferred): this step's push applies the previous step's
+  // merge tile by tile, and its own merge waits for the next push (or peer_flush); the
+  // separate mix pass and its cross-GPU wait disappear from the step, but params hold y
+  // until then
   const bool fuse = p.fuse && p.pieces == 1 && a.lrs == nullptr;
   p.last_fused = fuse;
   if (ev0) cudaEventRecord(ev0, st);
@@ -1900,6 +1932,14 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   }
   if (ev1) cudaEventRecord(ev1, st);
   return rc;
+}
+
+int peer_set_schedule(PeerState& p, int sched, cudaStream_t st) {
+  const int rc = peer_flush(p, st);
+  if (rc) return rc;
+  p.sched = sched;
+  p.fuse = sched == kSchedDeferred;
+  return CS_OK;
 }
 
 int peer_flush(PeerState& p, cudaStream_t st) {

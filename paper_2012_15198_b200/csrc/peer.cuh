@@ -9,6 +9,11 @@
 
 namespace cs {
 
+constexpr int kPeerTile = 2048;   // columns per push unit: 8 KB of one worker's row
+
+// Step schedules of the multi-GPU flat step (cs_set_schedule).
+enum { kSchedInStep = 0, kSchedDeferred = 1, kSchedSplit = 2 };
+
 struct PeerStepArgs {
   float* x;
   float* m;
@@ -39,6 +44,8 @@ struct PeerStepArgs {
   float eta, eps;
   const int32_t* tile_first;
   double* lars_part;
+  // nonzero: g is the rank's own exchange region + g_off (the hierarchical group mean)
+  size_t g_off;
 };
 
 struct PeerState {
@@ -48,6 +55,18 @@ struct PeerState {
   int64_t d = 0, ld = 0;
   int n_tiles = 0;
   int grid_push = 0, grid_mix = 0, grid_hier = 0;
+  // single-GPU emulation of the protocol over vranks ranks (one cooperative launch per
+  // kernel, CTAs split among the ranks; 1 = a real process per GPU).  nprocs == vranks then.
+  int vranks = 1;
+  // in-step merge schedule (k_push_merge, one worker per GPU): CTAs per rank and smem
+  int sched = kSchedInStep;
+  int grid_merge = 0;
+  size_t off_mflag = 0, off_hdr = 0;  // per-tile trailers uint4 [2][mflag_cap]; layout header
+  unsigned int* d_stats = nullptr;     // [0]: merge tiles re-read after a failed verification
+  size_t off_claim = 0;                // chunk claim counters [2] (by epoch parity)
+  int mflag_cap = 0;                   // tiles the trailers can cover
+  int32_t* d_chunk_t0 = nullptr;       // [n_chunks + 1] first tile of each chunk
+  int n_chunks = 0;
   int gs = 0;              // hierarchical group size in GPUs (0: flat only)
   int64_t chunk = 0;       // hierarchical reduce-scatter chunk (elements, multiple of 4)
   size_t bytes = 0;
@@ -107,7 +126,7 @@ struct PeerState {
 
 // gs: GPUs per hierarchical group when a hierarchical step is possible (one worker
 // per GPU and groups < world), else 0.
-int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs, int rank, int gs);
+int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs, int rank, int gs, int vranks = 1);
 void peer_release(PeerState& p);
 int peer_export(PeerState& p, char* handle_out);
 int peer_import(PeerState& p, const char* all_handles);
@@ -123,6 +142,19 @@ const struct TileDesc* peer_tiles(const PeerState& p);
 int peer_tile_count(const PeerState& p);
 // Completes a deferred merge (no-op if none is pending).
 int peer_flush(PeerState& p, cudaStream_t st);
+// Schedule of later flat steps (cs_set_schedule); completes a pending deferred merge first.
+int peer_set_schedule(PeerState& p, int sched, cudaStream_t st);
+// One flat step whose merge completes inside the step's own kernel (k_push_merge; one
+// worker per GPU).  hier: the leader exchange of a hierarchical step (g = group mean).
+int peer_merge_launch(PeerState& p, const PeerStepArgs& a, uint32_t epoch, cudaStream_t st);
+bool peer_merge_ok(const PeerState& p, const PeerStepArgs& a);
+size_t peer_merge_smem(int k, bool wire);
+std::vector<int32_t> peer_merge_chunks(const std::vector<int32_t>& seg_t0, int chunk, int grid);
+constexpr int kMergeChunk = 4;    // tiles per claimed chunk (one landed flag and release each)
+int peer_merge_capacity(int k);   // co-resident k_push_merge CTAs on this GPU
+// launch helper: plain launch, or a cooperative one over all emulated ranks
+cudaError_t peer_launch(const PeerState& p, const void* fn, int grid_per_rank, int threads, size_t smem,
+                        cudaStream_t st, void** args);
 int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEvent_t ev0,
                    cudaEvent_t ev1);
 // diagnostics of the current state (after a step), all GPUs; out: device double[2]

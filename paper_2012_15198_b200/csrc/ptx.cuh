@@ -103,6 +103,11 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 // wait until every committed bulk group has completed its writes
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// wait until at most N committed bulk groups have not completed their writes
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
 // shared-memory writes of the generic proxy -> later async-proxy (TMA) reads
 __device__ __forceinline__ void fence_proxy_async_shared() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -128,6 +133,14 @@ __device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// arrival counter: release this thread's (and, cumulatively, its CTA's) accesses, acquire
+// the earlier arrivals'
+__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ void red_add_relaxed_sys(uint32_t* p, uint32_t v) {
   asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -149,6 +162,24 @@ __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+// Bound of every cross-GPU wait: a peer that never arrives surfaces as CS_ETIMEOUT.
+constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;
+
+// Wait until (int32)(*p - target) >= 0 (epoch-tagged flags, modular comparison), polling
+// relaxed at system scope, then fence.acq_rel.sys (acquire pattern: everything the writer
+// released before its st.release.sys is visible after this returns).  false on timeout.
+__device__ __forceinline__ bool wait_geq_sys(const uint32_t* p, uint32_t target) {
+  uint64_t t0 = 0;
+  while ((int32_t)(ld_relaxed_sys(p) - target) < 0) {
+    const uint64_t now = globaltimer();
+    if (t0 == 0) t0 = now;
+    if (now - t0 > kSpinLimitNs) return false;
+    __nanosleep(32);
+  }
+  fence_acq_rel_sys();
+  return true;
 }
 
 }  // namespace ptx
