@@ -769,7 +769,7 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
   int rc = check_bound();
   if (rc) return rc;
   g.xnorm_valid = false;
-  if ((g.lars || g.n_layers > 0) && g.nprocs == 1 && (g.use_peer || !g.use_tma))
+  if ((g.lars || g.n_layers > 0) && g.nprocs == 1 && g.vranks <= 1 && (g.use_peer || !g.use_tma))
     return fail(CS_EUNSUPPORTED, "LARS / layer tables in the single-GPU hierarchical step need the bulk-TMA tiles");
   if (g.lars && g.n_layers == 0) return fail(CS_EINVAL, "LARS needs a layer table (cs_set_layers)");
   if (g.wire != CS_WIRE_FP32)
@@ -777,8 +777,8 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
   rc = check_step_args(params, grads, psw);
   if (rc) return rc;
   const bool diag = g.diag != 0;
-  if (g.nprocs > 1) {
-    if (g.n_loc != 1)
+  if (g.nprocs > 1 || g.vranks > 1) {  // across GPUs, or their single-GPU emulation
+    if ((g.vranks > 1 ? g.world / g.vranks : g.n_loc) != 1)
       return fail(CS_EUNSUPPORTED, "multi-GPU hierarchical step needs one worker per GPU (world == nprocs)");
     if (!g.peer.imported) return fail(CS_ENOTBOUND, "multi-GPU: cs_ipc_import has not been called");
     PeerStepArgs pa = peer_args(params, grads, psw, lr, momentum);

@@ -145,6 +145,7 @@ struct PeerKernelArgs {
   int fuse_mix;             // x holds y of epoch-1 and the inbox its received half: apply that
                             // step's merge x = (y + inbox)/2 (and psw) before this update
   int fused_topo;           // draw the topology in the push prologue (<= 64 ranks)
+  int vranks;               // > 1: one cooperative launch over all emulated ranks (peer_dev.cuh)
   size_t off_inbox, off_wbox, off_done, off_count, off_pdone, off_pcount, off_d2;
 };
 
@@ -220,7 +221,11 @@ __device__ __forceinline__ void receiver_of(const PeerKernelArgs& a, const Meta&
 }
 
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelArgs a) {
+__global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelArgs a0) {
+  PeerKernelArgs a = a0;
+  const RankCta rc = rank_cta(a0.vranks, a0.s.rank);
+  rank_view(a.s, a.peers, a0.vranks, rc.rank);
+  const int BX = rc.b, GX = rc.G;
   extern __shared__ __align__(128) float smem_f[];
   float* ringA = smem_f;                                     // [kStagesA][3][kPeerTile]
   float* ringY = ringA + (size_t)kStagesA * 3 * kPeerTile;   // [kSlotsY][kPeerTile]
@@ -235,8 +240,8 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
   char* mine = a.peers[s.rank];
   const int u_lo = a.tile_lo * s.n_loc;
   const int n_units = (a.tile_hi - a.tile_lo) * s.n_loc;
-  const int G = gridDim.x;
-  const int n_my = blockIdx.x < n_units ? (n_units - blockIdx.x + G - 1) / G : 0;
+  const int G = GX;
+  const int n_my = BX < n_units ? (n_units - BX + G - 1) / G : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   volatile int* timeout = &s_timeout;
 
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
     const int tid = threadIdx.x;
     int cur = 0;
     for (int i = 0; i < n_my && !*timeout; ++i) {
-      const Unit U = unit_at(a, M, u_lo + blockIdx.x + i * G, cur);
+      const Unit U = unit_at(a, M, u_lo + BX + i * G, cur);
       const int st = i % NS, sy = i % kSlotsY;
       ptx::mbar_wait(&a_full[st], (uint32_t)((i / NS) & 1));
       if (!a.final_only) ptx::mbar_wait(&y_empty[sy], (uint32_t)(((i / kSlotsY) & 1) ^ 1));
@@ -388,7 +393,7 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
       ptx::fence_proxy_async_global();  // acquired gbar (hierarchical) -> bulk-copy reads
       int cur = 0;
       for (int i = 0; i < n_my && !*timeout; ++i) {
-        const Unit U = unit_at(a, M, u_lo + blockIdx.x + i * G, cur);
+        const Unit U = unit_at(a, M, u_lo + BX + i * G, cur);
         const int st = i % NS;
         ptx::mbar_wait(&a_empty[st], (uint32_t)(((i / NS) & 1) ^ 1));
         const uint32_t bytes = (uint32_t)(((U.len + 3) & ~3) * 4);
@@ -417,7 +422,7 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
     if (lane == 0) {
       int cur = 0;
       for (int i = 0; i < n_my && !*timeout; ++i) {
-        const Unit U = unit_at(a, M, u_lo + blockIdx.x + i * G, cur);
+        const Unit U = unit_at(a, M, u_lo + BX + i * G, cur);
         const int sy = i % kSlotsY;
         ptx::mbar_wait(&y_full[sy], (uint32_t)((i / kSlotsY) & 1));
         int rp, rl;
@@ -479,7 +484,11 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
   }
 }
 
-__global__ void __launch_bounds__(kMixThreads) k_peer_mix(const PeerKernelArgs a) {
+__global__ void __launch_bounds__(kMixThreads) k_peer_mix(const PeerKernelArgs a0) {
+  PeerKernelArgs a = a0;
+  const RankCta rc = rank_cta(a0.vranks, a0.s.rank);
+  rank_view(a.s, a.peers, a0.vranks, rc.rank);
+  const int BX = rc.b, GX = rc.G;
   const PeerStepArgs& s = a.s;
   const uint32_t e = a.epoch;
   const int par = (int)(e & 1u);
@@ -498,9 +507,9 @@ __global__ void __launch_bounds__(kMixThreads) k_peer_mix(const PeerKernelArgs a
     const float* inbox0 = reinterpret_cast<const float*>(mine + a.off_inbox) + (int64_t)par * s.n_loc * s.ld;
     const int64_t ldw = (s.ld + 7) & ~7;
     const uint16_t* inbox0w = reinterpret_cast<const uint16_t*>(mine + a.off_inbox) + (int64_t)par * s.n_loc * ldw;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t stride = (int64_t)GX * blockDim.x;
     constexpr int U = 4;  // float4 pairs in flight per thread
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; base < total; base += U * stride) {
+    for (int64_t base = (int64_t)BX * blockDim.x + threadIdx.x; base < total; base += U * stride) {
       float4 yo[U], yi[U];
       int64_t off[U];
       int valid[U];
@@ -525,7 +534,7 @@ __global__ void __launch_bounds__(kMixThreads) k_peer_mix(const PeerKernelArgs a
       for (int h = 0; h < U; ++h)
         if (valid[h] > 0) st4_cs(s.x + off[h], mean4(yo[h], yi[h]), valid[h]);
     }
-    if (blockIdx.x == 0) {  // weights of the segments whose first tile is in this piece
+    if (BX == 0) {  // weights of the segments whose first tile is in this piece
       for (int i = threadIdx.x; i < s.n_loc * s.k; i += blockDim.x) {
         const int r = i / s.k, sg = i - r * s.k;
         if (a.seg_t0[sg] < a.tile_lo || a.seg_t0[sg] >= a.tile_hi) continue;
@@ -556,6 +565,8 @@ struct HierArgs {
   float inv_gs;
   uint32_t epoch;
   uint32_t c1_target, c2_target;  // arrival targets (see publish_when_last)
+  int vranks;                // > 1: emulated ranks (g is row `rank` of [vranks][ld])
+  int64_t ld;
   size_t off_gbox, off_gbar, off_d1, off_c1, off_d2, off_c2;
   int* err;
 };
@@ -571,13 +582,18 @@ struct HierArgs {
 //                   The own chunk stays in g.
 //   k_hier_reduce   member c: gbar = fl(sum over members, ascending) * fp32(1/|G|) of its
 //                   chunk (reading C-12), all-gathered into every member's gbar.
-__global__ void __launch_bounds__(kHierThreads) k_hier_scatter(const HierArgs h) {
+__global__ void __launch_bounds__(kHierThreads) k_hier_scatter(const HierArgs h0) {
+  HierArgs h = h0;
+  const RankCta rc = rank_cta(h0.vranks, h0.rank);
+  h.rank = rc.rank;
+  if (h0.vranks > 1) h.g += (int64_t)rc.rank * h0.ld;
+  const int BX = rc.b, GX = rc.G;
   const int grp = h.rank / h.gs, member = h.rank - grp * h.gs, gbase = grp * h.gs;
   const int64_t cv = h.chunk / 4;
   const int64_t nblk = (cv + 31) / 32;
   const int64_t total = nblk * 32 * h.gs;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t idx = (int64_t)BX * blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)GX * blockDim.x) {
     const int64_t b = idx >> 5;
     const int c = (int)((b + member) % h.gs);
     const int64_t v = (b / h.gs) * 32 + (idx & 31);
@@ -593,7 +609,12 @@ __global__ void __launch_bounds__(kHierThreads) k_hier_scatter(const HierArgs h)
     publish_when_last(h.peers, h.peers[h.rank], h.off_c1, h.off_d1, h.rank, gbase, h.gs, h.epoch, h.c1_target);
 }
 
-__global__ void __launch_bounds__(kHierThreads) k_hier_reduce(const HierArgs h) {
+__global__ void __launch_bounds__(kHierThreads) k_hier_reduce(const HierArgs h0) {
+  HierArgs h = h0;
+  const RankCta rc = rank_cta(h0.vranks, h0.rank);
+  h.rank = rc.rank;
+  if (h0.vranks > 1) h.g += (int64_t)rc.rank * h0.ld;
+  const int BX = rc.b, GX = rc.G;
   const int grp = h.rank / h.gs, member = h.rank - grp * h.gs, gbase = grp * h.gs;
   char* mine = h.peers[h.rank];
   __shared__ int s_timeout;
@@ -609,7 +630,7 @@ __global__ void __launch_bounds__(kHierThreads) k_hier_reduce(const HierArgs h) 
     const int64_t c0 = h.col_lo + member * h.chunk;
     const int64_t c1 = imin64(h.col_hi, c0 + h.chunk);
     const int64_t cv = (c1 - c0 + 3) / 4;
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < cv; v += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t v = (int64_t)BX * blockDim.x + threadIdx.x; v < cv; v += (int64_t)GX * blockDim.x) {
       const int64_t j = c0 + 4 * v;
       const int valid = (int)imin64(4, c1 - j);
       // reading C-12: gbar = fl(...fl(g_0 + g_1)... + g_{gs-1}) * fp32(1/|G|), ascending members
@@ -647,22 +668,31 @@ struct SyncArgs {
   size_t off_xsync, off_msync, off_wsync, off_d3, off_c3;
 };
 
-__global__ void __launch_bounds__(kHierThreads) k_hier_sync(const SyncArgs sa) {
+__global__ void __launch_bounds__(kHierThreads) k_hier_sync(const SyncArgs sa0) {
+  SyncArgs sa = sa0;
+  const RankCta rc = rank_cta(sa0.h.vranks, sa0.h.rank);
+  sa.h.rank = rc.rank;
+  if (sa0.h.vranks > 1) {
+    sa.x += (int64_t)rc.rank * sa0.ld;
+    sa.m += (int64_t)rc.rank * sa0.ld;
+    sa.psw += (int64_t)rc.rank * sa0.k;
+  }
   const HierArgs& h = sa.h;
+  const int BX = rc.b, GX = rc.G;
   const int grp = h.rank / h.gs, member = h.rank - grp * h.gs, gbase = grp * h.gs;
   char* mine = h.peers[h.rank];
   const int64_t nv = (h.d + 3) / 4;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t stride = (int64_t)GX * blockDim.x;
   if (member == 0) {
     for (int c = 1; c < h.gs; ++c) {
       char* dst = h.peers[gbase + c];
-      for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
+      for (int64_t v = (int64_t)BX * blockDim.x + threadIdx.x; v < nv; v += stride) {
         const int64_t j = 4 * v;
         const int valid = (int)imin64(4, h.d - j);
         st4(reinterpret_cast<float*>(dst + sa.off_xsync) + j, ld4_valid(sa.x + j, valid), valid);
         st4(reinterpret_cast<float*>(dst + sa.off_msync) + j, ld4_valid(sa.m + j, valid), valid);
       }
-      if (blockIdx.x == 0)
+      if (BX == 0)
         for (int s = threadIdx.x; s < sa.k; s += blockDim.x)
           reinterpret_cast<float*>(dst + sa.off_wsync)[s] = sa.psw[s];
     }
@@ -680,13 +710,13 @@ __global__ void __launch_bounds__(kHierThreads) k_hier_sync(const SyncArgs sa) {
       if (threadIdx.x == 0) atomicOr(h.err + kErrTimeout, 1);
       return;
     }
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
+    for (int64_t v = (int64_t)BX * blockDim.x + threadIdx.x; v < nv; v += stride) {
       const int64_t j = 4 * v;
       const int valid = (int)imin64(4, h.d - j);
       st4(sa.x + j, ld4_valid(reinterpret_cast<const float*>(mine + sa.off_xsync) + j, valid), valid);
       st4(sa.m + j, ld4_valid(reinterpret_cast<const float*>(mine + sa.off_msync) + j, valid), valid);
     }
-    if (blockIdx.x == 0)
+    if (BX == 0)
       for (int s = threadIdx.x; s < sa.k; s += blockDim.x)
         sa.psw[s] = __ldcg(reinterpret_cast<const float*>(mine + sa.off_wsync) + s);
   }
@@ -750,9 +780,34 @@ struct HybArgs {
   int n_layers;
   float wd;
   const int64_t* bounds;    // [k+1] the segment plan (layer plans move the bounds)
+  int vranks;               // > 1: emulated ranks (rows rank*n_loc.. of [vranks*n_loc][ld])
+  size_t tbl_stride;        // tail-table bytes per emulated rank
 };
 
-__global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
+// Rank `rank`'s view of hybrid-walk arguments given for rank 0 of an emulated launch.
+__device__ __forceinline__ void hyb_view(HybArgs& a, int rank) {
+  if (a.vranks <= 1) return;
+  const int64_t rows = (int64_t)rank * a.n_loc;
+  a.rank = rank;
+  a.first = rank * a.n_loc;
+  if (a.lrs) a.lrs += rows * a.n_layers;  // (x, m, g, psw: the kernels' own locals)
+  if (a.tail_tbl) a.tail_tbl += (size_t)rank * a.tbl_stride;
+  if (a.tail_prev) a.tail_prev += (size_t)rank * a.tbl_stride;
+}
+
+__global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a0) {
+  HybArgs a = a0;
+  const RankCta rc = rank_cta(a0.vranks, a0.rank);
+  hyb_view(a, rc.rank);
+  // the rank's rows, computed from the launch arguments (the body uses these locals)
+  const int64_t vrows = a0.vranks > 1 ? (int64_t)rc.rank * a0.n_loc : 0;
+  float* const aX = a0.x + vrows * a0.ld;
+  float* const aM = a0.m + vrows * a0.ld;
+  const float* const aG = a0.g + vrows * a0.ld;
+  float* const aPSW = a0.psw + vrows * a0.k;
+  (void)aM;
+  (void)aG;
+  const int BX = rc.b, GX = rc.G;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage_buf = reinterpret_cast<float*>(smem_raw);
   uint32_t* ord = reinterpret_cast<uint32_t*>(smem_raw + kHStages * kHStageBytes);  // [k][n_loc]
@@ -836,7 +891,7 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
           } while (pr != r0);
         }
       }
-      if (blockIdx.x == 0)
+      if (BX == 0)
         for (int r = lane; r < n_loc; r += 32) {
           const int sgl = row[first + r] - first;
           a.tail_tbl[sg * n_loc + r] = (sgl < 0 || sgl >= n_loc) ? 1 : 0;
@@ -861,7 +916,7 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
   for (int i = threadIdx.x; i < a.k * n_loc; i += blockDim.x) {
     const int sg = i / n_loc, r = i - sg * n_loc;
     const uint8_t tp = a.fuse ? a.tail_prev[i] : 0;
-    const float w = a.psw[(int64_t)r * a.k + sg];
+    const float w = aPSW[(int64_t)r * a.k + sg];
     tprev[i] = tp;
     cur_w[i] = tp ? pair_mean1(w, __ldcg(reinterpret_cast<const float*>(mine + a.off_wbox) +
                                          ((int64_t)(par ^ 1) * n_loc + r) * a.k + sg))
@@ -869,7 +924,7 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
   }
   __syncthreads();
   // push-sum weights of the chain heads go with their y (reading C-11)
-  if (blockIdx.x == 0 && !*timeout)
+  if (BX == 0 && !*timeout)
     for (int i = threadIdx.x; i < a.k * n_loc; i += blockDim.x) {
       const int sg = i / n_loc, r = i - sg * n_loc;
       const int dg = head_dst[sg * n_loc + r];
@@ -887,7 +942,7 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
     // ---------------- producer: rows of each tile in walk order ------------------
     if (lane == 0) {
       uint32_t it = 0;
-      for (int t = blockIdx.x; t < a.n_tiles && !*timeout; t += gridDim.x) {
+      for (int t = BX; t < a.n_tiles && !*timeout; t += GX) {
         const TileDesc td = a.tiles[t];
         const uint32_t bytes = (uint32_t)(((td.len + 3) & ~3) * sizeof(float));
         const uint32_t* o = ord + td.seg * n_loc;
@@ -901,9 +956,9 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
           const uint32_t ibytes = a.wire ? (uint32_t)(((td.len + 7) & ~7) * 2) : bytes;
           if (a.lrs) srate[st] = a.lrs[(int64_t)row * a.n_layers + td.layer];  // before the release-arrive
           ptx::mbar_arrive_expect_tx(&full[st], 3 * bytes + (merge ? ibytes : 0u));
-          ptx::bulk_g2s(buf, a.x + off, bytes, &full[st]);
-          ptx::bulk_g2s(buf + kTmaTileMax, a.m + off, bytes, &full[st]);
-          ptx::bulk_g2s(buf + 2 * kTmaTileMax, a.g + off, bytes, &full[st]);
+          ptx::bulk_g2s(buf, aX + off, bytes, &full[st]);
+          ptx::bulk_g2s(buf + kTmaTileMax, aM + off, bytes, &full[st]);
+          ptx::bulk_g2s(buf + 2 * kTmaTileMax, aG + off, bytes, &full[st]);
           if (merge && a.wire)  // the previous step's received y of this tail row (bf16 rows)
             ptx::bulk_g2s(buf + 3 * kTmaTileMax,
                           reinterpret_cast<const uint16_t*>(mine + a.off_inbox) +
@@ -921,7 +976,7 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
     // ---------------- consumers: the walk, heads pushed over NVLink, tails kept ------
     bool bad = false;
     uint32_t it = 0;
-    for (int t = blockIdx.x; t < a.n_tiles && !*timeout; t += gridDim.x) {
+    for (int t = BX; t < a.n_tiles && !*timeout; t += GX) {
       const TileDesc td = a.tiles[t];
       const uint32_t* o = ord + td.seg * n_loc;
       float4 yfirst[kHVPT], yprev[kHVPT];
@@ -959,7 +1014,7 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
             const float4 mn = mom4(cm, a.lrs ? decay4(cg, cx, a.wd) : cg, a.mu);
             const float4 y = sgd4(cx, mn, a.lrs ? srate[st] : a.lr);
             const int64_t j = td.c0 + 4 * v;
-            st4_cs(a.m + (int64_t)row * ld + j, mn, vv);
+            st4_cs(aM + (int64_t)row * ld + j, mn, vv);
             if (e & kHStart) {
               yfirst[c] = y;
               if (e & kHHead) {  // NVLink push of the chain head
@@ -967,11 +1022,11 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
                 else st4(inbox + j, y, vv);
               }
             } else {
-              st4_cs(a.x + (int64_t)prev_row * ld + j, mean4(yprev[c], a.wire ? bf16r4(y) : y), vv);
+              st4_cs(aX + (int64_t)prev_row * ld + j, mean4(yprev[c], a.wire ? bf16r4(y) : y), vv);
             }
             if (e & kHEnd) {
-              if (e & kHTail) st4(a.x + (int64_t)row * ld + j, y, vv);  // finished by k_hyb_tail
-              else st4_cs(a.x + (int64_t)row * ld + j, mean4(y, a.wire ? bf16r4(yfirst[c]) : yfirst[c]), vv);
+              if (e & kHTail) st4(aX + (int64_t)row * ld + j, y, vv);  // finished by k_hyb_tail
+              else st4_cs(aX + (int64_t)row * ld + j, mean4(y, a.wire ? bf16r4(yfirst[c]) : yfirst[c]), vv);
             }
             yprev[c] = y;
           }
@@ -1015,7 +1070,7 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
     for (int i = threadIdx.x; i < a.k * n_loc; i += blockDim.x) {
       const int sg = i / n_loc, r = i - sg * n_loc;
       // tails of this step keep their current weight; their merge comes with the next step
-      a.psw[(int64_t)r * a.k + sg] = a.tail_tbl[sg * n_loc + r] ? cur_w[i] : reinterpret_cast<const float*>(stage_buf)[i];
+      aPSW[(int64_t)r * a.k + sg] = a.tail_tbl[sg * n_loc + r] ? cur_w[i] : reinterpret_cast<const float*>(stage_buf)[i];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1029,7 +1084,19 @@ __global__ void __launch_bounds__(kHThreads, 2) k_hyb_walk(const HybArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_hyb_tail(const HybArgs a) {
+__global__ void __launch_bounds__(256) k_hyb_tail(const HybArgs a0) {
+  HybArgs a = a0;
+  const RankCta rc = rank_cta(a0.vranks, a0.rank);
+  hyb_view(a, rc.rank);
+  // the rank's rows, computed from the launch arguments (the body uses these locals)
+  const int64_t vrows = a0.vranks > 1 ? (int64_t)rc.rank * a0.n_loc : 0;
+  float* const aX = a0.x + vrows * a0.ld;
+  float* const aM = a0.m + vrows * a0.ld;
+  const float* const aG = a0.g + vrows * a0.ld;
+  float* const aPSW = a0.psw + vrows * a0.k;
+  (void)aM;
+  (void)aG;
+  const int BX = rc.b, GX = rc.G;
   __shared__ uint8_t tail[kHMaxTable];
   __shared__ int s_timeout;
   char* mine = a.peers[a.rank];
@@ -1050,8 +1117,8 @@ __global__ void __launch_bounds__(256) k_hyb_tail(const HybArgs a) {
         ? reinterpret_cast<const float*>(reinterpret_cast<const uint16_t*>(mine + a.off_inbox) +
                                          (int64_t)par * n_loc * ((a.ld + 7) & ~7))
         : reinterpret_cast<const float*>(mine + a.off_inbox) + (int64_t)par * n_loc * a.ld;
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t idx = (int64_t)BX * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)GX * blockDim.x) {
       const int64_t r = idx / nv, v = idx - r * nv;
       const int64_t j = 4 * v;
       int sg = 0;  // segment of column j: the last plan bound <= j
@@ -1061,18 +1128,18 @@ __global__ void __launch_bounds__(256) k_hyb_tail(const HybArgs a) {
       }
       if (!tail[sg * n_loc + r]) continue;
       const int64_t off = r * a.ld + j;
-      const float4 y = __ldcs(reinterpret_cast<const float4*>(a.x + off));
+      const float4 y = __ldcs(reinterpret_cast<const float4*>(aX + off));
       const float4 yi = a.wire ? unpack_bf16x4(__ldcs(reinterpret_cast<const uint2*>(
                                      reinterpret_cast<const uint16_t*>(inbox0) + r * ((a.ld + 7) & ~7) + j)))
                                : __ldcs(reinterpret_cast<const float4*>(inbox0 + off));
-      st4_cs(a.x + off, mean4(y, yi), (int)imin64(4, a.d - j));
+      st4_cs(aX + off, mean4(y, yi), (int)imin64(4, a.d - j));
     }
-    if (blockIdx.x == 0)
+    if (BX == 0)
       for (int i = threadIdx.x; i < a.k * n_loc; i += blockDim.x) {
         const int sg = i / n_loc, r = i - sg * n_loc;
         if (!tail[i]) continue;
         const float* wbox = reinterpret_cast<const float*>(mine + a.off_wbox) + ((int64_t)par * n_loc + r) * a.k;
-        float* wp = a.psw + (int64_t)r * a.k + sg;
+        float* wp = aPSW + (int64_t)r * a.k + sg;
         *wp = pair_mean1(*wp, __ldcg(wbox + sg));
       }
   }
@@ -1104,9 +1171,26 @@ struct DiagArgs {
   double* partials;  // [gridDim.x][2] scratch of k_diag_reduce
   double* out;       // [2] {CD, mean checksum}
   int* err;
+  int vranks;        // > 1: emulated ranks (x, psw: rows rank*n_loc.. of the whole-world buffers)
 };
 
-__global__ void __launch_bounds__(256) k_diag_scatter(const DiagArgs a) {
+__device__ __forceinline__ void diag_view(DiagArgs& a, int rank, int G) {
+  if (a.vranks <= 1) return;
+  const int64_t rows = (int64_t)rank * a.n_loc;
+  a.rank = rank;
+  a.first = rank * a.n_loc;
+  (void)rows;  // x, psw: k_diag_scatter's own locals
+  a.partials += (size_t)2 * rank * G;
+}
+
+__global__ void __launch_bounds__(256) k_diag_scatter(const DiagArgs a0) {
+  DiagArgs a = a0;
+  const RankCta rc = rank_cta(a0.vranks, a0.rank);
+  diag_view(a, rc.rank, rc.G);
+  const int BX = rc.b, GX = rc.G;
+  const int64_t vrows = a0.vranks > 1 ? (int64_t)rc.rank * a0.n_loc : 0;
+  const float* const aX = a0.x + vrows * a0.ld;      // the rank's rows (locals, as in k_hyb_walk)
+  const float* const aPSW = a0.psw + vrows * a0.k;
   char* mine = a.peers[a.rank];
   __shared__ int s_timeout;
   if (threadIdx.x == 0) s_timeout = 0;
@@ -1120,8 +1204,8 @@ __global__ void __launch_bounds__(256) k_diag_scatter(const DiagArgs a) {
   if (!s_timeout) {
     const int64_t cv = a.chunk / 4;
     const int64_t total = (int64_t)a.nprocs * a.n_loc * cv;
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t idx = (int64_t)BX * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)GX * blockDim.x) {
       const int q = (int)(idx / ((int64_t)a.n_loc * cv));
       const int64_t rem = idx - (int64_t)q * a.n_loc * cv;
       const int r = (int)(rem / cv);
@@ -1130,13 +1214,13 @@ __global__ void __launch_bounds__(256) k_diag_scatter(const DiagArgs a) {
       const int valid = (int)imin64(4, a.d - j);
       if (valid <= 0) continue;
       float* dst = reinterpret_cast<float*>(a.peers[q] + a.off_dx) + (int64_t)(a.first + r) * a.chunk + 4 * v;
-      st4(dst, ld4_valid(a.x + (int64_t)r * a.ld + j, valid), valid);
+      st4(dst, ld4_valid(aX + (int64_t)r * a.ld + j, valid), valid);
     }
-    if (blockIdx.x == 0)
+    if (BX == 0)
       for (int i = threadIdx.x; i < a.nprocs * a.n_loc * a.k; i += blockDim.x) {
         const int q = i / (a.n_loc * a.k), rem = i - q * a.n_loc * a.k;
         const int r = rem / a.k, s = rem - r * a.k;
-        reinterpret_cast<float*>(a.peers[q] + a.off_dw)[(int64_t)(a.first + r) * a.k + s] = a.psw[(int64_t)r * a.k + s];
+        reinterpret_cast<float*>(a.peers[q] + a.off_dw)[(int64_t)(a.first + r) * a.k + s] = aPSW[(int64_t)r * a.k + s];
       }
   }
   __syncthreads();
@@ -1147,7 +1231,11 @@ __global__ void __launch_bounds__(256) k_diag_scatter(const DiagArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_diag_reduce(const DiagArgs a) {
+__global__ void __launch_bounds__(256) k_diag_reduce(const DiagArgs a0) {
+  DiagArgs a = a0;
+  const RankCta rc = rank_cta(a0.vranks, a0.rank);
+  diag_view(a, rc.rank, rc.G);
+  const int BX = rc.b, GX = rc.G;
   extern __shared__ double wsum[];  // [k]: 1 / sum_i w_{i,s}
   __shared__ int s_timeout;
   __shared__ double red[2][8];
@@ -1171,8 +1259,8 @@ __global__ void __launch_bounds__(256) k_diag_reduce(const DiagArgs a) {
   if (!s_timeout) {
     const int64_t c0 = (int64_t)a.rank * a.chunk;
     const int64_t cols = imin64(a.chunk, a.d - c0);
-    for (int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; jj < cols;
-         jj += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t jj = (int64_t)BX * blockDim.x + threadIdx.x; jj < cols;
+         jj += (int64_t)GX * blockDim.x) {
       const int64_t j = c0 + jj;
       int s = 0;  // segment of column j: the last bound <= j (binary search over the plan)
       for (int lo = 0, hi = a.k - 1; lo <= hi;) {
@@ -1208,8 +1296,8 @@ __global__ void __launch_bounds__(256) k_diag_reduce(const DiagArgs a) {
   if (threadIdx.x == 0) {
     double da = 0.0, za = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { da += red[0][w]; za += red[1][w]; }
-    a.partials[2 * blockIdx.x] = da;
-    a.partials[2 * blockIdx.x + 1] = za;
+    a.partials[2 * BX] = da;
+    a.partials[2 * BX + 1] = za;
     __threadfence();
     uint32_t* cnt = reinterpret_cast<uint32_t*>(mine + a.off_dc2);
     s_last = (atomicAdd(cnt, 1u) + 1 == a.c2_target);
@@ -1218,7 +1306,7 @@ __global__ void __launch_bounds__(256) k_diag_reduce(const DiagArgs a) {
   if (s_last && threadIdx.x == 0) {
     __threadfence();
     double da = 0.0, za = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) {
+    for (int b = 0; b < (int)GX; ++b) {
       da += __ldcg(a.partials + 2 * b);
       za += __ldcg(a.partials + 2 * b + 1);
     }
@@ -1234,7 +1322,10 @@ __global__ void __launch_bounds__(256) k_diag_reduce(const DiagArgs a) {
   }
 }
 
-__global__ void k_diag_final(const DiagArgs a) {
+__global__ void k_diag_final(const DiagArgs a0) {
+  DiagArgs a = a0;
+  const RankCta rc = rank_cta(a0.vranks, a0.rank);
+  diag_view(a, rc.rank, rc.G);
   char* mine = a.peers[a.rank];
   if (threadIdx.x != 0) return;
   for (int q = 0; q < a.nprocs; ++q)
@@ -1250,6 +1341,14 @@ __global__ void k_diag_final(const DiagArgs a) {
   }
   a.out[0] = sqrt(fmax(da, 0.0) / (double)a.world);
   a.out[1] = za;
+}
+
+// Launch `fn(arg)` with `grid` CTAs per rank: a plain launch for a real rank, one
+// cooperative launch over every emulated rank otherwise (peer_launch).
+template <typename Arg>
+void plaunch(const PeerState& p, void (*fn)(Arg), int grid, int threads, size_t smem, cudaStream_t st, Arg arg) {
+  void* args[] = {&arg};
+  peer_launch(p, reinterpret_cast<const void*>(fn), grid, threads, smem, st, args);
 }
 
 }  // namespace
@@ -1284,6 +1383,8 @@ int peer_diag(PeerState& p, const PeerStepArgs& a, double* partials, int partial
   da.partials = partials;
   da.out = out;
   da.err = a.err;
+  da.vranks = p.vranks;
+  partials_cap /= p.vranks;
   const int64_t sv = (int64_t)a.nprocs * a.n_loc * (p.diag_chunk / 4);
   int gs = (int)((sv + 255) / 256);
   if (gs > p.grid_mix) gs = p.grid_mix;
@@ -1294,9 +1395,9 @@ int peer_diag(PeerState& p, const PeerStepArgs& a, double* partials, int partial
   if (gr < 1) gr = 1;
   da.c1_target = (p.tot_dc1 += (uint32_t)gs);
   da.c2_target = (p.tot_dc2 += (uint32_t)gr);
-  k_diag_scatter<<<gs, 256, 0, st>>>(da);
-  k_diag_reduce<<<gr, 256, sizeof(double) * a.k, st>>>(da);
-  k_diag_final<<<1, 32, 0, st>>>(da);
+  plaunch(p, k_diag_scatter, gs, 256, 0, st, da);
+  plaunch(p, k_diag_reduce, gr, 256, sizeof(double) * a.k, st, da);
+  plaunch(p, k_diag_final, 1, 32, 0, st, da);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "diagnostics launch", e);
 }
@@ -1441,10 +1542,12 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_h, k_hier_reduce, kHierThreads, 0);
   if (e != cudaSuccess || occ_push < 1 || occ_mix < 1 || occ_h < 1) return perr(CS_ECUDA, "occupancy", e);
   const int n_units = p.n_tiles * n_loc;
-  p.grid_push_max = sms * occ_push;
-  p.grid_push = sms * occ_push < n_units ? sms * occ_push : n_units;
-  p.grid_mix = sms * occ_mix;
-  p.grid_hier = sms * occ_h;
+  // emulated ranks share this GPU: each rank's CTAs are 1/vranks of the co-resident capacity
+  const int V = p.vranks;
+  p.grid_push_max = std::max(1, sms * occ_push / V);
+  p.grid_push = p.grid_push_max < n_units ? p.grid_push_max : n_units;
+  p.grid_mix = std::max(1, sms * occ_mix / V);
+  p.grid_hier = std::max(1, sms * occ_h / V);
   // hybrid flat step when several workers share a GPU (CS_PEER_HYBRID=0 disables it)
   {
     const char* hy = getenv("CS_PEER_HYBRID");
@@ -1457,8 +1560,8 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_w, k_hyb_walk, kHThreads, hs);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_t, k_hyb_tail, 256, 0);
     if (e != cudaSuccess || occ_w < 1 || occ_t < 1) return perr(CS_ECUDA, "hybrid occupancy", e);
-    p.grid_hyb = sms * occ_w;
-    p.grid_tail = sms * occ_t;
+    p.grid_hyb = std::max(1, sms * occ_w / p.vranks);
+    p.grid_tail = std::max(1, sms * occ_t / p.vranks);
     const int T = tma_tile_len(d, p.grid_hyb);
     std::vector<TileDesc> tiles;
     for (int s = 0; s < k; ++s)
@@ -1475,7 +1578,7 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
     e = cudaMalloc(&p.d_htiles, sizeof(TileDesc) * tiles.size());
     if (e == cudaSuccess)
       e = cudaMemcpy(p.d_htiles, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&p.d_tail_tbl, 2 * (size_t)k * n_loc);  // by step parity
+    if (e == cudaSuccess) e = cudaMalloc(&p.d_tail_tbl, 2 * (size_t)k * n_loc * p.vranks);  // by step parity, per rank
     if (e != cudaSuccess) return perr(CS_ECUDA, "hybrid tables", e);
   }
   // pieces per step (CS_PEER_PIECES)
@@ -1604,6 +1707,7 @@ PeerKernelArgs kernel_args(const PeerState& p, const PeerStepArgs& a, uint32_t e
   ka.final_only = final_only ? 1 : 0;
   ka.fuse_mix = 0;
   ka.fused_topo = fused_topo_ok(a.gs > 0 ? a.groups : a.world, a.k, a.n_loc) ? 1 : 0;
+  ka.vranks = p.vranks;
   ka.off_inbox = p.off_inbox;
   ka.off_wbox = p.off_wbox;
   ka.pieces = p.pieces;
@@ -1772,18 +1876,18 @@ int launch_push_mix(PeerState& p, const PeerKernelArgs& ka, cudaStream_t st) {
     const size_t smem = push_smem_bytes(ka.s.k, ka.s.n_loc);
     if (ka.final_only) {
       kq.done_target = (p.tot_count[q] += (uint32_t)grid);
-      k_peer_push<<<grid, kPushThreads, smem, st>>>(kq);
+      plaunch(p, k_peer_push, grid, kPushThreads, smem, st, kq);
       continue;
     }
     kq.pdone_target = (p.tot_pcount[q] += (uint32_t)grid);
     kq.done_target = (p.tot_count[q] += (uint32_t)p.grid_mix);
-    k_peer_push<<<grid, kPushThreads, smem, st>>>(kq);
+    plaunch(p, k_peer_push, grid, kPushThreads, smem, st, kq);
     if (P == 1) {
-      k_peer_mix<<<p.grid_mix, kMixThreads, 0, st>>>(kq);
+      plaunch(p, k_peer_mix, p.grid_mix, kMixThreads, 0, st, kq);
     } else {
       cudaEventRecord(p.ev_push[q], st);
       cudaStreamWaitEvent(p.aux, p.ev_push[q], 0);
-      k_peer_mix<<<p.grid_mix, kMixThreads, 0, p.aux>>>(kq);
+      plaunch(p, k_peer_mix, p.grid_mix, kMixThreads, 0, p.aux, kq);
     }
   }
   if (P > 1) {
@@ -1842,6 +1946,8 @@ HybArgs hyb_args(const PeerState& p, const PeerStepArgs& a, uint32_t epoch) {
   h.n_layers = a.n_layers;
   h.wd = a.wd;
   h.bounds = p.d_bounds;
+  h.vranks = p.vranks;
+  h.tbl_stride = 2 * (size_t)a.k * a.n_loc;
   return h;
 }
 }  // namespace
@@ -1849,7 +1955,9 @@ HybArgs hyb_args(const PeerState& p, const PeerStepArgs& a, uint32_t epoch) {
 int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEvent_t ev0,
                    cudaEvent_t ev1) {
   int rc = CS_OK;
-  if (p.use_hybrid && p.vranks > 1) return perr(CS_EUNSUPPORTED, "emulated ranks: hybrid walk not emulated", cudaSuccess);
+  // a flat step gives every worker its own state: the next hierarchical step re-replicates
+  // each group's leader to its members first
+  p.need_sync = true;
   if (p.use_hybrid) {
     // deferred merge: this step's chain tails are merged inside the next walk (or
     // peer_flush); the previous step's tails are merged here before their update
@@ -1870,13 +1978,13 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     if (fuse) {
       h.fuse = p.pending ? 1 : 0;
       h.tail_prev = p.d_tail_tbl + ((h.epoch - 1) & 1u) * tbl;
-      k_hyb_walk<<<p.grid_hyb, kHThreads, hyb_smem_bytes(a.k, a.n_loc), st>>>(h);
+      plaunch(p, k_hyb_walk, p.grid_hyb, kHThreads, hyb_smem_bytes(a.k, a.n_loc), st, h);
       p.pending = h.epoch;
       p.pending_args = a;
     } else {
       h.done_target = (p.tot_count[0] += (uint32_t)p.grid_tail);
-      k_hyb_walk<<<p.grid_hyb, kHThreads, hyb_smem_bytes(a.k, a.n_loc), st>>>(h);
-      k_hyb_tail<<<p.grid_tail, 256, 0, st>>>(h);
+      plaunch(p, k_hyb_walk, p.grid_hyb, kHThreads, hyb_smem_bytes(a.k, a.n_loc), st, h);
+      plaunch(p, k_hyb_tail, p.grid_tail, 256, 0, st, h);
     }
     if (ev1) cudaEventRecord(ev1, st);
     cudaError_t e = cudaGetLastError();
@@ -1898,7 +2006,6 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     if (ev1) cudaEventRecord(ev1, st);
     return CS_OK;
   }
-  if (p.vranks > 1) return perr(CS_EUNSUPPORTED, "emulated ranks: this schedule is not emulated", cudaSuccess);
   // deferred merge (opt-in, kSchedDeferred): this step's push applies the previous step's
   // merge tile by tile, and its own merge waits for the next push (or peer_flush); the
   // separate mix pass and its cross-GPU wait disappear from the step, but params hold y
@@ -1923,7 +2030,7 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     const int units = p.n_tiles * a.n_loc;
     const int grid = p.grid_push < units ? p.grid_push : (units > 0 ? units : 1);
     ka.pdone_target = (p.tot_pcount[0] += (uint32_t)grid);
-    k_peer_push<<<grid, kPushThreads, push_smem_bytes(a.k, a.n_loc), st>>>(ka);
+    plaunch(p, k_peer_push, grid, kPushThreads, push_smem_bytes(a.k, a.n_loc), st, ka);
     p.pending = ka.epoch;
     p.pending_args = ka.s;
     rc = cudaGetLastError() == cudaSuccess ? CS_OK : perr(CS_ECUDA, "fused push launch", cudaGetLastError());
@@ -1948,7 +2055,7 @@ int peer_flush(PeerState& p, cudaStream_t st) {
     HybArgs h = hyb_args(p, p.pending_args, p.pending);
     h.tail_tbl = p.d_tail_tbl + (p.pending & 1u) * (size_t)p.pending_args.k * p.pending_args.n_loc;
     h.done_target = (p.tot_count[0] += (uint32_t)p.grid_tail);
-    k_hyb_tail<<<p.grid_tail, 256, 0, st>>>(h);
+    plaunch(p, k_hyb_tail, p.grid_tail, 256, 0, st, h);
     p.pending = 0;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "deferred tail merge launch", e);
@@ -1960,7 +2067,7 @@ int peer_flush(PeerState& p, cudaStream_t st) {
   ka.col_lo = 0;
   ka.col_hi = p.d;
   ka.done_target = (p.tot_count[0] += (uint32_t)p.grid_mix);
-  k_peer_mix<<<p.grid_mix, kMixThreads, 0, st>>>(ka);
+  plaunch(p, k_peer_mix, p.grid_mix, kMixThreads, 0, st, ka);
   p.pending = 0;
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "deferred merge launch", e);
@@ -2046,9 +2153,14 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   h.off_d2 = p.off_d2;
   h.off_c2 = p.off_c2;
   h.err = a.err;
+  h.vranks = p.vranks;
+  h.ld = a.ld;
   PeerStepArgs b = a;
   b.g = reinterpret_cast<const float*>(p.base + p.off_gbar);  // the group mean
+  b.g_off = p.off_gbar;
   b.gs = p.gs;
+  // default schedule: the leader exchange merges inside its own kernel (k_push_merge)
+  const bool merge = exchange && !fuse && peer_merge_ok(p, a);
   if (a.lrs_out) {  // LARS with the group-reduced gradient: b.lrs is filled after h1 below
     b.lrs = a.lrs_out;
     if (p.hier_pieces != 1 && !exchange) return perr(CS_EUNSUPPORTED, "hierarchical LARS needs CS_HIER_PIECES=1", cudaSuccess);
@@ -2069,7 +2181,7 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     sa.off_wsync = p.off_wsync;
     sa.off_d3 = p.off_d3;
     sa.off_c3 = p.off_c3;
-    k_hier_sync<<<p.grid_hier, kHierThreads, 0, st>>>(sa);
+    plaunch(p, k_hier_sync, p.grid_hier, kHierThreads, 0, st, sa);
   }
   p.need_sync = false;
   // One group (no leader exchange): the vector is cut into P column pieces; h1 of piece
@@ -2090,23 +2202,37 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     h.c1_target = (p.tot_c1[q] += (uint32_t)p.grid_hier);
     h.c2_target = (p.tot_c2[q] += (uint32_t)p.grid_hier);
     phase_record(0, st);
-    k_hier_scatter<<<p.grid_hier, kHierThreads, 0, st>>>(h);
+    plaunch(p, k_hier_scatter, p.grid_hier, kHierThreads, 0, st, h);
     phase_record(1, st);
-    k_hier_reduce<<<p.grid_hier, kHierThreads, 0, st>>>(h);
+    plaunch(p, k_hier_reduce, p.grid_hier, kHierThreads, 0, st, h);
     phase_record(2, st);
     if (a.lrs_out) {  // rates from the leader replica's x and the group mean, once gbar is whole
       LarsWait w;
-      w.flags = reinterpret_cast<const uint32_t*>(p.base + p.off_d2);
-      w.first = (a.rank / p.gs) * p.gs;
-      w.count = p.gs;
-      w.epoch = epoch;
-      w.err = a.err;
-      cudaError_t le = launch_lars_rates(a.x, b.g, a.ld, p.d_ptiles, p.n_tiles, 1, a.tile_first, a.n_layers,
-                                         a.lars_part, a.lr, a.eta, a.wd, a.eps, a.lrs_out, st, w);
-      if (le != cudaSuccess) return perr(CS_ECUDA, "hierarchical LARS rates", le);
+      if (p.vranks <= 1) {
+        w.flags = reinterpret_cast<const uint32_t*>(p.base + p.off_d2);
+        w.first = (a.rank / p.gs) * p.gs;
+        w.count = p.gs;
+        w.epoch = epoch;
+        w.err = a.err;
+      }
+      // emulated ranks: one launch per rank (each has its own group mean); the reduce kernel
+      // before them has completed for every rank, so no wait
+      for (int r = 0; r < p.vranks; ++r) {
+        cudaError_t le = launch_lars_rates(
+            a.x + (int64_t)r * a.ld, reinterpret_cast<const float*>(p.peer_base[p.vranks > 1 ? r : a.rank] + p.off_gbar),
+            a.ld, p.d_ptiles, p.n_tiles, 1, a.tile_first, a.n_layers, a.lars_part + (size_t)2 * r * p.n_tiles, a.lr,
+            a.eta, a.wd, a.eps, a.lrs_out + (int64_t)r * a.n_layers, st, w);
+        if (le != cudaSuccess) return perr(CS_ECUDA, "hierarchical LARS rates", le);
+      }
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return perr(CS_ECUDA, "hierarchical launch", e);
+    if (merge) {  // update + exchange + merge of the leaders' step (replicated leader), one kernel
+      rc = peer_merge_launch(p, b, epoch, st);
+      if (rc) return perr(rc, "k_push_merge launch", cudaGetLastError());
+      phase_record(3, st);
+      continue;
+    }
     if (exchange && fuse) {  // the push only; its merge waits for the next push or a flush
       PeerKernelArgs kf = ka;
       kf.fuse_mix = p.pending ? 1 : 0;
@@ -2116,7 +2242,7 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
       kf.col_hi = p.d;
       const int grid = p.grid_push < p.n_tiles ? p.grid_push : (p.n_tiles > 0 ? p.n_tiles : 1);
       kf.pdone_target = (p.tot_pcount[0] += (uint32_t)grid);
-      k_peer_push<<<grid, kPushThreads, push_smem_bytes(a.k, a.n_loc), st>>>(kf);
+      plaunch(p, k_peer_push, grid, kPushThreads, push_smem_bytes(a.k, a.n_loc), st, kf);
       p.pending = epoch;
       p.pending_args = b;
       phase_record(3, st);
@@ -2140,11 +2266,11 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     kq.done_target = (p.tot_count[q] += (uint32_t)grid);
     const size_t smem = push_smem_bytes(ka.s.k, ka.s.n_loc);
     if (P == 1) {
-      k_peer_push<<<grid, kPushThreads, smem, st>>>(kq);
+      plaunch(p, k_peer_push, grid, kPushThreads, smem, st, kq);
     } else {
       cudaEventRecord(p.ev_push[q], st);
       cudaStreamWaitEvent(p.aux, p.ev_push[q], 0);
-      k_peer_push<<<grid, kPushThreads, smem, p.aux>>>(kq);
+      plaunch(p, k_peer_push, grid, kPushThreads, smem, p.aux, kq);
     }
     phase_record(3, P == 1 ? st : p.aux);
   }

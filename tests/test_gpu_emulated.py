@@ -82,13 +82,164 @@ def test_in_step_merge_many_steps_unsynchronised():
 
 
 @pytest.mark.parametrize("schedule", [1, 2])
-def test_emulated_schedules_agree(schedule):
-    # the deferred and split schedules give the same bits (they are not emulated for V > 1
-    # on the push path: the library refuses them rather than running them unsafely)
+@pytest.mark.parametrize("n_loc", [1, 3])
+def test_emulated_opt_in_schedules_bitwise(schedule, n_loc):
+    # the deferred (merge inside the next step, flushed by cs_sync) and split (push kernel +
+    # merge kernel) schedules give the same bits; n_loc = 3 runs the hybrid walk
     V, d, k = 2, 10_007, 3
-    x, m, w, bank2 = _bind_emulated(V, V, d, k, 9, schedule=schedule)
-    with pytest.raises(cs.CSError):
-        cs.cs_gossip_step(x, grads_view(bank2, V, 0), w, LR, MU)
+    n = V * n_loc
+    x, m, w, bank2 = _bind_emulated(V, n, d, k, 9, schedule=schedule)
+    orc = OracleRun(n, d, k, 9)
+    for t in range(6):
+        cs.cs_gossip_step(x, grads_view(bank2, n, t), w, LR, MU)
+        orc.step(LR, MU)
+    cs.cs_sync()
+    _check(x, m, w, orc, d)
+    cs.cs_finalize()
+
+
+@pytest.mark.parametrize("V,n_loc,d,k", [(2, 3, 50_001, 5), (4, 4, 30_011, 8), (2, 8, 20_000, 16), (4, 2, 7, 1)])
+def test_emulated_hybrid_walk_bitwise(V, n_loc, d, k):
+    # several workers per rank: cycles mixed in registers, chain heads pushed to other ranks'
+    # inboxes, chain tails merged by k_hyb_tail (default schedule: merged when the step ends)
+    n = V * n_loc
+    x, m, w, bank2 = _bind_emulated(V, n, d, k, 4)
+    orc = OracleRun(n, d, k, 4)
+    for t in range(5):
+        cs.cs_gossip_step(x, grads_view(bank2, n, t), w, LR, MU)
+        orc.step(LR, MU)
+        torch.cuda.current_stream().synchronize()
+        _check(x, m, w, orc, d)
+    assert cs.cs_kernel_info()[0] == "k_hyb_walk+k_hyb_tail"
+    cs.cs_finalize()
+
+
+def _hier_check(x, m, w, orc, V, groups, d, cols=None):
+    # members hold exact replicas of their leader's params, momentum and psw (reading B-6)
+    xg, mg, wg = x.cpu().numpy(), m.cpu().numpy(), w.cpu().numpy()
+    cols = np.arange(d) if cols is None else cols
+    gs = V // groups
+    assert np.array_equal(xg[:, cols], orc.x)
+    assert np.array_equal(wg, orc.w)
+    for r in range(V):
+        lead = (r // gs) * gs
+        assert np.array_equal(mg[r, cols], orc.m[lead]), r
+
+
+@pytest.mark.parametrize("V,groups,d,k", [(2, 1, 100_003, 3), (2, 2, 50_000, 4), (4, 1, 65_536, 2), (4, 2, 70_001, 5),
+                                          (4, 4, 40_003, 6), (8, 2, 1_000_003, 16), (8, 4, 30_001, 3)])
+def test_emulated_hierarchical_bitwise(V, groups, d, k):
+    # PAPER.md:197 across ranks: reduce-scatter of the gradient (k_hier_scatter), ascending
+    # sum x fp32(1/|G|) and all-gather (k_hier_reduce), replica sync (k_hier_sync), then the
+    # leaders' exchange merged in the same kernel (k_push_merge) or, with one group, the
+    # update alone.  (8, 2): BASELINE configs[3]'s 2 groups x 4 layout.
+    x, m, w, bank2 = _bind_emulated(V, V, d, k, 11, groups=groups)
+    orc = OracleRun(V, d, k, 11, groups=groups)
+    for t in range(4):
+        cs.cs_hier_step(x, grads_view(bank2, V, t), w, LR, MU)
+        orc.step(LR, MU)
+        torch.cuda.current_stream().synchronize()
+        _hier_check(x, m, w, orc, V, groups, d)
+    cs.cs_finalize()
+
+
+def test_emulated_hierarchical_configs3_full_size_sampled():
+    # BASELINE configs[3] exactly: 8 ranks as 2 groups x 4, ResNet-50-sized (25,557,032), k = 16
+    V, groups, d, k = 8, 2, 25_557_032, 16
+    x, m, w, bank2 = _bind_emulated(V, V, d, k, 0, groups=groups)
+    cols = synth.sample_columns(d, T.segment_bounds(d, k))
+    orc = OracleRun(V, d, k, 0, cols=cols, groups=groups)
+    for t in range(3):
+        cs.cs_hier_step(x, grads_view(bank2, V, t), w, LR, MU)
+        orc.step(LR, MU)
+    torch.cuda.synchronize()
+    _hier_check(x, m, w, orc, V, groups, d, cols=cols)
+    cs.cs_finalize()
+
+
+def test_emulated_flat_after_hierarchical_resyncs_members():
+    # a flat step between hierarchical steps gives members their own state; the
+    # next hierarchical step must re-replicate the leaders before using member replicas
+    V, groups, d, k = 4, 2, 20_011, 3
+    x, m, w, bank2 = _bind_emulated(V, V, d, k, 2, groups=groups)
+    orc = OracleRun(V, d, k, 2, groups=groups)
+    from oracle.gossip import gossip_step
+    from oracle.hierarchical import hier_step
+    for t, kind in enumerate(["h", "f", "h", "h"]):
+        g = synth.grads_at(orc.bank, V, t)
+        if kind == "h":
+            cs.cs_hier_step(x, grads_view(bank2, V, t), w, LR, MU)
+            orc.x, orc.m, orc.w, _ = hier_step(orc.x, orc.m, g, orc.w, groups, 2, t, k, orc.seg, LR, MU)
+            # reading B-6: across ranks every member holds its leader's momentum (the oracle
+            # leaves members' rows untouched), so the flat step after it starts from replicas
+            gs = V // groups
+            orc.m = np.repeat(orc.m[::gs], gs, axis=0)
+        else:
+            cs.cs_gossip_step(x, grads_view(bank2, V, t), w, LR, MU)
+            orc.x, orc.m, orc.w = gossip_step(orc.x, orc.m, g, orc.w, T.topology(2, t, V, k), orc.seg, LR, MU)
+        orc.t += 1
+    torch.cuda.synchronize()
+    assert np.array_equal(x.cpu().numpy()[:, :d], orc.x)
+    assert np.array_equal(w.cpu().numpy(), orc.w)
+    cs.cs_finalize()
+
+
+@pytest.mark.parametrize("V,n_loc,groups", [(2, 1, 0), (4, 3, 0), (4, 1, 2), (2, 1, 1)])
+def test_emulated_diagnostics(V, n_loc, groups):
+    # multi-rank diagnostics (k_diag_scatter/reduce/final): column chunks per rank,
+    # rank-ordered partials, within 1e-9 of the oracle (fp64, another summation order)
+    from oracle.diagnostics import consensus
+    n, d, k = V * n_loc, 40_003, 4
+    x, m, w, bank2 = _bind_emulated(V, n, d, k, 6, groups=groups or None)
+    orc = OracleRun(n, d, k, 6, groups=groups or None)
+    cs.cs_set_diag(True)
+    step = cs.cs_hier_step if groups else cs.cs_gossip_step
+    for t in range(3):
+        step(x, grads_view(bank2, n, t), w, LR, MU)
+        orc.step(LR, MU)
+        cd, ms = cs.cs_get_diag()
+        cd0, ms0 = consensus(orc.x, orc.w, orc.seg)
+        assert abs(cd - cd0) <= 1e-9 * abs(cd0), (t, cd, cd0)
+        assert abs(ms - ms0) <= 1e-9 * max(1.0, abs(ms0)) + 1e-9 * d, (t, ms, ms0)
+    cs.cs_set_diag(False)
+    cs.cs_finalize()
+
+
+@pytest.mark.parametrize("groups", [0, 1, 2])
+def test_emulated_lars(groups):
+    # LARS (C-18) on the in-step merge kernel (flat) and on the hierarchical step's group
+    # mean: rates within 1 ulp, params and momentum within 1e-6 (fp64 norm sums
+    # in another order), layer-plan segments
+    from oracle.lars import lars_gossip_step, lars_hier_step, plan_bounds, segment_plan
+    V, d, k = 2, 120_000, 4
+    ETA, WD, EPS, lr = 0.0025, 5e-5, 1e-9, 9.0
+    x, m, w, bank2 = _bind_emulated(V, V, d, k, 8, groups=groups or None)
+    rng = np.random.default_rng(10)
+    lb = np.concatenate([[0], np.unique(rng.integers(1, d // 4, size=9) * 4), [d]]).astype(np.int64)
+    plan = segment_plan(np.diff(lb).tolist(), k)
+    cs.cs_set_layers(lb, plan)
+    cs.cs_set_lars(ETA, WD, EPS)
+    orc = OracleRun(V, d, k, 8)
+    orc.seg = T.segment_of_columns(plan_bounds(lb, plan), orc.cols)
+    for t in range(4):
+        g = synth.grads_at(orc.bank, V, t)
+        if groups:
+            cs.cs_hier_step(x, grads_view(bank2, V, t), w, lr, MU)
+            orc.x, orc.m, orc.w, lrs = lars_hier_step(orc.x, orc.m, g, orc.w, groups, 8, t, k, orc.seg, lb, lr, MU,
+                                                      ETA, WD, EPS)
+        else:
+            cs.cs_gossip_step(x, grads_view(bank2, V, t), w, lr, MU)
+            orc.x, orc.m, orc.w, lrs = lars_gossip_step(orc.x, orc.m, g, orc.w, T.topology(8, t, V, k), orc.seg, lb,
+                                                        lr, MU, ETA, WD, EPS)
+        orc.t += 1
+        got = cs.cs_get_lars_rates(V, len(lb) - 1)
+        want = lrs if not groups else np.repeat(lrs, V // groups, axis=0)
+        assert np.all(np.abs(got.astype(np.float64) - want) <= np.spacing(np.abs(want))), t
+        xg, mg = x.cpu().numpy()[:, :d], m.cpu().numpy()[:, :d]
+        assert np.all(np.abs(xg - orc.x) <= 1e-6 * np.abs(orc.x).max(axis=1, keepdims=True)), t
+        mref = orc.m if not groups else np.repeat(orc.m[::V // groups], V // groups, axis=0)
+        assert np.all(np.abs(mg - mref) <= 1e-6 * np.abs(mref).max(axis=1, keepdims=True)), t
+    cs.cs_set_lars(0.0)
     cs.cs_finalize()
 
 

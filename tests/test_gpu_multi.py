@@ -43,6 +43,35 @@ def test_two_gpu_parity(n_loc, d, k, steps, full):
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("n_loc,d,k,extra", [(1, 100_003, 5, []), (1, 25_557_032, 8, []), (1, 50_001, 1, ["--exponential"]),
+                                             (1, 70_001, 4, ["--wire-bf16"]), (1, 200_000, 6, ["--hier-groups", "2"])])
+def test_two_gpu_in_step_merge_without_flush(n_loc, d, k, extra):
+    # the default schedule: after each step's work -- a plain stream synchronize, no cs_flush
+    # or cs_sync -- params and psw equal the oracle's merged x', w' bit for bit
+    args = ["--workers-per-gpu", n_loc, "--vector-len", d, "--segments", k, "--num-steps", 8, "--stream-sync"]
+    if d < 1_000_000:
+        args.append("--compare-all")
+    _run(2, *args, *extra)
+
+
+@pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
+@pytest.mark.parametrize("d,k,extra", [(25_557_032, 8, []), (300_001, 16, ["--hier-groups", "2"]),
+                                       (100_003, 3, ["--wire-bf16"])])
+def test_four_gpu_in_step_merge_without_flush(d, k, extra):
+    args = ["--workers-per-gpu", 1, "--vector-len", d, "--segments", k, "--num-steps", 8, "--stream-sync"]
+    if d < 1_000_000:
+        args.append("--compare-all")
+    _run(4, *args, *extra)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("schedule", ["deferred", "split"])
+def test_two_gpu_opt_in_schedules_bitwise(schedule):
+    _run(2, "--workers-per-gpu", 1, "--vector-len", 100_003, "--segments", 5, "--num-steps", 6, "--compare-all",
+         "--schedule", schedule)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 def test_two_gpu_resnet50_sampled():
     # BASELINE configs[2] layout (one worker per GPU, 25,557,032 fp32, k = 8)
     _run(2, "--workers-per-gpu", 1, "--vector-len", 25_557_032, "--segments", 8, "--num-steps", 10)
@@ -123,7 +152,7 @@ def test_two_gpu_deferred_merge_bitwise(n_loc, d, k, extra):
     args = ["--workers-per-gpu", n_loc, "--vector-len", d, "--segments", k, "--num-steps", 7, "--sync-at-end"]
     if d < 1_000_000:
         args.append("--compare-all")
-    _run(2, *args, *extra, env={"CS_PEER_HYBRID": "0"})
+    _run(2, *args, *extra, "--schedule", "deferred", env={"CS_PEER_HYBRID": "0"})
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
@@ -133,7 +162,7 @@ def test_two_gpu_deferred_merge_bitwise(n_loc, d, k, extra):
 def test_two_gpu_hybrid_deferred_tail_merge_bitwise(n_loc, d, k, extra):
     # several workers per GPU (hybrid walk): each step's chain tails merge inside the next walk
     _run(2, "--workers-per-gpu", n_loc, "--vector-len", d, "--segments", k, "--num-steps", 7, "--sync-at-end",
-         "--compare-all", *extra)
+         "--compare-all", "--schedule", "deferred", *extra)
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
@@ -157,13 +186,15 @@ def test_two_gpu_hier_deferred_exchange_merge_bitwise():
     # groups >= 2: the leader exchange's merge runs inside the next hierarchical push
     # (opt-in schedule, CS_HIER_FUSE=1)
     _run(2, "--workers-per-gpu", 1, "--vector-len", 150_001, "--segments", 5, "--num-steps", 6,
-         "--hier-groups", 2, "--compare-all", "--sync-at-end", env={"CS_HIER_FUSE": "1"})
+         "--hier-groups", 2, "--compare-all", "--sync-at-end", "--schedule", "deferred",
+         env={"CS_HIER_FUSE": "1"})
 
 
 @pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
 def test_four_gpu_hier_deferred_exchange_merge_bitwise():
     _run(4, "--workers-per-gpu", 1, "--vector-len", 150_001, "--segments", 7, "--num-steps", 6,
-         "--hier-groups", 2, "--compare-all", "--sync-at-end", env={"CS_HIER_FUSE": "1"})
+         "--hier-groups", 2, "--compare-all", "--sync-at-end", "--schedule", "deferred",
+         env={"CS_HIER_FUSE": "1"})
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
