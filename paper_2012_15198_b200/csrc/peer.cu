@@ -1408,7 +1408,7 @@ int upload_chunks(PeerState& p) {
   if (p.d_chunk_t0) cudaFree(p.d_chunk_t0);
   p.d_chunk_t0 = nullptr;
   p.n_chunks = (int)c.size() - 1;
-  if (p.n_tiles > p.mflag_cap) return CS_OK;  // no room: the in-step schedule is off (peer_merge_ok)
+  if ((int64_t)p.n_tiles * p.n_loc > p.mflag_cap) return CS_OK;  // no room: in-step off (peer_merge_ok)
   cudaError_t e = cudaSuccess;
   if (!p.d_stats) {
     e = cudaMalloc(&p.d_stats, sizeof(unsigned int) * 4);
@@ -1498,7 +1498,7 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   off += 192;
   // in-step merge schedule (k_push_merge): progress words [2][k][grid_merge]; the grid is
   // the same on every rank (same device model), checked through the header at import
-  if (n_loc == 1 && k <= 512) {
+  if (n_loc <= 64 && (int64_t)k * n_loc <= 2048 && k <= 512) {
     const int cap = peer_merge_capacity(k);
     p.grid_merge = cap / p.vranks;
     if (p.grid_merge < 1) p.grid_merge = 0;
@@ -1507,8 +1507,9 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   p.off_claim = off;
   off += 256;
   p.off_mflag = off;
-  // room for the chunks of any later layer table (its tiles split at up to CS_MAX_LAYERS bounds)
-  p.mflag_cap = p.grid_merge > 0 ? (int)((d + kPeerTile - 1) / kPeerTile) + k + CS_MAX_LAYERS + 16 : 0;
+  // trailers per (tile, row): room for a later layer table's extra tiles (one per layer bound,
+  // up to 1024 more; a table with more layers runs the split schedule)
+  p.mflag_cap = p.grid_merge > 0 ? ((int)((d + kPeerTile - 1) / kPeerTile) + k + 1024) * n_loc : 0;
   off = align_up(off + 16 * 2 * (size_t)p.mflag_cap, 256);
   p.off_hdr = off;
   off += 64;
@@ -1958,6 +1959,22 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   // a flat step gives every worker its own state: the next hierarchical step re-replicates
   // each group's leader to its members first
   p.need_sync = true;
+  if (peer_merge_ok(p, a)) {
+    // default: the merge completes inside this step's kernel (k_push_merge walks any n_loc)
+    p.last_fused = false;
+    if (ev0) cudaEventRecord(ev0, st);
+    rc = peer_flush(p, st);  // a merge left pending by the deferred schedule
+    if (rc) return rc;
+    if (a.world > 64) rc = launch_topology_for(a, a.world, CS_TAG_FLAT, st);
+    if (rc) return rc;
+    PeerStepArgs b = a;
+    b.gs = 0;
+    b.g_off = 0;
+    rc = peer_merge_launch(p, b, ++p.epoch, st);
+    if (rc) return perr(rc, "k_push_merge launch", cudaGetLastError());
+    if (ev1) cudaEventRecord(ev1, st);
+    return CS_OK;
+  }
   if (p.use_hybrid) {
     // deferred merge: this step's chain tails are merged inside the next walk (or
     // peer_flush); the previous step's tails are merged here before their update
@@ -1990,22 +2007,7 @@ int peer_flat_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "hybrid launch", e);
   }
-  if (peer_merge_ok(p, a)) {
-    // default (one worker per GPU): the merge completes inside this step's kernel
-    p.last_fused = false;
-    if (ev0) cudaEventRecord(ev0, st);
-    rc = peer_flush(p, st);  // a merge left pending by the deferred schedule
-    if (rc) return rc;
-    if (a.world > 64) rc = launch_topology_for(a, a.world, CS_TAG_FLAT, st);
-    if (rc) return rc;
-    PeerStepArgs b = a;
-    b.gs = 0;
-    b.g_off = 0;
-    rc = peer_merge_launch(p, b, ++p.epoch, st);
-    if (rc) return perr(rc, "k_push_merge launch", cudaGetLastError());
-    if (ev1) cudaEventRecord(ev1, st);
-    return CS_OK;
-  }
+
   // deferred merge (opt-in, kSchedDeferred): this step's push applies the previous step's
   // merge tile by tile, and its own merge waits for the next push (or peer_flush); the
   // separate mix pass and its cross-GPU wait disappear from the step, but params hold y

@@ -64,7 +64,7 @@ struct PeerState {
   size_t off_mflag = 0, off_hdr = 0;  // per-tile trailers uint4 [2][mflag_cap]; layout header
   unsigned int* d_stats = nullptr;     // [0]: merge tiles re-read after a failed verification
   size_t off_claim = 0;                // chunk claim counters [2] (by epoch parity)
-  int mflag_cap = 0;                   // tiles the trailers can cover
+  int mflag_cap = 0;                   // trailer slots per parity (tiles x n_loc)
   int32_t* d_chunk_t0 = nullptr;       // [n_chunks + 1] first tile of each chunk
   int n_chunks = 0;
   int gs = 0;              // hierarchical group size in GPUs (0: flat only)
@@ -148,7 +148,7 @@ int peer_set_schedule(PeerState& p, int sched, cudaStream_t st);
 // worker per GPU).  hier: the leader exchange of a hierarchical step (g = group mean).
 int peer_merge_launch(PeerState& p, const PeerStepArgs& a, uint32_t epoch, cudaStream_t st);
 bool peer_merge_ok(const PeerState& p, const PeerStepArgs& a);
-size_t peer_merge_smem(int k, bool wire);
+size_t peer_merge_smem(int k, int n_loc);
 std::vector<int32_t> peer_merge_chunks(const std::vector<int32_t>& seg_t0, int chunk, int grid);
 constexpr int kMergeChunk = 4;    // tiles per claimed chunk (one landed flag and release each)
 int peer_merge_capacity(int k);   // co-resident k_push_merge CTAs on this GPU

@@ -1,46 +1,51 @@
-// k_push_merge: one multi-GPU step (one worker per GPU) whose merge a5 completes inside
-// the step's own kernel, so params and psw hold the merged x', w' when the step's enqueued
-// work completes ("parameter averaging is processed after the gradient is applied",
-// PAPER.md:122; Alg. 1 l.12-17: wait for the segments, then average).
+// k_push_merge: one multi-GPU flat step (or the leader exchange of a hierarchical step)
+// whose merge a5 completes inside the step's own kernel, so params and psw hold the merged
+// x', w' when the step's enqueued work completes ("parameter averaging is processed after
+// the gradient is applied"; Alg. 1 l.12-17: wait for the
+// segments, then average).  Any number n_loc of workers per GPU.
 //
-// Work units are chunks of up to kMergeChunk segment-aligned tiles, numbered in segment
-// order.  Every GPU runs a persistent grid whose CTAs claim chunks from a per-GPU counter
-// (dynamic: with a static split, per-CTA timestamps showed SMs finishing between 90 and
-// 160 us), so all GPUs sweep the vector front to back at the same pace and tile t of a
-// receiver is pushed by its sender at about the time the receiver updates it.
-// Warp roles of a CTA:
+// Work: for every segment-aligned tile (2048 columns) the CTA walks the n_loc local rows in
+// the order of that segment's permutation restricted to this GPU (built in the prologue
+// from Alg. 2): local cycles c0 <- c1 <- ... (x'_{c_p} = mean(y_{c_p},
+// y_{c_{p+1}}), all in registers), and chains whose head's receiver and whose tail's
+// source are on other GPUs.  Per row that is one update (a3); a chain head's y goes to its
+// receiver's inbox over NVLink (a4), a chain tail merges with the y it receives (a5).
+// With one worker per GPU every row is a one-element chain (push and merge).
 //
-//   x/m/g warp        claims chunks, bulk-loads the x, m, g tiles (3-stage ring)
-//   update warps (8)  a3: m' = mu*m + g, y = x - lr*m'; m' -> HBM; y -> params (through L2:
-//                     the mix re-reads it soon) and into the push ring (bf16 on the bf16
-//                     wire), with two 32-bit checksums of the pushed words
-//   store warp        a4 (Alg.1 l.7 isend): one bulk copy per y tile into the inbox of the
-//                     tile's receiver over NVLink; once the copy has completed
-//                     (cp.async.bulk.wait_group) a 16-byte trailer for the tile
-//                     {epoch, xor ^ w, weighted sum, w} (w = the push-sum weight on a
+// Tiles are claimed in chunks from a per-GPU counter (dynamic: with a static split,
+// per-CTA timestamps showed SMs finishing between 90 and 160 us), in segment order, so
+// all GPUs sweep the vector front to back at the same pace.  Warp roles of a CTA:
+//
+//   x/m/g warp        claims chunks, bulk-loads the x, m, g row-tiles in walk order
+//   update warps (8)  a3 + the walk: m' -> HBM; x' of local pairs -> HBM; a chain tail's y
+//                     -> params (through L2, the mix re-reads it); a head's y into the push
+//                     ring (bf16 on the bf16 wire) with two 32-bit checksums of its words
+//   store warp        a head's tile: one bulk copy into its receiver's inbox row; once the
+//                     copy has completed (cp.async.bulk.wait_group) a 16-byte trailer
+//                     {epoch, xor ^ w, weighted sum, w} (w: the push-sum weight on a
 //                     segment's first tile) goes to the receiver
-//   inbox warp        waits for the tile's trailer epoch (Alg.1 l.14 "wait until ...
-//                     communication is completed", per tile), stages the received tile and
-//                     the own y tile (Alg.1 l.8 irecv)
-//   mix warps (4)     verify the received words against the trailer's checksums (re-read
-//                     from memory until they match), then a5: x' = fl(fl(y + y_recv) * 0.5)
-//                     -> params; a segment's first tile also merges psw (C-11)
+//   inbox warp        for a chain tail: stages the tile's trailer, the received tile and the
+//                     own y tile (Alg.1 l.8 irecv)
+//   mix warps (4)     verify the received words against the trailer's checksums (polling
+//                     the trailer and re-reading the words until they match: Alg.1 l.14
+//                     "wait until ... communication is completed", per tile), then
+//                     a5: x' = fl(fl(y + y_recv) * 0.5) -> params and the tail's psw
 //
 // Why trailers and not release/acquire flags: a system-scope fence waits for the SM's
 // in-flight NVLink copies, and under this load each one took ~13 us (measured: the
 // signalling warp spent 130 of 160 us in fences), so a per-chunk release lagged the merge
-// by tens of microseconds.  A trailer is written only after its tile's copy completed;
-// the receiver accepts the tile only when its words reproduce both checksums of that
-// exact trailer, so a tile is never mixed from partially arrived or stale data, whatever
-// order the fabric delivers writes in (a stale tile would have to match two 32-bit
-// checksums of new data).
+// by tens of microseconds.  A trailer is written only after its tile's copy completed; the
+// receiver accepts the tile only when its words reproduce both checksums of that exact
+// trailer, so a tile is never mixed from partially arrived or stale data, whatever order
+// the fabric delivers writes in (a stale tile would have to match two 32-bit checksums of
+// new data).  Measured: ~1.7 % of tiles are first read before their words are visible.
 //
 // Nothing that produces a tile (claim, update, push) waits for another GPU's progress in the
-// step: only the inbox warp and the mix do, and nothing waits for the mix.  So the merge
-// may trail the update by any distance, and the step has no grid-wide or cross-GPU barrier.
-// HBM per parameter: 12 B read (x, m, g) + 4 B m' + 4 B x' + 4 B inbox written by the
-// sender + 4 B inbox read = 28 B, + 8 B for y (write, re-read) where L2 does not absorb it;
-// NVLink 4 B out and 4 B in (+16 B per 8 KB tile of trailer).
+// step: only the inbox warp and the mix do, and nothing waits for the mix.  So the merge may
+// trail the update by any distance, and the step has no grid-wide or cross-GPU barrier.
+// HBM per parameter: 20 B (read x, m, g; write m', x') + for a tail 4 B inbox written by
+// the sender + 4 B inbox read (+ 8 B y write and re-read where L2 does not absorb it);
+// NVLink 4 B out per head parameter (+16 B per 8 KB tile of trailer).
 //
 // Ping-pong: inbox and trailers are indexed by the epoch parity.  Before writing parity
 // e & 1 into a receiver, the store warp checks that every rank consumed epoch e - 2 (its
@@ -76,18 +81,25 @@ constexpr int kWarps = kMThreads / 32;
 constexpr int kNA = 3, kNI = 3, kNY = 4;              // ring depths: x/m/g stages, inbox + own y, push
 constexpr int kLand = 1;                              // copies in flight before the store warp checks completion
 constexpr int kMaxK = 512;                            // segments (smem tables)
+constexpr int kMaxLoc = 64;                           // workers per GPU (64-bit walk masks)
+constexpr int kMaxKN = 2048;                          // k * n_loc (smem walk tables)
 constexpr int kMaxClaims = 1024;                      // chunks one CTA may claim per step (smem list)
 constexpr int kWLoadXmg = (kUpd + kMix) / 32, kWLoadIn = kWLoadXmg + 1, kWStore = kWLoadXmg + 2;
 constexpr int kPerU = kT / 4 / kUpd;                  // float4 per update thread per tile
 constexpr int kPerM = kT / 4 / kMix;                  // float4 per mix thread per tile
 constexpr int kMixBar = 1;                            // named barrier of the mix warps
+// walk-order entries: local row | flags
+constexpr uint32_t kWStart = 1u << 31, kWEnd = 1u << 30, kWHead = 1u << 29, kWTail = 1u << 28;
+constexpr uint32_t kWIdx = (1u << 28) - 1;
 
-size_t smem_bytes(int k) {
+size_t smem_bytes(int k, int n_loc) {
   size_t b = sizeof(float) * (size_t)kT * (3 * kNA + 2 * kNI + kNY);
-  b += sizeof(int64_t) * (k + 1) + sizeof(int32_t) * (k + 1) + sizeof(int32_t) * (size_t)k;
+  b += sizeof(int64_t) * (k + 1) + sizeof(int32_t) * (k + 1);
+  b += 2 * sizeof(uint32_t) * (size_t)k * n_loc;  // walk order, head receivers
   b += sizeof(int32_t) * kMaxClaims;
+  b += sizeof(float) * kMaxLoc;                    // psw snapshot of a segment's first tile
   b = (b + 15) & ~size_t(15);
-  b += sizeof(uint32_t) * 128 * kWarps;  // per-warp Alg. 2 scratch
+  b += sizeof(uint32_t) * 192 * kWarps;            // per-warp Alg. 2 / inverse scratch
   return b;
 }
 
@@ -99,11 +111,11 @@ struct MergeArgs {
   const TileDesc* tiles;    // explicit tiles (layer table) or nullptr
   const int32_t* chunk_t0;  // [n_chunks+1] first tile of each chunk (chunks never cross segments)
   int n_tiles, n_chunks;
-  int trl_cap;              // trailer slots per parity
+  int trl_cap;              // trailer slots per parity (tiles x n_loc)
   int lag;                  // the inbox warp stages position j once the update is at j + lag
   int vranks;
   uint32_t epoch;
-  int fused_topo;
+  int fused_topo;           // draw Alg. 2 in the prologue (<= 64 ranks), else read s.src
   unsigned long long* trace;  // measurement only (CS_MERGE_TRACE): per-CTA timestamps [G][8]
   unsigned int* retries;      // tiles whose first read failed verification (diagnostic counter)
   uint32_t done_target;     // arrival total at which this step's last CTA publishes done = epoch
@@ -135,12 +147,16 @@ __device__ __forceinline__ MTile mtile(const MergeArgs& a, const int64_t* bnd, c
   return u;
 }
 
-// A role's walk over the CTA's claimed chunks: position i -> tile.  claims[] is written by
-// the x/m/g warp before the first tile of a chunk is released to the pipeline (every other
-// role reaches that position after an acquire that follows the write).
+// A role's walk over the CTA's positions: claimed chunks -> tiles -> the n_loc rows of a
+// tile in walk order (p).  claims[] is written by the x/m/g warp before the first tile of a
+// chunk is released to the pipeline (every other role reaches that position after an
+// acquire that follows the write).
 struct Walk {
-  int ci = -1, t = 0, t_end = 0, chunk = -1;
-  __device__ __forceinline__ bool next(const int32_t* claims, const int32_t* chunk_t0) {
+  int ci = -1, t = 0, t_end = 0, chunk = -1, p = 0;
+  __device__ __forceinline__ void init(int n_loc) { p = n_loc - 1; }
+  __device__ __forceinline__ bool next(const int32_t* claims, const int32_t* chunk_t0, int n_loc) {
+    if (++p < n_loc) return true;
+    p = 0;
     if (t + 1 < t_end) {
       ++t;
       return true;
@@ -211,6 +227,13 @@ __device__ __forceinline__ void ck_add(uint32_t& cx, uint32_t& cs, uint32_t w, u
   cs += w * (2u * i + 1u);
 }
 
+// Wait until the update warps finished position j (true), or the walk ends before it (false).
+__device__ __forceinline__ bool wait_position(const uint32_t* y_stored, volatile int* end_pos, int j) {
+  while ((int32_t)(ld_acquire_cta(y_stored) - (uint32_t)(kUpd / 32) * (uint32_t)(j + 1)) < 0)
+    if (*end_pos <= j) return false;
+  return true;
+}
+
 __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) {
   extern __shared__ __align__(128) float smem_f[];
   float* ringA = smem_f;                                   // [kNA][3][kT]  x, m, g
@@ -218,25 +241,28 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
   float* ringY = ringI + (size_t)kNI * 2 * kT;             // [kNY][kT]     y to push (fp32 or bf16)
   const PeerStepArgs& s0 = a.s;
   const bool wire = s0.wire != 0;
+  const int n_loc = s0.n_loc;
   int64_t* bnd = reinterpret_cast<int64_t*>(ringY + (size_t)kNY * kT);
   int32_t* t0 = reinterpret_cast<int32_t*>(bnd + s0.k + 1);
-  int32_t* recv = t0 + s0.k + 1;                           // [k] rank receiving my segment s
-  int32_t* claims = recv + s0.k;                           // [kMaxClaims] chunks claimed, -1 ends
+  uint32_t* ord = reinterpret_cast<uint32_t*>(t0 + s0.k + 1);  // [k][n_loc] walk order per segment
+  int32_t* hdst = reinterpret_cast<int32_t*>(ord + s0.k * n_loc);  // [k][n_loc] receiver of a head row
+  int32_t* claims = hdst + s0.k * n_loc;                   // [kMaxClaims] chunks claimed, -1 ends
+  float* wsnap = reinterpret_cast<float*>(claims + kMaxClaims);  // [kMaxLoc] psw of a first tile's segment
   uint32_t* scratch = reinterpret_cast<uint32_t*>(
-      (reinterpret_cast<uintptr_t>(claims + kMaxClaims) + 15) & ~uintptr_t(15));  // [kWarps][128]
+      (reinterpret_cast<uintptr_t>(wsnap + kMaxLoc) + 15) & ~uintptr_t(15));  // [kWarps][192]
   __shared__ uint64_t a_full[kNA], a_empty[kNA], i_full[kNI], i_empty[kNI], y_full[kNY], y_free[kNY];
   __shared__ uint32_t ck_upd[kNY][kUpd / 32][2];  // per update warp: checksums of its pushed words
   __shared__ uint32_t w_upd[kNY];                 // push-sum weight bits sent with the tile (0: none)
+  __shared__ int32_t dst_upd[kNY];                // receiving worker of a head's tile (-1: not a head)
   __shared__ uint4 meta[kNI];                     // trailer of the staged received tile (bulk-loaded)
   __shared__ uint4 meta_re;                       // trailer re-read by the mix after a failed check
-  __shared__ uint32_t ck_mix[2][kMix / 32][2];    // per mix warp, double-buffered by tile parity
-  __shared__ uint32_t y_stored;  // update-warp arrivals: position j's y is in params at >= 8 (j + 1)
-  __shared__ int s_end;          // number of positions (tiles) this CTA processes; INT_MAX until known
+  __shared__ uint32_t ck_mix[2][kMix / 32][2];    // per mix warp, double-buffered by round parity
+  __shared__ uint32_t y_stored;  // update-warp arrivals: position j is done at >= 8 (j + 1)
+  __shared__ int s_end;          // number of positions this CTA processes; INT_MAX until known
   __shared__ int s_timeout;
   volatile int* timeout = &s_timeout;
   volatile int* end_pos = &s_end;
 
-  const unsigned long long t_entry = a.trace ? ptx::globaltimer() : 0;
   const RankCta rc = rank_cta(a.vranks, s0.rank);
   PeerStepArgs s = s0;
   rank_view(s, a.peers, a.vranks, rc.rank);
@@ -246,6 +272,11 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
   char* mine = a.peers[s.rank];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ld_bf = (s.ld + 7) & ~int64_t(7);
+  // the rank's rows as locals (computed from the launch arguments)
+  const int64_t vrows = a.vranks > 1 ? (int64_t)rc.rank * n_loc : 0;
+  float* const X = s0.x + vrows * s0.ld;
+  float* const M = s0.m + vrows * s0.ld;
+  float* const PSW = s0.psw + vrows * s0.k;
 
   for (int i = threadIdx.x; i <= s.k; i += blockDim.x) {
     bnd[i] = a.bounds[i];
@@ -265,60 +296,126 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     }
     for (int i = 0; i < kNY; ++i) {
       ptx::mbar_init(&y_full[i], kUpd / 32);
-      ptx::mbar_init(&y_free[i], 1);  // the store warp's copy has read the slot
+      ptx::mbar_init(&y_free[i], 1);  // the store warp is done with the slot
     }
     ptx::mbar_fence_init();
   }
-  // this step's receivers: Alg. 2 per segment, one warp per segment,
-  // then send_to = the rank that receives from me (Alg.1 l.6)
+  // ---- this step's topology restricted to this GPU's workers (Alg. 2):
+  // per segment the walk order (chains first, from their heads, then the local cycles) and
+  // the receiver of every chain head (send_to, Alg.1 l.6)
   {
+    uint32_t* u = scratch + warp * 192;
+    int32_t* srow = reinterpret_cast<int32_t*>(u + 64);   // [<= 64] the drawn row when fused
+    int32_t* dstl = reinterpret_cast<int32_t*>(u + 128);  // [n_loc] receiver of each local worker
     const int ntop = s.gs > 0 ? s.groups : s.world;
-    const int grp = s.gs > 0 ? s.rank / s.gs : 0;
-    const int target = s.gs > 0 ? grp : s.rank;
-    uint32_t* u = scratch + warp * 128;
-    int32_t* srow = reinterpret_cast<int32_t*>(u + 64);
     for (int sg = warp; sg < s.k; sg += kWarps) {
-      if (!a.fused_topo) {
-        if (lane == 0) recv[sg] = receiver_worker(s, sg, 0);
+      if (s.gs > 0) {  // hierarchical leader exchange (one worker per GPU, replicated leader)
+        if (lane == 0) dstl[0] = -1;
+        __syncwarp();
+        const int grp = s.rank / s.gs, member = s.rank - grp * s.gs;
+        const int32_t* row;
+        if (s.given != nullptr) row = s.given + (int64_t)sg * ntop;
+        else if (a.fused_topo) {
+          warp_alg2_small(s.seed, s.step, sg, ntop, CS_TAG_HIER, u, srow, s.err);
+          row = srow;
+        } else row = s.src + (int64_t)sg * ntop;
+        __syncwarp();
+        for (int jj = lane; jj < ntop; jj += 32)
+          if (row[jj] == grp) dstl[0] = jj * s.gs + member;  // the member of the same index
+        __syncwarp();
+        if (lane == 0) {
+          ord[sg] = 0u | kWStart | kWHead | kWEnd | kWTail;
+          hdst[sg] = dstl[0];
+        }
+        __syncwarp();
         continue;
       }
-      const int32_t* row = srow;
+      const int32_t* row;
       if (s.given != nullptr) row = s.given + (int64_t)sg * ntop;
-      else warp_alg2_small(s.seed, s.step, sg, ntop, s.gs > 0 ? CS_TAG_HIER : CS_TAG_FLAT, u, srow, s.err);
+      else if (a.fused_topo) {
+        warp_alg2_small(s.seed, s.step, sg, ntop, CS_TAG_FLAT, u, srow, s.err);
+        row = srow;
+      } else row = s.src + (int64_t)sg * ntop;
       __syncwarp();
-      for (int jj = lane; jj < ntop; jj += 32)
-        if (row[jj] == target) recv[sg] = s.gs > 0 ? jj * s.gs + (s.rank - grp * s.gs) : jj;
+      const int first = s.first;
+      for (int jj = lane; jj < ntop; jj += 32) {  // inverse on the local range: receivers
+        const int v = row[jj];
+        if (v >= first && v < first + n_loc) dstl[v - first] = jj;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        uint32_t* o = ord + sg * n_loc;
+        uint64_t seen = 0;
+        int pos = 0;
+        for (int r = 0; r < n_loc; ++r) {  // chains start where the receiver is remote
+          const int dg = dstl[r];
+          if (dg >= first && dg < first + n_loc) continue;
+          hdst[sg * n_loc + r] = dg;
+          int pr = r;
+          uint32_t flag = kWStart | kWHead;
+          while (true) {
+            seen |= 1ull << pr;
+            const int sgl = row[first + pr] - first;
+            if (sgl < 0 || sgl >= n_loc) {  // source remote: chain tail
+              o[pos++] = (uint32_t)pr | flag | kWEnd | kWTail;
+              break;
+            }
+            o[pos++] = (uint32_t)pr | flag;
+            flag = 0;
+            pr = sgl;
+          }
+        }
+        for (int r0 = 0; r0 < n_loc; ++r0) {  // the rest: cycles of local workers
+          if ((seen >> r0) & 1ull) continue;
+          int pr = r0;
+          uint32_t flag = kWStart;
+          do {
+            seen |= 1ull << pr;
+            const int nx = row[first + pr] - first;
+            o[pos++] = (uint32_t)pr | flag | (nx == r0 ? kWEnd : 0u);
+            flag = 0;
+            pr = nx;
+          } while (pr != r0);
+        }
+      }
       __syncwarp();
     }
   }
   __syncthreads();
   unsigned long long* tr = a.trace ? a.trace + ((size_t)s.rank * G + b) * 8 : nullptr;
-  if (tr && threadIdx.x == 0) {
-    tr[0] = ptx::globaltimer();
-    tr[5] = t_entry;
-  }
+  if (tr && threadIdx.x == 0) tr[0] = ptx::globaltimer();
   uint4* trl_in = reinterpret_cast<uint4*>(mine + a.off_trl) + (size_t)par * a.trl_cap;
 
   if (warp < kUpd / 32) {
-    // ---------------- update warps: a3 ------------------------------------------------
+    // ---------------- update warps: a3 and the walk ---------------------------------
     const int tid = threadIdx.x;
     bool bad = false;
     int cur = 0;
     Walk w;
+    w.init(n_loc);
+    float4 yfirst[kPerU], yprev[kPerU];
+    uint32_t prev_row = 0;
     for (int i = 0;; ++i) {
       const int st = i % kNA, sy = i % kNY;
       ptx::mbar_wait(&a_full[st], (uint32_t)((i / kNA) & 1));
       ptx::mbar_wait(&y_free[sy], (uint32_t)(((i / kNY) & 1) ^ 1));
-      if (!w.next(claims, a.chunk_t0)) {  // end marker: pass it on to the store warp
+      if (!w.next(claims, a.chunk_t0, n_loc)) {  // end marker: pass it on to the store warp
+        if (tid == 0) dst_upd[sy] = -2;
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&y_full[sy]);
         break;
       }
       const MTile U = mtile(a, bnd, t0, w.t, cur);
+      const uint32_t e_w = ord[U.seg * n_loc + w.p];
+      const uint32_t row = e_w & kWIdx;
+      const bool head = (e_w & kWHead) != 0, tail = (e_w & kWTail) != 0;
       const float* bx = ringA + (size_t)st * 3 * kT;
       float4* yt = reinterpret_cast<float4*>(ringY + (size_t)sy * kT);
-      const float rate = s.lrs ? __ldg(s.lrs + U.layer) : s.lr;
+      const float rate = s.lrs ? __ldg(s.lrs + (int64_t)row * s.n_layers + U.layer) : s.lr;
       const uint32_t nw = wire ? (uint32_t)(U.len + 1) / 2 : (uint32_t)U.len;  // pushed words checked
+      const int64_t rowoff = (int64_t)row * s.ld;
+      if (U.first && w.p == 0 && tid == 0)  // the segment's psw before any merge of this step
+        for (int r = 0; r < n_loc; ++r) wsnap[r] = PSW[(int64_t)r * s.k + U.seg];
       uint32_t cx = 0, cs = 0;
 #pragma unroll
       for (int q = 0; q < kPerU; ++q) {
@@ -326,43 +423,74 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
         const int valid = U.len - 4 * v;
         if (valid > 0) {
           const int vv = valid < 4 ? valid : 4;
+          const int64_t j = U.c0 + 4 * (int64_t)v;
           const float4 cxv = reinterpret_cast<const float4*>(bx)[v];
           const float4 cm = reinterpret_cast<const float4*>(bx + kT)[v];
           const float4 cg = reinterpret_cast<const float4*>(bx + 2 * kT)[v];
           bad |= nonfinite4(cg);
-          // LARS (C-18): m' = mu*m + (g + wd*x), y = x - lrs[layer]*m'
+          // LARS (C-18): m' = mu*m + (g + wd*x), y = x - lrs[row][layer]*m'
           const float4 mn = mom4(cm, s.lrs ? decay4(cg, cxv, s.wd) : cg, s.mu);
           const float4 y = sgd4(cxv, mn, rate);
-          st4_cs(s.m + U.c0 + 4 * v, mn, vv);
-          st4(s.x + U.c0 + 4 * v, y, vv);  // default policy: stays in L2 for the mix
-          if (wire) {  // what the receiver gets (C-20)
-            const uint2 pw = pack_bf16x4(y);
-            reinterpret_cast<uint2*>(yt)[v] = pw;
-            if (2u * v < nw) ck_add(cx, cs, pw.x, 2u * v);
-            if (2u * v + 1 < nw) ck_add(cx, cs, pw.y, 2u * v + 1);
-          } else {
-            yt[v] = y;
-            const uint32_t wv[4] = {__float_as_uint(y.x), __float_as_uint(y.y), __float_as_uint(y.z),
-                                    __float_as_uint(y.w)};
+          st4_cs(M + rowoff + j, mn, vv);
+          // the walk: x'_{prev} = mean(y_prev, y) (this row is prev's source, Alg.1 l.17),
+          // a cycle closes with its first y; what a worker receives is bf16 on the bf16 wire
+          if (e_w & kWStart) yfirst[q] = y;
+          else st4_cs(X + (int64_t)prev_row * s.ld + j, mean4(yprev[q], wire ? bf16r4(y) : y), vv);
+          if (e_w & kWEnd) {
+            if (tail) st4(X + rowoff + j, y, vv);  // merged by the mix warps (default policy: L2)
+            else st4_cs(X + rowoff + j, mean4(y, wire ? bf16r4(yfirst[q]) : yfirst[q]), vv);
+          }
+          yprev[q] = y;
+          if (head) {
+            if (wire) {  // what the receiver gets (C-20)
+              const uint2 pw = pack_bf16x4(y);
+              reinterpret_cast<uint2*>(yt)[v] = pw;
+              if (2u * v < nw) ck_add(cx, cs, pw.x, 2u * v);
+              if (2u * v + 1 < nw) ck_add(cx, cs, pw.y, 2u * v + 1);
+            } else {
+              yt[v] = y;
+              const uint32_t wv[4] = {__float_as_uint(y.x), __float_as_uint(y.y), __float_as_uint(y.z),
+                                      __float_as_uint(y.w)};
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-              if (c < vv) ck_add(cx, cs, wv[c], 4u * v + c);
+              for (int c = 0; c < 4; ++c)
+                if (c < vv) ck_add(cx, cs, wv[c], 4u * v + c);
+            }
           }
         }
       }
+      prev_row = row;
+      if (head) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        cx ^= __shfl_xor_sync(0xffffffffu, cx, o);
-        cs += __shfl_xor_sync(0xffffffffu, cs, o);
+        for (int o = 16; o > 0; o >>= 1) {
+          cx ^= __shfl_xor_sync(0xffffffffu, cx, o);
+          cs += __shfl_xor_sync(0xffffffffu, cs, o);
+        }
+        if (lane == 0) {
+          ck_upd[sy][warp][0] = cx;
+          ck_upd[sy][warp][1] = cs;
+        }
       }
-      if (lane == 0) {
-        ck_upd[sy][warp][0] = cx;
-        ck_upd[sy][warp][1] = cs;
+      if (tid == 0) {
+        // a head's tile goes to its receiver with the segment's weight on the first tile
+        dst_upd[sy] = head ? hdst[U.seg * n_loc + row] : -1;
+        w_upd[sy] = (head && U.first) ? __float_as_uint(wsnap[row]) : 0u;
+        if (U.first && w.p == n_loc - 1)  // psw of the rows with a local source
+          for (int p = 0; p < n_loc; ++p) {
+            const uint32_t o = ord[U.seg * n_loc + p];
+            if (o & kWTail) continue;  // merged with the received weight by the mix
+            const uint32_t src = (o & kWEnd) ? 0xffffffffu : (ord[U.seg * n_loc + p + 1] & kWIdx);
+            uint32_t sl = src;
+            if (o & kWEnd) {  // a cycle's last member's source is the cycle's first
+              int q2 = p;
+              while (!(ord[U.seg * n_loc + q2] & kWStart)) --q2;
+              sl = ord[U.seg * n_loc + q2] & kWIdx;
+            }
+            const uint32_t r = o & kWIdx;
+            PSW[(int64_t)r * s.k + U.seg] = pair_mean1(wsnap[r], wsnap[sl]);
+          }
       }
-      // the push-sum weight travels with the segment's first tile
-      if (tid == 0) w_upd[sy] = U.first ? __float_as_uint(s.psw[U.seg]) : 0u;
       ptx::fence_proxy_async_shared();  // push tile -> the store warp's bulk copy
-      ptx::fence_proxy_async_global();  // y in params -> the inbox warp's bulk copy
+      ptx::fence_proxy_async_global();  // a tail's y in params -> the inbox warp's bulk copy
       __syncwarp();
       if (lane == 0) {
         ptx::mbar_arrive(&a_empty[st]);
@@ -373,43 +501,51 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(s.err + kErrDiverged, 1);
     if (tr && threadIdx.x == 0) tr[1] = ptx::globaltimer();
   } else if (warp < (kUpd + kMix) / 32) {
-    // ---------------- mix warps: verify, then a5 ------------------------------------
+    // ---------------- mix warps: a chain tail's verify + a5 -------------------------
     const int tm = threadIdx.x - kUpd, mw = tm >> 5;
-    const float* inbox_f = reinterpret_cast<const float*>(mine + a.off_inbox) + par * s.ld;
-    const uint16_t* inbox_w = reinterpret_cast<const uint16_t*>(mine + a.off_inbox) + par * ld_bf;
-    int cur = 0, retried = 0, round = 0;  // round: checksum reductions so far (buffer parity)
+    int cur = 0, retried = 0, round = 0, q = 0;  // round: checksum reductions (buffer parity); q: tails
     Walk w;
+    w.init(n_loc);
     for (int j = 0;; ++j) {
-      const int si = j % kNI;
-      ptx::mbar_wait(&i_full[si], (uint32_t)((j / kNI) & 1));
-      if (!w.next(claims, a.chunk_t0)) break;
+      if (!wait_position(&y_stored, end_pos, j)) break;
+      w.next(claims, a.chunk_t0, n_loc);
       const MTile U = mtile(a, bnd, t0, w.t, cur);
+      const uint32_t e_w = ord[U.seg * n_loc + w.p];
+      if (!(e_w & kWTail)) continue;
+      const uint32_t row = e_w & kWIdx;
+      const int si = q % kNI;
+      ptx::mbar_wait(&i_full[si], (uint32_t)((q / kNI) & 1));
+      ++q;
       const float* it = ringI + (size_t)si * 2 * kT;
       const float4* yt = reinterpret_cast<const float4*>(it + kT);
       const uint32_t nw = wire ? (uint32_t)(U.len + 1) / 2 : (uint32_t)U.len;
+      const float* inbox_f = reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * n_loc + row) * s.ld;
+      const uint16_t* inbox_w =
+          reinterpret_cast<const uint16_t*>(mine + a.off_inbox) + ((int64_t)par * n_loc + row) * ld_bf;
+      const uint4* trl = trl_in + (size_t)w.t * n_loc + row;
       uint4 tl = meta[si];
       uint4 raw[kPerM];  // the received words as pushed (fp32 bits, or 2 x 2 bf16 in .x .y)
 #pragma unroll
-      for (int q = 0; q < kPerM; ++q) {
-        const int v = tm + q * kMix;
+      for (int qq = 0; qq < kPerM; ++qq) {
+        const int v = tm + qq * kMix;
         if (wire) {
           const uint2 pw = reinterpret_cast<const uint2*>(it)[v];
-          raw[q] = make_uint4(pw.x, pw.y, 0u, 0u);
+          raw[qq] = make_uint4(pw.x, pw.y, 0u, 0u);
         } else {
-          raw[q] = reinterpret_cast<const uint4*>(it)[v];
+          raw[qq] = reinterpret_cast<const uint4*>(it)[v];
         }
       }
       for (int attempt = 0;; ++attempt) {
         uint32_t cx = 0, cs = 0;
 #pragma unroll
-        for (int q = 0; q < kPerM; ++q) {
-          const int v = tm + q * kMix;
+        for (int qq = 0; qq < kPerM; ++qq) {
+          const int v = tm + qq * kMix;
           if (4 * v < U.len) {
             if (wire) {
-              if (2u * v < nw) ck_add(cx, cs, raw[q].x, 2u * v);
-              if (2u * v + 1 < nw) ck_add(cx, cs, raw[q].y, 2u * v + 1);
+              if (2u * v < nw) ck_add(cx, cs, raw[qq].x, 2u * v);
+              if (2u * v + 1 < nw) ck_add(cx, cs, raw[qq].y, 2u * v + 1);
             } else {
-              const uint32_t wv[4] = {raw[q].x, raw[q].y, raw[q].z, raw[q].w};
+              const uint32_t wv[4] = {raw[qq].x, raw[qq].y, raw[qq].z, raw[qq].w};
 #pragma unroll
               for (int c = 0; c < 4; ++c)
                 if (4 * v + c < U.len) ck_add(cx, cs, wv[c], 4u * v + c);
@@ -427,21 +563,20 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
           ck_mix[pb][mw][1] = cs;
         }
         ptx::named_bar_sync(kMixBar, kMix);
-        uint32_t X = 0, S = 0;
+        uint32_t Xc = 0, Sc = 0;
 #pragma unroll
         for (int m2 = 0; m2 < kMix / 32; ++m2) {
-          X ^= ck_mix[pb][m2][0];
-          S += ck_mix[pb][m2][1];
+          Xc ^= ck_mix[pb][m2][0];
+          Sc += ck_mix[pb][m2][1];
         }
-        if (((X ^ tl.w) == tl.y && S == tl.z && tl.x == e) || *timeout) break;
+        if (((Xc ^ tl.w) == tl.y && Sc == tl.z && tl.x == e) || *timeout) break;
         // not (yet) the tile the trailer describes: wait for this epoch's trailer, then read
         // trailer and words again from memory
         if (tm == 0) {
           if (tl.x == e) ++retried;  // the trailer had arrived but the words had not
-          const uint32_t* ep = reinterpret_cast<const uint32_t*>(trl_in + w.t);
           const uint64_t tin = tr ? ptx::globaltimer() : 0;
           uint64_t tw = 0;
-          while ((int32_t)(ld_volatile1(ep) - e) < 0) {
+          while ((int32_t)(ld_volatile1(trl) - e) < 0) {
             const uint64_t now = ptx::globaltimer();
             if (tw == 0) tw = now;
             if (now - tw > ptx::kSpinLimitNs) {
@@ -452,35 +587,36 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
           }
           if (tr) tr[4] += ptx::globaltimer() - tin;
           if (attempt > 0) __nanosleep(256);
-          meta_re = ld_volatile4(trl_in + w.t);
+          meta_re = ld_volatile4(trl);
         }
         ptx::named_bar_sync(kMixBar, kMix);
         tl = meta_re;
 #pragma unroll
-        for (int q = 0; q < kPerM; ++q) {
-          const int v = tm + q * kMix;
+        for (int qq = 0; qq < kPerM; ++qq) {
+          const int v = tm + qq * kMix;
           if (4 * v < U.len) {
             if (wire) {
               const uint2 pw = ld_volatile2(inbox_w + U.c0 + 4 * v);
-              raw[q] = make_uint4(pw.x, pw.y, 0u, 0u);
+              raw[qq] = make_uint4(pw.x, pw.y, 0u, 0u);
             } else {
-              raw[q] = ld_volatile4(inbox_f + U.c0 + 4 * v);
+              raw[qq] = ld_volatile4(inbox_f + U.c0 + 4 * v);
             }
           }
         }
       }
 #pragma unroll
-      for (int q = 0; q < kPerM; ++q) {
-        const int v = tm + q * kMix;
+      for (int qq = 0; qq < kPerM; ++qq) {
+        const int v = tm + qq * kMix;
         const int valid = U.len - 4 * v;
         if (valid > 0) {
-          const float4 yr = wire ? unpack_bf16x4(make_uint2(raw[q].x, raw[q].y))
-                                 : make_float4(__uint_as_float(raw[q].x), __uint_as_float(raw[q].y),
-                                               __uint_as_float(raw[q].z), __uint_as_float(raw[q].w));
-          st4_cs(s.x + U.c0 + 4 * v, mean4(yt[v], yr), valid < 4 ? valid : 4);  // Alg.1 l.17
+          const float4 yr = wire ? unpack_bf16x4(make_uint2(raw[qq].x, raw[qq].y))
+                                 : make_float4(__uint_as_float(raw[qq].x), __uint_as_float(raw[qq].y),
+                                               __uint_as_float(raw[qq].z), __uint_as_float(raw[qq].w));
+          st4_cs(X + (int64_t)row * s.ld + U.c0 + 4 * v, mean4(yt[v], yr), valid < 4 ? valid : 4);  // Alg.1 l.17
         }
       }
-      if (U.first && tm == 0) s.psw[U.seg] = pair_mean1(s.psw[U.seg], __uint_as_float(tl.w));
+      if (U.first && tm == 0) PSW[(int64_t)row * s.k + U.seg] = pair_mean1(PSW[(int64_t)row * s.k + U.seg],
+                                                                          __uint_as_float(tl.w));
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&i_empty[si]);
     }
@@ -498,80 +634,76 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       ptx::fence_proxy_async_global();
       // claim counters by epoch parity: this step's starts at 0 (reset by the previous step)
       uint32_t* counter = reinterpret_cast<uint32_t*>(mine + a.off_claim) + par;
-      int cur = 0, n_claims = 0, t = 0, t_end = 0;
+      const float* Gr = s.g;
+      const float* Mr = M;
+      int cur = 0, n_claims = 0, t = 0, t_end = 0, p = n_loc - 1;
       for (int i = 0;; ++i) {
         const int st = i % kNA;
         ptx::mbar_wait(&a_empty[st], (uint32_t)(((i / kNA) & 1) ^ 1));
-        if (t == t_end) {  // claim the next chunk (segment order: the pace every GPU keeps)
-          const int c = n_claims < kMaxClaims - 1 ? (int)atomicAdd(counter, 1u) : a.n_chunks;
-          if (c >= a.n_chunks) {  // nothing left (or this CTA's list is full): end marker
-            claims[n_claims] = -1;
-            *end_pos = i;
-            ptx::mbar_arrive(&a_full[st]);
-            break;
+        if (++p == n_loc) {
+          p = 0;
+          if (++t >= t_end) {  // claim the next chunk (segment order: the pace every GPU keeps)
+            const int c = n_claims < kMaxClaims - 1 ? (int)atomicAdd(counter, 1u) : a.n_chunks;
+            if (c >= a.n_chunks) {  // nothing left (or this CTA's list is full): end marker
+              claims[n_claims] = -1;
+              *end_pos = i;
+              ptx::mbar_arrive(&a_full[st]);
+              break;
+            }
+            claims[n_claims++] = c;
+            t = __ldg(a.chunk_t0 + c);
+            t_end = __ldg(a.chunk_t0 + c + 1);
           }
-          claims[n_claims++] = c;
-          t = __ldg(a.chunk_t0 + c);
-          t_end = __ldg(a.chunk_t0 + c + 1);
         }
         const MTile U = mtile(a, bnd, t0, t, cur);
-        ++t;
+        const int64_t off = (int64_t)(ord[U.seg * n_loc + p] & kWIdx) * s.ld + U.c0;
         const uint32_t bytes = (uint32_t)(((U.len + 3) & ~3) * 4);
         float* buf = ringA + (size_t)st * 3 * kT;
         ptx::mbar_arrive_expect_tx(&a_full[st], 3 * bytes);
-        ptx::bulk_g2s(buf, s.x + U.c0, bytes, &a_full[st]);
-        ptx::bulk_g2s(buf + kT, s.m + U.c0, bytes, &a_full[st]);
-        ptx::bulk_g2s(buf + 2 * kT, s.g + U.c0, bytes, &a_full[st]);
+        ptx::bulk_g2s(buf, X + off, bytes, &a_full[st]);
+        ptx::bulk_g2s(buf + kT, Mr + off, bytes, &a_full[st]);
+        ptx::bulk_g2s(buf + 2 * kT, Gr + off, bytes, &a_full[st]);
       }
     }
     __syncwarp();
   } else if (warp == kWLoadIn) {
-    // ---------------- inbox loader: wait for the tile's trailer, stage the tiles -------
+    // ---------------- inbox loader: a chain tail's trailer, received and own y tiles ---
     if (lane == 0) {
-      int cur = 0;
+      int cur = 0, q = 0;
       Walk w;
+      w.init(n_loc);
       for (int j = 0;; ++j) {
-        const int si = j % kNI;
-        // this CTA's own y of position j + lag is in params (the sender's copy of j has
-        // probably completed by then), or the walk ends before it
-        bool more = true;
-        while ((int32_t)(ld_acquire_cta(&y_stored) - (uint32_t)(kUpd / 32) * (uint32_t)(j + 1 + a.lag)) < 0) {
-          const int ep = *end_pos;
-          if (ep <= j + a.lag) {
-            more = ep > j;
-            if (more)  // the end is near: wait only for position j itself
-              while ((int32_t)(ld_acquire_cta(&y_stored) - (uint32_t)(kUpd / 32) * (uint32_t)(j + 1)) < 0) {
-              }
-            break;
-          }
-        }
-        ptx::mbar_wait(&i_empty[si], (uint32_t)(((j / kNI) & 1) ^ 1));
-        if (!more) {  // end marker for the mix warps
-          ptx::mbar_arrive(&i_full[si]);
-          break;
-        }
-        w.next(claims, a.chunk_t0);
+        if (!wait_position(&y_stored, end_pos, j)) break;
+        w.next(claims, a.chunk_t0, n_loc);
         const MTile U = mtile(a, bnd, t0, w.t, cur);
-        // no wait here: the trailer is staged with the tiles and checked by the mix, which
-        // polls only when it finds the trailer of an older epoch
+        const uint32_t e_w = ord[U.seg * n_loc + w.p];
+        if (!(e_w & kWTail)) continue;
+        const uint32_t row = e_w & kWIdx;
+        // stage it once the update is `lag` positions further (the sender's copy has probably
+        // completed by then), or at the end; the mix polls if the trailer is still old
+        if (a.lag > 0) wait_position(&y_stored, end_pos, j + a.lag);
+        const int si = q % kNI;
+        ptx::mbar_wait(&i_empty[si], (uint32_t)(((q / kNI) & 1) ^ 1));
+        ++q;
         ptx::fence_proxy_async_global();  // own y written by the update warps -> this bulk copy
         float* buf = ringI + (size_t)si * 2 * kT;
         const uint32_t yb = (uint32_t)(((U.len + 3) & ~3) * 4);
         const uint32_t ib = wire ? (uint32_t)(((U.len + 7) & ~7) * 2) : yb;
         ptx::mbar_arrive_expect_tx(&i_full[si], ib + yb + 16u);
-        ptx::bulk_g2s(&meta[si], trl_in + w.t, 16u, &i_full[si]);
+        ptx::bulk_g2s(&meta[si], trl_in + (size_t)w.t * n_loc + row, 16u, &i_full[si]);
         if (wire)
-          ptx::bulk_g2s(buf, reinterpret_cast<const uint16_t*>(mine + a.off_inbox) + par * ld_bf + U.c0, ib,
-                        &i_full[si]);
+          ptx::bulk_g2s(buf, reinterpret_cast<const uint16_t*>(mine + a.off_inbox) +
+                                 ((int64_t)par * n_loc + row) * ld_bf + U.c0,
+                        ib, &i_full[si]);
         else
-          ptx::bulk_g2s(buf, reinterpret_cast<const float*>(mine + a.off_inbox) + par * s.ld + U.c0, yb,
-                        &i_full[si]);
-        ptx::bulk_g2s(buf + kT, s.x + U.c0, yb, &i_full[si]);
+          ptx::bulk_g2s(buf, reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * n_loc + row) * s.ld + U.c0,
+                        yb, &i_full[si]);
+        ptx::bulk_g2s(buf + kT, X + (int64_t)row * s.ld + U.c0, yb, &i_full[si]);
       }
     }
     __syncwarp();
   } else if (warp == kWStore) {
-    // ---------------- store warp: push y tiles, then each completed tile's trailer ------
+    // ---------------- store warp: push head tiles, then each completed tile's trailer ---
     // every rank consumed epoch e-2 (the last reader of the inbox parity written now):
     // relaxed polls by the lanes, one acquire fence
     if (e >= 3) {
@@ -593,51 +725,66 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       if (lane == 0) ptx::fence_acq_rel_sys();
     }
     if (lane == 0) {
+      // copies issued but not yet known complete, oldest first: their trailers wait
       uint4* pend_dst[kLand + 1] = {};
       uint4 pend_trl[kLand + 1] = {};
-      int cur = 0, n = 0;
+      int pend_head = 0, npend = 0, cur = 0;
       Walk w;
-      auto completed = [&](int j) {  // copy j has completed: its trailer may go (Alg.1 l.14)
-        const int q = j % (kLand + 1);
-        st_volatile4(pend_dst[q], pend_trl[q]);
+      w.init(n_loc);
+      auto complete_oldest = [&]() {  // Alg.1 l.14: that copy has completed at its receiver
+        st_volatile4(pend_dst[pend_head], pend_trl[pend_head]);
+        pend_head = (pend_head + 1) % (kLand + 1);
+        --npend;
       };
       for (int i = 0;; ++i) {
         const int sy = i % kNY;
-        ptx::mbar_wait(&y_full[sy], (uint32_t)((i / kNY) & 1));
-        if (!w.next(claims, a.chunk_t0)) break;
+        const uint32_t ph = (uint32_t)((i / kNY) & 1);
+        if (npend > 0 && !ptx::mbar_test(&y_full[sy], ph)) {  // idle: finish what is in flight
+          ptx::bulk_wait_all();
+          ptx::fence_proxy_async_global();  // their async-proxy writes -> the trailer stores
+          while (npend > 0) complete_oldest();
+        }
+        ptx::mbar_wait(&y_full[sy], ph);
+        const int dg = dst_upd[sy];
+        if (dg == -2) break;  // end marker
+        w.next(claims, a.chunk_t0, n_loc);
+        if (dg < 0) {  // not a head: nothing to send
+          ptx::mbar_arrive(&y_free[sy]);
+          continue;
+        }
         const MTile U = mtile(a, bnd, t0, w.t, cur);
-        const int rp = recv[U.seg];
+        const int rp = dg / n_loc, rl = dg - rp * n_loc;
         if (wire)
-          ptx::bulk_s2g(reinterpret_cast<uint16_t*>(a.peers[rp] + a.off_inbox) + par * ld_bf + U.c0,
+          ptx::bulk_s2g(reinterpret_cast<uint16_t*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * n_loc + rl) * ld_bf + U.c0,
                         ringY + (size_t)sy * kT, (uint32_t)(((U.len + 7) & ~7) * 2));
         else
-          ptx::bulk_s2g(reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + par * s.ld + U.c0,
+          ptx::bulk_s2g(reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * n_loc + rl) * s.ld + U.c0,
                         ringY + (size_t)sy * kT, (uint32_t)(((U.len + 3) & ~3) * 4));
         ptx::bulk_commit();
-        uint32_t X = 0, S = 0;
+        uint32_t Xc = 0, Sc = 0;
 #pragma unroll
         for (int u = 0; u < kUpd / 32; ++u) {
-          X ^= ck_upd[sy][u][0];
-          S += ck_upd[sy][u][1];
+          Xc ^= ck_upd[sy][u][0];
+          Sc += ck_upd[sy][u][1];
         }
         const uint32_t wb = w_upd[sy];
-        const int q = i % (kLand + 1);
-        pend_dst[q] = reinterpret_cast<uint4*>(a.peers[rp] + a.off_trl) + (size_t)par * a.trl_cap + w.t;
-        pend_trl[q] = make_uint4(e, X ^ wb, S, wb);
-        ptx::bulk_wait_read<1>();
-        if (i >= 1) ptx::mbar_arrive(&y_free[(i - 1) % kNY]);
-        if (i >= kLand) {  // copies <= i - kLand have completed
+        const int q = (pend_head + npend) % (kLand + 1);
+        pend_dst[q] = reinterpret_cast<uint4*>(a.peers[rp] + a.off_trl) + (size_t)par * a.trl_cap +
+                      (size_t)w.t * n_loc + rl;
+        pend_trl[q] = make_uint4(e, Xc ^ wb, Sc, wb);
+        ++npend;
+        ptx::bulk_wait_read<0>();  // the slot has been read: free it
+        ptx::mbar_arrive(&y_free[sy]);
+        if (npend > kLand) {  // all but the newest kLand copies have completed
           ptx::bulk_wait<kLand>();
-          ptx::fence_proxy_async_global();  // their async-proxy writes -> the trailer store
-          completed(i - kLand);
+          ptx::fence_proxy_async_global();
+          while (npend > kLand) complete_oldest();
         }
-        n = i + 1;
       }
       ptx::bulk_wait_all();
       ptx::fence_proxy_async_global();
       if (tr) tr[2] = ptx::globaltimer();
-      if (n >= 1) ptx::mbar_arrive(&y_free[(n - 1) % kNY]);
-      for (int j = n - kLand > 0 ? n - kLand : 0; j < n; ++j) completed(j);
+      while (npend > 0) complete_oldest();
       if (tr) tr[3] = ptx::globaltimer();
     }
     __syncwarp();
@@ -662,16 +809,13 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
 
 }  // namespace
 
-size_t peer_merge_smem(int k, bool wire) {
-  (void)wire;
-  return smem_bytes(k);
-}
+size_t peer_merge_smem(int k, int n_loc) { return smem_bytes(k, n_loc); }
 
 int peer_merge_capacity(int k) {
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = smem_bytes(k < kMaxK ? k : kMaxK);
+  const size_t smem = smem_bytes(1, kMaxKN);  // the largest walk tables
   if (cudaFuncSetAttribute(k_push_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push_merge, kMThreads, smem) != cudaSuccess) return 0;
@@ -699,7 +843,8 @@ std::vector<int32_t> peer_merge_chunks(const std::vector<int32_t>& seg_t0, int c
 }
 
 bool peer_merge_ok(const PeerState& p, const PeerStepArgs& a) {
-  return p.sched == kSchedInStep && a.n_loc == 1 && a.k <= kMaxK && p.grid_merge > 0 && p.d_chunk_t0 != nullptr &&
+  return p.sched == kSchedInStep && a.n_loc <= kMaxLoc && (int64_t)a.k * a.n_loc <= kMaxKN && a.k <= kMaxK &&
+         p.grid_merge > 0 && p.d_chunk_t0 != nullptr && (int64_t)p.n_tiles * a.n_loc <= p.mflag_cap &&
          // every CTA's claims fit its list even if one CTA took 4x its share
          (int64_t)p.n_chunks < (int64_t)(kMaxClaims - 1) * p.grid_merge / 4;
 }
@@ -746,7 +891,7 @@ int peer_merge_launch(PeerState& p, const PeerStepArgs& a, uint32_t epoch, cudaS
     ma.trace = d_trace;
   }
   void* args[] = {&ma};
-  cudaError_t e = peer_launch(p, (const void*)k_push_merge, p.grid_merge, kMThreads, smem_bytes(a.k), st, args);
+  cudaError_t e = peer_launch(p, (const void*)k_push_merge, p.grid_merge, kMThreads, smem_bytes(a.k, a.n_loc), st, args);
   if (e != cudaSuccess) {
     fprintf(stderr, "k_push_merge launch: %s\n", cudaGetErrorString(e));
     return CS_ECUDA;

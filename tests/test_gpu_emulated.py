@@ -98,10 +98,12 @@ def test_emulated_opt_in_schedules_bitwise(schedule, n_loc):
     cs.cs_finalize()
 
 
-@pytest.mark.parametrize("V,n_loc,d,k", [(2, 3, 50_001, 5), (4, 4, 30_011, 8), (2, 8, 20_000, 16), (4, 2, 7, 1)])
-def test_emulated_hybrid_walk_bitwise(V, n_loc, d, k):
-    # several workers per rank: cycles mixed in registers, chain heads pushed to other ranks'
-    # inboxes, chain tails merged by k_hyb_tail (default schedule: merged when the step ends)
+@pytest.mark.parametrize("V,n_loc,d,k", [(2, 3, 50_001, 5), (4, 4, 30_011, 8), (2, 8, 20_000, 16), (4, 2, 7, 1),
+                                         (2, 40, 30_001, 8)])  # world 80 > 64: k_topology tables
+def test_emulated_walk_merge_bitwise(V, n_loc, d, k):
+    # several workers per rank (default schedule, k_push_merge): the walk mixes local cycles
+    # and chains in registers, pushes chain heads to other ranks' inboxes with trailers and
+    # merges chain tails in the same kernel -- merged when the step's work completes
     n = V * n_loc
     x, m, w, bank2 = _bind_emulated(V, n, d, k, 4)
     orc = OracleRun(n, d, k, 4)
@@ -110,7 +112,7 @@ def test_emulated_hybrid_walk_bitwise(V, n_loc, d, k):
         orc.step(LR, MU)
         torch.cuda.current_stream().synchronize()
         _check(x, m, w, orc, d)
-    assert cs.cs_kernel_info()[0] == "k_hyb_walk+k_hyb_tail"
+    assert cs.cs_kernel_info()[0] == "k_push_merge"
     cs.cs_finalize()
 
 
