@@ -174,7 +174,7 @@ class OracleSample:
 
     def record(self, per_step: float, steps: int) -> dict:
         return {"value": 4.0 * self.n * self.cols / per_step / 1e9, "unit": UNIT, "cores": 1,
-                "host_cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+                "host_cores": len(os.sched_getaffinity(0)), "cpu_model": cpu_model(), "kind": "oracle",
                 "sample": f"{self.n} workers x first {self.cols} of {self.d} columns, k={self.k}, {steps} steps, "
                           + ("LARS on whole layers, " if self.lars is not None else "")
                           + 
@@ -196,6 +196,28 @@ def emit(obj):
     print(json.dumps(obj), flush=True)
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def bench_config(args, desc, world, n_loc, d, k, lr, mu, world_size, lars):
+    """The `config` object of both arms' JSON lines (the same dict for the same run)."""
+    return {"workload": f"{args.config}: {desc}", "world": world, "workers_per_gpu": n_loc,
+            "d": d, "k": k, "seed": 0, "lr": lr, "momentum": mu,
+            "parallelism": f"workers partitioned over {world_size} GPU(s)", "scheme": args.scheme,
+            "schedule": args.schedule, "wire": args.wire,
+            "lars_x_norm_carry": bool(lars),
+            "l2": f"inputs larger than L2 ({20.0 * n_loc * d / 1e9:.2f} GB moved per step per GPU)"}
+
+
 def run_reference(args, rank, world_size):
     """The oracle as the reference arm: each of the W + K steps is one oracle step over
     all workers on a column sample sized so the whole run stays within ~90 s."""
@@ -204,6 +226,9 @@ def run_reference(args, rank, world_size):
     n_loc, d, k, desc = WORKLOADS[args.config]
     d = args.d or d
     k = args.k or k
+    if args.workers_per_gpu:
+        n_loc = args.workers_per_gpu
+        desc += f" [{n_loc} workers per GPU]"
     n = n_loc * world_size
     total = args.steps + args.warmup
     lars = LARS.get(args.config)
@@ -217,14 +242,20 @@ def run_reference(args, rank, world_size):
         o.step()
     res = [o.record(dt, 1) for dt in (o.step() for _ in range(max(1, args.steps)))]
     v = statistics.median(r["value"] for r in res)
+    ms_sample = statistics.median(r["s_per_step"] for r in res) * 1e3
     cb = dict(res[0])
     cb["value"] = v
     cb["sample"] = f"each step: one oracle step over {n} workers x the first {cols} of {d} columns, k={k}"
+    lr = lars[3] if lars else float(__import__("synth").DEFAULT_LR)
+    mu = float(__import__("synth").DEFAULT_MOMENTUM)
     emit({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world_size,
           "steps": args.steps, "warmup": args.warmup,
-          "ms_per_step": statistics.median(r["s_per_step"] for r in res) * 1e3 * d / cols,
+          # measured: one timed oracle step = the column sample (the value is the same metric,
+          # GB/s of params mixed and updated, so it needs no extrapolation)
+          "ms_per_step": ms_sample,
+          "ms_per_step_full_vector_extrapolated": ms_sample * d / cols,
           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-          "data": "synthetic", "config": {"workload": f"{args.config}: {desc}", "world": n, "d": d, "k": k},
+          "data": "synthetic", "config": bench_config(args, desc, n, n_loc, d, k, lr, mu, world_size, lars),
           "cpu_baseline": cb,
           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
 
@@ -329,6 +360,7 @@ def main():
             raise SystemExit("c6 needs the ResNet-50 vector (no --d)")
         cs.cs_set_layers(np.concatenate([[0], np.cumsum(sizes)]), block)
         cs.cs_set_lars(*lars[:3])
+        cs.cs_set_lars_carry(True)  # the bench loop writes params only through the library
     cs.cs_synth_fill(x, n_loc, d, d, seed, synth.TAG_INIT, first, 1.0)
     cs.cs_synth_fill(bank, B, d, d, seed, synth.TAG_GRAD, 0, float(synth.GRAD_SCALE))
     stream.synchronize()
@@ -398,25 +430,29 @@ def main():
             o = (tt + first) % B
             return host_bank[o:o + n_loc]
 
-        host_api = world_size == 1 and args.path != "peer"
+        host_api = world_size == 1 and args.path != "peer" and lars is None
+        xout = torch.empty(n_loc, d, pin_memory=True)   # the step's result: merged params and psw
+        wout = torch.empty(n_loc, k, pin_memory=True)
+        d2h = 4 * n_loc * d + 4 * n_loc * k
         if host_api:
-            cs.cs_gossip_step_host(x, hgrads(t), w, lr, mu)     # warm the staging buffer
+            # cs_gossip_step_io: grads in from pinned host memory, merged params + psw out to
+            # pinned host memory, in 8 column pieces that overlap both copy directions with
+            # the step kernel; synchronous, so the events bracket complete round trips
+            cs.cs_gossip_step_io(x, hgrads(t), w, lr, mu, xout, wout)   # warm the staging buffer
             t += 1
             e0 = time.perf_counter()
             torch.cuda.synchronize()
             ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ee0.record(stream)
             for _ in range(esteps):
-                cs.cs_gossip_step_host(x, hgrads(t), w, lr, mu)
+                cs.cs_gossip_step_io(x, hgrads(t), w, lr, mu, xout, wout)
                 t += 1
             ee1.record(stream)
             torch.cuda.synchronize()
             ems = ee0.elapsed_time(ee1)
             wall = time.perf_counter() - e0
-            d2h = 16
         else:
             stage = torch.empty(n_loc, d, device=dev)
-            wout = torch.empty(n_loc, k, pin_memory=True)
             barrier()
             torch.cuda.synchronize()
             ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -426,7 +462,8 @@ def main():
                 for _ in range(esteps):
                     stage.copy_(hgrads(t), non_blocking=True)
                     step_fn(x, stage, w, lr, mu)
-                    cs.cs_flush()  # the step's result is read: complete a deferred merge first
+                    cs.cs_flush()  # no-op on the in-step schedule (a deferred merge otherwise)
+                    xout.copy_(x, non_blocking=True)   # the step's result back to the host
                     wout.copy_(w, non_blocking=True)
                     stream.synchronize()
                     t += 1
@@ -435,7 +472,6 @@ def main():
             barrier()
             ems = ee0.elapsed_time(ee1)
             wall = time.perf_counter() - e0
-            d2h = 4 * n_loc * k
         et = torch.tensor([ems], dtype=torch.float64, device=dev)
         if world_size > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
@@ -443,8 +479,9 @@ def main():
         e2e = {"value": 4.0 * world * d / (ems / esteps * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": esteps,
                "ms_per_step": ems / esteps, "wall_s": wall,
-               "api": "cs_gossip_step_host" if host_api else "H2D copy + cs_gossip_step + cs_flush + psw D2H"}
-        del host_bank
+               "api": ("cs_gossip_step_io (grads H2D, params + psw D2H, 8 pipelined column pieces)" if host_api
+                       else "grads H2D + cs_gossip_step (merged in-step) + params and psw D2H, serial")}
+        del host_bank, xout, wout
 
     hpeak, hpeak_src = hbm_peak()
 
@@ -526,12 +563,7 @@ def main():
         emit({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": args.steps,
               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
               "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-              "config": {"workload": f"{args.config}: {desc}", "world": world, "workers_per_gpu": n_loc,
-                         "d": d, "k": k, "seed": seed, "lr": lr, "momentum": mu,
-                         "parallelism": f"workers partitioned over {world_size} GPU(s)", "scheme": args.scheme,
-                         "schedule": args.schedule,
-                         "wire": args.wire,
-                         "l2": f"inputs larger than L2 ({20.0 * n_loc * d / 1e9:.2f} GB moved per step per GPU)"},
+              "config": bench_config(args, desc, world, n_loc, d, k, lr, mu, world_size, lars),
               "step_us": ms_step * 1e3,
               "traffic_GBps": 20.0 * world * d / (ms_step * 1e-3) / 1e9,
               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "interval": interval,

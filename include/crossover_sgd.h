@@ -90,6 +90,10 @@ const char* cs_last_error(void);
 /* ABI version (major*10000 + minor*100 + patch). */
 int cs_version(void);
 
+/* Build id: the first 16 hex digits of the sha256 of the library's sources, this header and
+ * the nvcc flags it was compiled from (static string; "unknown-build-id" if built by hand). */
+const char* cs_build_id(void);
+
 /* ---- pure host functions (callable before cs_bind, no GPU needed) ---------- */
 
 /* Segment plan (reading C-2): bounds_out[s] = min(d, 32*floor(s*ceil(d/32)/k)),
@@ -214,6 +218,18 @@ int cs_gossip_step(float* params, const float* grads, float* psw, float lr, floa
 int cs_gossip_step_host(float* params, const float* grads_host, float* psw, float lr,
                         float momentum, double* diag_out);
 
+/* End-to-end variant with the step's input and result in HOST memory: the gradients come
+ * from grads_host ([n_loc][ld] fp32, pinned for full speed) and the merged params / psw are
+ * copied back to params_host_out ([n_loc][ld]) / psw_host_out ([n_loc][k]) before it
+ * returns (synchronous).  params / psw / momentum stay the device state of the job.  The
+ * vector is cut into 8 column pieces: the host->device copy of piece q+1 and the
+ * device->host copy of piece q-1 overlap the step kernel on piece q (copy engines in both
+ * directions, k_gossip_tma on a tile range; the last piece mixes the push-sum weights).
+ * Single-GPU bulk-TMA path without LARS or diagnostics (CS_EUNSUPPORTED otherwise).
+ * Errors as cs_gossip_step, CS_EINVAL (NULL host buffer). */
+int cs_gossip_step_io(float* params, const float* grads_host, float* psw, float lr, float momentum,
+                      float* params_host_out, float* psw_host_out);
+
 /* One hierarchical step (§3.3) at step t, then t += 1:
  *   h1  per group, gbar = fl(sum_{i in G, ascending} g_i) * fp32(1/|G|)
  *   h2  leaders apply a3 with gbar, then a4/a5 among the G leaders with the
@@ -283,6 +299,7 @@ int cs_set_layers(const int64_t* layer_bounds, int n_layers, const int32_t* seg_
  * 5e-5).  eta > 0 enables, eta == 0 disables.  With it enabled,
  * every flat step computes, for each worker i and layer l, from this step's x and g:
  *   scale = eta*|x_il| / ((|g_il| + wd*|x_il|) + eps)   (fp64; 1 if a norm is 0)
+ * (|x_il| of this step's x: recomputed every step unless cs_set_lars_carry(1) is on)
  *   lrs   = fp32(lr * scale)
  * and applies  m = mu*m + (g + wd*x),  y = x - lrs*m  before the exchange (C-18).
  * Needs a layer table at step time (CS_EINVAL otherwise).  Two extra launches per
@@ -291,6 +308,16 @@ int cs_set_layers(const int64_t* layer_bounds, int n_layers, const int32_t* seg_
  * off with LARS because the norms need the merged parameters).
  * Errors: CS_ENOTINIT, CS_EINVAL. */
 int cs_set_lars(float eta, float weight_decay, float eps);
+
+/* LARS x-norm carry (opt-in, default off; single-GPU bulk-TMA path).  With it enabled the
+ * step kernel also emits each worker's per-tile sums of x'^2, and the next LARS step on the
+ * same params buffer takes its ||x|| from them instead of reading x again (24 instead of 28
+ * B/param).  The caller then promises that nothing but the library writes params between
+ * LARS steps -- or calls cs_params_modified() after it did (a checkpoint load, a manual
+ * decay, any in-place op), which makes the next step read x again.  cs_set_step, cs_bind
+ * and cs_set_layers also drop the carry.  Errors: CS_ENOTINIT. */
+int cs_set_lars_carry(int enable);
+int cs_params_modified(void);
 
 /* Rates lrs [n_loc][n_layers] (host, row-major) of the most recent LARS step.
  * Synchronises the stream.  Errors: CS_EINVAL (no LARS step since cs_set_layers). */

@@ -43,6 +43,7 @@ _SIGS = {
     "cs_finalize": (None, []),
     "cs_last_error": (ctypes.c_char_p, []),
     "cs_version": (_c_int, []),
+    "cs_build_id": (ctypes.c_char_p, []),
     "cs_segment_bounds": (_c_int, [_c_i64, _vp]),
     "cs_topology": (_c_int, [_c_i64, _vp]),
     "cs_topology_hier": (_c_int, [_c_i64, _vp]),
@@ -55,6 +56,7 @@ _SIGS = {
     "cs_ipc_import": (_c_int, [_vp]),
     "cs_gossip_step": (_c_int, [_vp, _vp, _vp, _c_f, _c_f]),
     "cs_gossip_step_host": (_c_int, [_vp, _vp, _vp, _c_f, _c_f, _vp]),
+    "cs_gossip_step_io": (_c_int, [_vp, _vp, _vp, _c_f, _c_f, _vp, _vp]),
     "cs_hier_step": (_c_int, [_vp, _vp, _vp, _c_f, _c_f]),
     "cs_accumulate": (_c_int, [_vp, _vp, _c_int, _c_int]),
     "cs_set_topology_kind": (_c_int, [_c_int]),
@@ -64,6 +66,8 @@ _SIGS = {
     "cs_set_layers": (_c_int, [_vp, _c_int, _vp]),
     "cs_set_lars": (_c_int, [_c_f, _c_f, _c_f]),
     "cs_get_lars_rates": (_c_int, [_vp]),
+    "cs_set_lars_carry": (_c_int, [_c_int]),
+    "cs_params_modified": (_c_int, []),
     "cs_set_step": (_c_int, [_c_i64]),
     "cs_get_step": (_c_int, [_vp]),
     "cs_set_diag": (_c_int, [_c_int]),
@@ -125,6 +129,10 @@ def cs_last_error() -> str:
 
 def cs_version() -> int:
     return lib.cs_version()
+
+
+def cs_build_id() -> str:
+    return lib.cs_build_id().decode()
 
 
 def cs_init(world: int, groups: int, k_segments: int, seed: int) -> None:
@@ -194,6 +202,13 @@ def cs_gossip_step_host(params, grads_host, psw, lr: float, momentum: float) -> 
     _check(lib.cs_gossip_step_host(_ptr(params), _ptr(grads_host), _ptr(psw), lr, momentum,
                                    out.ctypes.data), "cs_gossip_step_host")
     return float(out[0]), float(out[1])
+
+
+def cs_gossip_step_io(params, grads_host, psw, lr: float, momentum: float, params_host_out, psw_host_out) -> None:
+    """One step with host-resident gradients in and the merged params / psw copied back to
+    host buffers (pipelined column pieces; synchronous)."""
+    _check(lib.cs_gossip_step_io(_ptr(params), _ptr(grads_host), _ptr(psw), lr, momentum, _ptr(params_host_out),
+                                 _ptr(psw_host_out)), "cs_gossip_step_io")
 
 
 def cs_hier_step(params, grads, psw, lr: float, momentum: float) -> None:
@@ -334,3 +349,14 @@ def cs_set_schedule(schedule: int) -> None:
 def cs_test_emulate_ranks(vranks: int) -> None:
     """Test hook: the multi-GPU protocol for `vranks` ranks on this one GPU (next cs_bind)."""
     _check(lib.cs_test_emulate_ranks(vranks), "cs_test_emulate_ranks")
+
+
+def cs_set_lars_carry(enable: bool) -> None:
+    """Opt in to reusing the previous LARS step's x norms (caller calls cs_params_modified
+    after writing params itself)."""
+    _check(lib.cs_set_lars_carry(1 if enable else 0), "cs_set_lars_carry")
+
+
+def cs_params_modified() -> None:
+    """Params were written outside the library: the next LARS step recomputes ||x||."""
+    _check(lib.cs_params_modified(), "cs_params_modified")

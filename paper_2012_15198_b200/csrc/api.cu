@@ -84,6 +84,10 @@ struct Ctx {
 
   float* d_stage = nullptr;   // cs_gossip_step_host staging buffer
   size_t stage_bytes = 0;
+  // cs_gossip_step_io: host copies of the bulk-TMA tiles' columns, copy streams and events
+  std::vector<int64_t> h_tile_c0, h_tile_end;
+  cudaStream_t io_h2d = nullptr, io_d2h = nullptr;
+  std::vector<cudaEvent_t> io_ev;
 
   PeerState peer;             // multi-GPU exchange region (nprocs > 1)
 
@@ -100,6 +104,7 @@ struct Ctx {
   bool lars_valid = false;
   // LARS carry: the .x halves of d_lars_part hold sum x'^2 of the last TMA LARS step on xnorm_x
   bool xnorm_valid = false;
+  bool lars_carry = false;    // cs_set_lars_carry: the caller promises cs_params_modified
   const float* xnorm_x = nullptr;
 
   // topology kind (cs_set_topology_kind): SGP's exponential graph as [H][k][world] tables
@@ -163,6 +168,12 @@ void free_device() {
   g.d_partials = nullptr; g.d_diag = nullptr; g.d_stage = nullptr; g.d_counter = nullptr;
   g.d_tiles = nullptr; g.n_tiles = 0; g.use_tma = false;
   g.stage_bytes = 0;
+  g.has_override = false;  // the injected topology lived in d_given
+  if (g.io_h2d) cudaStreamDestroy(g.io_h2d);
+  if (g.io_d2h) cudaStreamDestroy(g.io_d2h);
+  for (cudaEvent_t e : g.io_ev) cudaEventDestroy(e);
+  g.io_h2d = g.io_d2h = nullptr;
+  g.io_ev.clear();
   peer_release(g.peer);
 }
 
@@ -247,6 +258,12 @@ int build_tma_tiles() {
   g.d_tiles = nullptr;
   g.d_tile_first = nullptr;
   g.n_tiles = (int)tiles.size();
+  g.h_tile_c0.resize(tiles.size());
+  g.h_tile_end.resize(tiles.size());
+  for (size_t i = 0; i < tiles.size(); ++i) {
+    g.h_tile_c0[i] = tiles[i].c0;
+    g.h_tile_end[i] = tiles[i].c0 + tiles[i].len;
+  }
   CS_CUDA(cudaMalloc(&g.d_tiles, sizeof(TileDesc) * tiles.size()));
   CS_CUDA(cudaMemcpy(g.d_tiles, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice));
   CS_CUDA(cudaMalloc(&g.d_tile_first, sizeof(int32_t) * first.size()));
@@ -339,6 +356,7 @@ LocalArgs local_args(float* params, const float* grads, float* psw, int n, int g
   a.seg_bounds = nullptr;
   a.layer_bounds = nullptr;
   a.xnorm_out = nullptr;
+  a.skip_psw = 0;
   return a;
 }
 
@@ -422,7 +440,7 @@ int enqueue_flat_step(float* params, const float* grads, float* psw, float lr, f
       // per-(worker, layer) rates from this step's x and g, then the LARS step kernel.  The
       // x sums come from the previous LARS step's kernel when nothing else touched params
       // (the norm pass then reads only g: 24 instead of 28 B/param)
-      const bool carry = g.xnorm_valid && g.xnorm_x == params;
+      const bool carry = g.lars_carry && g.xnorm_valid && g.xnorm_x == params;
       CS_CUDA(launch_lars_rates(params, grads, g.ld, g.d_tiles, g.n_tiles, g.n_loc, g.d_tile_first,
                                 g.n_layers, g.d_lars_part, lr, g.lars_eta, g.lars_wd, g.lars_eps,
                                 g.d_lrs, g.stream, LarsWait(), carry));
@@ -464,7 +482,14 @@ int enqueue_flat_step(float* params, const float* grads, float* psw, float lr, f
 
 extern "C" {
 
-int cs_version(void) { return 200; }  // 0.2.0: interval, LARS, SGP topology, bf16 wire, cs_flush
+int cs_version(void) { return 300; }  // 0.3.0: in-step merge schedule, emulated ranks, build id
+
+#ifndef CS_BUILD_ID
+#define CS_BUILD_ID "unknown-build-id"
+#endif
+// The marker lets __graft_entry__.build() read the id from the file without loading it.
+static const char kBuildIdMarker[] = "CSBUILDID:" CS_BUILD_ID;
+const char* cs_build_id(void) { return kBuildIdMarker + 10; }
 
 const char* cs_last_error(void) { return g_err.c_str(); }
 
@@ -664,6 +689,16 @@ int cs_test_emulate_ranks(int vranks) {
 int cs_set_stream(void* stream) {
   int rc = check_bound();
   if (rc) return rc;
+  // the library's scratch (arrival counters, partials, a pending deferred merge) is shared by
+  // work on both streams: the new stream starts after everything queued on the old one
+  if ((cudaStream_t)stream != g.stream) {
+    cudaEvent_t ev;
+    CS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    cudaError_t e = cudaEventRecord(ev, g.stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent((cudaStream_t)stream, ev, 0);
+    cudaEventDestroy(ev);
+    if (e != cudaSuccess) return cuda_fail(e, "cs_set_stream ordering");
+  }
   g.stream = (cudaStream_t)stream;
   return CS_OK;
 }
@@ -762,6 +797,71 @@ int cs_gossip_step_host(float* params, const float* grads_host, float* psw, floa
   g.step += 1;
   CS_CUDA(cudaMemcpyAsync(diag_out, g.d_diag, 2 * sizeof(double), cudaMemcpyDeviceToHost, g.stream));
   CS_CUDA(cudaStreamSynchronize(g.stream));
+  return poll_device_errors();
+}
+
+int cs_gossip_step_io(float* params, const float* grads_host, float* psw, float lr, float momentum,
+                      float* params_host_out, float* psw_host_out) {
+  int rc = check_bound();
+  if (rc) return rc;
+  if (!grads_host || !params_host_out || !psw_host_out) return fail(CS_EINVAL, "NULL host buffer");
+  if (g.use_peer || !g.use_tma || g.lars || !fused_topology_ok(g.world, g.k))
+    return fail(CS_EUNSUPPORTED, "cs_gossip_step_io runs on the single-GPU bulk-TMA path without LARS");
+  const size_t bytes = sizeof(float) * (size_t)g.n_loc * (size_t)g.ld;
+  if (g.stage_bytes < bytes) {
+    if (g.d_stage) cudaFree(g.d_stage);
+    g.d_stage = nullptr;
+    CS_CUDA(cudaMalloc(&g.d_stage, bytes));
+    g.stage_bytes = bytes;
+  }
+  rc = check_step_args(params, g.d_stage, psw);
+  if (rc) return rc;
+  constexpr int P = 8;  // column pieces: H2D of piece q+1 and D2H of piece q-1 overlap step piece q
+  if (!g.io_h2d) {
+    CS_CUDA(cudaStreamCreateWithFlags(&g.io_h2d, cudaStreamNonBlocking));
+    CS_CUDA(cudaStreamCreateWithFlags(&g.io_d2h, cudaStreamNonBlocking));
+    g.io_ev.resize(2 * P + 1);
+    for (auto& e : g.io_ev) CS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  // the previous io step's reads of the staging buffer (its pieces) precede this step's copies
+  CS_CUDA(cudaEventRecord(g.io_ev[2 * P], g.stream));
+  CS_CUDA(cudaStreamWaitEvent(g.io_h2d, g.io_ev[2 * P], 0));
+  cudaEvent_t ev[2];
+  rc = next_event_pair(ev);
+  if (rc) return rc;
+  if (ev[0]) CS_CUDA(cudaEventRecord(ev[0], g.stream));
+  const int nt = g.n_tiles;
+  const size_t pitch = sizeof(float) * (size_t)g.ld;
+  for (int q = 0; q < P; ++q) {
+    const int t_lo = (int)((int64_t)q * nt / P), t_hi = (int)((int64_t)(q + 1) * nt / P);
+    if (t_hi <= t_lo) continue;
+    const int64_t c_lo = g.h_tile_c0[t_lo], c_hi = g.h_tile_end[t_hi - 1];
+    const size_t width = sizeof(float) * (size_t)(c_hi - c_lo);
+    CS_CUDA(cudaMemcpy2DAsync(g.d_stage + c_lo, pitch, grads_host + c_lo, pitch, width, g.n_loc,
+                              cudaMemcpyHostToDevice, g.io_h2d));
+    CS_CUDA(cudaEventRecord(g.io_ev[q], g.io_h2d));
+    CS_CUDA(cudaStreamWaitEvent(g.stream, g.io_ev[q], 0));
+    LocalArgs a = local_args(params, g.d_stage, psw, g.world, 1, CS_TAG_FLAT, lr, momentum);
+    a.given = flat_given();
+    a.tiles = g.d_tiles + t_lo;  // this piece's tiles; the last piece also mixes psw
+    a.n_tiles = t_hi - t_lo;
+    a.skip_psw = t_hi < nt ? 1 : 0;
+    CS_CUDA(launch_gossip_tma(a, false, g.tma_grid_plain, g.stream));
+    CS_CUDA(cudaEventRecord(g.io_ev[P + q], g.stream));
+    CS_CUDA(cudaStreamWaitEvent(g.io_d2h, g.io_ev[P + q], 0));
+    CS_CUDA(cudaMemcpy2DAsync(params_host_out + c_lo, pitch, params + c_lo, pitch, width, g.n_loc,
+                              cudaMemcpyDeviceToHost, g.io_d2h));
+  }
+  CS_CUDA(cudaMemcpyAsync(psw_host_out, psw, sizeof(float) * (size_t)g.n_loc * g.k, cudaMemcpyDeviceToHost,
+                          g.io_d2h));
+  CS_CUDA(cudaEventRecord(g.io_ev[2 * P], g.io_d2h));
+  CS_CUDA(cudaStreamWaitEvent(g.stream, g.io_ev[2 * P], 0));
+  if (ev[1]) CS_CUDA(cudaEventRecord(ev[1], g.stream));
+  g.launches_per_step = P;
+  g.hot_kernel = "k_gossip_tma";
+  g.xnorm_valid = false;
+  g.step += 1;
+  CS_CUDA(cudaStreamSynchronize(g.io_d2h));
   return poll_device_errors();
 }
 
@@ -980,6 +1080,19 @@ int cs_set_lars(float eta, float weight_decay, float eps) {
   return CS_OK;
 }
 
+int cs_set_lars_carry(int enable) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  g.lars_carry = enable != 0;
+  g.xnorm_valid = false;
+  return CS_OK;
+}
+
+int cs_params_modified(void) {
+  if (!g.inited) return fail(CS_ENOTINIT, "cs_init has not been called");
+  g.xnorm_valid = false;
+  return CS_OK;
+}
+
 int cs_get_lars_rates(float* rates_out) {
   int rc = check_bound();
   if (rc) return rc;
@@ -1110,7 +1223,7 @@ int cs_step_bytes(int64_t step, int hier, double* out) {
   if (!hier) {
     // read x, m, g; write x', m'; + LARS norms: x and g (28), or g alone when the previous
     // single-GPU LARS step carried the x norms (24)
-    out[0] = (g.lars ? ((g.xnorm_valid && !g.use_peer) ? 24.0 : 28.0) : 20.0) * g.n_loc * d;
+    out[0] = (g.lars ? ((g.lars_carry && g.xnorm_valid && !g.use_peer) ? 24.0 : 28.0) : 20.0) * g.n_loc * d;
     std::vector<int32_t> src((size_t)g.k * g.world);
     int rc = cs_topology(step, src.data());
     if (rc) return rc;

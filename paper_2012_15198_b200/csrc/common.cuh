@@ -80,6 +80,9 @@ struct LocalArgs {
   // LARS on k_gossip_tma: the step writes sum_j x'^2 per (tile, row) into the .x halves of
   // this double2 [n_tiles][rows] buffer, so the next step's norm pass reads only g
   double* xnorm_out;
+  // k_gossip_tma over a piece of the tiles (cs_gossip_step_io): only the step's last piece
+  // writes the mixed push-sum weights
+  int skip_psw;
 };
 
 // bf16 wire format (reading C-20): round to the nearest bf16 (ties to even), widen back.

@@ -280,7 +280,7 @@ __device__ void finish_step(const LocalArgs& a, const SmemTopo& t, double dacc, 
   if (!s_last) return;
   __threadfence();
   const int n = a.n, k = a.k, gs = a.group_size;
-  if (FUSED) {
+  if (FUSED && !a.skip_psw) {
     for (int e = threadIdx.x; e < n * k; e += blockDim.x) {
       const int i = e / k, s = e - i * k;
       const float wn = mixed_weight(t, n, k, s, i);

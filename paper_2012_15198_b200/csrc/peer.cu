@@ -324,8 +324,11 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
       const uint32_t* done = reinterpret_cast<const uint32_t*>(mine + a.off_done);
       if (!wait_acquire(done + threadIdx.x, e - 2)) atomicOr(&s_timeout, 1);
     }
-    ptx::named_bar_sync(1, kPushThreads - 32);
   }
+  // every warp, the load warp included, sees a timeout of the waits above before its loop:
+  // on timeout all roles skip their loops together, so none waits on an mbarrier phase the
+  // others never complete (these are the kernel's only cross-GPU waits)
+  __syncthreads();
 
   if (warp < kCompute / 32) {
     // ---------------- compute warps: m', y; y -> x and the y ring --------------------
@@ -1498,7 +1501,7 @@ int peer_alloc(PeerState& p, int n_loc, int64_t d, int64_t ld, int k, int nprocs
   off += 192;
   // in-step merge schedule (k_push_merge): progress words [2][k][grid_merge]; the grid is
   // the same on every rank (same device model), checked through the header at import
-  if (n_loc <= 64 && (int64_t)k * n_loc <= 2048 && k <= 512) {
+  if (n_loc <= 64 && (int64_t)k * n_loc <= 1024 && k <= 512) {
     const int cap = peer_merge_capacity(k);
     p.grid_merge = cap / p.vranks;
     if (p.grid_merge < 1) p.grid_merge = 0;

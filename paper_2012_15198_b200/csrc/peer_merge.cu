@@ -78,11 +78,12 @@ constexpr int kUpd = 256;                             // update warps' threads
 constexpr int kMix = 128;                             // mix warps' threads
 constexpr int kMThreads = kUpd + kMix + 96;           // + x/m/g loader, inbox loader, store warp
 constexpr int kWarps = kMThreads / 32;
-constexpr int kNA = 3, kNI = 3, kNY = 4;              // ring depths: x/m/g stages, inbox + own y, push
-constexpr int kLand = 1;                              // copies in flight before the store warp checks completion
+constexpr int kNA = 4, kNI = 3, kNY = 5;              // ring depths: x/m/g stages, inbox + own y, y out
+constexpr int kReadLag = kNY - 1;                     // y-out slots whose copies may still be reading
+constexpr int kQ = 8;                                 // store warp: positions with copies in flight (max)
 constexpr int kMaxK = 512;                            // segments (smem tables)
 constexpr int kMaxLoc = 64;                           // workers per GPU (64-bit walk masks)
-constexpr int kMaxKN = 2048;                          // k * n_loc (smem walk tables)
+constexpr int kMaxKN = 1024;                          // k * n_loc (smem walk tables)
 constexpr int kMaxClaims = 1024;                      // chunks one CTA may claim per step (smem list)
 constexpr int kWLoadXmg = (kUpd + kMix) / 32, kWLoadIn = kWLoadXmg + 1, kWStore = kWLoadXmg + 2;
 constexpr int kPerU = kT / 4 / kUpd;                  // float4 per update thread per tile
@@ -92,16 +93,20 @@ constexpr int kMixBar = 1;                            // named barrier of the mi
 constexpr uint32_t kWStart = 1u << 31, kWEnd = 1u << 30, kWHead = 1u << 29, kWTail = 1u << 28;
 constexpr uint32_t kWIdx = (1u << 28) - 1;
 
-size_t smem_bytes(int k, int n_loc) {
-  size_t b = sizeof(float) * (size_t)kT * (3 * kNA + 2 * kNI + kNY);
+size_t smem_bytes(int k, int n_loc, bool wire) {
+  size_t b = sizeof(float) * (size_t)kT * (3 * kNA + 2 * kNI + kNY) + (wire ? sizeof(uint16_t) * (size_t)kT * kNY : 0);
   b += sizeof(int64_t) * (k + 1) + sizeof(int32_t) * (k + 1);
   b += 2 * sizeof(uint32_t) * (size_t)k * n_loc;  // walk order, head receivers
   b += sizeof(int32_t) * kMaxClaims;
   b += sizeof(float) * kMaxLoc;                    // psw snapshot of a segment's first tile
-  b = (b + 15) & ~size_t(15);
-  b += sizeof(uint32_t) * 192 * kWarps;            // per-warp Alg. 2 / inverse scratch
-  return b;
+  return (b + 15) & ~size_t(15);                   // (the prologue's Alg. 2 scratch aliases the inbox ring)
 }
+static_assert(sizeof(float) * kT * (3 * kNA + 2 * kNI + kNY) + sizeof(uint16_t) * kT * kNY +
+                      (sizeof(int64_t) + sizeof(int32_t)) * (kMaxK + 1) + 2 * sizeof(uint32_t) * kMaxKN +
+                      sizeof(int32_t) * kMaxClaims + sizeof(float) * kMaxLoc + 16 + 2048 <=
+                  227 * 1024,
+              "k_push_merge shared memory exceeds 227 KB");
+static_assert(sizeof(uint32_t) * 192 * kWarps <= sizeof(float) * kT * 2 * kNI, "Alg. 2 scratch fits the inbox ring");
 
 struct MergeArgs {
   PeerStepArgs s;
@@ -220,6 +225,20 @@ __device__ __forceinline__ void st_volatile4(void* p, uint4 v) {
                : "memory");
 }
 
+// wait until at most n (runtime, 0..7) bulk groups of this thread are still writing
+__device__ __forceinline__ void bulk_wait_n(int n) {
+  switch (n) {
+    case 0: ptx::bulk_wait<0>(); break;
+    case 1: ptx::bulk_wait<1>(); break;
+    case 2: ptx::bulk_wait<2>(); break;
+    case 3: ptx::bulk_wait<3>(); break;
+    case 4: ptx::bulk_wait<4>(); break;
+    case 5: ptx::bulk_wait<5>(); break;
+    case 6: ptx::bulk_wait<6>(); break;
+    default: ptx::bulk_wait<7>(); break;
+  }
+}
+
 // The two checksums of a tile's pushed words w_i (i = word index in the tile):
 // xor of all w_i, and sum of w_i * (2i + 1) mod 2^32 (position-sensitive).
 __device__ __forceinline__ void ck_add(uint32_t& cx, uint32_t& cs, uint32_t w, uint32_t i) {
@@ -238,31 +257,37 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
   extern __shared__ __align__(128) float smem_f[];
   float* ringA = smem_f;                                   // [kNA][3][kT]  x, m, g
   float* ringI = ringA + (size_t)kNA * 3 * kT;             // [kNI][2][kT]  received y (fp32/bf16), own y
-  float* ringY = ringI + (size_t)kNI * 2 * kT;             // [kNY][kT]     y to push (fp32 or bf16)
+  float* ringY = ringI + (size_t)kNI * 2 * kT;             // [kNY][kT]     y out (fp32)
+  uint16_t* ringW = reinterpret_cast<uint16_t*>(ringY + (size_t)kNY * kT);  // [kNY][kT] bf16 image (wire)
   const PeerStepArgs& s0 = a.s;
   const bool wire = s0.wire != 0;
   const int n_loc = s0.n_loc;
-  int64_t* bnd = reinterpret_cast<int64_t*>(ringY + (size_t)kNY * kT);
+  int64_t* bnd = reinterpret_cast<int64_t*>(wire ? reinterpret_cast<float*>(ringW + (size_t)kNY * kT)
+                                                 : ringY + (size_t)kNY * kT);
   int32_t* t0 = reinterpret_cast<int32_t*>(bnd + s0.k + 1);
   uint32_t* ord = reinterpret_cast<uint32_t*>(t0 + s0.k + 1);  // [k][n_loc] walk order per segment
   int32_t* hdst = reinterpret_cast<int32_t*>(ord + s0.k * n_loc);  // [k][n_loc] receiver of a head row
   int32_t* claims = hdst + s0.k * n_loc;                   // [kMaxClaims] chunks claimed, -1 ends
   float* wsnap = reinterpret_cast<float*>(claims + kMaxClaims);  // [kMaxLoc] psw of a first tile's segment
-  uint32_t* scratch = reinterpret_cast<uint32_t*>(
-      (reinterpret_cast<uintptr_t>(wsnap + kMaxLoc) + 15) & ~uintptr_t(15));  // [kWarps][192]
+  // [kWarps][192] prologue scratch in the inbox ring: nothing is staged there before the
+  // topology barrier (the x/m/g warp, which may start early, uses its own ring)
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(ringI);
   __shared__ uint64_t a_full[kNA], a_empty[kNA], i_full[kNI], i_empty[kNI], y_full[kNY], y_free[kNY];
   __shared__ uint32_t ck_upd[kNY][kUpd / 32][2];  // per update warp: checksums of its pushed words
   __shared__ uint32_t w_upd[kNY];                 // push-sum weight bits sent with the tile (0: none)
   __shared__ int32_t dst_upd[kNY];                // receiving worker of a head's tile (-1: not a head)
+  __shared__ uint32_t tail_upd[kNY];              // 1: the slot's y is a chain tail's (copied to params)
   __shared__ uint4 meta[kNI];                     // trailer of the staged received tile (bulk-loaded)
   __shared__ uint4 meta_re;                       // trailer re-read by the mix after a failed check
   __shared__ uint32_t ck_mix[2][kMix / 32][2];    // per mix warp, double-buffered by round parity
   __shared__ uint32_t y_stored;  // update-warp arrivals: position j is done at >= 8 (j + 1)
+  __shared__ uint32_t tail_done; // chain tails whose y the store warp's bulk copy has put in params
   __shared__ int s_end;          // number of positions this CTA processes; INT_MAX until known
   __shared__ int s_timeout;
   volatile int* timeout = &s_timeout;
   volatile int* end_pos = &s_end;
 
+  const unsigned long long t_entry = a.trace ? ptx::globaltimer() : 0;
   const RankCta rc = rank_cta(a.vranks, s0.rank);
   PeerStepArgs s = s0;
   rank_view(s, a.peers, a.vranks, rc.rank);
@@ -286,6 +311,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     s_timeout = 0;
     s_end = 0x7fffffff;
     y_stored = 0;
+    tail_done = 0;
     for (int i = 0; i < kNA; ++i) {
       ptx::mbar_init(&a_full[i], 1);
       ptx::mbar_init(&a_empty[i], kUpd / 32);
@@ -300,6 +326,12 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     }
     ptx::mbar_fence_init();
   }
+  __syncthreads();  // mbarriers and segment tables ready
+  const unsigned long long t_topo = a.trace ? ptx::globaltimer() : 0;
+  // With one worker per GPU the walk is one row (a one-element chain): the x/m/g warp starts
+  // loading at once, while the others draw the topology
+  const bool solo = n_loc == 1;
+  const int topo_threads = solo ? kMThreads - 32 : kMThreads;
   // ---- this step's topology restricted to this GPU's workers (Alg. 2):
   // per segment the walk order (chains first, from their heads, then the local cycles) and
   // the receiver of every chain head (send_to, Alg.1 l.6)
@@ -308,7 +340,8 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     int32_t* srow = reinterpret_cast<int32_t*>(u + 64);   // [<= 64] the drawn row when fused
     int32_t* dstl = reinterpret_cast<int32_t*>(u + 128);  // [n_loc] receiver of each local worker
     const int ntop = s.gs > 0 ? s.groups : s.world;
-    for (int sg = warp; sg < s.k; sg += kWarps) {
+    const int tw0 = solo ? (warp < kWLoadXmg ? warp : warp - 1) : warp, tnw = solo ? kWarps - 1 : kWarps;
+    for (int sg = (solo && warp == kWLoadXmg) ? s.k : tw0; sg < s.k; sg += tnw) {
       if (s.gs > 0) {  // hierarchical leader exchange (one worker per GPU, replicated leader)
         if (lane == 0) dstl[0] = -1;
         __syncwarp();
@@ -381,9 +414,13 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       __syncwarp();
     }
   }
-  __syncthreads();
+  if (!(solo && warp == kWLoadXmg)) ptx::named_bar_sync(2, topo_threads);
   unsigned long long* tr = a.trace ? a.trace + ((size_t)s.rank * G + b) * 8 : nullptr;
-  if (tr && threadIdx.x == 0) tr[0] = ptx::globaltimer();
+  if (tr && threadIdx.x == 0) {
+    tr[0] = ptx::globaltimer();
+    tr[3] = t_topo;
+    tr[5] = t_entry;
+  }
   uint4* trl_in = reinterpret_cast<uint4*>(mine + a.off_trl) + (size_t)par * a.trl_cap;
 
   if (warp < kUpd / 32) {
@@ -395,11 +432,13 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     w.init(n_loc);
     float4 yfirst[kPerU], yprev[kPerU];
     uint32_t prev_row = 0;
+    int c = 0;  // positions with copies (chain heads and tails) so far: the y-out ring index
     for (int i = 0;; ++i) {
-      const int st = i % kNA, sy = i % kNY;
+      const int st = i % kNA;
       ptx::mbar_wait(&a_full[st], (uint32_t)((i / kNA) & 1));
-      ptx::mbar_wait(&y_free[sy], (uint32_t)(((i / kNY) & 1) ^ 1));
       if (!w.next(claims, a.chunk_t0, n_loc)) {  // end marker: pass it on to the store warp
+        const int sy = c % kNY;
+        ptx::mbar_wait(&y_free[sy], (uint32_t)(((c / kNY) & 1) ^ 1));
         if (tid == 0) dst_upd[sy] = -2;
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&y_full[sy]);
@@ -409,6 +448,9 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       const uint32_t e_w = ord[U.seg * n_loc + w.p];
       const uint32_t row = e_w & kWIdx;
       const bool head = (e_w & kWHead) != 0, tail = (e_w & kWTail) != 0;
+      const bool copy = head || tail;  // the store warp has work for this position
+      const int sy = c % kNY;
+      if (copy) ptx::mbar_wait(&y_free[sy], (uint32_t)(((c / kNY) & 1) ^ 1));
       const float* bx = ringA + (size_t)st * 3 * kT;
       float4* yt = reinterpret_cast<float4*>(ringY + (size_t)sy * kT);
       const float rate = s.lrs ? __ldg(s.lrs + (int64_t)row * s.n_layers + U.layer) : s.lr;
@@ -436,15 +478,24 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
           // a cycle closes with its first y; what a worker receives is bf16 on the bf16 wire
           if (e_w & kWStart) yfirst[q] = y;
           else st4_cs(X + (int64_t)prev_row * s.ld + j, mean4(yprev[q], wire ? bf16r4(y) : y), vv);
-          if (e_w & kWEnd) {
-            if (tail) st4(X + rowoff + j, y, vv);  // merged by the mix warps (default policy: L2)
-            else st4_cs(X + rowoff + j, mean4(y, wire ? bf16r4(yfirst[q]) : yfirst[q]), vv);
+          if ((e_w & kWEnd) && !tail)
+            st4_cs(X + rowoff + j, mean4(y, wire ? bf16r4(yfirst[q]) : yfirst[q]), vv);
+          if (tail) {
+            // a chain tail's y reaches params by the store warp's bulk copy (so the inbox warp's
+            // bulk read sees it once that copy completed); a last partial float4 of the row
+            // (never copied in bulk: the caller's padding columns) by a store made visible to
+            // the whole GPU before this position is released
+            yt[v] = y;
+            if (vv < 4) {
+              st4(X + rowoff + j, y, vv);
+              __threadfence();
+            }
           }
           yprev[q] = y;
           if (head) {
             if (wire) {  // what the receiver gets (C-20)
               const uint2 pw = pack_bf16x4(y);
-              reinterpret_cast<uint2*>(yt)[v] = pw;
+              reinterpret_cast<uint2*>(ringW + (size_t)sy * kT)[v] = pw;
               if (2u * v < nw) ck_add(cx, cs, pw.x, 2u * v);
               if (2u * v + 1 < nw) ck_add(cx, cs, pw.y, 2u * v + 1);
             } else {
@@ -472,8 +523,11 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       }
       if (tid == 0) {
         // a head's tile goes to its receiver with the segment's weight on the first tile
-        dst_upd[sy] = head ? hdst[U.seg * n_loc + row] : -1;
-        w_upd[sy] = (head && U.first) ? __float_as_uint(wsnap[row]) : 0u;
+        if (copy) {  // this position's slot (a position without copies has none)
+          dst_upd[sy] = head ? hdst[U.seg * n_loc + row] : -1;
+          tail_upd[sy] = tail ? 1u : 0u;
+          w_upd[sy] = (head && U.first) ? __float_as_uint(wsnap[row]) : 0u;
+        }
         if (U.first && w.p == n_loc - 1)  // psw of the rows with a local source
           for (int p = 0; p < n_loc; ++p) {
             const uint32_t o = ord[U.seg * n_loc + p];
@@ -489,14 +543,14 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
             PSW[(int64_t)r * s.k + U.seg] = pair_mean1(wsnap[r], wsnap[sl]);
           }
       }
-      ptx::fence_proxy_async_shared();  // push tile -> the store warp's bulk copy
-      ptx::fence_proxy_async_global();  // a tail's y in params -> the inbox warp's bulk copy
+      if (copy) ptx::fence_proxy_async_shared();  // y tile -> the store warp's bulk copies
       __syncwarp();
       if (lane == 0) {
         ptx::mbar_arrive(&a_empty[st]);
-        ptx::mbar_arrive(&y_full[sy]);
+        if (copy) ptx::mbar_arrive(&y_full[sy]);
         red_add_release_cta(&y_stored, 1u);
       }
+      if (copy) ++c;
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(s.err + kErrDiverged, 1);
     if (tr && threadIdx.x == 0) tr[1] = ptx::globaltimer();
@@ -656,7 +710,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
           }
         }
         const MTile U = mtile(a, bnd, t0, t, cur);
-        const int64_t off = (int64_t)(ord[U.seg * n_loc + p] & kWIdx) * s.ld + U.c0;
+        const int64_t off = (solo ? 0 : (int64_t)(ord[U.seg * n_loc + p] & kWIdx)) * s.ld + U.c0;
         const uint32_t bytes = (uint32_t)(((U.len + 3) & ~3) * 4);
         float* buf = ringA + (size_t)st * 3 * kT;
         ptx::mbar_arrive_expect_tx(&a_full[st], 3 * bytes);
@@ -682,10 +736,12 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
         // stage it once the update is `lag` positions further (the sender's copy has probably
         // completed by then), or at the end; the mix polls if the trailer is still old
         if (a.lag > 0) wait_position(&y_stored, end_pos, j + a.lag);
+        while ((int32_t)(ld_acquire_cta(&tail_done) - (uint32_t)(q + 1)) < 0) {
+        }  // this tail's own y is in params (its bulk copy completed)
         const int si = q % kNI;
         ptx::mbar_wait(&i_empty[si], (uint32_t)(((q / kNI) & 1) ^ 1));
         ++q;
-        ptx::fence_proxy_async_global();  // own y written by the update warps -> this bulk copy
+        ptx::fence_proxy_async_global();  // a partial float4's generic store -> this bulk copy
         float* buf = ringI + (size_t)si * 2 * kT;
         const uint32_t yb = (uint32_t)(((U.len + 3) & ~3) * 4);
         const uint32_t ib = wire ? (uint32_t)(((U.len + 7) & ~7) * 2) : yb;
@@ -725,67 +781,92 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       if (lane == 0) ptx::fence_acq_rel_sys();
     }
     if (lane == 0) {
-      // copies issued but not yet known complete, oldest first: their trailers wait
-      uint4* pend_dst[kLand + 1] = {};
-      uint4 pend_trl[kLand + 1] = {};
+      // positions whose copies were issued but are not yet known complete, oldest first: a
+      // head's trailer waits for its copy, a tail's release to the inbox warp for its own
+      const int land = solo ? 1 : 4;  // copies left in flight before their completion is awaited
+      uint4* pend_dst[kQ] = {};
+      uint4 pend_trl[kQ] = {};
+      bool pend_tail[kQ] = {};
       int pend_head = 0, npend = 0, cur = 0;
+      int unfreed = 0, free_next = 0;  // y-out slots whose copies may still read them, oldest first
+      auto free_oldest = [&]() {
+        ptx::mbar_arrive(&y_free[free_next]);
+        free_next = (free_next + 1) % kNY;
+        --unfreed;
+      };
       Walk w;
       w.init(n_loc);
-      auto complete_oldest = [&]() {  // Alg.1 l.14: that copy has completed at its receiver
-        st_volatile4(pend_dst[pend_head], pend_trl[pend_head]);
-        pend_head = (pend_head + 1) % (kLand + 1);
+      auto complete_oldest = [&]() {  // Alg.1 l.14: that position's copies have completed
+        if (pend_dst[pend_head]) st_volatile4(pend_dst[pend_head], pend_trl[pend_head]);
+        if (pend_tail[pend_head]) red_add_release_cta(&tail_done, 1u);
+        pend_head = (pend_head + 1) % kQ;
         --npend;
       };
-      for (int i = 0;; ++i) {
-        const int sy = i % kNY;
-        const uint32_t ph = (uint32_t)((i / kNY) & 1);
-        if (npend > 0 && !ptx::mbar_test(&y_full[sy], ph)) {  // idle: finish what is in flight
+      for (int c = 0;; ++c) {  // positions with copies only (chain heads and tails)
+        const int sy = c % kNY;
+        const uint32_t ph = (uint32_t)((c / kNY) & 1);
+        if ((npend > 0 || unfreed > 0) && !ptx::mbar_test(&y_full[sy], ph)) {  // idle: finish what is in flight
           ptx::bulk_wait_all();
           ptx::fence_proxy_async_global();  // their async-proxy writes -> the trailer stores
           while (npend > 0) complete_oldest();
+          while (unfreed > 0) free_oldest();
         }
         ptx::mbar_wait(&y_full[sy], ph);
         const int dg = dst_upd[sy];
         if (dg == -2) break;  // end marker
-        w.next(claims, a.chunk_t0, n_loc);
-        if (dg < 0) {  // not a head: nothing to send
-          ptx::mbar_arrive(&y_free[sy]);
-          continue;
-        }
-        const MTile U = mtile(a, bnd, t0, w.t, cur);
-        const int rp = dg / n_loc, rl = dg - rp * n_loc;
-        if (wire)
-          ptx::bulk_s2g(reinterpret_cast<uint16_t*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * n_loc + rl) * ld_bf + U.c0,
-                        ringY + (size_t)sy * kT, (uint32_t)(((U.len + 7) & ~7) * 2));
-        else
-          ptx::bulk_s2g(reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * n_loc + rl) * s.ld + U.c0,
-                        ringY + (size_t)sy * kT, (uint32_t)(((U.len + 3) & ~3) * 4));
-        ptx::bulk_commit();
-        uint32_t Xc = 0, Sc = 0;
+        const bool tl = tail_upd[sy] != 0;
+        MTile U;
+        do {  // this slot's position: the next one with copies
+          w.next(claims, a.chunk_t0, n_loc);
+          U = mtile(a, bnd, t0, w.t, cur);
+        } while (!(ord[U.seg * n_loc + w.p] & (kWHead | kWTail)));
+        const int q = (pend_head + npend) % kQ;
+        pend_dst[q] = nullptr;
+        pend_tail[q] = tl;
+        if (dg >= 0) {  // a head: its y tile to the receiver's inbox row over NVLink (a4)
+          const int rp = dg / n_loc, rl = dg - rp * n_loc;
+          if (wire)
+            ptx::bulk_s2g(reinterpret_cast<uint16_t*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * n_loc + rl) * ld_bf +
+                              U.c0,
+                          ringW + (size_t)sy * kT, (uint32_t)(((U.len + 7) & ~7) * 2));
+          else
+            ptx::bulk_s2g(reinterpret_cast<float*>(a.peers[rp] + a.off_inbox) + ((int64_t)par * n_loc + rl) * s.ld +
+                              U.c0,
+                          ringY + (size_t)sy * kT, (uint32_t)(((U.len + 3) & ~3) * 4));
+          uint32_t Xc = 0, Sc = 0;
 #pragma unroll
-        for (int u = 0; u < kUpd / 32; ++u) {
-          Xc ^= ck_upd[sy][u][0];
-          Sc += ck_upd[sy][u][1];
+          for (int u = 0; u < kUpd / 32; ++u) {
+            Xc ^= ck_upd[sy][u][0];
+            Sc += ck_upd[sy][u][1];
+          }
+          const uint32_t wb = w_upd[sy];
+          pend_dst[q] = reinterpret_cast<uint4*>(a.peers[rp] + a.off_trl) + (size_t)par * a.trl_cap +
+                        (size_t)w.t * n_loc + rl;
+          pend_trl[q] = make_uint4(e, Xc ^ wb, Sc, wb);
         }
-        const uint32_t wb = w_upd[sy];
-        const int q = (pend_head + npend) % (kLand + 1);
-        pend_dst[q] = reinterpret_cast<uint4*>(a.peers[rp] + a.off_trl) + (size_t)par * a.trl_cap +
-                      (size_t)w.t * n_loc + rl;
-        pend_trl[q] = make_uint4(e, Xc ^ wb, Sc, wb);
+        if (tl) {  // a tail: its own y into params, whole float4s (the partial one is generic)
+          const uint32_t row = ord[U.seg * n_loc + w.p] & kWIdx;
+          const uint32_t full4 = (uint32_t)(U.len & ~3) * 4u;
+          if (full4 > 0) ptx::bulk_s2g(X + (int64_t)row * s.ld + U.c0, ringY + (size_t)sy * kT, full4);
+        }
+        ptx::bulk_commit();
         ++npend;
-        ptx::bulk_wait_read<0>();  // the slot has been read: free it
-        ptx::mbar_arrive(&y_free[sy]);
-        if (npend > kLand) {  // all but the newest kLand copies have completed
-          ptx::bulk_wait<kLand>();
+        ++unfreed;
+        // slots are freed once their copies have read them, up to kReadLag positions late (the
+        // update warps may run kNY copy positions ahead, so this never waits on them)
+        ptx::bulk_wait_read<kReadLag>();
+        while (unfreed > kReadLag) free_oldest();
+        if (npend > land) {  // all but the newest `land` positions' copies have completed
+          bulk_wait_n(land);
           ptx::fence_proxy_async_global();
-          while (npend > kLand) complete_oldest();
+          while (npend > land) complete_oldest();
         }
       }
       ptx::bulk_wait_all();
       ptx::fence_proxy_async_global();
       if (tr) tr[2] = ptx::globaltimer();
       while (npend > 0) complete_oldest();
-      if (tr) tr[3] = ptx::globaltimer();
+      while (unfreed > 0) free_oldest();
     }
     __syncwarp();
   }
@@ -800,8 +881,9 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     if (prev + 1 == a.done_target) {
       // every CTA of this rank is past its claims: the next step's counter starts at 0
       reinterpret_cast<uint32_t*>(mine + a.off_claim)[par ^ 1] = 0u;
+      ptx::fence_acq_rel_sys();  // one release for all the done words (relaxed stores after it)
       for (int q = 0; q < s.nprocs; ++q)
-        ptx::st_release_sys(reinterpret_cast<uint32_t*>(a.peers[q] + a.off_done) + s.rank, e);
+        ptx::st_relaxed_sys(reinterpret_cast<uint32_t*>(a.peers[q] + a.off_done) + s.rank, e);
       if (a.trace) a.trace[(size_t)a.vranks * G * 8 + s.rank] = ptx::globaltimer();
     }
   }
@@ -809,16 +891,21 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
 
 }  // namespace
 
-size_t peer_merge_smem(int k, int n_loc) { return smem_bytes(k, n_loc); }
+size_t peer_merge_smem(int k, int n_loc) { return smem_bytes(k, n_loc, true); }
 
 int peer_merge_capacity(int k) {
   int dev = 0, sms = 0, occ = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = smem_bytes(1, kMaxKN);  // the largest walk tables
-  if (cudaFuncSetAttribute(k_push_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+  const size_t smem = smem_bytes(1, kMaxKN, true);  // the largest walk tables, bf16 image
+  cudaError_t e = cudaFuncSetAttribute(k_push_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push_merge, kMThreads, smem);
+  if (e != cudaSuccess || occ < 1) {  // never silently: the in-step schedule would be off
+    fprintf(stderr, "crossover_sgd: k_push_merge cannot be resident (%s, smem %zu); in-step merge disabled\n",
+            cudaGetErrorString(e), smem);
+    cudaGetLastError();
     return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_push_merge, kMThreads, smem) != cudaSuccess) return 0;
+  }
   return sms * occ;
 }
 
@@ -891,7 +978,7 @@ int peer_merge_launch(PeerState& p, const PeerStepArgs& a, uint32_t epoch, cudaS
     ma.trace = d_trace;
   }
   void* args[] = {&ma};
-  cudaError_t e = peer_launch(p, (const void*)k_push_merge, p.grid_merge, kMThreads, smem_bytes(a.k, a.n_loc), st, args);
+  cudaError_t e = peer_launch(p, (const void*)k_push_merge, p.grid_merge, kMThreads, smem_bytes(a.k, a.n_loc, a.wire != 0), st, args);
   if (e != cudaSuccess) {
     fprintf(stderr, "k_push_merge launch: %s\n", cudaGetErrorString(e));
     return CS_ECUDA;
@@ -903,7 +990,7 @@ int peer_merge_launch(PeerState& p, const PeerStepArgs& a, uint32_t epoch, cudaS
     cudaMemcpy(h.data(), ma.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     unsigned long long t0 = ~0ull;
     for (int c = 0; c < n; ++c) t0 = h[c * 8] && h[c * 8] < t0 ? h[c * 8] : t0;
-    const char* names[8] = {"start", "update_end", "push_landed", "trailers_end", "trailer_wait_us", "entry",
+    const char* names[8] = {"start", "update_end", "push_landed", "topo_begin", "trailer_wait_us", "entry",
                             "mix_end", "cta_end"};
     unsigned int retr = 0;
     if (p.d_stats) cudaMemcpy(&retr, p.d_stats, sizeof(retr), cudaMemcpyDeviceToHost);

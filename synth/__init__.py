@@ -11,8 +11,8 @@ DESIGN.md §"Input recipe" states (SURVEY.md §8(d) "Synthetic inputs"):
 
 The CUDA library implements the same definition independently in
 `cs_synth_fill` (test/bench input generator only); the two are compared
-bit-for-bit in tests/test_gpu_synth.py.  SplitMix64 is pinned to Vigna's
-reference outputs in tests/test_synth.py.
+bit-for-bit in tests/test_gpu_parity.py::test_synth_generator_bit_exact.  SplitMix64
+is pinned to Vigna's reference outputs in tests/test_oracle_rng.py.
 
 Recipe (all configs):
   x_i^0[j] = H(seed, TAG_INIT, i, j)                     (distinct per worker)

@@ -69,13 +69,14 @@ def test_layer_plan_bitwise(n, L, k):
     assert np.array_equal(w.cpu().numpy(), W)
 
 
-@pytest.mark.parametrize("n,L,k,plan,diag", [(8, 40, 6, True, False), (6, 25, 4, False, True),
-                                             (16, 161, 18, True, True), (2, 3, 2, True, False)])
-def test_lars_matches_oracle(n, L, k, plan, diag):
+@pytest.mark.parametrize("n,L,k,plan,diag,carry", [(8, 40, 6, True, False, False), (6, 25, 4, False, True, True),
+                                                   (16, 161, 18, True, True, True), (2, 3, 2, True, False, False)])
+def test_lars_matches_oracle(n, L, k, plan, diag, carry):
     sizes, lb = _layers(100 + L, L)
     seed = 5
     d, x, m, w, bank2, X, seg = _setup(n, sizes, lb, k, seed, plan)
     cs.cs_set_lars(ETA, WD, EPS)
+    cs.cs_set_lars_carry(carry)
     cs.cs_set_diag(diag)
     M, W = np.zeros_like(X), np.ones((n, k), F32)
     bank = synth.grad_bank(seed, n, d)
@@ -91,6 +92,8 @@ def test_lars_matches_oracle(n, L, k, plan, diag):
         xg = x.cpu().numpy()[:, :d]
         scale = np.abs(X).max(axis=1, keepdims=True)
         assert np.all(np.abs(xg - X) <= 1e-6 * scale), t
+        mg = m.cpu().numpy()[:, :d]  # momentum to the same tolerance
+        assert np.all(np.abs(mg - M) <= 1e-6 * np.abs(M).max(axis=1, keepdims=True)), t
         assert np.array_equal(w.cpu().numpy(), W)
         if diag:
             cd, ms = cs.cs_get_diag()
@@ -98,8 +101,39 @@ def test_lars_matches_oracle(n, L, k, plan, diag):
             assert abs(cd - cd0) <= 1e-9 * abs(cd0) and abs(ms - ms0) <= 1e-9 * max(1.0, abs(ms0))
     cs.cs_set_diag(False)
     cs.cs_set_lars(0.0)
+    cs.cs_set_lars_carry(False)
     if bitwise:  # the usual outcome: the parameters are then identical too
         assert np.array_equal(x.cpu().numpy()[:, :d], X)
+        assert np.array_equal(m.cpu().numpy()[:, :d], M)
+
+
+@pytest.mark.parametrize("carry", [False, True])
+def test_lars_params_modified_between_steps(carry):
+    # SPEC.md:368-376 / PAPER.md:35: the rates come from this step's x.  The caller rescales
+    # params in place between LARS steps (a checkpoint load or manual decay); by default the
+    # library recomputes ||x|| every step, and with the opt-in carry cs_params_modified()
+    # tells it to (the carry used to trust the pointer alone)
+    n, L, k, seed = 6, 20, 4, 12
+    sizes, lb = _layers(500 + L, L)
+    d, x, m, w, bank2, X, seg = _setup(n, sizes, lb, k, seed)
+    cs.cs_set_lars(ETA, WD, EPS)
+    cs.cs_set_lars_carry(carry)
+    M, W = np.zeros_like(X), np.ones((n, k), F32)
+    bank = synth.grad_bank(seed, n, d)
+    for t in range(6):
+        if t in (2, 4):
+            x.mul_(0.5)          # an outside in-place write of params
+            torch.cuda.synchronize()
+            X = (X * F32(0.5)).astype(F32)
+            if carry:
+                cs.cs_params_modified()
+        cs.cs_gossip_step(x, grads_view(bank2, n, t), w, 9.0, MU)
+        X, M, W, lrs = lars_gossip_step(X, M, synth.grads_at(bank, n, t), W, T.topology(seed, t, n, k), seg,
+                                        lb, 9.0, MU, ETA, WD, EPS)
+        assert _ulp_close(cs.cs_get_lars_rates(n, L), lrs), t
+    assert np.all(np.abs(x.cpu().numpy()[:, :d] - X) <= 1e-6 * np.abs(X).max(axis=1, keepdims=True))
+    cs.cs_set_lars(0.0)
+    cs.cs_set_lars_carry(False)
 
 
 @pytest.mark.parametrize("hybrid,plan", [(1, True), (0, True), (1, False)])

@@ -151,7 +151,14 @@ def test_host_exponential_topology_matches_oracle():
 
 
 def test_abi_version():
-    assert cs.cs_version() == 200  # 0.2.0
+    assert cs.cs_version() == 300  # 0.3.0
+
+
+def test_build_id_matches_sources():
+    # the library in the tree was built from exactly these sources (build()
+    # used to trust file times): __graft_entry__.build() rebuilds on any mismatch
+    import __graft_entry__ as entry
+    assert cs.cs_build_id() == entry.source_hash() == entry.built_id()
 
 
 def test_binding_constants_match_header():

@@ -14,7 +14,8 @@ h3  the leader's x', w' propagate to its members.
 
 Routed by the library's topology, computed on the oracle's arithmetic, and
 compared bitwise with the single-process `oracle.hierarchical.hier_step`: the
-contract `cs_hier_step` implements with NCCL + NVLink peer memory.  With LARS the
+contract `cs_hier_step` implements across GPUs with its own NVLink reduce-scatter /
+all-gather and the in-step merge kernel (or, opt-in, NCCL for h1).  With LARS the
 leader's per-layer rates come from its x and the group-reduced gradient (PAPER.md:197
 "LARS needs the gradient norm synchronised", reading C-18), compared with
 `oracle.lars.lars_hier_step`.
