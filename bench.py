@@ -127,6 +127,45 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+class NvlinkCounters:
+    """Hardware NVLink byte counters of this GPU (NVML field values, summed over its links),
+    read before and after the timed region: the NVLink traffic the step actually moved."""
+
+    FIELDS = (("tx", "NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES"), ("rx", "NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES"))
+
+    def __init__(self, index: int):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.links = [l for l in range(18) if self._link_up(l)]
+            self.ok = bool(self.links) and self.read() is not None
+        except Exception:  # noqa: BLE001
+            self.ok = False
+
+    def _link_up(self, link):
+        try:
+            return self.nv.nvmlDeviceGetNvLinkState(self.h, link) == 1
+        except Exception:  # noqa: BLE001
+            return False
+
+    def read(self):
+        """{tx, rx} bytes summed over the active links, or None."""
+        out = {}
+        for key, name in self.FIELDS:
+            fid = getattr(self.nv, name)
+            vals = self.nv.nvmlDeviceGetFieldValues(self.h, [(fid, l) for l in self.links])
+            tot = 0
+            for v in vals:
+                if v.nvmlReturn != 0:
+                    return None
+                tot += v.value.ullVal
+            out[key] = tot
+        return out
+
+
 class OracleSample:
     """The oracle as it stands, on all n workers x the first `cols` columns of the workload."""
 
@@ -287,6 +326,11 @@ def main():
                     help="multi-GPU step schedule (cs_set_schedule): instep = merged params when the step's "
                          "work completes (default); deferred = the merge runs inside the next step (opt-in, "
                          "params readable only after cs_flush); split = push kernel + merge kernel")
+    ap.add_argument("--h1", default="auto", choices=["auto", "nvls", "nvls-staged", "p2p"],
+                    help="multi-GPU hierarchical gradient average: nvls = in-switch reduction (cs_set_multicast) "
+                         "with the gradients in multicast memory; nvls-staged = the same with the gradients copied "
+                         "into the workspace each step; p2p = reduce-scatter + all-gather over peer stores; "
+                         "auto = nvls when the fabric has multicast")
     ap.add_argument("--path", default="auto", choices=["auto", "reg", "tma", "peer"],
                     help="library kernel path (cs_set_path); peer with 1 GPU = single-GPU emulation")
     args = ap.parse_args()
@@ -352,8 +396,15 @@ def main():
         x = torch.empty(n_loc, d, device=dev)
         m = torch.zeros(n_loc, d, device=dev)
         w = torch.ones(n_loc, k, device=dev)
-        bank = torch.empty(B + n_loc, d, device=dev)
     cs.cs_bind(m, d, d, rank, world_size, stream)
+    gs_h = world // groups
+    want_nvls = hier and world_size > 1 and gs_h > 1 and args.h1 != "p2p"
+    bank_mc = 0
+    if want_nvls and args.h1 in ("auto", "nvls"):  # the gradient bank in multicast memory (plumbing)
+        bank, bank_mc = cs.multicast_empty((B + n_loc, d), gs_h, dev)
+    else:
+        with torch.cuda.stream(stream):
+            bank = torch.empty(B + n_loc, d, device=dev)
     if lars is not None:
         sizes, block = synth.resnet50_layers()
         if d != sum(sizes):
@@ -366,8 +417,16 @@ def main():
     stream.synchronize()
     bank[B:] = bank[:n_loc]
     torch.cuda.synchronize()
+    h1 = "p2p" if hier and world_size > 1 and gs_h > 1 else None
     if world_size > 1:
         cs.setup_peers()
+        if want_nvls and cs.setup_multicast(gs_h, dev):
+            h1 = "nvls (in-switch reduce, gradients copied into the workspace)"
+            if bank_mc:
+                cs.register_multicast_grads(bank, bank_mc)
+                h1 = "nvls (in-switch reduce, gradients in multicast memory)"
+        elif args.h1 in ("nvls", "nvls-staged") and want_nvls:
+            raise SystemExit("--h1 nvls: this fabric gives no multicast")
 
     def grads(t):
         o = (t + first) % B
@@ -393,9 +452,11 @@ def main():
         nvl_max.append(nb)
     cs.cs_set_timing(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nvc = NvlinkCounters(local_rank) if world_size > 1 else None
     with ClockSampler(local_rank) as clk:
         barrier()
         torch.cuda.synchronize()
+        nv0 = nvc.read() if nvc and nvc.ok else None
         ev0.record(stream)
         for _ in range(args.steps):
             step_fn(x, grads(t), w, lr, mu)
@@ -403,6 +464,7 @@ def main():
         cs.cs_flush()  # the last step's deferred merge (multi-GPU push/mix) inside the timed region
         ev1.record(stream)
         torch.cuda.synchronize()
+        nv1 = nvc.read() if nv0 is not None else None
         barrier()
     cs.cs_sync()
     ms = ev0.elapsed_time(ev1)
@@ -410,10 +472,12 @@ def main():
     cs.cs_set_timing(False)
     hot_kernel, launches_per_step = cs.cs_kernel_info()
     nvl_b = float(sum(nvl_max))
-    stats = torch.tensor([ms, kern_ms, nvl_b], dtype=torch.float64, device=dev)
+    hw_tx = (nv1["tx"] - nv0["tx"]) / args.steps if nv1 else -1.0
+    hw_rx = (nv1["rx"] - nv0["rx"]) / args.steps if nv1 else -1.0
+    stats = torch.tensor([ms, kern_ms, nvl_b, hw_tx, hw_rx], dtype=torch.float64, device=dev)
     if world_size > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
-    ms, kern_ms_max, nvl_b_max = stats.tolist()
+    ms, kern_ms_max, nvl_b_max, hw_tx, hw_rx = stats.tolist()
     ms_step = ms / args.steps
     value = 4.0 * world * d / (ms_step * 1e-3) / 1e9
 
@@ -542,8 +606,15 @@ def main():
         # the step is bound by whichever resource needs longer for its algorithmic bytes
         nvl_per_launch = nvl_b_max / args.steps
         nvl_ach = nvl_per_launch / avg_kern_s / 1e9
+        # traffic: the hardware NVLink counters (NVML) over the timed region, per step, on the
+        # GPU that moved the most, in the direction the algorithmic bytes count (into a GPU)
+        traffic = {"rx_bytes_per_step": hw_rx, "tx_bytes_per_step": hw_tx,
+                   "rx_over_algorithmic": hw_rx / nvl_per_launch if nvl_per_launch else None,
+                   "source": "NVML NVLINK_COUNT_RCV/XMIT_BYTES summed over active links, max over ranks"} \
+            if hw_rx >= 0 else None
         roof_nvl = {"bound": "nvlink", "achieved": nvl_ach, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
-                    "frac": nvl_ach / NVLINK_PEER_GBS, "traffic": None,
+                    "frac": nvl_ach / NVLINK_PEER_GBS, "traffic": traffic,
+                    "achieved_hw_rx": hw_rx / avg_kern_s / 1e9 if hw_rx >= 0 else None,
                     "peak_source": "measured peer copy per direction (B200_PROFILING.md; 900 nominal)",
                     "kernel": hot_kernel, "algorithmic_bytes_per_launch": nvl_per_launch,
                     "bytes_formula": "4 B x remote-sourced segment elements (exact from the topology), "
@@ -563,7 +634,8 @@ def main():
         emit({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world_size, "steps": args.steps,
               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
               "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-              "config": bench_config(args, desc, world, n_loc, d, k, lr, mu, world_size, lars),
+              "config": {**bench_config(args, desc, world, n_loc, d, k, lr, mu, world_size, lars),
+                         **({"h1": h1, "groups": groups} if hier else {})},
               "step_us": ms_step * 1e3,
               "traffic_GBps": 20.0 * world * d / (ms_step * 1e-3) / 1e9,
               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "interval": interval,

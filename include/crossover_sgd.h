@@ -184,6 +184,33 @@ int cs_test_emulate_ranks(int vranks);
 int cs_ipc_export(char* handle_out);
 int cs_ipc_import(const char* all_handles /* nprocs * CS_IPC_HANDLE_BYTES */);
 
+/* Multi-GPU hierarchical step through the NVSwitch (NVLS): the intra-group gradient average
+ * h1 of cs_hier_step (section 3.3 "reduce the gradients in each group";
+ * reading C-12) as an in-switch reduction (multimem.ld_reduce) with a multicast store of
+ * the group mean (multimem.st), one kernel (k_hier_nvls) instead of the point-to-point
+ * reduce-scatter + all-gather.
+ *   cs_multicast_bytes  the workspace size this binding needs (after cs_bind).
+ *   cs_set_multicast    registers the caller's workspace: uc_base = this GPU's mapping of a
+ *                       buffer bound to a multicast object spanning exactly this process's
+ *                       hierarchical group (e.g. torch symmetric memory rendezvoused over
+ *                       the group), mc_base = the multicast mapping of the same buffer.
+ *                       Caller-owned; must stay mapped until cs_set_multicast(NULL, ...) or
+ *                       cs_finalize / cs_bind (which forget it).  Every member must register
+ *                       before any member steps (the words at the workspace start are
+ *                       zeroed here).  NULL uc_base returns to the point-to-point h1.
+ *   cs_add_multicast_grads  registers a caller buffer holding gradients that is bound to the
+ *                       same group's multicast object: a `grads` row inside it is reduced in
+ *                       place; any other `grads` is first copied into the workspace.
+ * Numerics: the switch sums the members' fp32 values in its own order, so for groups of
+ * >= 3 GPUs params match the oracle within the hierarchical tolerance (SURVEY 8(c):
+ * norm-wise <= 1e-6) rather than bitwise; groups of 2 stay bitwise.  Members still hold
+ * bit-identical replicas.  LARS keeps the point-to-point h1.
+ * Errors: CS_ENOTBOUND, CS_EINVAL, CS_ELAYOUT (not 256-B / 16-B aligned), CS_EUNSUPPORTED
+ * (one process, emulated ranks, groups of one GPU), CS_ECUDA. */
+int cs_multicast_bytes(int64_t* bytes_out);
+int cs_set_multicast(void* uc_base, void* mc_base, int64_t bytes);
+int cs_add_multicast_grads(void* uc_base, void* mc_base, int64_t bytes);
+
 /* ---- the hot path --------------------------------------------------------- */
 
 /* One flat Crossover-SGD step at the internal step counter t, then t += 1.
@@ -202,9 +229,10 @@ int cs_ipc_import(const char* all_handles /* nprocs * CS_IPC_HANDLE_BYTES */);
  *   psw     fp32 device [n_loc][k] push-sum weights, updated in place (start at 1).
  *   lr, momentum  fp32 scalars.
  * Every output reads only the pre-step snapshot.  Multi-GPU: every
- * process must call with the same t, and a5 of this step may be deferred into the
- * next step's kernel: call cs_flush or cs_sync before reading params / psw (see
- * cs_flush).  Also: cs_set_topology_kind (SGP graph), cs_set_wire (bf16 wire),
+ * process must call with the same t.  On the default schedule (CS_SCHED_INSTEP) params
+ * and psw hold the merged x', w' once the step's enqueued work completes; only the opt-in
+ * CS_SCHED_DEFERRED leaves a5 to the next step's kernel (then cs_flush or cs_sync before
+ * reading params / psw; see cs_set_schedule, cs_flush).  Also: cs_set_topology_kind (SGP graph), cs_set_wire (bf16 wire),
  * cs_set_lars + cs_set_layers (LARS).  Errors: CS_ENOTBOUND, CS_ELAYOUT, CS_EINVAL,
  * CS_ECUDA, CS_ETOPOLOGY, CS_EDIVERGED (from an earlier step), CS_ETIMEOUT,
  * CS_EUNSUPPORTED (a combination listed as such at the setters). */

@@ -54,6 +54,9 @@ _SIGS = {
     "cs_test_emulate_ranks": (_c_int, [_c_int]),
     "cs_ipc_export": (_c_int, [_vp]),
     "cs_ipc_import": (_c_int, [_vp]),
+    "cs_multicast_bytes": (_c_int, [_vp]),
+    "cs_set_multicast": (_c_int, [_vp, _vp, _c_i64]),
+    "cs_add_multicast_grads": (_c_int, [_vp, _vp, _c_i64]),
     "cs_gossip_step": (_c_int, [_vp, _vp, _vp, _c_f, _c_f]),
     "cs_gossip_step_host": (_c_int, [_vp, _vp, _vp, _c_f, _c_f, _vp]),
     "cs_gossip_step_io": (_c_int, [_vp, _vp, _vp, _c_f, _c_f, _vp, _vp]),
@@ -191,6 +194,71 @@ def setup_peers(group=None) -> None:
     dist.all_gather_object(allh, mine, group=group)
     cs_ipc_import(allh)
     dist.barrier(group=group)
+
+
+def cs_multicast_bytes() -> int:
+    out = ctypes.c_int64(0)
+    _check(lib.cs_multicast_bytes(ctypes.byref(out)), "cs_multicast_bytes")
+    return int(out.value)
+
+
+def cs_set_multicast(uc_ptr: int, mc_ptr: int, nbytes: int) -> None:
+    _check(lib.cs_set_multicast(uc_ptr or None, mc_ptr or None, nbytes), "cs_set_multicast")
+
+
+def cs_add_multicast_grads(uc_ptr: int, mc_ptr: int, nbytes: int) -> None:
+    _check(lib.cs_add_multicast_grads(uc_ptr, mc_ptr, nbytes), "cs_add_multicast_grads")
+
+
+# Symmetric (multicast-bound) buffers handed to the library must outlive their use.
+_MC_KEEP: list = []
+_MC_GROUP = {}
+
+
+def _hier_group(group_size: int):
+    """This process's hierarchical group (contiguous ranks) as a torch process group."""
+    import torch.distributed as dist
+    if group_size not in _MC_GROUP:
+        _MC_GROUP[group_size], _ = dist.new_subgroups(group_size=group_size)
+    return _MC_GROUP[group_size]
+
+
+def multicast_empty(shape, group_size: int, device):
+    """Plumbing, no arithmetic: an fp32 tensor in torch symmetric memory rendezvoused over this
+    process's hierarchical group, plus its multicast address (0 if the fabric has none).
+    Collective over the whole job."""
+    import torch
+    import torch.distributed._symmetric_memory as symm_mem
+    grp = _hier_group(group_size)
+    t = symm_mem.empty(*shape, dtype=torch.float32, device=device)
+    h = symm_mem.rendezvous(t, grp.group_name)
+    mc = h.multicast_ptr
+    if mc:
+        mc += t.data_ptr() - h.buffer_ptrs[h.rank]
+    _MC_KEEP.append((t, h))
+    return t, mc
+
+
+def setup_multicast(group_size: int, device) -> bool:
+    """Registers a multicast workspace over this process's hierarchical group (cs_set_multicast)
+    so cs_hier_step averages gradients in the NVSwitch.  False (nothing registered) if the
+    fabric gives no multicast.  Collective over the whole job; call after setup_peers()."""
+    import torch.distributed as dist
+    nbytes = cs_multicast_bytes()
+    t, mc = multicast_empty(((nbytes + 3) // 4,), group_size, device)
+    ok = mc != 0
+    flags = [None] * dist.get_world_size()
+    dist.all_gather_object(flags, ok)
+    if not all(flags):
+        return False
+    cs_set_multicast(t.data_ptr(), mc, 4 * t.numel())
+    dist.barrier()
+    return True
+
+
+def register_multicast_grads(t, mc: int) -> None:
+    """Gradient rows inside `t` (from multicast_empty) are reduced in place by cs_hier_step."""
+    cs_add_multicast_grads(t.data_ptr(), mc, 4 * t.numel())
 
 
 def cs_gossip_step(params, grads, psw, lr: float, momentum: float) -> None:

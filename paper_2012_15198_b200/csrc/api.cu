@@ -396,6 +396,7 @@ PeerStepArgs peer_args(float* params, const float* grads, float* psw, float lr, 
   pa.tile_first = nullptr;
   pa.lars_part = nullptr;
   pa.g_off = 0;
+  pa.gbar_local = 0;
   if (g.vranks > 1) {  // emulated ranks: rank 0's view; each CTA shifts to its own rank
     pa.n_loc = g.world / g.vranks;
     pa.nprocs = g.vranks;
@@ -721,6 +722,58 @@ int cs_ipc_import(const char* all_handles) {
   return rc ? fail(rc, "%s", peer_error()) : CS_OK;
 }
 
+int cs_multicast_bytes(int64_t* bytes_out) {
+  int rc = check_bound();
+  if (rc) return rc;
+  if (!bytes_out) return fail(CS_EINVAL, "NULL bytes_out");
+  *bytes_out = (int64_t)nvls_bytes(g.ld);
+  return CS_OK;
+}
+
+int cs_set_multicast(void* uc_base, void* mc_base, int64_t bytes) {
+  int rc = check_bound();
+  if (rc) return rc;
+  PeerState& p = g.peer;
+  if (uc_base == nullptr) {  // back to the point-to-point reduce-scatter
+    if ((rc = flush_pending()) != CS_OK) return rc;
+    CS_CUDA(cudaStreamSynchronize(g.stream));
+    p.mc_uc = p.mc_mc = nullptr;
+    p.mc_bytes = 0;
+    p.mc_grads.clear();
+    return CS_OK;
+  }
+  if (!mc_base) return fail(CS_EINVAL, "NULL mc_base");
+  if (g.nprocs < 2 || g.vranks > 1 || !p.imported)
+    return fail(CS_EUNSUPPORTED, "multicast h1 needs one process per GPU with the peers imported");
+  if (p.gs < 2) return fail(CS_EUNSUPPORTED, "multicast h1 needs hierarchical groups of >= 2 GPUs");
+  if (bytes < (int64_t)nvls_bytes(g.ld))
+    return fail(CS_EINVAL, "multicast workspace of %lld bytes < cs_multicast_bytes() = %lld", (long long)bytes,
+                (long long)nvls_bytes(g.ld));
+  if (((uintptr_t)uc_base | (uintptr_t)mc_base) % 256 != 0) return fail(CS_ELAYOUT, "multicast workspace not 256-B aligned");
+  CS_CUDA(cudaStreamSynchronize(g.stream));
+  if (!p.d_nvls_count) CS_CUDA(cudaMalloc(&p.d_nvls_count, 128));
+  CS_CUDA(cudaMemset(p.d_nvls_count, 0, 128));
+  CS_CUDA(cudaMemset(uc_base, 0, nvls_off_gbar()));  // barrier words (callers barrier before stepping)
+  CS_CUDA(cudaDeviceSynchronize());
+  p.mc_uc = static_cast<char*>(uc_base);
+  p.mc_mc = static_cast<char*>(mc_base);
+  p.mc_bytes = (size_t)bytes;
+  p.nvls_epoch = 0;
+  p.nvls_tot[0] = p.nvls_tot[1] = 0;
+  return CS_OK;
+}
+
+int cs_add_multicast_grads(void* uc_base, void* mc_base, int64_t bytes) {
+  int rc = check_bound();
+  if (rc) return rc;
+  if (!g.peer.mc_uc) return fail(CS_ENOTBOUND, "cs_set_multicast has not been called");
+  if (!uc_base || !mc_base || bytes <= 0) return fail(CS_EINVAL, "NULL region or bytes <= 0");
+  if (((uintptr_t)uc_base | (uintptr_t)mc_base) % 16 != 0) return fail(CS_ELAYOUT, "region not 16-B aligned");
+  if (g.peer.mc_grads.size() >= 8) return fail(CS_EINVAL, "at most 8 multicast gradient regions");
+  g.peer.mc_grads.push_back({static_cast<char*>(uc_base), static_cast<char*>(mc_base), (size_t)bytes});
+  return CS_OK;
+}
+
 int cs_gossip_step(float* params, const float* grads, float* psw, float lr, float momentum) {
   int rc = check_bound();
   if (rc) return rc;
@@ -895,6 +948,7 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
     cudaEvent_t ev[2];
     rc = next_event_pair(ev);
     if (rc) return rc;
+    const long launches0 = g_peer_launches;
     rc = peer_hier_step(g.peer, pa, g.stream, ev[0], ev[1]);
     if (rc) return fail(rc, "%s", peer_error());
     if (diag) {
@@ -904,9 +958,10 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
       g.diag_valid = true;
     }
     // (topology,) scatter, reduce, push (, mix unless the leader exchange's merge is deferred)
-    g.launches_per_step = (g.groups >= 2 ? (g.peer.last_fused ? 4 : 5) : 3) + (g.lars ? 2 : 0);
+    g.launches_per_step = (int)(g_peer_launches - launches0) + (g.lars ? 2 : 0);
     g.hot_kernel = g.lars ? "k_hier_scatter+k_hier_reduce+k_lars_norms+k_lars_scale+k_peer_push+k_peer_mix"
-                          : "k_hier_scatter+k_hier_reduce+k_peer_push+k_peer_mix";
+                   : g.peer.last_nvls ? (g.groups >= 2 ? "k_hier_nvls+k_push_merge" : "k_hier_nvls+k_peer_push")
+                                      : "k_hier_scatter+k_hier_reduce+k_peer_push+k_peer_mix";
     g.step += 1;
     return CS_OK;
   }
@@ -1243,10 +1298,13 @@ int cs_step_bytes(int64_t step, int hier, double* out) {
     // one worker per GPU: the group mean needs every member's g (reduce-scatter +
     // all-gather, (gs-1)/gs of 4 B each way), then the leader exchange (4 B per
     // parameter when there are >= 2 groups); HBM as a flat step on the group mean
+    // Through the NVSwitch (cs_set_multicast) a GPU takes in its reduced chunk (d/gs) and the
+    // other members' mean chunks ((gs-1)/gs of d): 4 B per parameter
     const int gs = g.world / g.groups;
     const double frac = (double)(gs - 1) / (double)gs;
+    const bool nvls = g.peer.mc_uc != nullptr && gs > 1 && !g.lars;
     out[0] = 20.0 * d;
-    out[1] = 2.0 * 4.0 * frac * d + (g.groups >= 2 ? 4.0 * d : 0.0);
+    out[1] = (nvls ? 4.0 * d : 2.0 * 4.0 * frac * d) + (g.groups >= 2 ? 4.0 * d : 0.0);
   }
   return CS_OK;
 }

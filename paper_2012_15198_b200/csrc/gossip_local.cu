@@ -26,7 +26,9 @@
 // FMA, so results are bit-identical to the oracle's separately rounded ops.
 #include <stdlib.h>
 
+#include "arith.cuh"
 #include "common.cuh"
+#include "ptx.cuh"
 #include "philox.cuh"
 #include "topo_device.cuh"
 
@@ -48,16 +50,7 @@ __device__ __forceinline__ void st_stream(float* p, const float4 v, int valid) {
   }
 }
 
-__device__ __forceinline__ float4 momentum_update(float4 m, float4 g, float mu) {
-  return make_float4(__fadd_rn(__fmul_rn(mu, m.x), g.x), __fadd_rn(__fmul_rn(mu, m.y), g.y),
-                     __fadd_rn(__fmul_rn(mu, m.z), g.z), __fadd_rn(__fmul_rn(mu, m.w), g.w));
-}
 
-// LARS's weight-decayed gradient g + wd*x (reading C-18)
-__device__ __forceinline__ float4 decay4(float4 g, float4 x, float wd) {
-  return make_float4(__fadd_rn(g.x, __fmul_rn(wd, x.x)), __fadd_rn(g.y, __fmul_rn(wd, x.y)),
-                     __fadd_rn(g.z, __fmul_rn(wd, x.z)), __fadd_rn(g.w, __fmul_rn(wd, x.w)));
-}
 
 // index of the last bound <= j among bounds[0 .. count) (bounds ascending, bounds[0] = 0)
 __device__ __forceinline__ int last_bound_le(const int64_t* bounds, int count, int64_t j) {
@@ -83,25 +76,9 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__device__ __forceinline__ float4 sgd_apply(float4 x, float4 m, float lr) {
-  return make_float4(__fsub_rn(x.x, __fmul_rn(lr, m.x)), __fsub_rn(x.y, __fmul_rn(lr, m.y)),
-                     __fsub_rn(x.z, __fmul_rn(lr, m.z)), __fsub_rn(x.w, __fmul_rn(lr, m.w)));
-}
 
-__device__ __forceinline__ float4 pair_mean(float4 a, float4 b) {
-  return make_float4(__fmul_rn(__fadd_rn(a.x, b.x), 0.5f), __fmul_rn(__fadd_rn(a.y, b.y), 0.5f),
-                     __fmul_rn(__fadd_rn(a.z, b.z), 0.5f), __fmul_rn(__fadd_rn(a.w, b.w), 0.5f));
-}
 
-__device__ __forceinline__ float pair_mean1(float a, float b) {
-  return __fmul_rn(__fadd_rn(a, b), 0.5f);
-}
 
-__device__ __forceinline__ bool nonfinite4(float4 g) {
-  const uint32_t e = 0x7f800000u;
-  return ((__float_as_uint(g.x) & e) == e) | ((__float_as_uint(g.y) & e) == e) |
-         ((__float_as_uint(g.z) & e) == e) | ((__float_as_uint(g.w) & e) == e);
-}
 
 // Per-column fp64 accumulators for the consensus diagnostics, shifted by the
 // first value c seen in the column so the variance does not cancel near consensus.
@@ -372,18 +349,18 @@ __global__ void __launch_bounds__(kThreads) k_gossip_local(const LocalArgs a) {
           const uint32_t row = e & kOrdIdx;
           const int64_t off = (int64_t)row * ld + j;
           bad |= nonfinite4(cg);
-          const float4 mn = momentum_update(cm, cg, mu);
-          const float4 y = sgd_apply(cx, mn, lr);
+          const float4 mn = mom4(cm, cg, mu);
+          const float4 y = sgd4(cx, mn, lr);
           st_stream(a.m + off, mn, valid);
           if (e & kOrdStart) {
             yfirst = y;
           } else {
-            const float4 xo = pair_mean(yprev, a.wire ? bf16r4(y) : y);
+            const float4 xo = mean4(yprev, a.wire ? bf16r4(y) : y);
             st_stream(a.x + prev_off, xo, valid);
             if (DIAG) { cd.add(xo, rw[prev_row], first_diag, 1.0); first_diag = false; }
           }
           if (e & kOrdEnd) {
-            const float4 xo = pair_mean(y, a.wire ? bf16r4(yfirst) : yfirst);
+            const float4 xo = mean4(y, a.wire ? bf16r4(yfirst) : yfirst);
             st_stream(a.x + off, xo, valid);
             if (DIAG) { cd.add(xo, rw[row], first_diag, 1.0); first_diag = false; }
           }
@@ -468,8 +445,8 @@ __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
                                       __fmul_rn(gsum.z, inv), __fmul_rn(gsum.w, inv));
       // LARS on the group-reduced gradient (C-18): m' = mu*m + (gbar + wd*x)
       const bool lars = LAYERS && a.lrs;
-      const float4 mn = momentum_update(cm, lars ? decay4(gbar, cx, a.wd) : gbar, mu);
-      const float4 y = sgd_apply(cx, mn, lars ? __ldg(a.lrs + (int64_t)G * a.n_layers + layer) : lr);
+      const float4 mn = mom4(cm, lars ? decay4(gbar, cx, a.wd) : gbar, mu);
+      const float4 y = sgd4(cx, mn, lars ? __ldg(a.lrs + (int64_t)G * a.n_layers + layer) : lr);
       st_stream(a.m + lead_off, mn, valid);
       if (L == 1) {
         for (int r = 0; r < gs; ++r) st_stream(a.x + lead_off + (int64_t)r * ld, y, valid);
@@ -479,13 +456,13 @@ __global__ void __launch_bounds__(kThreads) k_hier_local(const LocalArgs a) {
       if (e & kOrdStart) {
         yfirst = y;
       } else {
-        const float4 xo = pair_mean(yprev, y);
+        const float4 xo = mean4(yprev, y);
         const int64_t po = (int64_t)prev_leader * gs * ld + j;
         for (int r = 0; r < gs; ++r) st_stream(a.x + po + (int64_t)r * ld, xo, valid);
         if (DIAG) { cd.add(xo, rw[prev_leader], first_diag, (double)gs); first_diag = false; }
       }
       if (e & kOrdEnd) {
-        const float4 xo = pair_mean(y, yfirst);
+        const float4 xo = mean4(y, yfirst);
         for (int r = 0; r < gs; ++r) st_stream(a.x + lead_off + (int64_t)r * ld, xo, valid);
         if (DIAG) { cd.add(xo, rw[G], first_diag, (double)gs); first_diag = false; }
       }
@@ -519,38 +496,13 @@ constexpr int kVPT = kTmaTileMax / (4 * kTmaConsumers);  // float4 columns per c
 constexpr int kStages = 4;
 constexpr size_t kStageBytes = 3ull * kTmaTileMax * sizeof(float);
 
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_addr(bar)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
+using ptx::bulk_g2s;
+using ptx::mbar_arrive;
+using ptx::mbar_arrive_expect_tx;
+using ptx::mbar_init;
+using ptx::mbar_wait;
+using ptx::smem_addr;
+
 
 __host__ __device__ inline size_t tma_smem_bytes(int n, int k, bool diag) {
   return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t) + kStages * sizeof(float) +
@@ -643,20 +595,20 @@ __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
             const float4 cm = reinterpret_cast<const float4*>(buf + kTmaTileMax)[v];
             const float4 cg = reinterpret_cast<const float4*>(buf + 2 * kTmaTileMax)[v];
             bad |= nonfinite4(cg);
-            const float4 mn = momentum_update(cm, LARS ? decay4(cg, cx, a.wd) : cg, mu);
-            const float4 y = sgd_apply(cx, mn, rate);
+            const float4 mn = mom4(cm, LARS ? decay4(cg, cx, a.wd) : cg, mu);
+            const float4 y = sgd4(cx, mn, rate);
             const int64_t j = td.c0 + 4 * v;
             st_stream(a.m + (int64_t)row * ld + j, mn, vv);
             if (e & kOrdStart) {
               yfirst[c] = y;
             } else {
-              const float4 xo = pair_mean(yprev[c], a.wire ? bf16r4(y) : y);
+              const float4 xo = mean4(yprev[c], a.wire ? bf16r4(y) : y);
               st_stream(a.x + (int64_t)prev_row * ld + j, xo, vv);
               if (DIAG) cd[c].add(xo, rw[prev_row], first_diag, 1.0);
               if (LARS) qa = sumsq4(qa, xo, vv);
             }
             if (e & kOrdEnd) {
-              const float4 xo = pair_mean(y, a.wire ? bf16r4(yfirst[c]) : yfirst[c]);
+              const float4 xo = mean4(y, a.wire ? bf16r4(yfirst[c]) : yfirst[c]);
               st_stream(a.x + (int64_t)row * ld + j, xo, vv);
               if (DIAG) cd[c].add(xo, rw[row], first_diag && (e & kOrdStart), 1.0);
               if (LARS) qb = sumsq4(qb, xo, vv);

@@ -71,6 +71,8 @@
 
 namespace cs {
 
+long g_peer_launches = 0;
+
 namespace {
 
 std::string g_peer_err;
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
   if (warp == kLoadWarp) {
     // the load warp starts streaming at once; hierarchical: it is the only reader of the
     // group mean (gbar), so it alone waits for it to be complete on this GPU
-    if (s.gs > 0 && lane < s.gs) {
+    if (s.gs > 0 && !s.gbar_local && lane < s.gs) {
       const uint32_t* d2 = reinterpret_cast<const uint32_t*>(mine + a.off_d2);
       const int gbase = (s.rank / s.gs) * s.gs;
       if (!wait_acquire(d2 + gbase + lane, e)) atomicOr(&s_timeout, 1);
@@ -1350,6 +1352,7 @@ __global__ void k_diag_final(const DiagArgs a0) {
 // cooperative launch over every emulated rank otherwise (peer_launch).
 template <typename Arg>
 void plaunch(const PeerState& p, void (*fn)(Arg), int grid, int threads, size_t smem, cudaStream_t st, Arg arg) {
+  ++g_peer_launches;
   void* args[] = {&arg};
   peer_launch(p, reinterpret_cast<const void*>(fn), grid, threads, smem, st, args);
 }
@@ -1650,6 +1653,7 @@ void peer_release(PeerState& p) {
   if (p.d_tail_tbl) cudaFree(p.d_tail_tbl);
   if (p.d_chunk_t0) cudaFree(p.d_chunk_t0);
   if (p.d_stats) cudaFree(p.d_stats);
+  if (p.d_nvls_count) cudaFree(p.d_nvls_count);
   p = PeerState();
 }
 
@@ -1740,6 +1744,7 @@ int launch_topology_for(const PeerStepArgs& a, int n, int tag, cudaStream_t st) 
   t.rw = nullptr;
   t.inv_wsum = nullptr;
   t.err = a.err;
+  ++g_peer_launches;
   cudaError_t e = launch_topology(t, st);
   return e == cudaSuccess ? CS_OK : perr(CS_ECUDA, "topology launch", e);
 }
@@ -2170,6 +2175,20 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     b.lrs = a.lrs_out;
     if (p.hier_pieces != 1 && !exchange) return perr(CS_EUNSUPPORTED, "hierarchical LARS needs CS_HIER_PIECES=1", cudaSuccess);
   }
+  // NVLS h1 (hier_nvls.cu): the group mean by in-switch reduction into this GPU's
+  // multicast workspace; the update below then reads a complete gbar
+  const bool nvls = p.mc_uc != nullptr && p.vranks <= 1 && a.lrs_out == nullptr && !fuse;
+  const float* g_mc = nullptr;
+  if (nvls) {
+    for (const auto& r : p.mc_grads)
+      if (reinterpret_cast<const char*>(a.g) >= r.uc &&
+          reinterpret_cast<const char*>(a.g) + (size_t)a.d * sizeof(float) <= r.uc + r.bytes)
+        g_mc = reinterpret_cast<const float*>(r.mc + (reinterpret_cast<const char*>(a.g) - r.uc));
+    b.g = reinterpret_cast<const float*>(p.mc_uc + nvls_off_gbar());
+    b.g_off = 0;
+    b.gbar_local = 1;
+  }
+  p.last_nvls = nvls;
   PeerKernelArgs ka = kernel_args(p, b, epoch, !exchange);
   if (ev0) cudaEventRecord(ev0, st);
   if (p.need_sync && p.gs > 1) {  // members become exact replicas of their leader
@@ -2192,7 +2211,7 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   // One group (no leader exchange): the vector is cut into P column pieces; h1 of piece
   // q+1 (NVLink-bound) runs on the caller's stream while the update of piece q (HBM-bound,
   // k_peer_push in final_only mode, waiting on piece q's d2 flags) runs on the aux stream.
-  const int P = exchange ? 1 : p.hier_pieces;
+  const int P = exchange || nvls ? 1 : p.hier_pieces;
   h.gstride = a.ld;
   int rc = CS_OK;
   for (int q = 0; q < P; ++q) {
@@ -2207,10 +2226,16 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     h.c1_target = (p.tot_c1[q] += (uint32_t)p.grid_hier);
     h.c2_target = (p.tot_c2[q] += (uint32_t)p.grid_hier);
     phase_record(0, st);
-    plaunch(p, k_hier_scatter, p.grid_hier, kHierThreads, 0, st, h);
-    phase_record(1, st);
-    plaunch(p, k_hier_reduce, p.grid_hier, kHierThreads, 0, st, h);
-    phase_record(2, st);
+    if (nvls) {
+      if (nvls_h1(p, a.g, g_mc, a.rank % p.gs, a.inv_gs, a.err, st))
+        return perr(CS_ECUDA, "k_hier_nvls launch", cudaGetLastError());
+      phase_record(2, st);
+    } else {
+      plaunch(p, k_hier_scatter, p.grid_hier, kHierThreads, 0, st, h);
+      phase_record(1, st);
+      plaunch(p, k_hier_reduce, p.grid_hier, kHierThreads, 0, st, h);
+      phase_record(2, st);
+    }
     if (a.lrs_out) {  // rates from the leader replica's x and the group mean, once gbar is whole
       LarsWait w;
       if (p.vranks <= 1) {

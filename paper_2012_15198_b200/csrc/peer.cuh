@@ -46,6 +46,9 @@ struct PeerStepArgs {
   double* lars_part;
   // nonzero: g is the rank's own exchange region + g_off (the hierarchical group mean)
   size_t g_off;
+  // 1: the hierarchical group mean g is complete on this GPU before the kernel starts
+  // (NVLS h1, hier_nvls.cu), so the update does not wait for the reduce flags
+  int gbar_local;
 };
 
 struct PeerState {
@@ -122,7 +125,29 @@ struct PeerState {
   struct TileDesc* d_htiles = nullptr;
   int n_htiles = 0, grid_hyb = 0, grid_tail = 0;
   uint8_t* d_tail_tbl = nullptr;
+  // NVLS h1 (hier_nvls.cu): the caller's multicast workspace of this GPU's group (unicast and
+  // multicast views, cs_set_multicast) and multicast-bound gradient regions it registered
+  char* mc_uc = nullptr;
+  char* mc_mc = nullptr;
+  size_t mc_bytes = 0;
+  struct McRegion { char* uc; char* mc; size_t bytes; };
+  std::vector<McRegion> mc_grads;
+  uint32_t* d_nvls_count = nullptr;   // local arrival counters [2] at 64-byte stride
+  uint32_t nvls_epoch = 0;
+  uint32_t nvls_tot[2] = {0, 0};
+  bool last_nvls = false;   // the last hierarchical step's h1 ran through NVLS
 };
+
+// kernels the multi-GPU steps launched (plaunch / peer_launch / topology / NVLS): the
+// bench's launch count is the difference across a step
+extern long g_peer_launches;
+
+// NVLS h1 (hier_nvls.cu)
+size_t nvls_off_gbar();
+size_t nvls_bytes(int64_t ld);
+// g_mc: multicast address of g when g lies in a registered multicast region, else nullptr
+// (the kernel stages g into the workspace first)
+int nvls_h1(PeerState& p, const float* g, const float* g_mc, int member, float inv_gs, int* err, cudaStream_t st);
 
 // gs: GPUs per hierarchical group when a hierarchical step is possible (one worker
 // per GPU and groups < world), else 0.

@@ -678,7 +678,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     if (tr && tm == 0) tr[6] = ptx::globaltimer();
   } else if (warp == kWLoadXmg) {
     // ---------------- claims + x, m, g loader ----------------------------------------
-    if (s.gs > 0 && lane < s.gs) {  // hierarchical: the group mean is complete on this GPU
+    if (s.gs > 0 && !s.gbar_local && lane < s.gs) {  // hierarchical: the group mean is complete on this GPU
       const uint32_t* d2 = reinterpret_cast<const uint32_t*>(mine + a.off_d2);
       const int gbase = (s.rank / s.gs) * s.gs;
       if (!ptx::wait_geq_sys(d2 + gbase + lane, e)) atomicOr(&s_timeout, 1);
@@ -938,6 +938,7 @@ bool peer_merge_ok(const PeerState& p, const PeerStepArgs& a) {
 
 cudaError_t peer_launch(const PeerState& p, const void* fn, int grid_per_rank, int threads, size_t smem,
                         cudaStream_t st, void** args) {
+  ++g_peer_launches;
   if (p.vranks <= 1) return cudaLaunchKernel(fn, dim3(grid_per_rank), dim3(threads), args, smem, st);
   return cudaLaunchCooperativeKernel(fn, dim3(grid_per_rank * p.vranks), dim3(threads), args, smem, st);
 }

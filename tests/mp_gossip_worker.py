@@ -49,6 +49,11 @@ def main():
                     help="no cs_sync between steps (deferred merges run inside the next push); compare at the end")
     ap.add_argument("--schedule", default="instep", choices=["instep", "deferred", "split"],
                     help="cs_set_schedule: instep (default) merges inside each step")
+    ap.add_argument("--nvls", action="store_true",
+                    help="hierarchical h1 through the NVSwitch (cs_set_multicast): tolerance parity for groups "
+                         ">= 3 GPUs (switch summation order), bitwise for groups of 2; members bitwise equal")
+    ap.add_argument("--mc-bank", action="store_true",
+                    help="with --nvls: the gradient bank lives in multicast memory (reduced in place)")
     ap.add_argument("--stream-sync", action="store_true",
                     help="read params after a plain stream synchronize (no cs_sync / cs_flush): the step's "
                          "enqueued work alone must leave merged params (in-step schedule)")
@@ -76,14 +81,26 @@ def main():
     m = torch.zeros(n_loc, ld, device=dev)
     w = torch.ones(n_loc, k, device=dev)
     B = world + 1
-    bank = torch.zeros(B + n_loc, ld, device=dev)
-    cs.cs_bind(m, d, ld, rank, ws, stream)
+    gs_h = world // groups
+    if a.nvls and a.mc_bank:  # symmetric memory over the hierarchical group (plumbing only)
+        cs.cs_bind(m, d, ld, rank, ws, stream)
+        bank, bank_mc = cs.multicast_empty((B + n_loc, ld), gs_h, dev)
+        bank.zero_()
+    else:
+        bank = torch.zeros(B + n_loc, ld, device=dev)
+        cs.cs_bind(m, d, ld, rank, ws, stream)
     cs.cs_synth_fill(x, n_loc, d, ld, seed, synth.TAG_INIT, first, 1.0)
     cs.cs_synth_fill(bank, B, d, ld, seed, synth.TAG_GRAD, 0, float(synth.GRAD_SCALE))
     torch.cuda.synchronize()
     bank[B:] = bank[:n_loc]
     torch.cuda.synchronize()
     cs.setup_peers()
+    if a.nvls:
+        if not cs.setup_multicast(gs_h, dev):
+            print("no multicast on this fabric: FAIL", flush=True)
+            sys.exit(1)
+        if a.mc_bank:
+            cs.register_multicast_grads(bank, bank_mc)
 
     cols = np.arange(d) if a.compare_all else synth.sample_columns(d, T.segment_bounds(d, k))
     orc = OracleRun(world, d, k, seed, cols=cols, groups=a.hier_groups or None)
@@ -187,6 +204,7 @@ def main():
         # hierarchical: momentum is defined at leaders only (members hold a replica)
         gs = world // groups
         m_ok = np.array_equal(ms, orc.m[rows]) if (not a.hier_groups or first % gs == 0) else True
+        lead = (first // gs) * gs
         if a.hier_groups and first % gs != 0:
             lead = (first // gs) * gs
             m_ok = np.array_equal(ms, orc.m[lead:lead + 1])  # the replica equals its leader's
@@ -195,8 +213,22 @@ def main():
             # hierarchical members hold their leader's momentum (reading B-4)
             mref = orc.m[lead:lead + 1] if (a.hier_groups and first % gs != 0) else orc.m[rows]
             m_ok = np.all(np.abs(ms - mref) <= 1e-6 * np.abs(mref).max(axis=1, keepdims=True))
+        elif a.nvls and gs > 2:  # the switch's summation order (hierarchical tolerance)
+            ref, refm = orc.x[rows], orc.m[lead:lead + 1] if first % gs != 0 else orc.m[rows]
+            xs_ok = bool(np.all(np.linalg.norm((xs - ref).astype(np.float64), axis=1)
+                                <= 1e-6 * np.linalg.norm(ref.astype(np.float64), axis=1))
+                         and np.abs(xs - ref).max() <= 1e-6 * np.abs(ref).max())
+            m_ok = bool(np.abs(ms - refm).max() <= 1e-6 * np.abs(refm).max())
         else:
             xs_ok = np.array_equal(xs, orc.x[rows])
+        if a.hier_groups:  # members hold bit-identical replicas of their leader (P12)
+            xt = torch.from_numpy(np.ascontiguousarray(xs)).to(dev)
+            allx = [torch.empty_like(xt) for _ in range(ws)]
+            dist.all_gather(allx, xt)
+            lead_r = (first // gs) * gs // n_loc
+            if not torch.equal(allx[lead_r], xt):
+                print(f"rank {rank} step {t}: member differs from its leader", flush=True)
+                ok = False
         if not (xs_ok and m_ok and np.array_equal(w.cpu().numpy(), orc.w[rows])):
             bad = np.argwhere(xs != orc.x[rows])
             print(f"rank {rank} step {t}: mismatch at {bad[:5].tolist()} of {bad.shape[0]}", flush=True)

@@ -237,3 +237,27 @@ def test_four_gpu_diagnostics(n_loc, groups):
 @pytest.mark.parametrize("n_loc,d,k", [(1, 25_557_032, 8), (8, 1_000_000, 16)])
 def test_four_gpu_parity(n_loc, d, k):
     _run(4, "--workers-per-gpu", n_loc, "--vector-len", d, "--segments", k, "--num-steps", 6)
+
+
+# ---- NVLS h1: the intra-group gradient average in the NVSwitch (cs_set_multicast) ----------
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("groups,d,k,mc_bank", [(1, 100_003, 3, False), (1, 100_003, 3, True),
+                                                (2, 50_001, 4, True)])
+def test_two_gpu_hierarchical_nvls(groups, d, k, mc_bank):
+    # groups of 2 GPUs sum two values: order-free, so bitwise vs the oracle
+    _run(2, "--workers-per-gpu", 1, "--vector-len", d, "--segments", k, "--num-steps", 5,
+         "--hier-groups", groups, "--compare-all", "--nvls", *(["--mc-bank"] if mc_bank else []))
+
+
+@pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
+@pytest.mark.parametrize("groups,d,k,steps,mc_bank,full", [(1, 300_001, 5, 5, True, True),
+                                                          (1, 1_000_003, 8, 100, False, False),
+                                                          (2, 1_000_003, 16, 6, True, True),
+                                                          (1, 25_557_032, 16, 3, True, False)])
+def test_four_gpu_hierarchical_nvls(groups, d, k, steps, mc_bank, full):
+    # groups of 4: the switch's summation order -> norm-wise <= 1e-6 vs the oracle (the
+    # hierarchical tolerance; 100 steps: the north_star criterion); groups of 2
+    # (configs[3] layout at 4 GPUs) bitwise; members bit-identical to their leader always
+    _run(4, "--workers-per-gpu", 1, "--vector-len", d, "--segments", k, "--num-steps", steps,
+         "--hier-groups", groups, "--nvls", *(["--mc-bank"] if mc_bank else []),
+         *(["--compare-all"] if full else []))
