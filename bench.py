@@ -326,11 +326,10 @@ def main():
                     help="multi-GPU step schedule (cs_set_schedule): instep = merged params when the step's "
                          "work completes (default); deferred = the merge runs inside the next step (opt-in, "
                          "params readable only after cs_flush); split = push kernel + merge kernel")
-    ap.add_argument("--h1", default="auto", choices=["auto", "nvls", "nvls-staged", "p2p"],
-                    help="multi-GPU hierarchical gradient average: nvls = in-switch reduction (cs_set_multicast) "
-                         "with the gradients in multicast memory; nvls-staged = the same with the gradients copied "
-                         "into the workspace each step; p2p = reduce-scatter + all-gather over peer stores; "
-                         "auto = nvls when the fabric has multicast")
+    ap.add_argument("--h1", default="p2p", choices=["nvls", "p2p"],
+                    help="multi-GPU hierarchical gradient average: p2p = reduce-scatter + all-gather over peer "
+                         "stores (default, bitwise); nvls = in-switch reduction (cs_set_multicast), the gradient "
+                         "copied into the multicast workspace each step (measured slower for fp32, DESIGN §8)")
     ap.add_argument("--path", default="auto", choices=["auto", "reg", "tma", "peer"],
                     help="library kernel path (cs_set_path); peer with 1 GPU = single-GPU emulation")
     args = ap.parse_args()
@@ -398,13 +397,9 @@ def main():
         w = torch.ones(n_loc, k, device=dev)
     cs.cs_bind(m, d, d, rank, world_size, stream)
     gs_h = world // groups
-    want_nvls = hier and world_size > 1 and gs_h > 1 and args.h1 != "p2p"
-    bank_mc = 0
-    if want_nvls and args.h1 in ("auto", "nvls"):  # the gradient bank in multicast memory (plumbing)
-        bank, bank_mc = cs.multicast_empty((B + n_loc, d), gs_h, dev)
-    else:
-        with torch.cuda.stream(stream):
-            bank = torch.empty(B + n_loc, d, device=dev)
+    want_nvls = hier and world_size > 1 and gs_h > 1 and args.h1 == "nvls"
+    with torch.cuda.stream(stream):
+        bank = torch.empty(B + n_loc, d, device=dev)
     if lars is not None:
         sizes, block = synth.resnet50_layers()
         if d != sum(sizes):
@@ -420,13 +415,10 @@ def main():
     h1 = "p2p" if hier and world_size > 1 and gs_h > 1 else None
     if world_size > 1:
         cs.setup_peers()
-        if want_nvls and cs.setup_multicast(gs_h, dev):
-            h1 = "nvls (in-switch reduce, gradients copied into the workspace)"
-            if bank_mc:
-                cs.register_multicast_grads(bank, bank_mc)
-                h1 = "nvls (in-switch reduce, gradients in multicast memory)"
-        elif args.h1 in ("nvls", "nvls-staged") and want_nvls:
-            raise SystemExit("--h1 nvls: this fabric gives no multicast")
+        if want_nvls:
+            if not cs.setup_multicast(gs_h, dev):
+                raise SystemExit("--h1 nvls: this fabric gives no multicast")
+            h1 = "nvls (in-switch reduce, gradient copied into the multicast workspace)"
 
     def grads(t):
         o = (t + first) % B

@@ -200,7 +200,9 @@ int cs_ipc_import(const char* all_handles /* nprocs * CS_IPC_HANDLE_BYTES */);
  *                       zeroed here).  NULL uc_base returns to the point-to-point h1.
  *   cs_add_multicast_grads  registers a caller buffer holding gradients that is bound to the
  *                       same group's multicast object: a `grads` row inside it is reduced in
- *                       place; any other `grads` is first copied into the workspace.
+ *                       place, which requires every member to pass `grads` at the same offset
+ *                       of its buffer (a training loop's flat gradient buffer); any other
+ *                       `grads` is first copied into the workspace.
  * Numerics: the switch sums the members' fp32 values in its own order, so for groups of
  * >= 3 GPUs params match the oracle within the hierarchical tolerance (SURVEY 8(c):
  * norm-wise <= 1e-6) rather than bitwise; groups of 2 stay bitwise.  Members still hold

@@ -80,6 +80,10 @@ struct Ctx {
   TileDesc* d_tiles = nullptr;
   int n_tiles = 0;
   int tma_grid_plain = 0, tma_grid_diag = 0;
+  // k_gossip_tma claims tiles dynamically (CS_TMA_DYNAMIC=0: static round robin); the
+  // launch sequence number picks the claim counter (two, alternating by launch)
+  bool tma_dynamic = true;
+  unsigned claim_seq = 0;
   bool has_override = false;
 
   float* d_stage = nullptr;   // cs_gossip_step_host staging buffer
@@ -226,6 +230,15 @@ int upload_exponential() {
   return CS_OK;
 }
 
+// Dynamic tile claims of the next k_gossip_tma launch (consecutive launches on the bound
+// stream alternate between two counters; each launch's last CTA zeroes the other one).
+void tma_claims(LocalArgs& a) {
+  if (!g.tma_dynamic) return;
+  const unsigned q = g.claim_seq++ & 1u;
+  a.claim = g.d_counter + 1 + q;
+  a.claim_next = g.d_counter + 1 + (q ^ 1u);
+}
+
 // Bulk-TMA tiles: every (segment, layer) intersection in column order, cut into pieces
 // of at most T columns, so each tile lies in one segment and one layer and the tiles of
 // a layer are a contiguous range.  Without a layer table the whole vector is layer 0.
@@ -233,7 +246,12 @@ int build_tma_tiles() {
   const std::vector<int64_t>& b = g.plan;
   std::vector<int64_t> lb = g.layer_bounds.empty() ? std::vector<int64_t>{0, g.d} : g.layer_bounds;
   const int L = (int)lb.size() - 1;
-  const int T = tma_tile_len(g.d, g.tma_grid_plain);
+  // static schedule: a tile length giving a whole number of waves; dynamic claims: full
+  // tiles, then small ones over the last columns so the final claims are short
+  const int T = g.tma_dynamic ? kTmaTileMax : tma_tile_len(g.d, g.tma_grid_plain);
+  const int T_tail = 512;
+  const int64_t tail_start =
+      g.tma_dynamic ? std::max<int64_t>(0, (g.d - (int64_t)2 * g.tma_grid_plain * T_tail) / 32 * 32) : g.d;
   std::vector<TileDesc> tiles;
   std::vector<int32_t> first(L + 1, 0);
   int l = 0;
@@ -241,7 +259,7 @@ int build_tma_tiles() {
     int64_t c = b[s];
     while (c < b[s + 1]) {
       while (lb[l + 1] <= c) first[++l] = (int32_t)tiles.size();
-      const int64_t end = std::min(std::min(b[s + 1], lb[l + 1]), c + T);
+      const int64_t end = std::min(std::min(b[s + 1], lb[l + 1]), c + (c >= tail_start ? T_tail : T));
       TileDesc td;
       td.c0 = c;
       td.seg = s;
@@ -357,6 +375,8 @@ LocalArgs local_args(float* params, const float* grads, float* psw, int n, int g
   a.layer_bounds = nullptr;
   a.xnorm_out = nullptr;
   a.skip_psw = 0;
+  a.claim = nullptr;
+  a.claim_next = nullptr;
   return a;
 }
 
@@ -454,6 +474,7 @@ int enqueue_flat_step(float* params, const float* grads, float* psw, float lr, f
     } else {
       g.xnorm_valid = false;
     }
+    tma_claims(a);
     CS_CUDA(launch_gossip_tma(a, diag, diag ? g.tma_grid_diag : g.tma_grid_plain, g.stream));
     if (ev[1]) CS_CUDA(cudaEventRecord(ev[1], g.stream));
     g.launches_per_step = g.lars ? 3 : 1;
@@ -604,8 +625,10 @@ int cs_bind(float* momentum, int64_t d, int64_t ld, int proc_rank, int nprocs, v
   CS_CUDA(cudaMemset(g.d_err, 0, sizeof(int) * kNumErr));
   CS_CUDA(cudaMalloc(&g.d_diag, sizeof(double) * 2));
   CS_CUDA(cudaMalloc(&g.d_partials, sizeof(double) * 2 * (size_t)local_max_grid()));
-  CS_CUDA(cudaMalloc(&g.d_counter, sizeof(unsigned)));
-  CS_CUDA(cudaMemset(g.d_counter, 0, sizeof(unsigned)));
+  CS_CUDA(cudaMalloc(&g.d_counter, 4 * sizeof(unsigned)));  // arrival counter, 2 tile-claim counters
+  CS_CUDA(cudaMemset(g.d_counter, 0, 4 * sizeof(unsigned)));
+  g.claim_seq = 0;
+  g.tma_dynamic = !(getenv("CS_TMA_DYNAMIC") && getenv("CS_TMA_DYNAMIC")[0] == '0');
   if (g.vranks > 1 && (nprocs != 1 || g.world % g.vranks != 0))
     return fail(CS_EINVAL, "emulated ranks need nprocs == 1 and vranks dividing world");
   g.use_peer = nprocs > 1 || g.path == CS_PATH_PEER || g.vranks > 1;
@@ -899,6 +922,7 @@ int cs_gossip_step_io(float* params, const float* grads_host, float* psw, float 
     a.tiles = g.d_tiles + t_lo;  // this piece's tiles; the last piece also mixes psw
     a.n_tiles = t_hi - t_lo;
     a.skip_psw = t_hi < nt ? 1 : 0;
+    tma_claims(a);
     CS_CUDA(launch_gossip_tma(a, false, g.tma_grid_plain, g.stream));
     CS_CUDA(cudaEventRecord(g.io_ev[P + q], g.stream));
     CS_CUDA(cudaStreamWaitEvent(g.io_d2h, g.io_ev[P + q], 0));

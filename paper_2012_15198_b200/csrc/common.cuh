@@ -83,6 +83,10 @@ struct LocalArgs {
   // k_gossip_tma over a piece of the tiles (cs_gossip_step_io): only the step's last piece
   // writes the mixed push-sum weights
   int skip_psw;
+  // k_gossip_tma dynamic tile claims (nullptr: static round robin): this launch's counter,
+  // 0 at launch; the launch's last CTA zeroes claim_next, the next launch's counter
+  unsigned* claim;
+  unsigned* claim_next;
 };
 
 // bf16 wire format (reading C-20): round to the nearest bf16 (ties to even), widen back.

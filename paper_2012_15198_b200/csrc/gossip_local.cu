@@ -280,7 +280,10 @@ __device__ void finish_step(const LocalArgs& a, const SmemTopo& t, double dacc, 
       a.diag_out[1] = za;
     }
   }
-  if (threadIdx.x == 0) *a.counter = 0u;
+  if (threadIdx.x == 0) {
+    if (a.claim_next) *a.claim_next = 0u;  // the next launch's tile counter
+    *a.counter = 0u;
+  }
 }
 
 }  // namespace
@@ -505,7 +508,7 @@ using ptx::smem_addr;
 
 
 __host__ __device__ inline size_t tma_smem_bytes(int n, int k, bool diag) {
-  return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t) + kStages * sizeof(float) +
+  return kStages * kStageBytes + 2 * kStages * sizeof(uint64_t) + kStages * (sizeof(float) + sizeof(int)) +
          sizeof(double) * (kTmaConsumers / 32) * (size_t)n +  // LARS: per-warp x'^2 sums per row
          fused_smem_bytes(n, k, kTmaThreads / 32, diag);
 }
@@ -522,7 +525,8 @@ __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
   float* srate = reinterpret_cast<float*>(empty + kStages);  // [kStages]
-  double* wpart = reinterpret_cast<double*>(srate + kStages);  // [n][8] (LARS carry)
+  int* stile = reinterpret_cast<int*>(srate + kStages);       // [kStages] tile of a slot's first row; -1 ends
+  double* wpart = reinterpret_cast<double*>(stile + kStages);  // [n][8] (LARS carry)
   SmemTopo t = carve(reinterpret_cast<unsigned char*>(wpart + (kTmaConsumers / 32) * a.n), a.n, a.k, DIAG);
 
   const int n = a.n;
@@ -540,8 +544,19 @@ __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
   double dacc = 0.0, zacc = 0.0;
   if (warp == kTmaConsumers / 32) {
     // ---------------- producer warp -------------------------------------------
+    // tiles: claimed one at a time from the launch's counter (dynamic: CTAs that stream
+    // faster take more; the table ends in small tiles so the last claims are short), or
+    // round robin.  The tile index travels with the slot of its first row; -1 ends.
     uint32_t it = 0;
-    for (int u = blockIdx.x; u < a.n_tiles; u += gridDim.x) {
+    auto next_tile = [&](int prev) {
+      int u = prev < 0 ? (int)blockIdx.x : prev + (int)gridDim.x;
+      if (a.claim) {
+        if (lane == 0) u = (int)atomicAdd(a.claim, 1u);
+        u = __shfl_sync(0xffffffffu, u, 0);
+      }
+      return u;
+    };
+    for (int u = next_tile(-1); u < a.n_tiles; u = next_tile(u)) {
       const TileDesc td = a.tiles[u];
       const uint32_t bytes = (uint32_t)(((td.len + 3) & ~3) * sizeof(float));
       const uint32_t* ord = t.ord + td.seg * n;
@@ -552,6 +567,7 @@ __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
           const int64_t off = (int64_t)(ord[p] & kOrdIdx) * ld + td.c0;
           float* buf = stage_buf + (size_t)st * 3 * kTmaTileMax;
           if (LARS) srate[st] = a.lrs[(int64_t)(ord[p] & kOrdIdx) * a.n_layers + td.layer];
+          if (p == 0) stile[st] = u;
           mbar_arrive_expect_tx(&full[st], 3 * bytes);
           bulk_g2s(buf, a.x + off, bytes, &full[st]);
           bulk_g2s(buf + kTmaTileMax, a.m + off, bytes, &full[st]);
@@ -560,12 +576,21 @@ __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
         __syncwarp();
       }
     }
+    if (lane == 0) {  // end marker
+      const int st = (int)(it % kStages);
+      mbar_wait(&empty[st], ((it / kStages) & 1u) ^ 1u);
+      stile[st] = -1;
+      mbar_arrive(&full[st]);
+    }
   } else {
     // ---------------- consumer warps ------------------------------------------
     const float mu = a.mu, lr = a.lr;
     bool bad = false;
     uint32_t it = 0;
-    for (int u = blockIdx.x; u < a.n_tiles; u += gridDim.x) {
+    for (;;) {
+      mbar_wait(&full[it % kStages], (it / kStages) & 1u);  // the tile's first row (or the end)
+      const int u = stile[it % kStages];
+      if (u < 0) break;
       const TileDesc td = a.tiles[u];
       const uint32_t* ord = t.ord + td.seg * n;
       const double* rw = DIAG ? t.rw + td.seg * n : nullptr;
@@ -579,7 +604,7 @@ __global__ void __launch_bounds__(kTmaThreads) k_gossip_tma(const LocalArgs a) {
       uint32_t prev_row = 0;
       for (int p = 0; p < n; ++p, ++it) {
         const int st = (int)(it % kStages);
-        mbar_wait(&full[st], (it / kStages) & 1u);
+        if (p > 0) mbar_wait(&full[st], (it / kStages) & 1u);
         const float* buf = stage_buf + (size_t)st * 3 * kTmaTileMax;
         const uint32_t e = ord[p];
         const uint32_t row = e & kOrdIdx;

@@ -184,6 +184,15 @@ __device__ __forceinline__ void st4(float* p, float4 v, int valid) {
     if (valid > 2) p[2] = v.z;
   }
 }
+// plain (generic, default-policy) load of the first `valid` floats
+__device__ __forceinline__ float4 ld4_plain(const float* p, int valid) {
+  if (valid >= 4) return *reinterpret_cast<const float4*>(p);
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (valid > 0) v.x = p[0];
+  if (valid > 1) v.y = p[1];
+  if (valid > 2) v.z = p[2];
+  return v;
+}
 __device__ __forceinline__ void st4_cs(float* p, float4 v, int valid) {
   if (valid == 4) {
     __stcs(reinterpret_cast<float4*>(p), v);
@@ -276,12 +285,10 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
   __shared__ uint32_t ck_upd[kNY][kUpd / 32][2];  // per update warp: checksums of its pushed words
   __shared__ uint32_t w_upd[kNY];                 // push-sum weight bits sent with the tile (0: none)
   __shared__ int32_t dst_upd[kNY];                // receiving worker of a head's tile (-1: not a head)
-  __shared__ uint32_t tail_upd[kNY];              // 1: the slot's y is a chain tail's (copied to params)
   __shared__ uint4 meta[kNI];                     // trailer of the staged received tile (bulk-loaded)
   __shared__ uint4 meta_re;                       // trailer re-read by the mix after a failed check
   __shared__ uint32_t ck_mix[2][kMix / 32][2];    // per mix warp, double-buffered by round parity
   __shared__ uint32_t y_stored;  // update-warp arrivals: position j is done at >= 8 (j + 1)
-  __shared__ uint32_t tail_done; // chain tails whose y the store warp's bulk copy has put in params
   __shared__ int s_end;          // number of positions this CTA processes; INT_MAX until known
   __shared__ int s_timeout;
   volatile int* timeout = &s_timeout;
@@ -311,7 +318,6 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     s_timeout = 0;
     s_end = 0x7fffffff;
     y_stored = 0;
-    tail_done = 0;
     for (int i = 0; i < kNA; ++i) {
       ptx::mbar_init(&a_full[i], 1);
       ptx::mbar_init(&a_empty[i], kUpd / 32);
@@ -448,7 +454,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       const uint32_t e_w = ord[U.seg * n_loc + w.p];
       const uint32_t row = e_w & kWIdx;
       const bool head = (e_w & kWHead) != 0, tail = (e_w & kWTail) != 0;
-      const bool copy = head || tail;  // the store warp has work for this position
+      const bool copy = head;  // the store warp has work for this position (a push)
       const int sy = c % kNY;
       if (copy) ptx::mbar_wait(&y_free[sy], (uint32_t)(((c / kNY) & 1) ^ 1));
       const float* bx = ringA + (size_t)st * 3 * kT;
@@ -480,17 +486,10 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
           else st4_cs(X + (int64_t)prev_row * s.ld + j, mean4(yprev[q], wire ? bf16r4(y) : y), vv);
           if ((e_w & kWEnd) && !tail)
             st4_cs(X + rowoff + j, mean4(y, wire ? bf16r4(yfirst[q]) : yfirst[q]), vv);
-          if (tail) {
-            // a chain tail's y reaches params by the store warp's bulk copy (so the inbox warp's
-            // bulk read sees it once that copy completed); a last partial float4 of the row
-            // (never copied in bulk: the caller's padding columns) by a store made visible to
-            // the whole GPU before this position is released
-            yt[v] = y;
-            if (vv < 4) {
-              st4(X + rowoff + j, y, vv);
-              __threadfence();
-            }
-          }
+          // a chain tail's y waits in params (default policy: L2) for the mix warps, which
+          // read it back with plain loads after this position's CTA-scope release (generic
+          // proxy on both sides: no async-proxy read of generic writes)
+          if (tail) st4(X + rowoff + j, y, vv);
           yprev[q] = y;
           if (head) {
             if (wire) {  // what the receiver gets (C-20)
@@ -523,10 +522,9 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       }
       if (tid == 0) {
         // a head's tile goes to its receiver with the segment's weight on the first tile
-        if (copy) {  // this position's slot (a position without copies has none)
-          dst_upd[sy] = head ? hdst[U.seg * n_loc + row] : -1;
-          tail_upd[sy] = tail ? 1u : 0u;
-          w_upd[sy] = (head && U.first) ? __float_as_uint(wsnap[row]) : 0u;
+        if (copy) {  // this position's slot (a position without a push has none)
+          dst_upd[sy] = hdst[U.seg * n_loc + row];
+          w_upd[sy] = U.first ? __float_as_uint(wsnap[row]) : 0u;
         }
         if (U.first && w.p == n_loc - 1)  // psw of the rows with a local source
           for (int p = 0; p < n_loc; ++p) {
@@ -571,7 +569,6 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       ptx::mbar_wait(&i_full[si], (uint32_t)((q / kNI) & 1));
       ++q;
       const float* it = ringI + (size_t)si * 2 * kT;
-      const float4* yt = reinterpret_cast<const float4*>(it + kT);
       const uint32_t nw = wire ? (uint32_t)(U.len + 1) / 2 : (uint32_t)U.len;
       const float* inbox_f = reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * n_loc + row) * s.ld;
       const uint16_t* inbox_w =
@@ -666,7 +663,9 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
           const float4 yr = wire ? unpack_bf16x4(make_uint2(raw[qq].x, raw[qq].y))
                                  : make_float4(__uint_as_float(raw[qq].x), __uint_as_float(raw[qq].y),
                                                __uint_as_float(raw[qq].z), __uint_as_float(raw[qq].w));
-          st4_cs(X + (int64_t)row * s.ld + U.c0 + 4 * v, mean4(yt[v], yr), valid < 4 ? valid : 4);  // Alg.1 l.17
+          float* xr = X + (int64_t)row * s.ld + U.c0 + 4 * v;
+          const float4 yo = ld4_plain(xr, valid);  // own y, stored by the update warps
+          st4_cs(xr, mean4(yo, yr), valid < 4 ? valid : 4);  // Alg.1 l.17
         }
       }
       if (U.first && tm == 0) PSW[(int64_t)row * s.k + U.seg] = pair_mean1(PSW[(int64_t)row * s.k + U.seg],
@@ -736,16 +735,13 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
         // stage it once the update is `lag` positions further (the sender's copy has probably
         // completed by then), or at the end; the mix polls if the trailer is still old
         if (a.lag > 0) wait_position(&y_stored, end_pos, j + a.lag);
-        while ((int32_t)(ld_acquire_cta(&tail_done) - (uint32_t)(q + 1)) < 0) {
-        }  // this tail's own y is in params (its bulk copy completed)
         const int si = q % kNI;
         ptx::mbar_wait(&i_empty[si], (uint32_t)(((q / kNI) & 1) ^ 1));
         ++q;
-        ptx::fence_proxy_async_global();  // a partial float4's generic store -> this bulk copy
         float* buf = ringI + (size_t)si * 2 * kT;
         const uint32_t yb = (uint32_t)(((U.len + 3) & ~3) * 4);
         const uint32_t ib = wire ? (uint32_t)(((U.len + 7) & ~7) * 2) : yb;
-        ptx::mbar_arrive_expect_tx(&i_full[si], ib + yb + 16u);
+        ptx::mbar_arrive_expect_tx(&i_full[si], ib + 16u);
         ptx::bulk_g2s(&meta[si], trl_in + (size_t)w.t * n_loc + row, 16u, &i_full[si]);
         if (wire)
           ptx::bulk_g2s(buf, reinterpret_cast<const uint16_t*>(mine + a.off_inbox) +
@@ -754,7 +750,6 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
         else
           ptx::bulk_g2s(buf, reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * n_loc + row) * s.ld + U.c0,
                         yb, &i_full[si]);
-        ptx::bulk_g2s(buf + kT, X + (int64_t)row * s.ld + U.c0, yb, &i_full[si]);
       }
     }
     __syncwarp();
@@ -786,7 +781,6 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       const int land = solo ? 1 : 4;  // copies left in flight before their completion is awaited
       uint4* pend_dst[kQ] = {};
       uint4 pend_trl[kQ] = {};
-      bool pend_tail[kQ] = {};
       int pend_head = 0, npend = 0, cur = 0;
       int unfreed = 0, free_next = 0;  // y-out slots whose copies may still read them, oldest first
       auto free_oldest = [&]() {
@@ -798,7 +792,6 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       w.init(n_loc);
       auto complete_oldest = [&]() {  // Alg.1 l.14: that position's copies have completed
         if (pend_dst[pend_head]) st_volatile4(pend_dst[pend_head], pend_trl[pend_head]);
-        if (pend_tail[pend_head]) red_add_release_cta(&tail_done, 1u);
         pend_head = (pend_head + 1) % kQ;
         --npend;
       };
@@ -814,15 +807,13 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
         ptx::mbar_wait(&y_full[sy], ph);
         const int dg = dst_upd[sy];
         if (dg == -2) break;  // end marker
-        const bool tl = tail_upd[sy] != 0;
         MTile U;
         do {  // this slot's position: the next one with copies
           w.next(claims, a.chunk_t0, n_loc);
           U = mtile(a, bnd, t0, w.t, cur);
-        } while (!(ord[U.seg * n_loc + w.p] & (kWHead | kWTail)));
+        } while (!(ord[U.seg * n_loc + w.p] & kWHead));
         const int q = (pend_head + npend) % kQ;
         pend_dst[q] = nullptr;
-        pend_tail[q] = tl;
         if (dg >= 0) {  // a head: its y tile to the receiver's inbox row over NVLink (a4)
           const int rp = dg / n_loc, rl = dg - rp * n_loc;
           if (wire)
@@ -843,11 +834,6 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
           pend_dst[q] = reinterpret_cast<uint4*>(a.peers[rp] + a.off_trl) + (size_t)par * a.trl_cap +
                         (size_t)w.t * n_loc + rl;
           pend_trl[q] = make_uint4(e, Xc ^ wb, Sc, wb);
-        }
-        if (tl) {  // a tail: its own y into params, whole float4s (the partial one is generic)
-          const uint32_t row = ord[U.seg * n_loc + w.p] & kWIdx;
-          const uint32_t full4 = (uint32_t)(U.len & ~3) * 4u;
-          if (full4 > 0) ptx::bulk_s2g(X + (int64_t)row * s.ld + U.c0, ringY + (size_t)sy * kT, full4);
         }
         ptx::bulk_commit();
         ++npend;

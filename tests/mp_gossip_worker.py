@@ -82,13 +82,13 @@ def main():
     w = torch.ones(n_loc, k, device=dev)
     B = world + 1
     gs_h = world // groups
-    if a.nvls and a.mc_bank:  # symmetric memory over the hierarchical group (plumbing only)
-        cs.cs_bind(m, d, ld, rank, ws, stream)
-        bank, bank_mc = cs.multicast_empty((B + n_loc, ld), gs_h, dev)
-        bank.zero_()
-    else:
-        bank = torch.zeros(B + n_loc, ld, device=dev)
-        cs.cs_bind(m, d, ld, rank, ws, stream)
+    bank = torch.zeros(B + n_loc, ld, device=dev)
+    cs.cs_bind(m, d, ld, rank, ws, stream)
+    gcur = None
+    if a.nvls and a.mc_bank:
+        # the caller's gradient buffer in symmetric memory over the group, at the same offset
+        # on every member (as a training loop's flat gradient buffer): reduced in place
+        gcur, gcur_mc = cs.multicast_empty((n_loc, ld), gs_h, dev)
     cs.cs_synth_fill(x, n_loc, d, ld, seed, synth.TAG_INIT, first, 1.0)
     cs.cs_synth_fill(bank, B, d, ld, seed, synth.TAG_GRAD, 0, float(synth.GRAD_SCALE))
     torch.cuda.synchronize()
@@ -100,7 +100,7 @@ def main():
             print("no multicast on this fabric: FAIL", flush=True)
             sys.exit(1)
         if a.mc_bank:
-            cs.register_multicast_grads(bank, bank_mc)
+            cs.register_multicast_grads(gcur, gcur_mc)
 
     cols = np.arange(d) if a.compare_all else synth.sample_columns(d, T.segment_bounds(d, k))
     orc = OracleRun(world, d, k, seed, cols=cols, groups=a.hier_groups or None)
@@ -162,7 +162,11 @@ def main():
         from oracle.diagnostics import consensus
     for t in range(a.num_steps):
         o = (t + first) % B
-        step_fn(x, bank[o:o + n_loc], w, lr, mu)
+        if gcur is not None:
+            gcur.copy_(bank[o:o + n_loc])  # "backward" writes this step's gradient
+            step_fn(x, gcur, w, lr, mu)
+        else:
+            step_fn(x, bank[o:o + n_loc], w, lr, mu)
         if a.lars:  # full rows (--compare-all): LARS needs whole layers
             g_all = synth.grads_at(orc.bank, world, orc.t)
             if a.hier_groups:  # LARS on the group-reduced gradient
