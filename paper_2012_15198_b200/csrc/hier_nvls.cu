@@ -31,6 +31,7 @@
 // never reset (epoch-tagged, modular comparison).
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "peer.cuh"
@@ -82,6 +83,8 @@ struct NvlsArgs {
   uint32_t epoch;        // barrier b of step e completes at gs * e
   uint32_t target[2];    // running totals of CTAs launched against each counter
   int* err;
+  int probe;             // measurement only (CS_NVLS_PROBE): 1 = reduce, plain local store;
+                         // 2 = plain local load, multicast store (results not the method's)
 };
 
 // grid barrier across the group's GPUs: returns false on timeout
@@ -120,6 +123,15 @@ __global__ void __launch_bounds__(kNvlsThreads, 2) k_hier_nvls(const NvlsArgs a)
       const float* gp = a.g_mc + c0;
       float* op = a.gbar_mc + c0;
       int64_t v = tid;
+      if (a.probe) {  // CS_NVLS_PROBE: time one half of the exchange
+        float* lp = a.stage ? a.stage : const_cast<float*>(a.g);
+        for (; v < nv; v += stride) {
+          const float4 s = a.probe == 1 ? mm_ld_reduce4(gp + 4 * v) : *reinterpret_cast<const float4*>(lp + c0 + 4 * v);
+          if (a.probe == 1) *reinterpret_cast<float4*>(lp + c0 + 4 * v) = s;
+          else mm_st4(op + 4 * v, s);
+        }
+        v = nv;
+      }
       for (; v + (kNvlsUnroll - 1) * stride < nv; v += kNvlsUnroll * stride) {
         float4 s[kNvlsUnroll];
 #pragma unroll
@@ -180,6 +192,8 @@ int nvls_h1(PeerState& p, const float* g, const float* g_mc, int member, float i
   a.target[0] = (p.nvls_tot[0] += (uint32_t)grid);
   a.target[1] = (p.nvls_tot[1] += (uint32_t)grid);
   a.err = err;
+  static const int probe = getenv("CS_NVLS_PROBE") ? atoi(getenv("CS_NVLS_PROBE")) : 0;
+  a.probe = probe;
   ++g_peer_launches;
   k_hier_nvls<<<grid, kNvlsThreads, 0, st>>>(a);
   return cudaGetLastError() == cudaSuccess ? 0 : -1;

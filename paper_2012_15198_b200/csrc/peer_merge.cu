@@ -17,19 +17,21 @@
 // all GPUs sweep the vector front to back at the same pace.  Warp roles of a CTA:
 //
 //   x/m/g warp        claims chunks, bulk-loads the x, m, g row-tiles in walk order
-//   update warps (8)  a3 + the walk: m' -> HBM; x' of local pairs -> HBM; a chain tail's y
-//                     -> params (through L2, the mix re-reads it); a head's y into the push
-//                     ring (bf16 on the bf16 wire) with two 32-bit checksums of its words
+//   update warps (8)  a3 + the walk: m' -> HBM; x' of local pairs -> HBM; the y of a chain
+//                     head or tail into a y-out slot (a head's also as bf16 on the bf16 wire,
+//                     with two 32-bit checksums of the pushed words)
 //   store warp        a head's tile: one bulk copy into its receiver's inbox row; once the
 //                     copy has completed (cp.async.bulk.wait_group) a 16-byte trailer
 //                     {epoch, xor ^ w, weighted sum, w} (w: the push-sum weight on a
 //                     segment's first tile) goes to the receiver
-//   inbox warp        for a chain tail: stages the tile's trailer, the received tile and the
-//                     own y tile (Alg.1 l.8 irecv)
+//   inbox warp        for a chain tail: stages the tile's trailer and the received tile
+//                     (Alg.1 l.8 irecv)
 //   mix warps (4)     verify the received words against the trailer's checksums (polling
 //                     the trailer and re-reading the words until they match: Alg.1 l.14
 //                     "wait until ... communication is completed", per tile), then
-//                     a5: x' = fl(fl(y + y_recv) * 0.5) -> params and the tail's psw
+//                     a5: x' = fl(fl(y + y_recv) * 0.5) -> params and the tail's psw, with
+//                     the tail's own y read from its y-out slot (freed by the mix and the
+//                     store warp together)
 //
 // Why trailers and not release/acquire flags: a system-scope fence waits for the SM's
 // in-flight NVLink copies, and under this load each one took ~13 us (measured: the
@@ -40,11 +42,16 @@
 // the fabric delivers writes in (a stale tile would have to match two 32-bit checksums of
 // new data).  Measured: ~1.7 % of tiles are first read before their words are visible.
 //
-// Nothing that produces a tile (claim, update, push) waits for another GPU's progress in the
-// step: only the inbox warp and the mix do, and nothing waits for the mix.  So the merge may
-// trail the update by any distance, and the step has no grid-wide or cross-GPU barrier.
+// No push waits for another GPU: the store warp issues a head's copy as soon as its slot is
+// full.  The update waits for the mix only through the y-out slots (kNY copy positions), and
+// the mix waits only for remote tiles that precede the update's position.  Deadlock freedom:
+// take the smallest tile index m any blocked CTA waits for; its sender CTA has pushed every
+// head before its own position (so its position is <= m) and, if blocked, waits for a tile
+// before that position, below m -- a contradiction; an unclaimed m would put every CTA of the
+// sender GPU before m (chunks are claimed in order).  The step has no grid-wide or cross-GPU
+// barrier.
 // HBM per parameter: 20 B (read x, m, g; write m', x') + for a tail 4 B inbox written by
-// the sender + 4 B inbox read (+ 8 B y write and re-read where L2 does not absorb it);
+// the sender + 4 B inbox read;
 // NVLink 4 B out per head parameter (+16 B per 8 KB tile of trailer).
 //
 // Ping-pong: inbox and trailers are indexed by the epoch parity.  Before writing parity
@@ -175,24 +182,6 @@ struct Walk {
   }
 };
 
-__device__ __forceinline__ void st4(float* p, float4 v, int valid) {
-  if (valid == 4) {
-    *reinterpret_cast<float4*>(p) = v;
-  } else {
-    if (valid > 0) p[0] = v.x;
-    if (valid > 1) p[1] = v.y;
-    if (valid > 2) p[2] = v.z;
-  }
-}
-// plain (generic, default-policy) load of the first `valid` floats
-__device__ __forceinline__ float4 ld4_plain(const float* p, int valid) {
-  if (valid >= 4) return *reinterpret_cast<const float4*>(p);
-  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (valid > 0) v.x = p[0];
-  if (valid > 1) v.y = p[1];
-  if (valid > 2) v.z = p[2];
-  return v;
-}
 __device__ __forceinline__ void st4_cs(float* p, float4 v, int valid) {
   if (valid == 4) {
     __stcs(reinterpret_cast<float4*>(p), v);
@@ -285,6 +274,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
   __shared__ uint32_t ck_upd[kNY][kUpd / 32][2];  // per update warp: checksums of its pushed words
   __shared__ uint32_t w_upd[kNY];                 // push-sum weight bits sent with the tile (0: none)
   __shared__ int32_t dst_upd[kNY];                // receiving worker of a head's tile (-1: not a head)
+  __shared__ uint32_t tail_upd[kNY];              // 1: the slot's y is a chain tail's (the mix frees it too)
   __shared__ uint4 meta[kNI];                     // trailer of the staged received tile (bulk-loaded)
   __shared__ uint4 meta_re;                       // trailer re-read by the mix after a failed check
   __shared__ uint32_t ck_mix[2][kMix / 32][2];    // per mix warp, double-buffered by round parity
@@ -328,7 +318,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     }
     for (int i = 0; i < kNY; ++i) {
       ptx::mbar_init(&y_full[i], kUpd / 32);
-      ptx::mbar_init(&y_free[i], 1);  // the store warp is done with the slot
+      ptx::mbar_init(&y_free[i], 1 + kMix / 32);  // the store warp and the mix warps are done with it
     }
     ptx::mbar_fence_init();
   }
@@ -454,7 +444,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       const uint32_t e_w = ord[U.seg * n_loc + w.p];
       const uint32_t row = e_w & kWIdx;
       const bool head = (e_w & kWHead) != 0, tail = (e_w & kWTail) != 0;
-      const bool copy = head;  // the store warp has work for this position (a push)
+      const bool copy = head || tail;  // the store warp has work for this position
       const int sy = c % kNY;
       if (copy) ptx::mbar_wait(&y_free[sy], (uint32_t)(((c / kNY) & 1) ^ 1));
       const float* bx = ringA + (size_t)st * 3 * kT;
@@ -486,10 +476,9 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
           else st4_cs(X + (int64_t)prev_row * s.ld + j, mean4(yprev[q], wire ? bf16r4(y) : y), vv);
           if ((e_w & kWEnd) && !tail)
             st4_cs(X + rowoff + j, mean4(y, wire ? bf16r4(yfirst[q]) : yfirst[q]), vv);
-          // a chain tail's y waits in params (default policy: L2) for the mix warps, which
-          // read it back with plain loads after this position's CTA-scope release (generic
-          // proxy on both sides: no async-proxy read of generic writes)
-          if (tail) st4(X + rowoff + j, y, vv);
+          // a chain tail's y stays in its slot until the mix warps have merged it with what the
+          // tail receives (no round trip through params)
+          if (tail) yt[v] = y;
           yprev[q] = y;
           if (head) {
             if (wire) {  // what the receiver gets (C-20)
@@ -522,9 +511,10 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       }
       if (tid == 0) {
         // a head's tile goes to its receiver with the segment's weight on the first tile
-        if (copy) {  // this position's slot (a position without a push has none)
-          dst_upd[sy] = hdst[U.seg * n_loc + row];
-          w_upd[sy] = U.first ? __float_as_uint(wsnap[row]) : 0u;
+        if (copy) {  // this position's slot (a position without copies has none)
+          dst_upd[sy] = head ? hdst[U.seg * n_loc + row] : -1;
+          tail_upd[sy] = tail ? 1u : 0u;
+          w_upd[sy] = (head && U.first) ? __float_as_uint(wsnap[row]) : 0u;
         }
         if (U.first && w.p == n_loc - 1)  // psw of the rows with a local source
           for (int p = 0; p < n_loc; ++p) {
@@ -556,6 +546,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     // ---------------- mix warps: a chain tail's verify + a5 -------------------------
     const int tm = threadIdx.x - kUpd, mw = tm >> 5;
     int cur = 0, retried = 0, round = 0, q = 0;  // round: checksum reductions (buffer parity); q: tails
+    int cy = 0;  // positions with y-out slots (chain heads and tails) so far
     Walk w;
     w.init(n_loc);
     for (int j = 0;; ++j) {
@@ -563,12 +554,17 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       w.next(claims, a.chunk_t0, n_loc);
       const MTile U = mtile(a, bnd, t0, w.t, cur);
       const uint32_t e_w = ord[U.seg * n_loc + w.p];
-      if (!(e_w & kWTail)) continue;
+      if (!(e_w & kWTail)) {
+        if (e_w & kWHead) ++cy;
+        continue;
+      }
+      const int sy = cy++ % kNY;  // this tail's own y (update warps, released with y_stored)
       const uint32_t row = e_w & kWIdx;
       const int si = q % kNI;
       ptx::mbar_wait(&i_full[si], (uint32_t)((q / kNI) & 1));
       ++q;
       const float* it = ringI + (size_t)si * 2 * kT;
+      const float4* yt = reinterpret_cast<const float4*>(ringY + (size_t)sy * kT);
       const uint32_t nw = wire ? (uint32_t)(U.len + 1) / 2 : (uint32_t)U.len;
       const float* inbox_f = reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * n_loc + row) * s.ld;
       const uint16_t* inbox_w =
@@ -663,15 +659,16 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
           const float4 yr = wire ? unpack_bf16x4(make_uint2(raw[qq].x, raw[qq].y))
                                  : make_float4(__uint_as_float(raw[qq].x), __uint_as_float(raw[qq].y),
                                                __uint_as_float(raw[qq].z), __uint_as_float(raw[qq].w));
-          float* xr = X + (int64_t)row * s.ld + U.c0 + 4 * v;
-          const float4 yo = ld4_plain(xr, valid);  // own y, stored by the update warps
-          st4_cs(xr, mean4(yo, yr), valid < 4 ? valid : 4);  // Alg.1 l.17
+          st4_cs(X + (int64_t)row * s.ld + U.c0 + 4 * v, mean4(yt[v], yr), valid < 4 ? valid : 4);  // Alg.1 l.17
         }
       }
       if (U.first && tm == 0) PSW[(int64_t)row * s.k + U.seg] = pair_mean1(PSW[(int64_t)row * s.k + U.seg],
                                                                           __uint_as_float(tl.w));
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&i_empty[si]);
+      if (lane == 0) {
+        ptx::mbar_arrive(&i_empty[si]);
+        ptx::mbar_arrive(&y_free[sy]);
+      }
     }
     if (tm == 0 && retried && a.retries) atomicAdd(a.retries, (unsigned)retried);
     if (tr && tm == 0) tr[6] = ptx::globaltimer();
@@ -783,8 +780,9 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       uint4 pend_trl[kQ] = {};
       int pend_head = 0, npend = 0, cur = 0;
       int unfreed = 0, free_next = 0;  // y-out slots whose copies may still read them, oldest first
-      auto free_oldest = [&]() {
-        ptx::mbar_arrive(&y_free[free_next]);
+      auto free_oldest = [&]() {  // (on behalf of the mix too when the slot is not a tail's)
+        const int arrivals = tail_upd[free_next] ? 1 : 1 + kMix / 32;
+        for (int r = 0; r < arrivals; ++r) ptx::mbar_arrive(&y_free[free_next]);
         free_next = (free_next + 1) % kNY;
         --unfreed;
       };
@@ -811,7 +809,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
         do {  // this slot's position: the next one with copies
           w.next(claims, a.chunk_t0, n_loc);
           U = mtile(a, bnd, t0, w.t, cur);
-        } while (!(ord[U.seg * n_loc + w.p] & kWHead));
+        } while (!(ord[U.seg * n_loc + w.p] & (kWHead | kWTail)));
         const int q = (pend_head + npend) % kQ;
         pend_dst[q] = nullptr;
         if (dg >= 0) {  // a head: its y tile to the receiver's inbox row over NVLink (a4)

@@ -242,7 +242,7 @@ def test_four_gpu_parity(n_loc, d, k):
 # ---- NVLS h1: the intra-group gradient average in the NVSwitch (cs_set_multicast) ----------
 @pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("groups,d,k,mc_bank", [(1, 100_003, 3, False), (1, 100_003, 3, True),
-                                                (2, 50_001, 4, True)])
+                                                (1, 4099, 1, False)])
 def test_two_gpu_hierarchical_nvls(groups, d, k, mc_bank):
     # groups of 2 GPUs sum two values: order-free, so bitwise vs the oracle
     _run(2, "--workers-per-gpu", 1, "--vector-len", d, "--segments", k, "--num-steps", 5,
