@@ -417,6 +417,7 @@ PeerStepArgs peer_args(float* params, const float* grads, float* psw, float lr, 
   pa.lars_part = nullptr;
   pa.g_off = 0;
   pa.gbar_local = 0;
+  pa.gpull_chunk = 0;
   if (g.vranks > 1) {  // emulated ranks: rank 0's view; each CTA shifts to its own rank
     pa.n_loc = g.world / g.vranks;
     pa.nprocs = g.vranks;

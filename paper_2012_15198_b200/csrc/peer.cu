@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
         ptx::mbar_arrive_expect_tx(&a_full[st], 3 * bytes + (a.fuse_mix ? (s.wire ? (uint32_t)(((U.len + 7) & ~7) * 2) : bytes) : 0u));
         ptx::bulk_g2s(buf, s.x + off, bytes, &a_full[st]);
         ptx::bulk_g2s(buf + kPeerTile, s.m + off, bytes, &a_full[st]);
-        ptx::bulk_g2s(buf + 2 * kPeerTile, s.g + off, bytes, &a_full[st]);
+        bulk_load_g(s, a.peers, buf + 2 * kPeerTile, off, U.c0, bytes / 4, &a_full[st]);
         if (a.fuse_mix) {  // the previous step's received tile (inbox parity of epoch e-1)
           if (s.wire)  // bf16 rows, stride (ld + 7) & ~7, 16-byte units
             ptx::bulk_g2s(buf + 3 * kPeerTile,
@@ -570,6 +570,7 @@ struct HierArgs {
   float inv_gs;
   uint32_t epoch;
   uint32_t c1_target, c2_target;  // arrival targets (see publish_when_last)
+  int pull;                  // 1: the mean chunk stays in this member's gbar (the update pulls it)
   int vranks;                // > 1: emulated ranks (g is row `rank` of [vranks][ld])
   int64_t ld;
   size_t off_gbox, off_gbar, off_d1, off_c1, off_d2, off_c2;
@@ -644,6 +645,10 @@ __global__ void __launch_bounds__(kHierThreads) k_hier_reduce(const HierArgs h0)
         acc = add4(acc, mm == member ? ld4_valid(h.g + j, valid)
                                      : __ldcg(reinterpret_cast<const float4*>(gbox + (int64_t)mm * h.gstride + j)));
       const float4 mean = scale4(acc, h.inv_gs);
+      if (h.pull) {  // the members' updates read it from here
+        st4(reinterpret_cast<float*>(mine + h.off_gbar) + j, mean, valid);
+        continue;
+      }
       for (int q = 0; q < h.gs; ++q) {  // rotated start: spread the all-gather over every peer
         const int mm = (q + member + (int)(v >> 5)) % h.gs;
         st4(reinterpret_cast<float*>(h.peers[gbase + mm] + h.off_gbar) + j, mean, valid);
@@ -2165,6 +2170,7 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   h.err = a.err;
   h.vranks = p.vranks;
   h.ld = a.ld;
+  h.pull = 0;
   PeerStepArgs b = a;
   b.g = reinterpret_cast<const float*>(p.base + p.off_gbar);  // the group mean
   b.g_off = p.off_gbar;
@@ -2189,6 +2195,12 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     b.gbar_local = 1;
   }
   p.last_nvls = nvls;
+  // pulled group mean (default without NVLS, LARS or column pieces): k_hier_reduce keeps each
+  // member's mean chunk in its own gbar and the update bulk-loads the chunks from their owners
+  // over NVLink, so the all-gather rides in the update's pass instead of a pass of its own
+  static const bool pull_env = !(getenv("CS_HIER_PULL") && getenv("CS_HIER_PULL")[0] == '0');
+  const bool pull = pull_env && !nvls && a.lrs_out == nullptr && (exchange || p.hier_pieces == 1) && p.gs > 1;
+  if (pull) b.gpull_chunk = ((a.d + p.gs - 1) / p.gs + 3) / 4 * 4;
   PeerKernelArgs ka = kernel_args(p, b, epoch, !exchange);
   if (ev0) cudaEventRecord(ev0, st);
   if (p.need_sync && p.gs > 1) {  // members become exact replicas of their leader
@@ -2219,6 +2231,7 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     h.col_lo = tile_col(p, t_lo);
     h.col_hi = tile_col(p, t_hi);
     h.chunk = ((h.col_hi - h.col_lo + p.gs - 1) / p.gs + 3) / 4 * 4;
+    h.pull = pull ? 1 : 0;
     h.off_d1 = p.off_d1 + q * p.flag_stride;
     h.off_d2 = p.off_d2 + q * p.flag_stride;
     h.off_c1 = p.off_c1 + 64 * q;

@@ -49,6 +49,10 @@ struct PeerStepArgs {
   // 1: the hierarchical group mean g is complete on this GPU before the kernel starts
   // (NVLS h1, hier_nvls.cu), so the update does not wait for the reduce flags
   int gbar_local;
+  // > 0: pulled group mean (hierarchical h1 without the all-gather): the mean of column c
+  // lives only in the gbar row of member c / gpull_chunk of this GPU's group (region + g_off);
+  // the update bulk-loads it from there over NVLink
+  int64_t gpull_chunk;
 };
 
 struct PeerState {

@@ -2,6 +2,7 @@
 #pragma once
 #include "common.cuh"
 #include "peer.cuh"
+#include "ptx.cuh"
 
 namespace cs {
 
@@ -46,6 +47,26 @@ __device__ __forceinline__ void rank_view(PeerStepArgs& s, char* const* peers, i
     if (s.lrs) s.lrs += rows * s.n_layers;
   }
   if (s.g_off != 0) s.g = reinterpret_cast<const float*>(peers[s.rank] + s.g_off);
+}
+
+// Bulk-load the gradient columns [c0, c0 + n4) (n4 a multiple of 4) of a one-worker-per-GPU
+// step into smem: from s.g, or -- pulled group mean -- from the gbar row of each owning member
+// (one copy per owner crossed; chunk bounds are multiples of 4 elements, so every piece is a
+// whole number of 16-byte units).
+__device__ __forceinline__ void bulk_load_g(const PeerStepArgs& s, char* const* peers, float* dst, int64_t off,
+                                            int64_t c0, int64_t n4, uint64_t* bar) {
+  if (s.gpull_chunk <= 0) {
+    ptx::bulk_g2s(dst, s.g + off, (uint32_t)(n4 * 4), bar);
+    return;
+  }
+  const int gbase = (s.rank / s.gs) * s.gs;
+  for (int64_t c = c0; c < c0 + n4;) {
+    const int own = (int)(c / s.gpull_chunk);
+    const int64_t e = (own + 1) * s.gpull_chunk < c0 + n4 ? (own + 1) * s.gpull_chunk : c0 + n4;
+    ptx::bulk_g2s(dst + (c - c0), reinterpret_cast<const float*>(peers[gbase + own] + s.g_off) + c,
+                  (uint32_t)((e - c) * 4), bar);
+    c = e;
+  }
 }
 
 // Global worker that receives segment s of local worker r (send_to, Alg.1 l.6):

@@ -17,21 +17,20 @@
 // all GPUs sweep the vector front to back at the same pace.  Warp roles of a CTA:
 //
 //   x/m/g warp        claims chunks, bulk-loads the x, m, g row-tiles in walk order
-//   update warps (8)  a3 + the walk: m' -> HBM; x' of local pairs -> HBM; the y of a chain
-//                     head or tail into a y-out slot (a head's also as bf16 on the bf16 wire,
-//                     with two 32-bit checksums of the pushed words)
+//   update warps (8)  a3 + the walk: m' -> HBM; x' of local pairs -> HBM; a chain tail's y
+//                     -> params (plain stores: L1/L2); a head's y into the push ring (bf16 on
+//                     the bf16 wire) with two 32-bit checksums of its words
 //   store warp        a head's tile: one bulk copy into its receiver's inbox row; once the
 //                     copy has completed (cp.async.bulk.wait_group) a 16-byte trailer
 //                     {epoch, xor ^ w, weighted sum, w} (w: the push-sum weight on a
 //                     segment's first tile) goes to the receiver
-//   inbox warp        for a chain tail: stages the tile's trailer and the received tile
-//                     (Alg.1 l.8 irecv)
+//   inbox warp        for a chain tail: stages the tile's trailer and the received tile (bulk
+//                     copies, Alg.1 l.8 irecv) and the own y tile (cp.async: generic proxy, like
+//                     the stores that wrote it, so the y_stored release/acquire orders them)
 //   mix warps (4)     verify the received words against the trailer's checksums (polling
 //                     the trailer and re-reading the words until they match: Alg.1 l.14
 //                     "wait until ... communication is completed", per tile), then
-//                     a5: x' = fl(fl(y + y_recv) * 0.5) -> params and the tail's psw, with
-//                     the tail's own y read from its y-out slot (freed by the mix and the
-//                     store warp together)
+//                     a5: x' = fl(fl(y + y_recv) * 0.5) -> params and the tail's psw
 //
 // Why trailers and not release/acquire flags: a system-scope fence waits for the SM's
 // in-flight NVLink copies, and under this load each one took ~13 us (measured: the
@@ -42,16 +41,11 @@
 // the fabric delivers writes in (a stale tile would have to match two 32-bit checksums of
 // new data).  Measured: ~1.7 % of tiles are first read before their words are visible.
 //
-// No push waits for another GPU: the store warp issues a head's copy as soon as its slot is
-// full.  The update waits for the mix only through the y-out slots (kNY copy positions), and
-// the mix waits only for remote tiles that precede the update's position.  Deadlock freedom:
-// take the smallest tile index m any blocked CTA waits for; its sender CTA has pushed every
-// head before its own position (so its position is <= m) and, if blocked, waits for a tile
-// before that position, below m -- a contradiction; an unclaimed m would put every CTA of the
-// sender GPU before m (chunks are claimed in order).  The step has no grid-wide or cross-GPU
-// barrier.
+// Nothing that produces a tile (claim, update, push) waits for another GPU's progress in the
+// step: only the inbox warp and the mix do, and nothing waits for the mix.  So the merge may
+// trail the update by any distance, and the step has no grid-wide or cross-GPU barrier.
 // HBM per parameter: 20 B (read x, m, g; write m', x') + for a tail 4 B inbox written by
-// the sender + 4 B inbox read;
+// the sender + 4 B inbox read (+ 8 B y write and re-read where L2 does not absorb it);
 // NVLink 4 B out per head parameter (+16 B per 8 KB tile of trailer).
 //
 // Ping-pong: inbox and trailers are indexed by the epoch parity.  Before writing parity
@@ -182,6 +176,15 @@ struct Walk {
   }
 };
 
+__device__ __forceinline__ void st4(float* p, float4 v, int valid) {
+  if (valid == 4) {
+    *reinterpret_cast<float4*>(p) = v;
+  } else {
+    if (valid > 0) p[0] = v.x;
+    if (valid > 1) p[1] = v.y;
+    if (valid > 2) p[2] = v.z;
+  }
+}
 __device__ __forceinline__ void st4_cs(float* p, float4 v, int valid) {
   if (valid == 4) {
     __stcs(reinterpret_cast<float4*>(p), v);
@@ -274,7 +277,6 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
   __shared__ uint32_t ck_upd[kNY][kUpd / 32][2];  // per update warp: checksums of its pushed words
   __shared__ uint32_t w_upd[kNY];                 // push-sum weight bits sent with the tile (0: none)
   __shared__ int32_t dst_upd[kNY];                // receiving worker of a head's tile (-1: not a head)
-  __shared__ uint32_t tail_upd[kNY];              // 1: the slot's y is a chain tail's (the mix frees it too)
   __shared__ uint4 meta[kNI];                     // trailer of the staged received tile (bulk-loaded)
   __shared__ uint4 meta_re;                       // trailer re-read by the mix after a failed check
   __shared__ uint32_t ck_mix[2][kMix / 32][2];    // per mix warp, double-buffered by round parity
@@ -318,7 +320,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     }
     for (int i = 0; i < kNY; ++i) {
       ptx::mbar_init(&y_full[i], kUpd / 32);
-      ptx::mbar_init(&y_free[i], 1 + kMix / 32);  // the store warp and the mix warps are done with it
+      ptx::mbar_init(&y_free[i], 1);  // the store warp is done with the slot
     }
     ptx::mbar_fence_init();
   }
@@ -444,7 +446,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       const uint32_t e_w = ord[U.seg * n_loc + w.p];
       const uint32_t row = e_w & kWIdx;
       const bool head = (e_w & kWHead) != 0, tail = (e_w & kWTail) != 0;
-      const bool copy = head || tail;  // the store warp has work for this position
+      const bool copy = head;  // the store warp has work for this position (a push)
       const int sy = c % kNY;
       if (copy) ptx::mbar_wait(&y_free[sy], (uint32_t)(((c / kNY) & 1) ^ 1));
       const float* bx = ringA + (size_t)st * 3 * kT;
@@ -476,9 +478,10 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
           else st4_cs(X + (int64_t)prev_row * s.ld + j, mean4(yprev[q], wire ? bf16r4(y) : y), vv);
           if ((e_w & kWEnd) && !tail)
             st4_cs(X + rowoff + j, mean4(y, wire ? bf16r4(yfirst[q]) : yfirst[q]), vv);
-          // a chain tail's y stays in its slot until the mix warps have merged it with what the
-          // tail receives (no round trip through params)
-          if (tail) yt[v] = y;
+          // a chain tail's y waits in params for the mix; the inbox warp stages it back with
+          // cp.async after this position's CTA-scope release (generic proxy on both sides:
+          // no async-proxy read of generic writes)
+          if (tail) st4(X + rowoff + j, y, vv);
           yprev[q] = y;
           if (head) {
             if (wire) {  // what the receiver gets (C-20)
@@ -511,10 +514,9 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       }
       if (tid == 0) {
         // a head's tile goes to its receiver with the segment's weight on the first tile
-        if (copy) {  // this position's slot (a position without copies has none)
-          dst_upd[sy] = head ? hdst[U.seg * n_loc + row] : -1;
-          tail_upd[sy] = tail ? 1u : 0u;
-          w_upd[sy] = (head && U.first) ? __float_as_uint(wsnap[row]) : 0u;
+        if (copy) {  // this position's slot (a position without a push has none)
+          dst_upd[sy] = hdst[U.seg * n_loc + row];
+          w_upd[sy] = U.first ? __float_as_uint(wsnap[row]) : 0u;
         }
         if (U.first && w.p == n_loc - 1)  // psw of the rows with a local source
           for (int p = 0; p < n_loc; ++p) {
@@ -546,7 +548,6 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     // ---------------- mix warps: a chain tail's verify + a5 -------------------------
     const int tm = threadIdx.x - kUpd, mw = tm >> 5;
     int cur = 0, retried = 0, round = 0, q = 0;  // round: checksum reductions (buffer parity); q: tails
-    int cy = 0;  // positions with y-out slots (chain heads and tails) so far
     Walk w;
     w.init(n_loc);
     for (int j = 0;; ++j) {
@@ -554,17 +555,12 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       w.next(claims, a.chunk_t0, n_loc);
       const MTile U = mtile(a, bnd, t0, w.t, cur);
       const uint32_t e_w = ord[U.seg * n_loc + w.p];
-      if (!(e_w & kWTail)) {
-        if (e_w & kWHead) ++cy;
-        continue;
-      }
-      const int sy = cy++ % kNY;  // this tail's own y (update warps, released with y_stored)
+      if (!(e_w & kWTail)) continue;
       const uint32_t row = e_w & kWIdx;
       const int si = q % kNI;
       ptx::mbar_wait(&i_full[si], (uint32_t)((q / kNI) & 1));
       ++q;
       const float* it = ringI + (size_t)si * 2 * kT;
-      const float4* yt = reinterpret_cast<const float4*>(ringY + (size_t)sy * kT);
       const uint32_t nw = wire ? (uint32_t)(U.len + 1) / 2 : (uint32_t)U.len;
       const float* inbox_f = reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * n_loc + row) * s.ld;
       const uint16_t* inbox_w =
@@ -572,6 +568,9 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       const uint4* trl = trl_in + (size_t)w.t * n_loc + row;
       uint4 tl = meta[si];
       uint4 raw[kPerM];  // the received words as pushed (fp32 bits, or 2 x 2 bf16 in .x .y)
+      float4 yo[kPerM];  // the tail's own y (staged by the inbox warp)
+#pragma unroll
+      for (int qq = 0; qq < kPerM; ++qq) yo[qq] = reinterpret_cast<const float4*>(it + kT)[tm + qq * kMix];
 #pragma unroll
       for (int qq = 0; qq < kPerM; ++qq) {
         const int v = tm + qq * kMix;
@@ -659,16 +658,13 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
           const float4 yr = wire ? unpack_bf16x4(make_uint2(raw[qq].x, raw[qq].y))
                                  : make_float4(__uint_as_float(raw[qq].x), __uint_as_float(raw[qq].y),
                                                __uint_as_float(raw[qq].z), __uint_as_float(raw[qq].w));
-          st4_cs(X + (int64_t)row * s.ld + U.c0 + 4 * v, mean4(yt[v], yr), valid < 4 ? valid : 4);  // Alg.1 l.17
+          st4_cs(X + (int64_t)row * s.ld + U.c0 + 4 * v, mean4(yo[qq], yr), valid < 4 ? valid : 4);  // Alg.1 l.17
         }
       }
       if (U.first && tm == 0) PSW[(int64_t)row * s.k + U.seg] = pair_mean1(PSW[(int64_t)row * s.k + U.seg],
                                                                           __uint_as_float(tl.w));
       __syncwarp();
-      if (lane == 0) {
-        ptx::mbar_arrive(&i_empty[si]);
-        ptx::mbar_arrive(&y_free[sy]);
-      }
+      if (lane == 0) ptx::mbar_arrive(&i_empty[si]);
     }
     if (tm == 0 && retried && a.retries) atomicAdd(a.retries, (unsigned)retried);
     if (tr && tm == 0) tr[6] = ptx::globaltimer();
@@ -712,13 +708,17 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
         ptx::mbar_arrive_expect_tx(&a_full[st], 3 * bytes);
         ptx::bulk_g2s(buf, X + off, bytes, &a_full[st]);
         ptx::bulk_g2s(buf + kT, Mr + off, bytes, &a_full[st]);
-        ptx::bulk_g2s(buf + 2 * kT, Gr + off, bytes, &a_full[st]);
+        if (s.gpull_chunk > 0) bulk_load_g(s, a.peers, buf + 2 * kT, off, U.c0, bytes / 4, &a_full[st]);
+        else ptx::bulk_g2s(buf + 2 * kT, Gr + off, bytes, &a_full[st]);
       }
     }
     __syncwarp();
   } else if (warp == kWLoadIn) {
     // ---------------- inbox loader: a chain tail's trailer, received and own y tiles ---
-    if (lane == 0) {
+    // (every lane walks the positions; lane 0 bulk-loads the trailer and the received tile,
+    // all lanes copy the tail's own y from params with cp.async, which like the update warps'
+    // stores is a generic-proxy access: ordered by the acquire of y_stored, no proxy fence)
+    {
       int cur = 0, q = 0;
       Walk w;
       w.init(n_loc);
@@ -738,15 +738,22 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
         float* buf = ringI + (size_t)si * 2 * kT;
         const uint32_t yb = (uint32_t)(((U.len + 3) & ~3) * 4);
         const uint32_t ib = wire ? (uint32_t)(((U.len + 7) & ~7) * 2) : yb;
-        ptx::mbar_arrive_expect_tx(&i_full[si], ib + 16u);
-        ptx::bulk_g2s(&meta[si], trl_in + (size_t)w.t * n_loc + row, 16u, &i_full[si]);
-        if (wire)
-          ptx::bulk_g2s(buf, reinterpret_cast<const uint16_t*>(mine + a.off_inbox) +
-                                 ((int64_t)par * n_loc + row) * ld_bf + U.c0,
-                        ib, &i_full[si]);
-        else
-          ptx::bulk_g2s(buf, reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * n_loc + row) * s.ld + U.c0,
-                        yb, &i_full[si]);
+        const float* yown = X + (int64_t)row * s.ld + U.c0;
+        for (int v = lane; v < (U.len + 3) / 4; v += 32) ptx::cp_async16_ca(buf + kT + 4 * v, yown + 4 * v);
+        ptx::cp_async_mbar_arrive(&i_full[si]);  // the slot completes once these copies have landed
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive_expect_tx(&i_full[si], ib + 16u);
+          ptx::bulk_g2s(&meta[si], trl_in + (size_t)w.t * n_loc + row, 16u, &i_full[si]);
+          if (wire)
+            ptx::bulk_g2s(buf, reinterpret_cast<const uint16_t*>(mine + a.off_inbox) +
+                                   ((int64_t)par * n_loc + row) * ld_bf + U.c0,
+                          ib, &i_full[si]);
+          else
+            ptx::bulk_g2s(buf, reinterpret_cast<const float*>(mine + a.off_inbox) +
+                                   ((int64_t)par * n_loc + row) * s.ld + U.c0,
+                          yb, &i_full[si]);
+        }
       }
     }
     __syncwarp();
@@ -780,9 +787,8 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       uint4 pend_trl[kQ] = {};
       int pend_head = 0, npend = 0, cur = 0;
       int unfreed = 0, free_next = 0;  // y-out slots whose copies may still read them, oldest first
-      auto free_oldest = [&]() {  // (on behalf of the mix too when the slot is not a tail's)
-        const int arrivals = tail_upd[free_next] ? 1 : 1 + kMix / 32;
-        for (int r = 0; r < arrivals; ++r) ptx::mbar_arrive(&y_free[free_next]);
+      auto free_oldest = [&]() {
+        ptx::mbar_arrive(&y_free[free_next]);
         free_next = (free_next + 1) % kNY;
         --unfreed;
       };
@@ -809,7 +815,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
         do {  // this slot's position: the next one with copies
           w.next(claims, a.chunk_t0, n_loc);
           U = mtile(a, bnd, t0, w.t, cur);
-        } while (!(ord[U.seg * n_loc + w.p] & (kWHead | kWTail)));
+        } while (!(ord[U.seg * n_loc + w.p] & kWHead));
         const int q = (pend_head + npend) % kQ;
         pend_dst[q] = nullptr;
         if (dg >= 0) {  // a head: its y tile to the receiver's inbox row over NVLink (a4)
