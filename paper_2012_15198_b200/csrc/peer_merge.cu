@@ -248,9 +248,13 @@ __device__ __forceinline__ void ck_add(uint32_t& cx, uint32_t& cs, uint32_t w, u
 }
 
 // Wait until the update warps finished position j (true), or the walk ends before it (false).
+// Position j is done when EVERY update warp has released it: each warp counts its own
+// positions (a shared total would let warps that run ahead -- up to kNA stages -- stand in for
+// one still storing its part of position j).  false once j is past the CTA's last position.
 __device__ __forceinline__ bool wait_position(const uint32_t* y_stored, volatile int* end_pos, int j) {
-  while ((int32_t)(ld_acquire_cta(y_stored) - (uint32_t)(kUpd / 32) * (uint32_t)(j + 1)) < 0)
-    if (*end_pos <= j) return false;
+  for (int w = 0; w < kUpd / 32; ++w)
+    while ((int32_t)(ld_acquire_cta(y_stored + w) - (uint32_t)(j + 1)) < 0)
+      if (*end_pos <= j) return false;
   return true;
 }
 
@@ -280,7 +284,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
   __shared__ uint4 meta[kNI];                     // trailer of the staged received tile (bulk-loaded)
   __shared__ uint4 meta_re;                       // trailer re-read by the mix after a failed check
   __shared__ uint32_t ck_mix[2][kMix / 32][2];    // per mix warp, double-buffered by round parity
-  __shared__ uint32_t y_stored;  // update-warp arrivals: position j is done at >= 8 (j + 1)
+  __shared__ uint32_t y_stored[kUpd / 32];  // per update warp: positions it has released
   __shared__ int s_end;          // number of positions this CTA processes; INT_MAX until known
   __shared__ int s_timeout;
   volatile int* timeout = &s_timeout;
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
   if (threadIdx.x == 0) {
     s_timeout = 0;
     s_end = 0x7fffffff;
-    y_stored = 0;
+    for (int w = 0; w < kUpd / 32; ++w) y_stored[w] = 0;
     for (int i = 0; i < kNA; ++i) {
       ptx::mbar_init(&a_full[i], 1);
       ptx::mbar_init(&a_empty[i], kUpd / 32);
@@ -538,7 +542,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       if (lane == 0) {
         ptx::mbar_arrive(&a_empty[st]);
         if (copy) ptx::mbar_arrive(&y_full[sy]);
-        red_add_release_cta(&y_stored, 1u);
+        red_add_release_cta(&y_stored[warp], 1u);
       }
       if (copy) ++c;
     }
@@ -551,7 +555,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     Walk w;
     w.init(n_loc);
     for (int j = 0;; ++j) {
-      if (!wait_position(&y_stored, end_pos, j)) break;
+      if (!wait_position(y_stored, end_pos, j)) break;
       w.next(claims, a.chunk_t0, n_loc);
       const MTile U = mtile(a, bnd, t0, w.t, cur);
       const uint32_t e_w = ord[U.seg * n_loc + w.p];
@@ -723,7 +727,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       Walk w;
       w.init(n_loc);
       for (int j = 0;; ++j) {
-        if (!wait_position(&y_stored, end_pos, j)) break;
+        if (!wait_position(y_stored, end_pos, j)) break;
         w.next(claims, a.chunk_t0, n_loc);
         const MTile U = mtile(a, bnd, t0, w.t, cur);
         const uint32_t e_w = ord[U.seg * n_loc + w.p];
@@ -731,7 +735,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
         const uint32_t row = e_w & kWIdx;
         // stage it once the update is `lag` positions further (the sender's copy has probably
         // completed by then), or at the end; the mix polls if the trailer is still old
-        if (a.lag > 0) wait_position(&y_stored, end_pos, j + a.lag);
+        if (a.lag > 0) wait_position(y_stored, end_pos, j + a.lag);
         const int si = q % kNI;
         ptx::mbar_wait(&i_empty[si], (uint32_t)(((q / kNI) & 1) ^ 1));
         ++q;
