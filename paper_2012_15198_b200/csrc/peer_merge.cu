@@ -24,9 +24,8 @@
 //                     copy has completed (cp.async.bulk.wait_group) a 16-byte trailer
 //                     {epoch, xor ^ w, weighted sum, w} (w: the push-sum weight on a
 //                     segment's first tile) goes to the receiver
-//   inbox warp        for a chain tail: stages the tile's trailer and the received tile (bulk
-//                     copies, Alg.1 l.8 irecv) and the own y tile (cp.async: generic proxy, like
-//                     the stores that wrote it, so the y_stored release/acquire orders them)
+//   inbox warp        for a chain tail: stages the tile's trailer, the received tile and the
+//                     own y tile (Alg.1 l.8 irecv), once every update warp released the position
 //   mix warps (4)     verify the received words against the trailer's checksums (polling
 //                     the trailer and re-reading the words until they match: Alg.1 l.14
 //                     "wait until ... communication is completed", per tile), then
@@ -482,9 +481,8 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
           else st4_cs(X + (int64_t)prev_row * s.ld + j, mean4(yprev[q], wire ? bf16r4(y) : y), vv);
           if ((e_w & kWEnd) && !tail)
             st4_cs(X + rowoff + j, mean4(y, wire ? bf16r4(yfirst[q]) : yfirst[q]), vv);
-          // a chain tail's y waits in params for the mix; the inbox warp stages it back with
-          // cp.async after this position's CTA-scope release (generic proxy on both sides:
-          // no async-proxy read of generic writes)
+          // a chain tail's y waits in params for the mix; the inbox warp bulk-loads it back
+          // after every update warp released this position (proxy fence below)
           if (tail) st4(X + rowoff + j, y, vv);
           yprev[q] = y;
           if (head) {
@@ -538,6 +536,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
           }
       }
       if (copy) ptx::fence_proxy_async_shared();  // y tile -> the store warp's bulk copies
+      if (tail) ptx::fence_proxy_async_global();  // y in params -> the inbox warp's bulk read
       __syncwarp();
       if (lane == 0) {
         ptx::mbar_arrive(&a_empty[st]);
@@ -719,9 +718,9 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     __syncwarp();
   } else if (warp == kWLoadIn) {
     // ---------------- inbox loader: a chain tail's trailer, received and own y tiles ---
-    // (every lane walks the positions; lane 0 bulk-loads the trailer and the received tile,
-    // all lanes copy the tail's own y from params with cp.async, which like the update warps'
-    // stores is a generic-proxy access: ordered by the acquire of y_stored, no proxy fence)
+    // (lane 0 bulk-loads the trailer, the received tile and the tail's own y; the update warps'
+    // generic stores of that y precede their fence.proxy.async and per-warp release, which
+    // this warp acquires for every update warp before the bulk read)
     {
       int cur = 0, q = 0;
       Walk w;
@@ -742,12 +741,9 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
         float* buf = ringI + (size_t)si * 2 * kT;
         const uint32_t yb = (uint32_t)(((U.len + 3) & ~3) * 4);
         const uint32_t ib = wire ? (uint32_t)(((U.len + 7) & ~7) * 2) : yb;
-        const float* yown = X + (int64_t)row * s.ld + U.c0;
-        for (int v = lane; v < (U.len + 3) / 4; v += 32) ptx::cp_async16_ca(buf + kT + 4 * v, yown + 4 * v);
-        ptx::cp_async_mbar_arrive(&i_full[si]);  // the slot completes once these copies have landed
-        __syncwarp();
         if (lane == 0) {
-          ptx::mbar_arrive_expect_tx(&i_full[si], ib + 16u);
+          ptx::mbar_arrive_expect_tx(&i_full[si], ib + yb + 16u);
+          ptx::bulk_g2s(buf + kT, X + (int64_t)row * s.ld + U.c0, yb, &i_full[si]);  // own y
           ptx::bulk_g2s(&meta[si], trl_in + (size_t)w.t * n_loc + row, 16u, &i_full[si]);
           if (wire)
             ptx::bulk_g2s(buf, reinterpret_cast<const uint16_t*>(mine + a.off_inbox) +
