@@ -118,6 +118,7 @@ struct MergeArgs {
   int n_tiles, n_chunks;
   int trl_cap;              // trailer slots per parity (tiles x n_loc)
   int lag;                  // the inbox warp stages position j once the update is at j + lag
+  int read_lag;             // y-out slots left unfreed while their copies may still read them (0..kNY-1)
   int vranks;
   uint32_t epoch;
   int fused_topo;           // draw Alg. 2 in the prologue (<= 64 ranks), else read s.src
@@ -196,11 +197,6 @@ __device__ __forceinline__ void st4_cs(float* p, float4 v, int valid) {
 __device__ __forceinline__ void red_add_release_cta(uint32_t* p, uint32_t v) {
   asm volatile("red.release.cta.shared::cta.add.u32 [%0], %1;" ::"r"(ptx::smem_addr(p)), "r"(v) : "memory");
 }
-__device__ __forceinline__ uint32_t ld_acquire_cta(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(ptx::smem_addr(p)) : "memory");
-  return v;
-}
 // memory reads that bypass L1 (another GPU writes these words)
 __device__ __forceinline__ uint4 ld_volatile4(const void* p) {
   uint4 v;
@@ -223,6 +219,17 @@ __device__ __forceinline__ uint32_t ld_volatile1(const void* p) {
 __device__ __forceinline__ void st_volatile4(void* p, uint4 v) {
   asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
+}
+
+// wait until at most n (runtime, 0..4) bulk groups of this thread still read their source
+__device__ __forceinline__ void bulk_wait_read_n(int n) {
+  switch (n) {
+    case 0: ptx::bulk_wait_read<0>(); break;
+    case 1: ptx::bulk_wait_read<1>(); break;
+    case 2: ptx::bulk_wait_read<2>(); break;
+    case 3: ptx::bulk_wait_read<3>(); break;
+    default: ptx::bulk_wait_read<4>(); break;
+  }
 }
 
 // wait until at most n (runtime, 0..7) bulk groups of this thread are still writing
@@ -250,10 +257,17 @@ __device__ __forceinline__ void ck_add(uint32_t& cx, uint32_t& cs, uint32_t w, u
 // Position j is done when EVERY update warp has released it: each warp counts its own
 // positions (a shared total would let warps that run ahead -- up to kNA stages -- stand in for
 // one still storing its part of position j).  false once j is past the CTA's last position.
+// Polls with relaxed shared loads and acquires once (fence.acq_rel.cta) when all have passed.
 __device__ __forceinline__ bool wait_position(const uint32_t* y_stored, volatile int* end_pos, int j) {
-  for (int w = 0; w < kUpd / 32; ++w)
-    while ((int32_t)(ld_acquire_cta(y_stored + w) - (uint32_t)(j + 1)) < 0)
-      if (*end_pos <= j) return false;
+  const volatile uint32_t* ys = y_stored;
+  for (;;) {
+    bool all = true;
+#pragma unroll
+    for (int w = 0; w < kUpd / 32; ++w) all &= (int32_t)(ys[w] - (uint32_t)(j + 1)) >= 0;
+    if (all) break;
+    if (*end_pos <= j) return false;
+  }
+  asm volatile("fence.acq_rel.cta;" ::: "memory");
   return true;
 }
 
@@ -844,8 +858,8 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
         ++unfreed;
         // slots are freed once their copies have read them, up to kReadLag positions late (the
         // update warps may run kNY copy positions ahead, so this never waits on them)
-        ptx::bulk_wait_read<kReadLag>();
-        while (unfreed > kReadLag) free_oldest();
+        bulk_wait_read_n(a.read_lag);
+        while (unfreed > a.read_lag) free_oldest();
         if (npend > land) {  // all but the newest `land` positions' copies have completed
           bulk_wait_n(land);
           ptx::fence_proxy_async_global();
@@ -952,6 +966,8 @@ int peer_merge_launch(PeerState& p, const PeerStepArgs& a, uint32_t epoch, cudaS
   ma.trl_cap = p.mflag_cap;
   static const int lag = getenv("CS_MERGE_LAG") ? atoi(getenv("CS_MERGE_LAG")) : 2;
   ma.lag = lag < 0 ? 0 : lag;
+  static const int read_lag = getenv("CS_MERGE_READLAG") ? atoi(getenv("CS_MERGE_READLAG")) : kReadLag;
+  ma.read_lag = read_lag < 0 ? 0 : (read_lag > kReadLag ? kReadLag : read_lag);
   ma.retries = p.d_stats;
   ma.off_done = p.off_done;
   ma.off_count = p.off_count;
