@@ -257,18 +257,27 @@ __device__ __forceinline__ void ck_add(uint32_t& cx, uint32_t& cs, uint32_t w, u
 // Position j is done when EVERY update warp has released it: each warp counts its own
 // positions (a shared total would let warps that run ahead -- up to kNA stages -- stand in for
 // one still storing its part of position j).  false once j is past the CTA's last position.
-// Polls with relaxed shared loads and acquires once (fence.acq_rel.cta) when all have passed.
+// Called by whole warps: lane 0 polls with relaxed shared loads (backing off, so spinning
+// warps leave issue slots to the update warps), the warp acquires once (fence.acq_rel.cta).
 __device__ __forceinline__ bool wait_position(const uint32_t* y_stored, volatile int* end_pos, int j) {
-  const volatile uint32_t* ys = y_stored;
-  for (;;) {
-    bool all = true;
+  int ok = 1;
+  if ((threadIdx.x & 31) == 0) {
+    const volatile uint32_t* ys = y_stored;
+    for (;;) {
+      bool all = true;
 #pragma unroll
-    for (int w = 0; w < kUpd / 32; ++w) all &= (int32_t)(ys[w] - (uint32_t)(j + 1)) >= 0;
-    if (all) break;
-    if (*end_pos <= j) return false;
+      for (int w = 0; w < kUpd / 32; ++w) all &= (int32_t)(ys[w] - (uint32_t)(j + 1)) >= 0;
+      if (all) break;
+      if (*end_pos <= j) {
+        ok = 0;
+        break;
+      }
+      __nanosleep(20);
+    }
   }
+  ok = __shfl_sync(0xffffffffu, ok, 0);
   asm volatile("fence.acq_rel.cta;" ::: "memory");
-  return true;
+  return ok != 0;
 }
 
 __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) {
