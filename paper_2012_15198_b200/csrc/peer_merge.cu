@@ -89,6 +89,7 @@ constexpr int kWLoadXmg = (kUpd + kMix) / 32, kWLoadIn = kWLoadXmg + 1, kWStore 
 constexpr int kPerU = kT / 4 / kUpd;                  // float4 per update thread per tile
 constexpr int kPerM = kT / 4 / kMix;                  // float4 per mix thread per tile
 constexpr int kMixBar = 1;                            // named barrier of the mix warps
+constexpr int kUpdBar = 3;                            // named barrier of the update warps (2: prologue)
 // walk-order entries: local row | flags
 constexpr uint32_t kWStart = 1u << 31, kWEnd = 1u << 30, kWHead = 1u << 29, kWTail = 1u << 28;
 constexpr uint32_t kWIdx = (1u << 28) - 1;
@@ -257,27 +258,15 @@ __device__ __forceinline__ void ck_add(uint32_t& cx, uint32_t& cs, uint32_t w, u
 // Position j is done when EVERY update warp has released it: each warp counts its own
 // positions (a shared total would let warps that run ahead -- up to kNA stages -- stand in for
 // one still storing its part of position j).  false once j is past the CTA's last position.
-// Called by whole warps: lane 0 polls with relaxed shared loads (backing off, so spinning
-// warps leave issue slots to the update warps), the warp acquires once (fence.acq_rel.cta).
+// Position j is done once the position counter (released by update thread 0 after all update
+// warps met at kUpdBar) exceeds j; relaxed polls, one acquire fence.  false once j is past the
+// CTA's last position.
 __device__ __forceinline__ bool wait_position(const uint32_t* y_stored, volatile int* end_pos, int j) {
-  int ok = 1;
-  if ((threadIdx.x & 31) == 0) {
-    const volatile uint32_t* ys = y_stored;
-    for (;;) {
-      bool all = true;
-#pragma unroll
-      for (int w = 0; w < kUpd / 32; ++w) all &= (int32_t)(ys[w] - (uint32_t)(j + 1)) >= 0;
-      if (all) break;
-      if (*end_pos <= j) {
-        ok = 0;
-        break;
-      }
-      __nanosleep(20);
-    }
-  }
-  ok = __shfl_sync(0xffffffffu, ok, 0);
+  const volatile uint32_t* ys = y_stored;
+  while ((int32_t)(*ys - (uint32_t)(j + 1)) < 0)
+    if (*end_pos <= j) return false;
   asm volatile("fence.acq_rel.cta;" ::: "memory");
-  return ok != 0;
+  return true;
 }
 
 __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) {
@@ -306,7 +295,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
   __shared__ uint4 meta[kNI];                     // trailer of the staged received tile (bulk-loaded)
   __shared__ uint4 meta_re;                       // trailer re-read by the mix after a failed check
   __shared__ uint32_t ck_mix[2][kMix / 32][2];    // per mix warp, double-buffered by round parity
-  __shared__ uint32_t y_stored[kUpd / 32];  // per update warp: positions it has released
+  __shared__ uint32_t y_stored[1];  // positions every update warp has finished
   __shared__ int s_end;          // number of positions this CTA processes; INT_MAX until known
   __shared__ int s_timeout;
   volatile int* timeout = &s_timeout;
@@ -335,7 +324,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
   if (threadIdx.x == 0) {
     s_timeout = 0;
     s_end = 0x7fffffff;
-    for (int w = 0; w < kUpd / 32; ++w) y_stored[w] = 0;
+    y_stored[0] = 0;
     for (int i = 0; i < kNA; ++i) {
       ptx::mbar_init(&a_full[i], 1);
       ptx::mbar_init(&a_empty[i], kUpd / 32);
@@ -564,8 +553,11 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
       if (lane == 0) {
         ptx::mbar_arrive(&a_empty[st]);
         if (copy) ptx::mbar_arrive(&y_full[sy]);
-        red_add_release_cta(&y_stored[warp], 1u);
       }
+      // the position is done when all update warps are: they meet here (bar.sync orders their
+      // stores before thread 0's release of the single position counter)
+      ptx::named_bar_sync(kUpdBar, kUpd);
+      if (tid == 0) red_add_release_cta(y_stored, 1u);
       if (copy) ++c;
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(s.err + kErrDiverged, 1);
