@@ -12,10 +12,12 @@ per GPU with a ResNet-50-sized vector (25,557,032), c5 eight workers per GPU.
 
 value   = whole-job "params mixed+updated" GB/s = 4 B * world * d / step time
           (device-timed with CUDA events, max over ranks)
-e2e     = the same metric through the host-buffer entry point (grads copied
-          host->device every step, diagnostics copied back)
+e2e     = the same metric through the host-buffer entry point cs_gossip_step_io (N = 1:
+          grads copied host->device and the merged params + psw copied back every step,
+          pipelined in column pieces); N > 1: grads H2D, cs_gossip_step, params + psw D2H
 roofline = the hot kernel's algorithmic bytes / its CUDA-event duration vs the
-          measured HBM copy peak (N = 1) or the measured NVLink peer bandwidth (N > 1)
+          measured HBM copy peak (N = 1) or the measured NVLink peer bandwidth (N > 1);
+          N > 1 adds the NVLink bytes the hardware counted (NVML) as `traffic`
 cpu_baseline = the oracle (oracle/, plain NumPy) timed on this host on a bounded
           column sample of the same workload (rank 0, N = 1 only).
 """
@@ -131,38 +133,40 @@ class NvlinkCounters:
     """Hardware NVLink byte counters of this GPU (NVML field values, summed over its links),
     read before and after the timed region: the NVLink traffic the step actually moved."""
 
-    FIELDS = (("tx", "NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES"), ("rx", "NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES"))
+    # (tx field, rx field, bytes per unit): byte counters, else the KiB throughput counters
+    FIELDS = (("NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES", "NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES", 1),
+              ("NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX", "NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX", 1024))
 
     def __init__(self, index: int):
-        self.ok = False
+        self.ok, self.source = False, None
         try:
             import pynvml
             pynvml.nvmlInit()
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.links = [l for l in range(18) if self._link_up(l)]
-            self.ok = bool(self.links) and self.read() is not None
+            for tx, rx, unit in self.FIELDS:
+                links = [l for l in range(18) if self._ok(tx, l) and self._ok(rx, l)]
+                if links:
+                    self.fields, self.links, self.unit = (tx, rx), links, unit
+                    self.ok, self.source = True, f"NVML {tx}/{rx} over {len(links)} links"
+                    break
         except Exception:  # noqa: BLE001
             self.ok = False
 
-    def _link_up(self, link):
+    def _ok(self, name, link):
         try:
-            return self.nv.nvmlDeviceGetNvLinkState(self.h, link) == 1
+            return self.nv.nvmlDeviceGetFieldValues(self.h, [(getattr(self.nv, name), link)])[0].nvmlReturn == 0
         except Exception:  # noqa: BLE001
             return False
 
     def read(self):
-        """{tx, rx} bytes summed over the active links, or None."""
+        """{tx, rx} bytes summed over the links, or None."""
         out = {}
-        for key, name in self.FIELDS:
-            fid = getattr(self.nv, name)
-            vals = self.nv.nvmlDeviceGetFieldValues(self.h, [(fid, l) for l in self.links])
-            tot = 0
-            for v in vals:
-                if v.nvmlReturn != 0:
-                    return None
-                tot += v.value.ullVal
-            out[key] = tot
+        for key, name in zip(("tx", "rx"), self.fields):
+            vals = self.nv.nvmlDeviceGetFieldValues(self.h, [(getattr(self.nv, name), l) for l in self.links])
+            if any(v.nvmlReturn != 0 for v in vals):
+                return None
+            out[key] = sum(v.value.ullVal for v in vals) * self.unit
         return out
 
 
@@ -602,7 +606,7 @@ def main():
         # GPU that moved the most, in the direction the algorithmic bytes count (into a GPU)
         traffic = {"rx_bytes_per_step": hw_rx, "tx_bytes_per_step": hw_tx,
                    "rx_over_algorithmic": hw_rx / nvl_per_launch if nvl_per_launch else None,
-                   "source": "NVML NVLINK_COUNT_RCV/XMIT_BYTES summed over active links, max over ranks"} \
+                   "source": (nvc.source if nvc else "") + ", max over ranks"} \
             if hw_rx >= 0 else None
         roof_nvl = {"bound": "nvlink", "achieved": nvl_ach, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
                     "frac": nvl_ach / NVLINK_PEER_GBS, "traffic": traffic,
