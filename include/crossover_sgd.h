@@ -210,6 +210,21 @@ int cs_ipc_import(const char* all_handles /* nprocs * CS_IPC_HANDLE_BYTES */);
  * Errors: CS_ENOTBOUND, CS_EINVAL, CS_ELAYOUT (not 256-B / 16-B aligned), CS_EUNSUPPORTED
  * (one process, emulated ranks, groups of one GPU), CS_ECUDA. */
 int cs_multicast_bytes(int64_t* bytes_out);
+/* Multi-GPU hierarchical step with the intra-group gradient sum done by NCCL (ncclAllReduce
+ * over a communicator of the group's GPUs; north_star: "NCCL over NVLink is used only for
+ * the intra-group average of hierarchical mode"); the update kernels multiply the sum by
+ * fp32(1/|G|) as they load it.  NCCL is loaded at run time (libnccl.so.2).
+ *   cs_nccl_unique_id  fills id_out[CS_NCCL_ID_BYTES] (call on the group's first member).
+ *   cs_set_hier_nccl   every member of a group passes the same id (collective over the
+ *                      group: blocks until all members joined); NULL returns to the
+ *                      point-to-point h1.  Replaces a registered multicast workspace.
+ * Numerics: NCCL's summation order, so groups of >= 3 GPUs match the oracle within the
+ * hierarchical tolerance; groups of 2 bitwise.  LARS keeps the point-to-point h1.
+ * Errors: CS_ENOTBOUND, CS_EINVAL, CS_EUNSUPPORTED (no libnccl, one process, emulated ranks,
+ * groups of one GPU), CS_ECUDA (NCCL error). */
+#define CS_NCCL_ID_BYTES 128
+int cs_nccl_unique_id(char* id_out);
+int cs_set_hier_nccl(const char* group_id);
 int cs_set_multicast(void* uc_base, void* mc_base, int64_t bytes);
 int cs_add_multicast_grads(void* uc_base, void* mc_base, int64_t bytes);
 

@@ -55,6 +55,8 @@ _SIGS = {
     "cs_ipc_export": (_c_int, [_vp]),
     "cs_ipc_import": (_c_int, [_vp]),
     "cs_multicast_bytes": (_c_int, [_vp]),
+    "cs_nccl_unique_id": (_c_int, [_vp]),
+    "cs_set_hier_nccl": (_c_int, [_vp]),
     "cs_set_multicast": (_c_int, [_vp, _vp, _c_i64]),
     "cs_add_multicast_grads": (_c_int, [_vp, _vp, _c_i64]),
     "cs_gossip_step": (_c_int, [_vp, _vp, _vp, _c_f, _c_f]),
@@ -254,6 +256,32 @@ def setup_multicast(group_size: int, device) -> bool:
     cs_set_multicast(t.data_ptr(), mc, 4 * t.numel())
     dist.barrier()
     return True
+
+
+CS_NCCL_ID_BYTES = 128
+
+
+def cs_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(CS_NCCL_ID_BYTES)
+    _check(lib.cs_nccl_unique_id(buf), "cs_nccl_unique_id")
+    return buf.raw
+
+
+def cs_set_hier_nccl(group_id) -> None:
+    _check(lib.cs_set_hier_nccl(ctypes.c_char_p(group_id) if group_id else None), "cs_set_hier_nccl")
+
+
+def setup_hier_nccl(group_size: int) -> None:
+    """Plumbing, no arithmetic: each group's first member draws an NCCL id, the ids are
+    all-gathered over torch.distributed and every member joins its group's communicator
+    (cs_set_hier_nccl).  Collective over the whole job; call after setup_peers()."""
+    import torch.distributed as dist
+    r = dist.get_rank()
+    lead = (r // group_size) * group_size
+    ids = [None] * dist.get_world_size()
+    dist.all_gather_object(ids, cs_nccl_unique_id() if r == lead else None)
+    cs_set_hier_nccl(ids[lead])
+    dist.barrier()
 
 
 def register_multicast_grads(t, mc: int) -> None:

@@ -418,6 +418,7 @@ PeerStepArgs peer_args(float* params, const float* grads, float* psw, float lr, 
   pa.g_off = 0;
   pa.gbar_local = 0;
   pa.gpull_chunk = 0;
+  pa.g_scale = 1.f;
   if (g.vranks > 1) {  // emulated ranks: rank 0's view; each CTA shifts to its own rank
     pa.n_loc = g.world / g.vranks;
     pa.nprocs = g.vranks;
@@ -779,11 +780,36 @@ int cs_set_multicast(void* uc_base, void* mc_base, int64_t bytes) {
   CS_CUDA(cudaMemset(p.d_nvls_count, 0, 128));
   CS_CUDA(cudaMemset(uc_base, 0, nvls_off_gbar()));  // barrier words (callers barrier before stepping)
   CS_CUDA(cudaDeviceSynchronize());
+  nccl_group_release(p);  // one h1 route at a time
   p.mc_uc = static_cast<char*>(uc_base);
   p.mc_mc = static_cast<char*>(mc_base);
   p.mc_bytes = (size_t)bytes;
   p.nvls_epoch = 0;
   p.nvls_tot[0] = p.nvls_tot[1] = 0;
+  return CS_OK;
+}
+
+int cs_nccl_unique_id(char* id_out) {
+  if (!id_out) return fail(CS_EINVAL, "NULL id_out");
+  if (nccl_unique_id(id_out)) return fail(CS_EUNSUPPORTED, "%s", nccl_error());
+  return CS_OK;
+}
+
+int cs_set_hier_nccl(const char* group_id) {
+  int rc = check_bound();
+  if (rc) return rc;
+  PeerState& p = g.peer;
+  if (group_id && (g.nprocs < 2 || g.vranks > 1 || !p.imported))
+    return fail(CS_EUNSUPPORTED, "NCCL h1 needs one process per GPU with the peers imported");
+  if (group_id && p.gs < 2) return fail(CS_EUNSUPPORTED, "NCCL h1 needs hierarchical groups of >= 2 GPUs");
+  if ((rc = flush_pending()) != CS_OK) return rc;
+  CS_CUDA(cudaStreamSynchronize(g.stream));
+  if (group_id && p.mc_uc) {  // one h1 route at a time
+    p.mc_uc = p.mc_mc = nullptr;
+    p.mc_grads.clear();
+  }
+  if (nccl_group_init(p, group_id, p.gs > 0 ? g.rank % p.gs : 0))
+    return fail(CS_ECUDA, "%s", nccl_error());
   return CS_OK;
 }
 
@@ -986,6 +1012,7 @@ int cs_hier_step(float* params, float* grads, float* psw, float lr, float moment
     g.launches_per_step = (int)(g_peer_launches - launches0) + (g.lars ? 2 : 0);
     g.hot_kernel = g.lars ? "k_hier_scatter+k_hier_reduce+k_lars_norms+k_lars_scale+k_peer_push+k_peer_mix"
                    : g.peer.last_nvls ? (g.groups >= 2 ? "k_hier_nvls+k_push_merge" : "k_hier_nvls+k_peer_push")
+                   : g.peer.last_nccl ? (g.groups >= 2 ? "ncclAllReduce+k_push_merge" : "ncclAllReduce+k_peer_push")
                                       : "k_hier_scatter+k_hier_reduce+k_peer_push+k_peer_mix";
     g.step += 1;
     return CS_OK;

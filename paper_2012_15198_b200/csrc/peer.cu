@@ -353,7 +353,8 @@ __global__ void __launch_bounds__(kPushThreads, 2) k_peer_push(const PeerKernelA
           const int vv = valid < 4 ? valid : 4;
           float4 cx = reinterpret_cast<const float4*>(bx)[v];
           const float4 cm = reinterpret_cast<const float4*>(bx + kPeerTile)[v];
-          const float4 cg = reinterpret_cast<const float4*>(bx + 2 * kPeerTile)[v];
+          float4 cg = reinterpret_cast<const float4*>(bx + 2 * kPeerTile)[v];
+          if (s.g_scale != 1.f) cg = scale4(cg, s.g_scale);  // NCCL h1: the group sum -> mean
           if (a.fuse_mix)  // the previous step's a5: x = (y + received y) / 2 (Alg.1 l.17)
             cx = mean4(cx, s.wire ? unpack_bf16x4(reinterpret_cast<const uint2*>(bx + 3 * kPeerTile)[v])
                                   : reinterpret_cast<const float4*>(bx + 3 * kPeerTile)[v]);
@@ -1659,6 +1660,7 @@ void peer_release(PeerState& p) {
   if (p.d_chunk_t0) cudaFree(p.d_chunk_t0);
   if (p.d_stats) cudaFree(p.d_stats);
   if (p.d_nvls_count) cudaFree(p.d_nvls_count);
+  nccl_group_release(p);
   p = PeerState();
 }
 
@@ -2195,11 +2197,24 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     b.gbar_local = 1;
   }
   p.last_nvls = nvls;
-  // pulled group mean (default without NVLS, LARS or column pieces): k_hier_reduce keeps each
-  // member's mean chunk in its own gbar and the update bulk-loads the chunks from their owners
-  // over NVLink, so the all-gather rides in the update's pass instead of a pass of its own
-  static const bool pull_env = !(getenv("CS_HIER_PULL") && getenv("CS_HIER_PULL")[0] == '0');
-  const bool pull = pull_env && !nvls && a.lrs_out == nullptr && (exchange || p.hier_pieces == 1) && p.gs > 1;
+  // NCCL h1 (hier_nccl.cu): ncclAllReduce of the group's gradients into this GPU's gbar; the
+  // update scales the sum by fp32(1/|G|)
+  const bool nccl = !nvls && p.nccl_comm != nullptr && p.vranks <= 1 && a.lrs_out == nullptr && !fuse;
+  p.last_nccl = nccl;
+  if (nccl) {
+    b.g = reinterpret_cast<const float*>(p.base + p.off_gbar);
+    b.gbar_local = 1;
+    b.g_scale = a.inv_gs;
+  }
+  // pulled group mean (groups of 2 GPUs without NVLS, LARS or column pieces): k_hier_reduce
+  // keeps each member's mean chunk in its own gbar and the update bulk-loads the chunks from
+  // their owners over NVLink, so the all-gather rides in the update's pass.  Measured: 285.7
+  // vs 306.8 us at 1 x 2 GPUs, but 440 vs 404 us at 1 x 4 and 450 vs 399 us at 2 x 2 (three
+  // owners' peer reads per tile are slower than the stores of the all-gather); CS_HIER_PULL
+  // = 0 / 1 forces it off / on
+  static const int pull_env = getenv("CS_HIER_PULL") ? atoi(getenv("CS_HIER_PULL")) : -1;
+  const bool pull = (pull_env < 0 ? p.gs == 2 : pull_env == 1) && !nvls && !nccl && a.lrs_out == nullptr &&
+                    (exchange || p.hier_pieces == 1) && p.gs > 1;
   if (pull) b.gpull_chunk = ((a.d + p.gs - 1) / p.gs + 3) / 4 * 4;
   PeerKernelArgs ka = kernel_args(p, b, epoch, !exchange);
   if (ev0) cudaEventRecord(ev0, st);
@@ -2223,7 +2238,7 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
   // One group (no leader exchange): the vector is cut into P column pieces; h1 of piece
   // q+1 (NVLink-bound) runs on the caller's stream while the update of piece q (HBM-bound,
   // k_peer_push in final_only mode, waiting on piece q's d2 flags) runs on the aux stream.
-  const int P = exchange || nvls ? 1 : p.hier_pieces;
+  const int P = exchange || nvls || nccl ? 1 : p.hier_pieces;
   h.gstride = a.ld;
   int rc = CS_OK;
   for (int q = 0; q < P; ++q) {
@@ -2242,6 +2257,10 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     if (nvls) {
       if (nvls_h1(p, a.g, g_mc, a.rank % p.gs, a.inv_gs, a.err, st))
         return perr(CS_ECUDA, "k_hier_nvls launch", cudaGetLastError());
+      phase_record(2, st);
+    } else if (nccl) {
+      if (nccl_h1(p, a.g, reinterpret_cast<float*>(p.base + p.off_gbar), a.d, st))
+        return perr(CS_ECUDA, nccl_error(), cudaSuccess);
       phase_record(2, st);
     } else {
       plaunch(p, k_hier_scatter, p.grid_hier, kHierThreads, 0, st, h);

@@ -53,6 +53,9 @@ struct PeerStepArgs {
   // lives only in the gbar row of member c / gpull_chunk of this GPU's group (region + g_off);
   // the update bulk-loads it from there over NVLink
   int64_t gpull_chunk;
+  // != 1: g holds the group's gradient SUM (NCCL h1); the update multiplies it by g_scale
+  // (fp32(1/|G|), the oracle's final operation of the mean) as it loads it
+  float g_scale;
 };
 
 struct PeerState {
@@ -140,7 +143,17 @@ struct PeerState {
   uint32_t nvls_epoch = 0;
   uint32_t nvls_tot[2] = {0, 0};
   bool last_nvls = false;   // the last hierarchical step's h1 ran through NVLS
+  // NCCL h1 (hier_nccl.cu): a communicator over this GPU's hierarchical group (cs_set_hier_nccl)
+  void* nccl_comm = nullptr;
+  bool last_nccl = false;
 };
+
+// NCCL h1 (hier_nccl.cu; NCCL loaded at run time)
+int nccl_unique_id(char* out /* 128 bytes */);
+int nccl_group_init(PeerState& p, const char* id_bytes /* nullptr: release */, int member);
+void nccl_group_release(PeerState& p);
+int nccl_h1(PeerState& p, const float* g, float* gsum, int64_t d, cudaStream_t st);
+const char* nccl_error();
 
 // kernels the multi-GPU steps launched (plaunch / peer_launch / topology / NVLS): the
 // bench's launch count is the difference across a step

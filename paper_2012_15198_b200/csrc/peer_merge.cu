@@ -481,7 +481,8 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
           const int64_t j = U.c0 + 4 * (int64_t)v;
           const float4 cxv = reinterpret_cast<const float4*>(bx)[v];
           const float4 cm = reinterpret_cast<const float4*>(bx + kT)[v];
-          const float4 cg = reinterpret_cast<const float4*>(bx + 2 * kT)[v];
+          float4 cg = reinterpret_cast<const float4*>(bx + 2 * kT)[v];
+          if (s.g_scale != 1.f) cg = scale4(cg, s.g_scale);  // NCCL h1: the group sum -> mean
           bad |= nonfinite4(cg);
           // LARS (C-18): m' = mu*m + (g + wd*x), y = x - lrs[row][layer]*m'
           const float4 mn = mom4(cm, s.lrs ? decay4(cg, cxv, s.wd) : cg, s.mu);

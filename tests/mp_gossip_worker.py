@@ -52,6 +52,9 @@ def main():
     ap.add_argument("--nvls", action="store_true",
                     help="hierarchical h1 through the NVSwitch (cs_set_multicast): tolerance parity for groups "
                          ">= 3 GPUs (switch summation order), bitwise for groups of 2; members bitwise equal")
+    ap.add_argument("--nccl", action="store_true",
+                    help="hierarchical h1 through NCCL (cs_set_hier_nccl): tolerance parity for groups >= 3 GPUs "
+                         "(NCCL's summation order), bitwise for groups of 2; members bitwise equal")
     ap.add_argument("--mc-bank", action="store_true",
                     help="with --nvls: the gradient bank lives in multicast memory (reduced in place)")
     ap.add_argument("--stream-sync", action="store_true",
@@ -95,6 +98,8 @@ def main():
     bank[B:] = bank[:n_loc]
     torch.cuda.synchronize()
     cs.setup_peers()
+    if a.nccl:
+        cs.setup_hier_nccl(gs_h)
     if a.nvls:
         if not cs.setup_multicast(gs_h, dev):
             print("no multicast on this fabric: FAIL", flush=True)
@@ -217,7 +222,7 @@ def main():
             # hierarchical members hold their leader's momentum (reading B-4)
             mref = orc.m[lead:lead + 1] if (a.hier_groups and first % gs != 0) else orc.m[rows]
             m_ok = np.all(np.abs(ms - mref) <= 1e-6 * np.abs(mref).max(axis=1, keepdims=True))
-        elif a.nvls and gs > 2:  # the switch's summation order (hierarchical tolerance)
+        elif (a.nvls or a.nccl) and gs > 2:  # the switch's / NCCL's summation order
             ref, refm = orc.x[rows], orc.m[lead:lead + 1] if first % gs != 0 else orc.m[rows]
             xs_ok = bool(np.all(np.linalg.norm((xs - ref).astype(np.float64), axis=1)
                                 <= 1e-6 * np.linalg.norm(ref.astype(np.float64), axis=1))

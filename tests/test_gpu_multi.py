@@ -261,3 +261,19 @@ def test_four_gpu_hierarchical_nvls(groups, d, k, steps, mc_bank, full):
     _run(4, "--workers-per-gpu", 1, "--vector-len", d, "--segments", k, "--num-steps", steps,
          "--hier-groups", groups, "--nvls", *(["--mc-bank"] if mc_bank else []),
          *(["--compare-all"] if full else []))
+
+
+# ---- NCCL h1: the intra-group gradient sum by ncclAllReduce (cs_set_hier_nccl) -------------
+@pytest.mark.skipif(NGPU < 2, reason="needs 2 GPUs")
+def test_two_gpu_hierarchical_nccl():
+    # a group of 2 GPUs: NCCL's sum of two values is order-free, so bitwise vs the oracle
+    _run(2, "--workers-per-gpu", 1, "--vector-len", 100_003, "--segments", 3, "--num-steps", 5,
+         "--hier-groups", 1, "--compare-all", "--nccl")
+
+
+@pytest.mark.skipif(NGPU < 4, reason="needs 4 GPUs")
+@pytest.mark.parametrize("groups,d,k,steps,full", [(1, 1_000_003, 8, 100, False), (2, 300_001, 16, 6, True)])
+def test_four_gpu_hierarchical_nccl(groups, d, k, steps, full):
+    # groups of 4: NCCL's order -> norm-wise <= 1e-6 after 100 steps; 2 x 2: bitwise
+    _run(4, "--workers-per-gpu", 1, "--vector-len", d, "--segments", k, "--num-steps", steps,
+         "--hier-groups", groups, "--nccl", *(["--compare-all"] if full else []))
