@@ -330,11 +330,12 @@ def main():
                     help="multi-GPU step schedule (cs_set_schedule): instep = merged params when the step's "
                          "work completes (default); deferred = the merge runs inside the next step (opt-in, "
                          "params readable only after cs_flush); split = push kernel + merge kernel")
-    ap.add_argument("--h1", default="p2p", choices=["nvls", "nccl", "p2p"],
+    ap.add_argument("--h1", default="auto", choices=["auto", "nvls", "nccl", "p2p"],
                     help="multi-GPU hierarchical gradient average: p2p = reduce-scatter + all-gather over peer "
-                         "stores (default, bitwise); nvls = in-switch reduction (cs_set_multicast), the gradient "
-                         "copied into the multicast workspace each step (measured slower for fp32, DESIGN §8); "
-                         "nccl = ncclAllReduce over the group's communicator (cs_set_hier_nccl)")
+                         "stores (bitwise); nccl = ncclAllReduce over the group's communicator "
+                         "(cs_set_hier_nccl; NCCL's order, tolerance parity for groups >= 3); nvls = in-switch "
+                         "reduction (cs_set_multicast), measured slower for fp32 (DESIGN §8); auto = the faster "
+                         "measured route: nccl for one group of >= 3 GPUs, else p2p")
     ap.add_argument("--path", default="auto", choices=["auto", "reg", "tma", "peer"],
                     help="library kernel path (cs_set_path); peer with 1 GPU = single-GPU emulation")
     args = ap.parse_args()
@@ -420,7 +421,7 @@ def main():
     h1 = "p2p" if hier and world_size > 1 and gs_h > 1 else None
     if world_size > 1:
         cs.setup_peers()
-        if hier and gs_h > 1 and args.h1 == "nccl":
+        if hier and gs_h > 1 and (args.h1 == "nccl" or (args.h1 == "auto" and gs_h >= 3 and groups == 1)):
             cs.setup_hier_nccl(gs_h)
             h1 = "nccl (ncclAllReduce over the group, the update scales by 1/|G|)"
         if want_nvls:

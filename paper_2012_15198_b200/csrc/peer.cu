@@ -2206,15 +2206,15 @@ int peer_hier_step(PeerState& p, const PeerStepArgs& a, cudaStream_t st, cudaEve
     b.gbar_local = 1;
     b.g_scale = a.inv_gs;
   }
-  // pulled group mean (groups of 2 GPUs without NVLS, LARS or column pieces): k_hier_reduce
-  // keeps each member's mean chunk in its own gbar and the update bulk-loads the chunks from
-  // their owners over NVLink, so the all-gather rides in the update's pass.  Measured: 285.7
-  // vs 306.8 us at 1 x 2 GPUs, but 440 vs 404 us at 1 x 4 and 450 vs 399 us at 2 x 2 (three
-  // owners' peer reads per tile are slower than the stores of the all-gather); CS_HIER_PULL
-  // = 0 / 1 forces it off / on
+  // pulled group mean (one group of 2 GPUs, without NVLS, NCCL, LARS or column pieces):
+  // k_hier_reduce keeps each member's mean chunk in its own gbar and the update bulk-loads the
+  // chunks from their owners over NVLink, so the all-gather rides in the update's pass.
+  // Measured: 285.7 vs 306.8 us at 1 x 2 GPUs, but 440 vs 404 us at 1 x 4 and 450 vs 399 us at
+  // 2 x 2 (peer reads are slower than the all-gather's stores once several owners or the leader
+  // exchange share the links); CS_HIER_PULL = 0 / 1 forces it off / on
   static const int pull_env = getenv("CS_HIER_PULL") ? atoi(getenv("CS_HIER_PULL")) : -1;
-  const bool pull = (pull_env < 0 ? p.gs == 2 : pull_env == 1) && !nvls && !nccl && a.lrs_out == nullptr &&
-                    (exchange || p.hier_pieces == 1) && p.gs > 1;
+  const bool pull = (pull_env < 0 ? (p.gs == 2 && !exchange) : pull_env == 1) && !nvls && !nccl &&
+                    a.lrs_out == nullptr && (exchange || p.hier_pieces == 1) && p.gs > 1;
   if (pull) b.gpull_chunk = ((a.d + p.gs - 1) / p.gs + 3) / 4 * 4;
   PeerKernelArgs ka = kernel_args(p, b, epoch, !exchange);
   if (ev0) cudaEventRecord(ev0, st);
