@@ -120,6 +120,7 @@ struct MergeArgs {
   int trl_cap;              // trailer slots per parity (tiles x n_loc)
   int lag;                  // the inbox warp stages position j once the update is at j + lag
   int read_lag;             // y-out slots left unfreed while their copies may still read them (0..kNY-1)
+  int land;                 // > 0: positions whose copies stay in flight before the store warp awaits them (<= 7)
   int vranks;
   uint32_t epoch;
   int fused_topo;           // draw Alg. 2 in the prologue (<= 64 ranks), else read s.src
@@ -798,7 +799,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     if (lane == 0) {
       // positions whose copies were issued but are not yet known complete, oldest first: a
       // head's trailer waits for its copy, a tail's release to the inbox warp for its own
-      const int land = solo ? 1 : 4;  // copies left in flight before their completion is awaited
+      const int land = a.land > 0 ? a.land : (solo ? 1 : 4);  // copies in flight before completion is awaited
       uint4* pend_dst[kQ] = {};
       uint4 pend_trl[kQ] = {};
       int pend_head = 0, npend = 0, cur = 0;
@@ -970,6 +971,8 @@ int peer_merge_launch(PeerState& p, const PeerStepArgs& a, uint32_t epoch, cudaS
   ma.lag = lag < 0 ? 0 : lag;
   static const int read_lag = getenv("CS_MERGE_READLAG") ? atoi(getenv("CS_MERGE_READLAG")) : kReadLag;
   ma.read_lag = read_lag < 0 ? 0 : (read_lag > kReadLag ? kReadLag : read_lag);
+  static const int land = getenv("CS_MERGE_LAND") ? atoi(getenv("CS_MERGE_LAND")) : 0;
+  ma.land = land < 0 ? 0 : (land > kQ - 1 ? kQ - 1 : land);
   ma.retries = p.d_stats;
   ma.off_done = p.off_done;
   ma.off_count = p.off_count;
