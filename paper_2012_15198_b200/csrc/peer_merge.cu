@@ -799,7 +799,9 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
     if (lane == 0) {
       // positions whose copies were issued but are not yet known complete, oldest first: a
       // head's trailer waits for its copy, a tail's release to the inbox warp for its own
-      const int land = a.land > 0 ? a.land : (solo ? 1 : 4);  // copies in flight before completion is awaited
+      // copies in flight before completion is awaited (c3 at 2 GPUs: 194.2 / 192.0 / 191.6 /
+      // 191.3 us for 1 / 2 / 4 / 7; bf16 wire 198.2 -> 186.0 us; profiles/r02/m16)
+      const int land = a.land > 0 ? a.land : 4;
       uint4* pend_dst[kQ] = {};
       uint4 pend_trl[kQ] = {};
       int pend_head = 0, npend = 0, cur = 0;
