@@ -89,7 +89,6 @@ constexpr int kWLoadXmg = (kUpd + kMix) / 32, kWLoadIn = kWLoadXmg + 1, kWStore 
 constexpr int kPerU = kT / 4 / kUpd;                  // float4 per update thread per tile
 constexpr int kPerM = kT / 4 / kMix;                  // float4 per mix thread per tile
 constexpr int kMixBar = 1;                            // named barrier of the mix warps
-constexpr int kUpdBar = 3;                            // named barrier of the update warps (2: prologue)
 // walk-order entries: local row | flags
 constexpr uint32_t kWStart = 1u << 31, kWEnd = 1u << 30, kWHead = 1u << 29, kWTail = 1u << 28;
 constexpr uint32_t kWIdx = (1u << 28) - 1;
@@ -128,6 +127,11 @@ struct MergeArgs {
   unsigned int* retries;      // tiles whose first read failed verification (diagnostic counter)
   uint32_t done_target;     // arrival total at which this step's last CTA publishes done = epoch
   size_t off_inbox, off_trl, off_done, off_count, off_claim, off_d2;
+};
+
+struct MixMeta {   // what the mix needs of a staged tail (written before the slot's i_full arrive)
+  int64_t c0;
+  int len, seg, first, row, t;
 };
 
 struct MTile {
@@ -259,13 +263,19 @@ __device__ __forceinline__ void ck_add(uint32_t& cx, uint32_t& cs, uint32_t w, u
 // Position j is done when EVERY update warp has released it: each warp counts its own
 // positions (a shared total would let warps that run ahead -- up to kNA stages -- stand in for
 // one still storing its part of position j).  false once j is past the CTA's last position.
-// Position j is done once the position counter (released by update thread 0 after all update
-// warps met at kUpdBar) exceeds j; relaxed polls, one acquire fence.  false once j is past the
-// CTA's last position.
+// Position j is done when EVERY update warp has released it (each counts its own positions:
+// a shared total would let warps running up to kNA stages ahead stand in for one still
+// storing its slice of position j).  Relaxed polls, one acquire fence; false once j is past
+// the CTA's last position.  Only the inbox warp waits here (the mix follows its slots).
 __device__ __forceinline__ bool wait_position(const uint32_t* y_stored, volatile int* end_pos, int j) {
   const volatile uint32_t* ys = y_stored;
-  while ((int32_t)(*ys - (uint32_t)(j + 1)) < 0)
+  for (;;) {
+    bool all = true;
+#pragma unroll
+    for (int w = 0; w < kUpd / 32; ++w) all &= (int32_t)(ys[w] - (uint32_t)(j + 1)) >= 0;
+    if (all) break;
     if (*end_pos <= j) return false;
+  }
   asm volatile("fence.acq_rel.cta;" ::: "memory");
   return true;
 }
@@ -296,7 +306,8 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
   __shared__ uint4 meta[kNI];                     // trailer of the staged received tile (bulk-loaded)
   __shared__ uint4 meta_re;                       // trailer re-read by the mix after a failed check
   __shared__ uint32_t ck_mix[2][kMix / 32][2];    // per mix warp, double-buffered by round parity
-  __shared__ uint32_t y_stored[1];  // positions every update warp has finished
+  __shared__ uint32_t y_stored[kUpd / 32];  // per update warp: positions it has released
+  __shared__ MixMeta mmeta[kNI];            // the tail staged in each inbox slot (row < 0: end)
   __shared__ int s_end;          // number of positions this CTA processes; INT_MAX until known
   __shared__ int s_timeout;
   volatile int* timeout = &s_timeout;
@@ -325,7 +336,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
   if (threadIdx.x == 0) {
     s_timeout = 0;
     s_end = 0x7fffffff;
-    y_stored[0] = 0;
+    for (int w = 0; w < kUpd / 32; ++w) y_stored[w] = 0;
     for (int i = 0; i < kNA; ++i) {
       ptx::mbar_init(&a_full[i], 1);
       ptx::mbar_init(&a_empty[i], kUpd / 32);
@@ -556,10 +567,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
         ptx::mbar_arrive(&a_empty[st]);
         if (copy) ptx::mbar_arrive(&y_full[sy]);
       }
-      // the position is done when all update warps are: they meet here (bar.sync orders their
-      // stores before thread 0's release of the single position counter)
-      ptx::named_bar_sync(kUpdBar, kUpd);
-      if (tid == 0) red_add_release_cta(y_stored, 1u);
+      if (lane == 0) red_add_release_cta(&y_stored[warp], 1u);  // this warp's part of the position
       if (copy) ++c;
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(s.err + kErrDiverged, 1);
@@ -567,25 +575,25 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
   } else if (warp < (kUpd + kMix) / 32) {
     // ---------------- mix warps: a chain tail's verify + a5 -------------------------
     const int tm = threadIdx.x - kUpd, mw = tm >> 5;
-    int cur = 0, retried = 0, round = 0, q = 0;  // round: checksum reductions (buffer parity); q: tails
-    Walk w;
-    w.init(n_loc);
-    for (int j = 0;; ++j) {
-      if (!wait_position(y_stored, end_pos, j)) break;
-      w.next(claims, a.chunk_t0, n_loc);
-      const MTile U = mtile(a, bnd, t0, w.t, cur);
-      const uint32_t e_w = ord[U.seg * n_loc + w.p];
-      if (!(e_w & kWTail)) continue;
-      const uint32_t row = e_w & kWIdx;
+    int retried = 0, round = 0, q = 0;  // round: checksum reductions (buffer parity); q: tails
+    for (;;) {  // the tails in the order the inbox warp stages them
       const int si = q % kNI;
       ptx::mbar_wait(&i_full[si], (uint32_t)((q / kNI) & 1));
       ++q;
+      const MixMeta mm = mmeta[si];
+      if (mm.row < 0) break;  // end marker
+      MTile U;
+      U.c0 = mm.c0;
+      U.len = mm.len;
+      U.seg = mm.seg;
+      U.first = mm.first != 0;
+      const uint32_t row = (uint32_t)mm.row;
       const float* it = ringI + (size_t)si * 2 * kT;
       const uint32_t nw = wire ? (uint32_t)(U.len + 1) / 2 : (uint32_t)U.len;
       const float* inbox_f = reinterpret_cast<const float*>(mine + a.off_inbox) + ((int64_t)par * n_loc + row) * s.ld;
       const uint16_t* inbox_w =
           reinterpret_cast<const uint16_t*>(mine + a.off_inbox) + ((int64_t)par * n_loc + row) * ld_bf;
-      const uint4* trl = trl_in + (size_t)w.t * n_loc + row;
+      const uint4* trl = trl_in + (size_t)mm.t * n_loc + row;
       uint4 tl = meta[si];
       uint4 raw[kPerM];  // the received words as pushed (fp32 bits, or 2 x 2 bf16 in .x .y)
       float4 yo[kPerM];  // the tail's own y (staged by the inbox warp)
@@ -759,6 +767,7 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
         const uint32_t yb = (uint32_t)(((U.len + 3) & ~3) * 4);
         const uint32_t ib = wire ? (uint32_t)(((U.len + 7) & ~7) * 2) : yb;
         if (lane == 0) {
+          mmeta[si] = MixMeta{U.c0, U.len, U.seg, U.first ? 1 : 0, (int)row, w.t};  // published by the arrive
           ptx::mbar_arrive_expect_tx(&i_full[si], ib + yb + 16u);
           ptx::bulk_g2s(buf + kT, X + (int64_t)row * s.ld + U.c0, yb, &i_full[si]);  // own y
           ptx::bulk_g2s(&meta[si], trl_in + (size_t)w.t * n_loc + row, 16u, &i_full[si]);
@@ -771,6 +780,13 @@ __global__ void __launch_bounds__(kMThreads, 1) k_push_merge(const MergeArgs a) 
                                    ((int64_t)par * n_loc + row) * s.ld + U.c0,
                           yb, &i_full[si]);
         }
+      }
+      // end marker for the mix (a plain arrive completes the slot's phase)
+      const int si = q % kNI;
+      ptx::mbar_wait(&i_empty[si], (uint32_t)(((q / kNI) & 1) ^ 1));
+      if (lane == 0) {
+        mmeta[si].row = -1;
+        ptx::mbar_arrive(&i_full[si]);
       }
     }
     __syncwarp();
