@@ -26,7 +26,9 @@
 //                     segment's first tile) goes to the receiver
 //   inbox warp        for a chain tail: stages the tile's trailer, the received tile and the
 //                     own y tile (Alg.1 l.8 irecv), once every update warp released the position
-//   mix warps (4)     verify the received words against the trailer's checksums (polling
+//   mix warps (4)     take the tails in the order the inbox warp staged them (each slot carries
+//                     the tail's row and tile; an end marker closes the step), and
+//                     verify the received words against the trailer's checksums (polling
 //                     the trailer and re-reading the words until they match: Alg.1 l.14
 //                     "wait until ... communication is completed", per tile), then
 //                     a5: x' = fl(fl(y + y_recv) * 0.5) -> params and the tail's psw
