@@ -72,16 +72,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-// 16-byte cp.async global -> shared through L1 (a generic-proxy access, unlike cp.async.bulk)
-__device__ __forceinline__ void cp_async16_ca(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
-
-// the mbarrier's current phase also waits for this thread's earlier cp.async copies
-__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-
 // L2 evict-first access policy (streamed-once data)
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
