@@ -206,7 +206,10 @@ int cs_ipc_import(const char* all_handles /* nprocs * CS_IPC_HANDLE_BYTES */);
  * Numerics: the switch sums the members' fp32 values in its own order, so for groups of
  * >= 3 GPUs params match the oracle within the hierarchical tolerance (SURVEY 8(c):
  * norm-wise <= 1e-6) rather than bitwise; groups of 2 stay bitwise.  Members still hold
- * bit-identical replicas.  LARS keeps the point-to-point h1.
+ * bit-identical replicas.  LARS keeps the point-to-point h1.  k_hier_nvls keeps all its CTAs
+ * co-resident (two per SM) for its two group barriers: other work running on the GPU at the
+ * same time delays it, bounded by the 20 s wait limit (CS_ETIMEOUT).  Measured slower than the
+ * point-to-point h1 for fp32 on this pool: an opt-in.
  * Errors: CS_ENOTBOUND, CS_EINVAL, CS_ELAYOUT (not 256-B / 16-B aligned), CS_EUNSUPPORTED
  * (one process, emulated ranks, groups of one GPU), CS_ECUDA. */
 int cs_multicast_bytes(int64_t* bytes_out);
