@@ -476,7 +476,8 @@ int enqueue_flat_step(float* params, const float* grads, float* psw, float lr, f
     } else {
       g.xnorm_valid = false;
     }
-    tma_claims(a);
+    if (!diag) tma_claims(a);  // diagnostics: round-robin tiles, so each CTA's fp64 partials
+                               // (summed in CTA order by the last CTA) are the same every run
     CS_CUDA(launch_gossip_tma(a, diag, diag ? g.tma_grid_diag : g.tma_grid_plain, g.stream));
     if (ev[1]) CS_CUDA(cudaEventRecord(ev[1], g.stream));
     g.launches_per_step = g.lars ? 3 : 1;
