@@ -173,3 +173,25 @@ def test_binding_constants_match_header():
         assert getattr(cs, name) == defs[name], name
     for name in ("TOPO_CROSSOVER", "TOPO_EXPONENTIAL", "WIRE_FP32", "WIRE_BF16"):
         assert getattr(cs, name) == defs["CS_" + name], name
+
+
+def test_nccl_group_id_and_h1_setters_need_a_binding():
+    # cs_nccl_unique_id is the host half of the NCCL h1 setup (reading B-8): NCCL loaded at run
+    # time, a fresh 128-byte id per call; the setters that join or register a group need a
+    # bound library (and so a GPU)
+    try:
+        a, b = cs.cs_nccl_unique_id(), cs.cs_nccl_unique_id()
+    except cs.CSError as e:  # no usable libnccl on this host
+        pytest.skip(f"NCCL unavailable: {e}")
+    assert len(a) == cs.CS_NCCL_ID_BYTES == 128 and a != b
+    cs.cs_finalize()
+    for call in (lambda: cs.cs_set_hier_nccl(a), lambda: cs.cs_set_multicast(0, 0, 0), cs.cs_multicast_bytes):
+        with pytest.raises(cs.CSError) as e:
+            call()
+        assert e.value.code == -7  # CS_ENOTINIT
+    cs.cs_init(4, 2, 2, 0)
+    for call in (lambda: cs.cs_set_hier_nccl(a), lambda: cs.cs_set_multicast(0, 0, 0), cs.cs_multicast_bytes):
+        with pytest.raises(cs.CSError) as e:
+            call()
+        assert e.value.code == -8  # CS_ENOTBOUND
+    cs.cs_finalize()
