@@ -42,7 +42,7 @@ namespace cs {
 namespace {
 
 constexpr int kNvlsThreads = 512;
-constexpr int kNvlsUnroll = 4;   // float4 reductions in flight per thread
+constexpr int kNvlsUnroll = 2;   // float4 reductions in flight per thread (4 spilled at 64 registers)
 
 __device__ __forceinline__ float4 mm_ld_reduce4(const float* mc) {
   float4 v;
